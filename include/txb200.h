@@ -1,0 +1,179 @@
+/*
+ * txb200 -- C ABI of the B200-native WriteImm/ImmCounter MoE dispatch/combine
+ * path (libtxb200.so, sm_100a).
+ *
+ * The reference (railtx, /root/reference/pkg/src/railtx) is pure Python and
+ * has no FFI of its own; its seam is the Python API of railtx.moe /
+ * railtx.engine.  Each entry point below replaces one piece of that API and
+ * cites the reference it stands in for.  The Python mirror of the reference
+ * interface (paper_2510_27656_b200/moe.py, engine.py) binds these through
+ * ctypes; INTEGRATION.md shows the binding.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only; device pointers are CUDA device
+ *     addresses, `stream` is a cudaStream_t passed as void*.
+ *   - Every call returns an int status: TXB_OK, or a negative error class
+ *     mirroring the reference exception taxonomy (errors.py:4-25).
+ *     txb_last_error() returns the calling thread's last message.
+ *   - Hot-path calls never allocate and never synchronise the stream.
+ *   - Device-side failures (route validation, counter timeouts, capacity)
+ *     are latched into the rank's error word (TXB_EV_* bits) and read back
+ *     with txb_moe_status() at the next host sync point.
+ */
+#ifndef TXB200_H
+#define TXB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TXB_OK 0
+#define TXB_ERR_PROTOCOL (-1) /* railtx.errors.ProtocolError  (errors.py:20) */
+#define TXB_ERR_TRANSFER (-2) /* railtx.errors.TransferError  (errors.py:16) */
+#define TXB_ERR_REGION (-3)   /* railtx.errors.RegionError    (errors.py:12) */
+#define TXB_ERR_CUDA (-4)     /* CUDA runtime failure (RailtxError)        */
+
+#define TXB_MAX_RANKS 128
+#define TXB_IPC_HANDLE_BYTES 64
+
+/* Device error-word bits (latched per rank). */
+#define TXB_EV_ROUTE_RANGE 0x1u     /* expert index out of range (moe.py:150-151) */
+#define TXB_EV_ROUTE_DUP 0x2u       /* duplicate expert in a token (moe.py:152-154) */
+#define TXB_EV_WAIT_ROUTE 0x4u      /* timed out waiting for route rows            */
+#define TXB_EV_WAIT_TOKEN 0x8u      /* timed out waiting for token writes          */
+#define TXB_EV_WAIT_BARRIER 0x10u   /* timed out waiting for peers' step barrier   */
+#define TXB_EV_WAIT_COMBINE 0x20u   /* timed out waiting for combine writes        */
+#define TXB_EV_CAPACITY 0x40u       /* destination needs more slots than capacity  */
+#define TXB_EV_WAIT_IMM 0x80u       /* txb_imm_wait timeout (engine primitive)     */
+
+/* Row encodings (RoutingSpec.elem_size, moe.py:40-50; 2 = bf16 extension). */
+#define TXB_ELEM_FP8 1
+#define TXB_ELEM_BF16 2
+#define TXB_ELEM_F32 4
+
+/* Source kinds for txb_moe_dispatch / txb_encode_rows. */
+#define TXB_SRC_ROWS 0 /* pre-encoded wire rows u8[n, P] (dispatch_send payload)  */
+#define TXB_SRC_F32 1  /* f32 values [n, hidden]: encoded inside the kernel       */
+#define TXB_SRC_BF16 2 /* bf16 values [n, hidden]: encoded inside the kernel      */
+
+/*
+ * Static shape of one expert-parallel mesh (RoutingSpec, moe.py:36-89) plus
+ * the byte layout of each rank's symmetric region.  txb_moe_plan() fills
+ * the derived fields; the struct is passed by pointer to every call.
+ */
+typedef struct txb_moe_shape {
+  /* RoutingSpec */
+  int32_t ranks, experts, max_tokens, topk, hidden, elem_size, scales;
+  /* combine wire format: elem size of the rows combine_send carries */
+  int32_t comb_elem_size, comb_scales;
+  int32_t me;     /* this rank */
+  int32_t device; /* CUDA device of this rank's region and stream */
+  /* derived by txb_moe_plan */
+  int32_t local_experts;
+  int64_t payload_bytes;  /* dispatch row bytes  = hidden*elem + 4*scales */
+  int64_t comb_bytes;     /* combine row bytes                            */
+  int64_t capacity;       /* N*T*max(R, L) (moe.py:80-83)                 */
+  int64_t grouped_rows;   /* allocated grouped rows (tight bound + padding) */
+  int64_t comb_rows;      /* T*R */
+  uint64_t off_flags, off_route, off_grouped, off_comb, region_bytes;
+} txb_moe_shape;
+
+/* ------------------------------------------------------------ runtime */
+
+const char* txb_last_error(void);
+int txb_version(void);
+int txb_device_count(int* out);
+
+/* Region registration (stands in for TransferEngine.reg_mr/dereg_mr,
+ * engine.py:314-350; MrDesc = the IPC handle, wire.py:64-87). */
+int txb_alloc(int device, uint64_t bytes, void** out_ptr);
+int txb_free(int device, void* ptr);
+int txb_memset(int device, void* ptr, int value, uint64_t bytes, void* stream);
+int txb_ipc_export(int device, void* ptr, uint8_t* out_handle /*[64]*/);
+int txb_ipc_import(int device, const uint8_t* handle /*[64]*/, void** out_ptr);
+int txb_ipc_close(int device, void* ptr);
+int txb_enable_peer(int device, int peer_device);
+
+/* ------------------------------------------------------- MoE hot path */
+
+/* Validate a RoutingSpec (moe.py:52-70) and fill the derived fields. */
+int txb_moe_plan(txb_moe_shape* s);
+
+/* Route/count kernel: MoeRank._stage count row + _check_routes +
+ * route-row scatter with the route immediate (moe.py:142-155, 499-523,
+ * 538-553).  routes: i64 or i32 [n, R] device.  Writes pos[n, R] (i64,
+ * moe.py:510-520) and the per-copy stable rank (i32 [n*R]) to scratch,
+ * stores the own count row into every peer's route matrix and
+ * release-publishes the step tag.  peers: device array of N region bases. */
+int txb_moe_route(const txb_moe_shape* s, const void* routes, int routes_i32, int64_t n,
+                  void* const* peers, void* region, int32_t* rank_scratch, int64_t* pos,
+                  uint64_t timeout_ns, void* stream);
+
+/* Dispatch kernel: waits for all route rows and for every peer's previous
+ * step barrier, derives the layout (compute_layout, moe.py:200-225) and
+ * writes each token copy straight to its final grouped row on the owning
+ * peer (moe.py:556-643 + the pack_rows regroup at 699-722), encoding on
+ * the fly for TXB_SRC_F32/BF16 (encode_tokens, moe.py:231-246).  Each CTA
+ * release-adds the rows it wrote to every destination's token counter. */
+int txb_moe_dispatch(const txb_moe_shape* s, const void* x, int src_kind, int64_t n,
+                     const void* routes, int routes_i32, const int32_t* rank_scratch,
+                     void* const* peers, void* region, uint64_t timeout_ns, int grid,
+                     void* stream);
+
+/* Receive side (dispatch_recv, moe.py:665-735): fills rows/sources (i64
+ * [grouped_rows]) and the combine return slot (i32), zeroes padding rows,
+ * writes info = [group_sizes L][group_starts L][padded_total][recv_total]
+ * [error word] (i64, 2L+3 entries) and acquire-waits until the token
+ * counter reaches the expected receipts. */
+int txb_moe_dispatch_recv(const txb_moe_shape* s, void* region, int64_t* rows, int64_t* sources,
+                          int32_t* ret_slot, int64_t* info, uint64_t timeout_ns, void* stream);
+
+/* combine_send (moe.py:739-796): every valid grouped row g of `outputs`
+ * (row stride ld bytes, comb_bytes wide) goes back to its source's combine
+ * buffer at the originating copy's send slot; per-source release-add of
+ * row counts, then the step barrier tag to every peer (moe.dbar). */
+int txb_moe_combine_send(const txb_moe_shape* s, const void* outputs, int64_t ld,
+                         void* const* peers, void* region, const int64_t* sources,
+                         const int32_t* ret_slot, const int64_t* info, int grid, void* stream);
+
+/* combine_recv (moe.py:802-833): acquire-wait for n*R returned rows, then
+ * out[t] = sum_j w[t,j] * decode(row pos[t,j]) in fp32, j ascending, no FMA
+ * (kernels.weighted_combine, kernels.py:206-242).  out_bf16: 0 -> f32 out,
+ * 1 -> bf16 RNE out (kernels.bf16_encode, kernels.py:144-150). */
+int txb_moe_combine_recv(const txb_moe_shape* s, void* region, const int64_t* pos,
+                         const float* weights, int64_t n, void* out, int out_bf16,
+                         uint64_t timeout_ns, void* stream);
+
+/* Read the rank's latched error word and counters (synchronous, for the
+ * host's ProtocolError diagnostics, moe.py:869-899).  counters receives
+ * [step, tok_ctr, tok_target, comb_ctr, comb_target] followed by
+ * route_tag[2][N] and done[N]; pass NULL to skip. */
+int txb_moe_status(const txb_moe_shape* s, void* region, uint32_t* err, uint64_t* counters,
+                   int64_t ncounters);
+
+/* ----------------------------------- codecs (kernels.py registry "cuda") */
+
+/* encode_tokens (moe.py:231-246): values (f32 or bf16 [n, hidden]) ->
+ * wire rows u8[n, hidden*elem + 4*scales]. */
+int txb_encode_rows(const void* values, int src_kind, int64_t n, int32_t hidden,
+                    int32_t elem_size, int32_t scales, void* out, void* stream);
+/* decode_tokens (moe.py:249-262): wire rows -> f32 [n, hidden]. */
+int txb_decode_rows(const void* rows, int64_t n, int32_t hidden, int32_t elem_size,
+                    int32_t scales, float* out, void* stream);
+/* kernels.pack_rows (kernels.py:184-203): out[k] = src[rows[k]]. */
+int txb_pack_rows(const void* src, int64_t width, const int64_t* rows, int64_t k, void* out,
+                  void* stream);
+/* kernels.weighted_combine (kernels.py:206-242). */
+int txb_weighted_combine(const float* y, int64_t hidden, const int64_t* pos, const float* w,
+                         int64_t n, int32_t topk, float* out, void* stream);
+/* kernels.fp8_encode / fp8_decode / bf16_encode elementwise. */
+int txb_fp8_encode(const float* x, int64_t n, uint8_t* out, void* stream);
+int txb_fp8_decode(const uint8_t* b, int64_t n, float* out, void* stream);
+int txb_bf16_encode(const float* x, int64_t n, uint16_t* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TXB200_H */

@@ -1,0 +1,227 @@
+// Shared device helpers for libtxb200 (sm_100a).
+//
+// Memory-model primitives used for the order-free completion protocol:
+//   - payload: plain (weak) 16-byte st.global to peer addresses over NVLink;
+//   - completion: __syncthreads() then one thread issues fence.sc.sys and a
+//     red.release.sys add (counters) or st.release.sys (tags) on the peer;
+//   - waiter: ld.acquire.sys spin with a %globaltimer deadline.
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/txb200.h"
+
+namespace txb {
+
+// ------------------------------------------------------------ error string
+
+void set_error(const char* fmt, ...);
+int cuda_fail(cudaError_t e, const char* what);
+
+#define TXB_CUDA(call)                                   \
+  do {                                                   \
+    cudaError_t _e = (call);                             \
+    if (_e != cudaSuccess) return ::txb::cuda_fail(_e, #call); \
+  } while (0)
+
+// ------------------------------------------------------------ PTX wrappers
+
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ void red_release_sys_add(uint64_t* p, uint64_t v) {
+  asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ void fence_sys() { asm volatile("fence.sc.sys;" ::: "memory"); }
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Spin until *p >= target (acquire, system scope) or the deadline passes.
+__device__ __forceinline__ bool spin_ge(const uint64_t* p, uint64_t target, uint64_t deadline) {
+  uint32_t it = 0;
+  while (ld_acquire_sys(p) < target) {
+    if (((++it) & 255u) == 0 && globaltimer() > deadline) return ld_acquire_sys(p) >= target;
+  }
+  return true;
+}
+
+// ------------------------------------------------------------ region layout
+
+// Per-rank flag block at region offset off_flags (4 KiB aligned).
+// route_tag/done are written by peers (single writer per slot, monotone);
+// tok_ctr/comb_ctr receive release-adds from every peer; the rest is local.
+struct Flags {
+  uint64_t route_tag[2][TXB_MAX_RANKS];  // [step parity][source] = step
+  uint64_t done[TXB_MAX_RANKS];          // [peer] = last step whose combine_send finished
+  uint64_t tok_ctr;                      // rows received (dispatch)
+  uint64_t comb_ctr;                     // rows received (combine)
+  uint64_t pad0[6];
+  // local-only state (written by this rank's kernels, in stream order)
+  uint64_t step;         // current step number (1-based), bumped by route kernel
+  uint64_t tok_target;   // cumulative expected tok_ctr
+  uint64_t comb_target;  // cumulative expected comb_ctr
+  uint32_t err;          // TXB_EV_* latch
+  uint32_t ticket;       // last-CTA detection in combine_send
+  uint64_t pad1[4];
+};
+
+__host__ __device__ inline Flags* flags_of(void* region, const txb_moe_shape& s) {
+  return reinterpret_cast<Flags*>(reinterpret_cast<char*>(region) + s.off_flags);
+}
+__host__ __device__ inline uint32_t* route_of(void* region, const txb_moe_shape& s, int slot) {
+  return reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(region) + s.off_route) +
+         (size_t)slot * s.ranks * s.experts;
+}
+__host__ __device__ inline uint8_t* grouped_of(void* region, const txb_moe_shape& s) {
+  return reinterpret_cast<uint8_t*>(region) + s.off_grouped;
+}
+__host__ __device__ inline uint8_t* comb_of(void* region, const txb_moe_shape& s) {
+  return reinterpret_cast<uint8_t*>(region) + s.off_comb;
+}
+
+// ------------------------------------------------------------- block scan
+
+// Exclusive prefix sum of a[0..len) in shared memory, in place; every thread
+// of the block must call it.  Returns the total.  `tmp` needs 33 ints.
+template <typename T>
+__device__ T block_excl_scan(T* a, int len, T* tmp) {
+  const int nt = blockDim.x, tid = threadIdx.x;
+  const int per = (len + nt - 1) / nt;
+  const int lo = min(len, tid * per), hi = min(len, lo + per);
+  T sum = 0;
+  for (int i = lo; i < hi; ++i) sum += a[i];
+  // warp inclusive scan of per-thread sums
+  const int lane = tid & 31, warp = tid >> 5;
+  T x = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) tmp[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = (nt + 31) >> 5;
+    T w = lane < nw ? tmp[lane] : T(0);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      T y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < nw) tmp[lane] = w;  // inclusive warp totals
+    if (lane == nw - 1) tmp[32] = w;
+  }
+  __syncthreads();
+  T run = (x - sum) + (warp ? tmp[warp - 1] : T(0));
+  for (int i = lo; i < hi; ++i) {
+    T v = a[i];
+    a[i] = run;
+    run += v;
+  }
+  T total = tmp[32];
+  __syncthreads();
+  return total;
+}
+
+// ------------------------------------------------------------- row copy
+
+// Copy `bytes` from src to dst with the widest vector the alignment allows;
+// the calling group is `nthr` threads with index `t`.
+__device__ __forceinline__ int vec_width(const void* a, const void* b, int64_t bytes) {
+  uintptr_t m = reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b) | (uintptr_t)bytes;
+  if ((m & 15) == 0) return 16;
+  if ((m & 7) == 0) return 8;
+  if ((m & 3) == 0) return 4;
+  return 1;
+}
+
+__device__ __forceinline__ void copy_row(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src,
+                                         int64_t bytes, int t, int nthr) {
+  const int w = vec_width(dst, src, bytes);
+  if (w == 16) {
+    const int4* s = reinterpret_cast<const int4*>(src);
+    int4* d = reinterpret_cast<int4*>(dst);
+    const int64_t nv = bytes >> 4;
+    int64_t i = t;
+    for (; i + 3 * nthr < nv; i += 4 * nthr) {
+      int4 a = s[i], b = s[i + nthr], c = s[i + 2 * nthr], e = s[i + 3 * nthr];
+      d[i] = a; d[i + nthr] = b; d[i + 2 * nthr] = c; d[i + 3 * nthr] = e;
+    }
+    for (; i < nv; i += nthr) d[i] = s[i];
+  } else if (w == 8) {
+    const int2* s = reinterpret_cast<const int2*>(src);
+    int2* d = reinterpret_cast<int2*>(dst);
+    for (int64_t i = t; i < (bytes >> 3); i += nthr) d[i] = s[i];
+  } else if (w == 4) {
+    const int* s = reinterpret_cast<const int*>(src);
+    int* d = reinterpret_cast<int*>(dst);
+    for (int64_t i = t; i < (bytes >> 2); i += nthr) d[i] = s[i];
+  } else {
+    for (int64_t i = t; i < bytes; i += nthr) dst[i] = src[i];
+  }
+}
+
+__device__ __forceinline__ void zero_row(uint8_t* dst, int64_t bytes, int t, int nthr) {
+  const int w = vec_width(dst, dst, bytes);
+  if (w == 16) {
+    int4 z = make_int4(0, 0, 0, 0);
+    for (int64_t i = t; i < (bytes >> 4); i += nthr) reinterpret_cast<int4*>(dst)[i] = z;
+  } else if (w >= 4) {
+    for (int64_t i = t; i < (bytes >> 2); i += nthr) reinterpret_cast<int*>(dst)[i] = 0;
+  } else {
+    for (int64_t i = t; i < bytes; i += nthr) dst[i] = 0;
+  }
+}
+
+// -------------------------------------------------------------- codecs
+
+// e4m3 RNE satfinite; NaN -> 0x7F regardless of sign (kernels.py:65-76).
+__device__ __forceinline__ uint32_t fp8x2(float a, float b) {
+  uint16_t r;
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(b), "f"(a));
+  uint32_t v = r;
+  if (isnan(a)) v = (v & 0xFF00u) | 0x7Fu;
+  if (isnan(b)) v = (v & 0x00FFu) | 0x7F00u;
+  return v;
+}
+
+// Exact e4m3 -> f32 (every e4m3 value is an f16 value).
+__device__ __forceinline__ float2 fp8x2_to_f2(uint16_t v) {
+  uint32_t h2;
+  asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h2) : "h"(v));
+  __half2_raw raw;
+  raw.x = (unsigned short)(h2 & 0xFFFF);
+  raw.y = (unsigned short)(h2 >> 16);
+  return __half22float2(*reinterpret_cast<__half2*>(&raw));
+}
+
+// bf16 RNE with the reference NaN rule 0x7FC0|hi (kernels.py:144-150).
+__device__ __forceinline__ uint16_t bf16_rne(float x) {
+  uint32_t b = __float_as_uint(x);
+  if ((b & 0x7F800000u) == 0x7F800000u && (b & 0x007FFFFFu)) return (uint16_t)(0x7FC0u | (b >> 16));
+  return (uint16_t)((b + 0x7FFFu + ((b >> 16) & 1u)) >> 16);
+}
+
+__device__ __forceinline__ float bf16_to_f(uint16_t h) { return __uint_as_float(((uint32_t)h) << 16); }
+
+}  // namespace txb

@@ -1,0 +1,246 @@
+"""GPU parity: the sm_100a dispatch/combine path vs the reference goldens
+and the CPU oracle.  Bit-exact for payload bytes, indices, counts and the
+fp32 combine; bf16 combine output within rtol 1e-2 / atol 1e-3
+(BASELINE.json north_star)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from golden_io import load_moe, moe_cases
+from oracle import moe_oracle as mo
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from moe_driver import close_mesh, make_mesh, ospec_of, run_moe_round
+    from paper_2510_27656_b200 import moe
+    from paper_2510_27656_b200.engine import local_engines
+    from paper_2510_27656_b200.errors import ProtocolError
+
+
+def _np(x):
+    return x.cpu().numpy() if isinstance(x, torch.Tensor) else np.asarray(x)
+
+
+@pytest.mark.parametrize("name", moe_cases())
+def test_golden_round_bit_exact(name):
+    """Whole reference rounds (goldens from railtx itself) through the
+    device path, host-mode API, threaded driver like the reference's."""
+    case = load_moe(name)
+    spec = moe.RoutingSpec(**case.spec_args)
+    mesh = make_mesh(spec)
+    try:
+        for st in case.steps:
+            res = run_moe_round(mesh, spec, st.routes, st.values, st.weights)
+            for q in range(spec.ranks):
+                g, comb, pos = res[q]
+                assert np.array_equal(pos, st.pos[q]), f"pos rank {q}"
+                assert np.array_equal(_np(g.group_sizes), st.group_sizes[q])
+                assert np.array_equal(_np(g.group_starts), st.group_starts[q])
+                assert np.array_equal(_np(g.rows), st.rows[q]), f"rows rank {q}"
+                assert np.array_equal(_np(g.sources), st.sources[q]), f"sources rank {q}"
+                assert np.array_equal(_np(g.data), st.data[q]), f"data rank {q}"
+                assert comb.shape == st.combined[q].shape
+                assert np.array_equal(comb, st.combined[q]), f"combine rank {q}"
+            if st.counts is not None:
+                lay = mesh[0].last_layout
+                assert np.array_equal(lay.counts, st.counts)
+    finally:
+        close_mesh(mesh)
+
+
+def _oracle_round(ospec, routes, values_or_payloads, encoded=False):
+    payloads = values_or_payloads if encoded else [mo.encode_tokens(ospec, v) for v in values_or_payloads]
+    return mo.dispatch(ospec, routes, payloads), payloads
+
+
+@pytest.mark.parametrize("elem,src", [(1, torch.float32), (1, torch.bfloat16), (2, torch.float32),
+                                      (2, torch.bfloat16), (4, torch.float32)])
+def test_fused_encode_dispatch_matches_oracle(elem, src):
+    """Device mode: f32/bf16 values encoded inside the dispatch kernel
+    (fp8 per-token scale / bf16 RNE / f32) == encode_tokens then dispatch."""
+    N = 1
+    spec = moe.RoutingSpec(ranks=N, experts=32, max_tokens=64, topk=4, hidden=512,
+                           elem_size=elem, scales=8 if elem == 1 else 0)
+    os_ = ospec_of(spec)
+    rng = np.random.default_rng(5)
+    routes, values, weights = mo.random_step(os_, rng, tokens=64)
+    vals = [torch.from_numpy(v).to(src) for v in values]
+    ref_vals = [v.float().numpy() for v in vals]      # bf16-rounded inputs for the oracle
+    res, _ = _oracle_round(os_, routes, ref_vals)
+    mesh = moe.build_mesh(local_engines([0]), spec)
+    try:
+        rk = mesh[0]
+        rk.dispatch_send(vals[0].cuda(), torch.from_numpy(routes[0]).cuda())
+        g = rk.dispatch_recv()
+        want = res.ranks[0].grouped
+        assert np.array_equal(_np(g.data), want.data)
+        assert np.array_equal(_np(g.rows), want.rows)
+        rk.combine_send(g.data)
+        out = rk.combine_recv(torch.from_numpy(weights[0]).cuda())
+        ref = mo.combine(os_, res, [want.data], weights)[0]
+        assert np.array_equal(_np(out), ref)
+    finally:
+        close_mesh(mesh)
+
+
+def test_dsv3_decode_ep1_full_size():
+    """DeepSeek-V3 decode shape at EP=1 (128 tok, H=7168, E=256, top-8),
+    fp8 dispatch from bf16 values, bf16 combine rows, bf16 out; several
+    steps back to back on one mesh (counter epochs, buffer reuse)."""
+    spec = moe.RoutingSpec(ranks=1, experts=256, max_tokens=128, topk=8, hidden=7168,
+                           elem_size=1, scales=56, comb_elem_size=2, comb_scales=0)
+    os_ = ospec_of(spec)
+    cs = mo.Spec(1, 256, 128, 8, hidden=7168, elem_size=2, scales=0)
+    mesh = moe.build_mesh(local_engines([0]), spec)
+    rk = mesh[0]
+    try:
+        for step in range(3):
+            rng = np.random.default_rng(100 + step)
+            routes, values, weights = mo.random_step(os_, rng, tokens=128)
+            xb = torch.from_numpy(values[0]).to(torch.bfloat16)
+            res, _ = _oracle_round(os_, routes, [xb.float().numpy()])
+            rk.dispatch_send(xb.cuda(), torch.from_numpy(routes[0]).cuda())
+            g = rk.dispatch_recv()
+            want = res.ranks[0].grouped
+            assert np.array_equal(_np(g.data), want.data)
+            assert np.array_equal(_np(g.sources), want.sources)
+            # expert stand-in: decode the fp8 rows, scale by (1 + expert), bf16 rows back
+            y = torch.zeros((g.data.shape[0], spec.hidden), dtype=torch.bfloat16, device="cuda")
+            dec = moe.decode_tokens(spec, g.data)
+            for le in range(spec.local_experts):
+                s0, c = int(g.group_starts[le]), int(g.group_sizes[le])
+                if c:
+                    y[s0:s0 + c] = (dec[s0:s0 + c] * (1.0 + 0.01 * le)).to(torch.bfloat16)
+            rk.combine_send(y)
+            out = rk.combine_recv(torch.from_numpy(weights[0]).cuda(), out_dtype=torch.bfloat16)
+            outs = [mo.bf16_encode(y.float().cpu().numpy()).view(np.uint8).reshape(y.shape[0], -1)]
+            ref = mo.combine(os_, res, outs, weights, comb_spec=cs)[0]
+            got = out.float().cpu().numpy()
+            np.testing.assert_allclose(got, ref, rtol=1e-2, atol=1e-3)
+            # the fp32 accumulation itself is exact: bf16(out) == bf16(ref)
+            assert np.array_equal(mo.bf16_encode(ref), out.view(torch.int16).cpu().numpy().view(np.uint16))
+    finally:
+        rk.close()
+
+
+def test_multi_step_and_empty_steps():
+    """Ragged token counts including empty steps, several steps in a row."""
+    spec = moe.RoutingSpec(ranks=2, experts=8, max_tokens=12, topk=3, hidden=64, elem_size=4, scales=0)
+    os_ = ospec_of(spec)
+    mesh = make_mesh(spec)
+    try:
+        rng = np.random.default_rng(3)
+        for step in range(6):
+            tokens = 0 if step in (1, 4) else None
+            routes, values, weights = mo.random_step(os_, rng, tokens)
+            res = run_moe_round(mesh, spec, routes, values, weights)
+            ref, pay = _oracle_round(os_, routes, values)
+            outs = mo.apply_experts(os_, ref)
+            comb = mo.combine(os_, ref, outs, weights)
+            for q in range(spec.ranks):
+                assert np.array_equal(_np(res[q][0].data), ref.ranks[q].grouped.data)
+                assert np.array_equal(res[q][1], comb[q])
+    finally:
+        close_mesh(mesh)
+
+
+def test_route_errors_host_and_device():
+    spec = moe.RoutingSpec(ranks=1, experts=8, max_tokens=4, topk=2, hidden=16, elem_size=4, scales=0)
+    mesh = moe.build_mesh(local_engines([0]), spec)
+    rk = mesh[0]
+    try:
+        pay = np.zeros((2, spec.payload_bytes), np.uint8)
+        with pytest.raises(ProtocolError, match="duplicate"):
+            rk.dispatch_send(pay, np.array([[1, 1], [2, 3]]))
+        with pytest.raises(ProtocolError, match="out of range"):
+            rk.dispatch_send(pay, np.array([[1, 9], [2, 3]]))
+        with pytest.raises(ProtocolError, match="token limit"):
+            rk.dispatch_send(np.zeros((5, spec.payload_bytes), np.uint8), np.zeros((5, 2), np.int64))
+        with pytest.raises(ProtocolError, match="payload shape"):
+            rk.dispatch_send(np.zeros((2, 3), np.uint8), np.array([[1, 2], [2, 3]]))
+        with pytest.raises(ProtocolError, match="combine before dispatch"):
+            rk.combine_send(np.zeros((8, spec.payload_bytes), np.uint8))
+        # device-validated routes: latched, raised at dispatch_recv
+        rk.dispatch_send(torch.zeros((2, spec.payload_bytes), dtype=torch.uint8, device="cuda"),
+                         torch.tensor([[1, 1], [2, 3]], device="cuda"))
+        with pytest.raises(ProtocolError, match="duplicate"):
+            rk.dispatch_recv()
+    finally:
+        rk.close()
+
+
+def test_step_in_flight_error():
+    spec = moe.RoutingSpec(ranks=1, experts=4, max_tokens=4, topk=1, hidden=16, elem_size=4, scales=0)
+    mesh = moe.build_mesh(local_engines([0]), spec)
+    rk = mesh[0]
+    try:
+        pay = np.zeros((1, spec.payload_bytes), np.uint8)
+        rk.dispatch_send(pay, np.array([[0]]))
+        with pytest.raises(ProtocolError, match="in flight"):
+            rk.dispatch_send(pay, np.array([[0]]))
+        g = rk.dispatch_recv()
+        rk.combine_send(np.zeros_like(g.data))
+        out = rk.combine_recv(np.ones((1, 1), np.float32))
+        assert out.shape == (1, 16)
+    finally:
+        rk.close()
+
+
+def test_no_sync_mode_matches_sync():
+    """dispatch_recv(sync=False): max-shape views + device sizes; the whole
+    step is launch-only (what the bench and CUDA graphs use)."""
+    spec = moe.RoutingSpec(ranks=1, experts=64, max_tokens=32, topk=4, hidden=256,
+                           elem_size=1, scales=4, comb_elem_size=2, comb_scales=0)
+    os_ = ospec_of(spec)
+    rng = np.random.default_rng(9)
+    routes, values, weights = mo.random_step(os_, rng, tokens=32)
+    mesh = moe.build_mesh(local_engines([0]), spec)
+    rk = mesh[0]
+    try:
+        x = torch.from_numpy(values[0]).cuda()
+        r = torch.from_numpy(routes[0]).cuda()
+        w = torch.from_numpy(weights[0]).cuda()
+        y = torch.randn(int(rk._shape.grouped_rows), spec.hidden, device="cuda").to(torch.bfloat16)
+        rk.dispatch_send(x, r, sync=False)
+        g = rk.dispatch_recv(sync=False)
+        rk.combine_send(y)
+        out1 = rk.combine_recv(w, sync=False)
+        torch.cuda.synchronize()
+        rk.dispatch_send(x, r)
+        g2 = rk.dispatch_recv()
+        total = g2.data.shape[0]
+        assert int(g.padded_total) == total
+        rk.combine_send(y[:total].contiguous())
+        out2 = rk.combine_recv(w)
+        assert torch.equal(out1, out2)
+    finally:
+        rk.close()
+
+
+def test_codecs_match_reference_goldens():
+    from golden_io import load_codecs
+    from paper_2510_27656_b200 import kernels
+    c = load_codecs()
+    assert np.array_equal(kernels.fp8_encode(c["fp8_in"]), c["fp8_out"])
+    assert np.array_equal(kernels.bf16_encode(c["bf16_in"]), c["bf16_out"])
+    dec = kernels.fp8_decode(np.arange(256, dtype=np.uint8))
+    assert np.array_equal(dec, c["fp8_table"], equal_nan=True)
+    spec = moe.RoutingSpec(ranks=1, experts=1, max_tokens=12, topk=1, hidden=96, elem_size=1, scales=3)
+    assert np.array_equal(moe.encode_tokens(spec, c["rows"]), c["rows_enc"])
+    assert np.array_equal(moe.decode_tokens(spec, c["rows_enc"]), c["rows_dec"], equal_nan=True)
+
+
+def test_kernel_registry_matches_oracle():
+    from paper_2510_27656_b200 import kernels
+    rng = np.random.default_rng(4)
+    src = rng.integers(0, 256, (50, 37), dtype=np.uint8)
+    rows = rng.integers(0, 50, 80)
+    assert np.array_equal(kernels.pack_rows(src, rows), src[rows])
+    y = rng.standard_normal((40, 24)).astype(np.float32)
+    pos = rng.integers(0, 40, (10, 3))
+    w = rng.random((10, 3)).astype(np.float32)
+    assert np.array_equal(kernels.weighted_combine(y, pos, w), mo.weighted_combine(y, pos, w))
