@@ -1,0 +1,404 @@
+"""Benchmark: MoE dispatch+combine p50 latency (decode) on B200.
+
+Workload (BASELINE.json configs[1], DeepSeek-V3 decode): 128 tokens per
+rank, hidden 7168, 256 experts, top-8; dispatch carries fp8 e4m3 rows with
+per-token f32 scales (7168 + 56*4 = 7392 B, encoded inside the dispatch
+kernel from bf16 activations), combine carries bf16 rows (14336 B) and
+produces bf16 outputs.  EP = number of GPUs (1 = loopback through HBM).
+
+A step = dispatch_send -> dispatch_recv -> combine_send -> combine_recv
+through the public MoeRank API (launch-only, sync=False), timed per step
+with CUDA events on the rank's stream after a device-side all-rank
+barrier; L2 is flushed (write of a 512 MiB buffer) before every timed step.
+value = p50 over steps of the max over ranks of the step time (us).
+
+Usage:  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+        torchrun --nproc-per-node N bench.py --gpus N ...
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+T, H, E, R, SCALES = 128, 7168, 256, 8, 56
+METRIC = "dispatch+combine p50 us (decode, DeepSeek-V3 shape)"
+
+
+def _args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--tokens", type=int, default=T)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--kernel-times", action="store_true", default=True)
+    return ap.parse_args()
+
+
+def _dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def _inputs(rank: int, tokens: int, seed: int = 0):
+    rng = np.random.default_rng((seed << 8) + rank)
+    x = rng.standard_normal((tokens, H)).astype(np.float32)
+    routes = np.argsort(rng.random((tokens, E)), axis=1)[:, :R].astype(np.int64)
+    w = rng.random((tokens, R)).astype(np.float32)
+    return x, routes, w
+
+
+# ------------------------------------------------------------ CPU baseline
+
+
+def cpu_port_step(ospec, cspec, x_bf16_f32, routes, w, mo):
+    """One decode step of the reference algorithm on the host (oracle port):
+    encode (fp8 per token) -> dispatch regroup -> identity expert in bf16 ->
+    combine return -> fp32 weighted sum -> bf16 out."""
+    pay = mo.encode_tokens(ospec, x_bf16_f32)
+    res = mo.dispatch(ospec, [routes], [pay])
+    g = res.ranks[0].grouped
+    y = mo.decode_tokens(ospec, g.data)
+    outs = [mo.bf16_encode(y).view(np.uint8).reshape(y.shape[0], -1)]
+    comb = mo.combine(ospec, res, outs, [w], comb_spec=cspec)[0]
+    return mo.bf16_encode(comb)
+
+
+def cpu_baseline(tokens: int, seconds: float) -> dict:
+    from oracle import moe_oracle as mo
+    ospec = mo.Spec(1, E, tokens, R, hidden=H, elem_size=1, scales=SCALES)
+    cspec = mo.Spec(1, E, tokens, R, hidden=H, elem_size=2, scales=0)
+    x, routes, w = _inputs(0, tokens)
+    xb = mo.bf16_decode(mo.bf16_encode(x))
+    cpu_port_step(ospec, cspec, xb, routes, w, mo)  # warm
+    times = []
+    t_end = time.perf_counter() + seconds
+    while time.perf_counter() < t_end or len(times) < 3:
+        t0 = time.perf_counter()
+        cpu_port_step(ospec, cspec, xb, routes, w, mo)
+        times.append((time.perf_counter() - t0) * 1e6)
+    return {"value": statistics.median(times), "unit": "us", "cores": 1, "kind": "port",
+            "sample": f"{len(times)} full EP=1 decode steps ({tokens} tok, H={H}, E={E}, top-{R}, "
+                      f"fp8 dispatch + bf16 combine), numpy oracle port, single thread, p50"}
+
+
+# ------------------------------------------------------------ clocks
+
+
+class Clocks:
+    def __init__(self, device: int) -> None:
+        self.p = None
+        self.path = Path(f"/tmp/txb_clocks_{os.getpid()}.csv")
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(device), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.p.terminate()
+        self.p.wait()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.path.read_text().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------ GPU arm
+
+
+def run_b200(a) -> None:
+    import torch
+    world, rank, local = _dist()
+    n_gpu = world
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    from paper_2510_27656_b200 import moe
+    from paper_2510_27656_b200.engine import NvlinkFabric, TransferEngine
+
+    spec = moe.RoutingSpec(ranks=n_gpu, experts=E, max_tokens=a.tokens, topk=R, hidden=H,
+                           elem_size=1, scales=SCALES, comb_elem_size=2, comb_scales=0)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        eng = TransferEngine(NvlinkFabric(group=dist.group.WORLD), device=local)
+        rk = moe.connect_process_group(eng, spec)
+    else:
+        eng = TransferEngine(NvlinkFabric(), device=local)
+        rk = moe.build_mesh([eng], spec)[0]
+    rk.record_stats = False
+    tokens = a.tokens
+    x, routes, w = _inputs(rank, tokens)
+    xd = torch.from_numpy(x).to(dev).to(torch.bfloat16)
+    rd = torch.from_numpy(routes).to(dev)
+    wd = torch.from_numpy(w).to(dev)
+    G = int(rk._shape.grouped_rows)
+    y = torch.randn(G, H, device=dev).to(torch.bfloat16)     # synthetic expert outputs
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        rk.dispatch_send(xd, rd, sync=False)
+        rk.dispatch_recv(sync=False)
+        rk.combine_send(y)
+        return rk.combine_recv(wd, out_dtype=torch.bfloat16, sync=False)
+
+    for _ in range(max(3, a.warmup)):
+        step()
+    torch.cuda.synchronize()
+    err, _ = rk.status()
+    assert err == 0, f"device error word {err:#x} during warm-up"
+
+    # -------- timed: per step events, L2 flush + barrier outside the span
+    K = a.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    clocks = Clocks(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+    for k in range(K):
+        flush.fill_(k & 0xFF)
+        if world > 1:
+            rk.barrier()
+        ev[k][0].record(stream)
+        rk.dispatch_send(xd, rd, sync=False)
+        rk.dispatch_recv(sync=False)
+        ev[k][1].record(stream)
+        rk.combine_send(y)
+        rk.combine_recv(wd, out_dtype=torch.bfloat16, sync=False)
+        ev[k][2].record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    err, _ = rk.status()
+    assert err == 0, f"device error word {err:#x}"
+    tot = np.array([e0.elapsed_time(e2) * 1e3 for e0, e1, e2 in ev])
+    dsp = np.array([e0.elapsed_time(e1) * 1e3 for e0, e1, e2 in ev])
+    cmb = np.array([e1.elapsed_time(e2) * 1e3 for e0, e1, e2 in ev])
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor(np.stack([tot, dsp, cmb]), device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot, dsp, cmb = (t.cpu().numpy()[i] for i in range(3))
+
+    # -------- per-kernel durations (separate pass, events between launches)
+    kt = kernel_times(rk, xd, rd, wd, y, flush, stream, reps=max(20, K // 4))
+
+    # -------- e2e through the public API with pinned host buffers
+    e2e = e2e_times(rk, x, routes, w, stream, flush, dev, K, world)
+
+    # -------- bytes / roofline
+    ex = expected_rows(rank, n_gpu, tokens)
+    P, Pc = spec.payload_bytes, spec.comb_payload_bytes
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    nvl_peak = 770.0
+    bytes_k = {
+        "dispatch": tokens * H * 2 + tokens * R * P if n_gpu == 1 else max(ex["out_rows"], ex["in_rows"]) * P,
+        "comb_send": 2 * ex["valid_rows"] * Pc if n_gpu == 1 else max(ex["valid_rows"] - ex["self_rows"], ex["out_rows"]) * Pc,
+        "comb_recv": tokens * R * Pc + tokens * H * 2,
+        "recv": ex["pad_rows"] * P,
+        "route": tokens * R * 8 * 2 + n_gpu * E * 4,
+    }
+    dom = max(("dispatch", "comb_send", "comb_recv"), key=lambda k: kt[k])
+    dom_local = dom == "comb_recv" or n_gpu == 1
+    peak = hbm_peak if dom_local else nvl_peak
+    achieved = bytes_k[dom] / (kt[dom] * 1e-6) / 1e9
+    roofline = {"bound": "hbm" if dom_local else "nvlink", "kernel": f"k_{dom}",
+                "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": None,
+                "peak_source": ("MEASURED_PEAKS.json hbm_gbs (burst copy)" if dom_local
+                                else "B200_PROFILING.md measured peer copy 770 GB/s (fallback)"),
+                "algorithmic_bytes": int(bytes_k[dom]), "kernel_us": round(kt[dom], 2)}
+    step_bytes = (tokens * R * P + tokens * R * Pc)
+    res = {
+        "metric": METRIC, "value": round(float(np.median(tot)), 2), "unit": "us",
+        "n_gpus": n_gpu, "steps": K, "warmup": a.warmup,
+        "ms_per_step": round(float(np.median(tot)) / 1e3, 5),
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+        "dtype": "fp8-e4m3 dispatch / bf16 combine (fp32 accumulate)", "data": "synthetic",
+        "config": {"workload": "DeepSeek-V3 decode dispatch+combine", "tokens_per_rank": tokens,
+                   "hidden": H, "experts": E, "topk": R, "ep": n_gpu,
+                   "dispatch_row_bytes": P, "combine_row_bytes": Pc, "routing": "uniform top-8",
+                   "l2": "flushed before every step (512 MiB write)", "parallelism": f"ep{n_gpu}"},
+        "p50_dispatch_us": round(float(np.median(dsp)), 2),
+        "p50_combine_us": round(float(np.median(cmb)), 2),
+        "p90_us": round(float(np.percentile(tot, 90)), 2),
+        "p99_us": round(float(np.percentile(tot, 99)), 2),
+        "tokens_per_s": round(n_gpu * tokens / (float(np.median(tot)) * 1e-6), 1),
+        "payload_gbs_per_rank": round(step_bytes / (float(np.median(tot)) * 1e-6) / 1e9, 1),
+        "kernel_us": {k: round(v, 2) for k, v in kt.items()},
+        "roofline": roofline,
+        "e2e": e2e,
+        "gpu_launches": 5 * K,
+        "clocks": clk,
+    }
+    if rank == 0 and n_gpu == 1 and not a.no_cpu_baseline:
+        res["cpu_baseline"] = cpu_baseline(tokens, a.cpu_seconds)
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    rk.close()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def expected_rows(rank: int, n: int, tokens: int) -> dict:
+    """Per-rank row counts for this rank's inputs (uniform routes)."""
+    L = E // n
+    all_routes = [_inputs(q, tokens)[1] for q in range(n)]
+    mine = all_routes[rank]
+    dest = mine // L
+    out_rows = int((dest != rank).sum())
+    self_rows = int((dest == rank).sum())
+    in_rows = int(sum(((r // L) == rank).sum() for q, r in enumerate(all_routes) if q != rank))
+    counts = np.zeros(L, np.int64)
+    for r in all_routes:
+        e = r.ravel()
+        e = e[e // L == rank] - rank * L
+        counts += np.bincount(e, minlength=L)
+    pad = int(((-counts) % 8).sum())
+    return {"out_rows": out_rows, "in_rows": in_rows, "self_rows": self_rows,
+            "valid_rows": int(counts.sum()), "pad_rows": pad}
+
+
+def kernel_times(rk, xd, rd, wd, y, flush, stream, reps: int) -> dict:
+    """Average device time of each of the five kernels (events between
+    launches on the rank's stream, L2 flushed before each step)."""
+    import torch
+    names = ["route", "dispatch", "recv", "comb_send", "comb_recv"]
+    acc = {k: [] for k in names}
+    for _ in range(reps):
+        flush.fill_(1)
+        if rk.spec.ranks > 1:
+            rk.barrier()
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+        evs[0].record(stream)
+        # route + dispatch are launched by dispatch_send; split them with a
+        # mid event by calling the two C entry points through the API pieces
+        rk.dispatch_send(xd, rd, sync=False, _mid_event=evs[1])
+        evs[2].record(stream)
+        rk.dispatch_recv(sync=False)
+        evs[3].record(stream)
+        rk.combine_send(y)
+        evs[4].record(stream)
+        rk.combine_recv(wd, out_dtype=torch.bfloat16, sync=False)
+        evs[5].record(stream)
+        torch.cuda.synchronize()
+        for i, k in enumerate(names):
+            acc[k].append(evs[i].elapsed_time(evs[i + 1]) * 1e3)
+    return {k: float(np.median(v)) for k, v in acc.items()}
+
+
+def e2e_times(rk, x, routes, w, stream, flush, dev, K: int, world: int) -> dict:
+    """Same step through the public API with pinned HOST buffers: H2D of
+    activations (bf16), routes (i64) and weights (f32) and D2H of the
+    combined bf16 output inside the timed span."""
+    import torch
+    xh = torch.from_numpy(x).to(torch.bfloat16).pin_memory()
+    rh = torch.from_numpy(routes).pin_memory()
+    wh = torch.from_numpy(w).pin_memory()
+    oh = torch.empty((x.shape[0], x.shape[1]), dtype=torch.bfloat16).pin_memory()
+    G = int(rk._shape.grouped_rows)
+    y = torch.randn(G, x.shape[1], device=dev).to(torch.bfloat16)
+    times = []
+    for k in range(K + 5):
+        flush.fill_(2)
+        if world > 1:
+            rk.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        xd = xh.to(dev, non_blocking=True)
+        rd = rh.to(dev, non_blocking=True)
+        wd = wh.to(dev, non_blocking=True)
+        rk.dispatch_send(xd, rd, sync=False)
+        rk.dispatch_recv(sync=False)
+        rk.combine_send(y)
+        out = rk.combine_recv(wd, out_dtype=torch.bfloat16, sync=False)
+        oh.copy_(out, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if k >= 5:
+            times.append(e0.elapsed_time(e1) * 1e3)
+    t = np.array(times)
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor(t, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = tt.cpu().numpy()
+    bi = x.shape[0] * x.shape[1] * 2 + routes.size * 8 + w.size * 4
+    return {"value": round(float(np.median(t)), 2), "unit": "us",
+            "h2d_bytes_per_step": int(bi), "d2h_bytes_per_step": int(x.shape[0] * x.shape[1] * 2)}
+
+
+# ------------------------------------------------------------ reference arm
+
+
+def run_reference(a) -> None:
+    world, rank, _ = _dist()
+    if rank != 0:
+        return
+    cb = cpu_baseline(a.tokens, max(2.0, min(a.cpu_seconds, 30.0)))
+    res = {"impl": "reference", "metric": METRIC, "value": round(cb["value"], 2), "unit": "us",
+           "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "higher_is_better": False,
+           "scaling": "weak", "vs_baseline": None, "dtype": "fp8-e4m3 dispatch / bf16 combine (fp32 accumulate)",
+           "data": "synthetic",
+           "config": {"workload": "DeepSeek-V3 decode dispatch+combine", "tokens_per_rank": a.tokens,
+                      "hidden": H, "experts": E, "topk": R, "ep": 1},
+           "cpu_baseline": cb,
+           "e2e": {"value": round(cb["value"], 2), "unit": "us", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0},
+           "note": "reference railtx is pure Python and cannot travel to the GPU box; this arm times "
+                   "the oracle port of its algorithm (oracle/moe_oracle.py) on the host cores"}
+    print(json.dumps(res), flush=True)
+
+
+def main() -> None:
+    a = _args()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_b200(a)
+
+
+if __name__ == "__main__":
+    main()

@@ -146,6 +146,12 @@ int txb_moe_combine_recv(const txb_moe_shape* s, void* region, const int64_t* po
                          const float* weights, int64_t n, void* out, int out_bf16,
                          uint64_t timeout_ns, void* stream);
 
+/* Device-side all-rank barrier over the mesh (engine submit_barrier,
+ * engine.py:599-619): each rank release-stores its epoch into every peer,
+ * then acquire-waits for every peer's epoch.  Used to align step starts. */
+int txb_moe_barrier(const txb_moe_shape* s, void* const* peers, void* region, uint64_t timeout_ns,
+                    void* stream);
+
 /* Read the rank's latched error word and counters (synchronous, for the
  * host's ProtocolError diagnostics, moe.py:869-899).  counters receives
  * [step, tok_ctr, tok_target, comb_ctr, comb_target] followed by

@@ -76,6 +76,7 @@ SIGNATURES: dict[str, list] = {
     "txb_moe_dispatch_recv": [C.POINTER(Shape), _VP, _VP, _VP, _VP, _VP, _U64, _VP],
     "txb_moe_combine_send": [C.POINTER(Shape), _VP, _I64, _VP, _VP, _VP, _VP, _VP, _INT, _VP],
     "txb_moe_combine_recv": [C.POINTER(Shape), _VP, _VP, _VP, _I64, _VP, _INT, _U64, _VP],
+    "txb_moe_barrier": [C.POINTER(Shape), _VP, _VP, _U64, _VP],
     "txb_moe_status": [C.POINTER(Shape), _VP, C.POINTER(C.c_uint32), C.POINTER(_U64), _I64],
     "txb_encode_rows": [_VP, _INT, _I64, _I32, _I32, _I32, _VP, _VP],
     "txb_decode_rows": [_VP, _I64, _I32, _I32, _I32, _VP, _VP],

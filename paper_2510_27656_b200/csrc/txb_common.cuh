@@ -82,7 +82,9 @@ struct Flags {
   uint64_t comb_target;  // cumulative expected comb_ctr
   uint32_t err;          // TXB_EV_* latch
   uint32_t ticket;       // last-CTA detection in combine_send
-  uint64_t pad1[4];
+  uint64_t bar_epoch;    // local epoch of txb_moe_barrier
+  uint64_t pad1[3];
+  uint64_t bar[TXB_MAX_RANKS];  // [peer] = last barrier epoch peer reached
 };
 
 __host__ __device__ inline Flags* flags_of(void* region, const txb_moe_shape& s) {

@@ -408,6 +408,30 @@ k_comb_recv(txb_moe_shape s, void* region, const int64_t* __restrict__ pos, cons
   combine_rows<ELEM>(comb_of(region, s), s.comb_bytes, s.hidden, pos, w, n, s.topk, out, out_bf16);
 }
 
+// -------------------------------------------------------------- k_barrier
+
+// All-rank device barrier (the reference's submit_barrier with one imm per
+// peer, engine.py:599-619): publish my epoch into every peer's slot, then
+// acquire-wait until every peer's epoch has reached mine.
+__global__ void k_barrier(txb_moe_shape s, void* const* __restrict__ peers, void* region, uint64_t timeout_ns) {
+  Flags* f = flags_of(region, s);
+  __shared__ uint64_t ep;
+  __shared__ uint32_t fail;
+  if (threadIdx.x == 0) {
+    ep = f->bar_epoch + 1;
+    f->bar_epoch = ep;
+    fail = 0;
+  }
+  __syncthreads();
+  const int N = s.ranks;
+  for (int q = threadIdx.x; q < N; q += blockDim.x) st_release_sys(&flags_of(peers[q], s)->bar[s.me], ep);
+  const uint64_t dl = globaltimer() + timeout_ns;
+  for (int q = threadIdx.x; q < N; q += blockDim.x)
+    if (!spin_ge(&f->bar[q], ep, dl)) atomicOr(&fail, TXB_EV_WAIT_BARRIER);
+  __syncthreads();
+  if (threadIdx.x == 0 && fail) atomicOr(&f->err, fail);
+}
+
 // ------------------------------------------------------------------ host
 
 static int sm_count(int dev) {
@@ -592,6 +616,14 @@ int txb_moe_combine_recv(const txb_moe_shape* s, void* region, const int64_t* po
     case 2: k_comb_recv<2><<<grid, kCombRecvThreads, 0, st>>>(*s, region, pos, weights, n, out, out_bf16, timeout_ns); break;
     default: k_comb_recv<4><<<grid, kCombRecvThreads, 0, st>>>(*s, region, pos, weights, n, out, out_bf16, timeout_ns); break;
   }
+  TXB_CUDA(cudaGetLastError());
+  return TXB_OK;
+}
+
+int txb_moe_barrier(const txb_moe_shape* s, void* const* peers, void* region, uint64_t timeout_ns, void* stream) {
+  if (int rc = check_shape(s)) return rc;
+  TXB_CUDA(cudaSetDevice(s->device));
+  k_barrier<<<1, 128, 0, (cudaStream_t)stream>>>(*s, peers, region, timeout_ns);
   TXB_CUDA(cudaGetLastError());
   return TXB_OK;
 }

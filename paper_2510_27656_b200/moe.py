@@ -522,7 +522,7 @@ class MoeRank:
 
     # ------------------------------------------------------------ dispatch
 
-    def dispatch_send(self, payload, routes, *, sync: bool = True) -> None:
+    def dispatch_send(self, payload, routes, *, sync: bool = True, _mid_event=None) -> None:
         """Count, exchange route rows and store every token copy at its final
         grouped row on the owning rank (moe.py:470-497, 538-643)."""
         spec = self.spec
@@ -574,6 +574,8 @@ class MoeRank:
         _lib.call("txb_moe_route", self._shape_p, _sp(r_dev), i32, n, self._peer_table_p,
                   C.c_void_p(self.region.ptr), _sp(self._rank_scratch), _sp(self._pos),
                   self._tmo(None), sid)
+        if _mid_event is not None:
+            _mid_event.record(_stream(self.device))
         if self.host_gated:
             step = st.step
             self._gate(lambda c: all(v >= step for v in c["route_tag"][step & 1])
@@ -663,13 +665,13 @@ class MoeRank:
         else:
             raise ProtocolError(f"output dtype {out.dtype} does not match combine element size {ce}")
         rows_needed = g.data.shape[0]
-        if out.ndim != 2 or out.shape[1] != width or out.stride(1) != 1:
+        if out.ndim != 2 or out.shape[1] != width or (out.numel() and out.stride(1) != 1):
             raise ProtocolError(f"output shape {tuple(out.shape)} != ({rows_needed}, {width})")
         if g.padded_total is None and out.shape[0] != rows_needed:
             raise ProtocolError(f"output shape {tuple(out.shape)} != ({rows_needed}, {width})")
         if out.shape[0] < rows_needed and g.padded_total is not None:
             raise ProtocolError(f"output rows {out.shape[0]} below the receive capacity {rows_needed}")
-        ld = out.stride(0) * out.element_size()
+        ld = (out.stride(0) if out.numel() else width) * out.element_size()
         st.keep.append(out)
         _lib.call("txb_moe_combine_send", self._shape_p, _sp(out), ld, self._peer_table_p,
                   C.c_void_p(self.region.ptr), _sp(self._sources), _sp(self._ret), _sp(self._info),
@@ -725,6 +727,14 @@ class MoeRank:
         if st.host:
             return out.float().cpu().numpy() if out_dtype == torch.float32 else out.cpu()
         return out
+
+    def barrier(self, timeout: float | None = None) -> None:
+        """Device-side barrier across the mesh on the current stream
+        (launch only; a later stream operation observes completion)."""
+        if self.host_gated:
+            raise ProtocolError("device barrier needs one device per rank")
+        _lib.call("txb_moe_barrier", self._shape_p, self._peer_table_p, C.c_void_p(self.region.ptr),
+                  self._tmo(timeout), self._sid())
 
     @property
     def pos(self) -> torch.Tensor:
