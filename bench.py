@@ -171,7 +171,8 @@ def run_b200(a) -> None:
     G = int(rk._shape.grouped_rows)
     y = torch.randn(G, H, device=dev).to(torch.bfloat16)     # synthetic expert outputs
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
-    stream = torch.cuda.current_stream(dev)
+    stream = torch.cuda.Stream(dev)          # graphs capture on a non-default stream
+    torch.cuda.set_stream(stream)
 
     def step():
         rk.dispatch_send(xd, rd, sync=False)
@@ -185,10 +186,41 @@ def run_b200(a) -> None:
     err, _ = rk.status()
     assert err == 0, f"device error word {err:#x} during warm-up"
 
+    # The step is launch-only and keeps all per-step state on the device
+    # (step counter, counter targets), so it is captured once into a CUDA
+    # graph and replayed: the timed span is device work, not Python.
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        step()
+    # one graph per kernel (route | dispatch | recv | comb_send | comb_recv)
+    # for the per-kernel event timing pass
+    pool = torch.cuda.graph_pool_handle()
+    gk = [torch.cuda.CUDAGraph() for _ in range(5)]
+    torch.cuda.synchronize()
+
+    def _switch():
+        gk[0].capture_end()
+        gk[1].capture_begin(pool=pool)
+    gk[0].capture_begin(pool=pool)
+    rk.dispatch_send(xd, rd, sync=False, _between=_switch)
+    gk[1].capture_end()
+    gk[2].capture_begin(pool=pool)
+    rk.dispatch_recv(sync=False)
+    gk[2].capture_end()
+    gk[3].capture_begin(pool=pool)
+    rk.combine_send(y)
+    gk[3].capture_end()
+    gk[4].capture_begin(pool=pool)
+    rk.combine_recv(wd, out_dtype=torch.bfloat16, sync=False)
+    gk[4].capture_end()
+    for _ in range(max(3, a.warmup)):
+        graph.replay()
+    torch.cuda.synchronize()
+
     # -------- timed: per step events, L2 flush + barrier outside the span
     K = a.steps
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
-           torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(K)]
     clocks = Clocks(local)
     if world > 1:
         import torch.distributed as dist
@@ -199,27 +231,40 @@ def run_b200(a) -> None:
         if world > 1:
             rk.barrier()
         ev[k][0].record(stream)
-        rk.dispatch_send(xd, rd, sync=False)
-        rk.dispatch_recv(sync=False)
+        graph.replay()
         ev[k][1].record(stream)
-        rk.combine_send(y)
-        rk.combine_recv(wd, out_dtype=torch.bfloat16, sync=False)
-        ev[k][2].record(stream)
     torch.cuda.synchronize()
     clk = clocks.stop()
     err, _ = rk.status()
     assert err == 0, f"device error word {err:#x}"
-    tot = np.array([e0.elapsed_time(e2) * 1e3 for e0, e1, e2 in ev])
-    dsp = np.array([e0.elapsed_time(e1) * 1e3 for e0, e1, e2 in ev])
-    cmb = np.array([e1.elapsed_time(e2) * 1e3 for e0, e1, e2 in ev])
+    tot = np.array([e0.elapsed_time(e1) * 1e3 for e0, e1 in ev])
+
+    # -------- per-kernel durations: events between the kernels of the graph
+    names = ["route", "dispatch", "recv", "comb_send", "comb_recv"]
+    acc = {k: [] for k in names}
+    for _ in range(max(20, K // 2)):
+        flush.fill_(3)
+        if world > 1:
+            rk.barrier()
+        kev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+        kev[0].record(stream)
+        for i in range(5):
+            gk[i].replay()
+            kev[i + 1].record(stream)
+        torch.cuda.synchronize()
+        for i, k in enumerate(names):
+            acc[k].append(kev[i].elapsed_time(kev[i + 1]) * 1e3)
+    kt = {k: float(np.median(v)) for k, v in acc.items()}
+    dsp = np.array(acc["route"]) + np.array(acc["dispatch"]) + np.array(acc["recv"])
+    cmb = np.array(acc["comb_send"]) + np.array(acc["comb_recv"])
     if world > 1:
         import torch.distributed as dist
-        t = torch.tensor(np.stack([tot, dsp, cmb]), device=dev)
+        t = torch.tensor(tot, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        tot, dsp, cmb = (t.cpu().numpy()[i] for i in range(3))
-
-    # -------- per-kernel durations (separate pass, events between launches)
-    kt = kernel_times(rk, xd, rd, wd, y, flush, stream, reps=max(20, K // 4))
+        tot = t.cpu().numpy()
+        kk = torch.tensor([kt[k] for k in names], device=dev)
+        dist.all_reduce(kk, op=dist.ReduceOp.MAX)
+        kt = dict(zip(names, kk.cpu().numpy().tolist()))
 
     # -------- e2e through the public API with pinned host buffers
     e2e = e2e_times(rk, x, routes, w, stream, flush, dev, K, world)
@@ -298,34 +343,6 @@ def expected_rows(rank: int, n: int, tokens: int) -> dict:
     pad = int(((-counts) % 8).sum())
     return {"out_rows": out_rows, "in_rows": in_rows, "self_rows": self_rows,
             "valid_rows": int(counts.sum()), "pad_rows": pad}
-
-
-def kernel_times(rk, xd, rd, wd, y, flush, stream, reps: int) -> dict:
-    """Average device time of each of the five kernels (events between
-    launches on the rank's stream, L2 flushed before each step)."""
-    import torch
-    names = ["route", "dispatch", "recv", "comb_send", "comb_recv"]
-    acc = {k: [] for k in names}
-    for _ in range(reps):
-        flush.fill_(1)
-        if rk.spec.ranks > 1:
-            rk.barrier()
-        evs = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
-        evs[0].record(stream)
-        # route + dispatch are launched by dispatch_send; split them with a
-        # mid event by calling the two C entry points through the API pieces
-        rk.dispatch_send(xd, rd, sync=False, _mid_event=evs[1])
-        evs[2].record(stream)
-        rk.dispatch_recv(sync=False)
-        evs[3].record(stream)
-        rk.combine_send(y)
-        evs[4].record(stream)
-        rk.combine_recv(wd, out_dtype=torch.bfloat16, sync=False)
-        evs[5].record(stream)
-        torch.cuda.synchronize()
-        for i, k in enumerate(names):
-            acc[k].append(evs[i].elapsed_time(evs[i + 1]) * 1e3)
-    return {k: float(np.median(v)) for k, v in acc.items()}
 
 
 def e2e_times(rk, x, routes, w, stream, flush, dev, K: int, world: int) -> dict:

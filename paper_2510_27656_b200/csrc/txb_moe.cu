@@ -126,7 +126,7 @@ k_route(txb_moe_shape s, const void* __restrict__ routes, int i32, int64_t n,
 
 // ------------------------------------------------------------- k_dispatch
 
-constexpr int kDispThreads = 256;
+constexpr int kDispThreads = 512;
 
 template <int SRC, int ELEM>
 __global__ void __launch_bounds__(kDispThreads)
@@ -233,19 +233,22 @@ k_dispatch(txb_moe_shape s, const void* __restrict__ x, int64_t n, const void* _
 
 constexpr int kRecvThreads = 256;
 
+// Receive side: every CTA derives the (small) per-(source, local expert)
+// tables from the route matrix, then the grid walks the grouped rows with
+// one warp per row: metadata by lane 0, zero fill of padding rows by the
+// whole warp.  CTA 0 finally acquire-waits for the token receipts.
 __global__ void __launch_bounds__(kRecvThreads)
 k_recv(txb_moe_shape s, void* region, int64_t* __restrict__ rows, int64_t* __restrict__ sources,
        int32_t* __restrict__ ret, int64_t* __restrict__ info, uint64_t timeout_ns) {
   extern __shared__ int64_t rsm[];
   const int N = s.ranks, E = s.experts, L = s.local_experts, me = s.me;
-  int64_t* a = rsm;                 // [N][L] counts into my experts
-  int64_t* rowbase = a + N * L;     // [N][L] recv slot base (moe.py:178-184)
-  int64_t* retbase = rowbase + N * L;  // [N][L] send slot base on the source
+  int64_t* a = rsm;                    // [N][L] counts into my experts
+  int64_t* rowbase = a + N * L;        // [N*L+1] flattened exclusive prefix = recv slot base
+  int64_t* retbase = rowbase + N * L + 1;  // [N][L] send slot base on the source
   int64_t* gstart = retbase + N * L;   // [L+1] group starts (padded)
   int64_t* gsize = gstart + L + 1;     // [L]
   int64_t* srcpre = gsize + L;         // [L][N+1] prefix over sources within a group
-  int64_t* rstart = srcpre + L * (N + 1);  // [N+1] recv_start[me][q]
-  int64_t* pre_all = rstart + N + 1;       // [N] sum_{e' < me*L} C[q][e']
+  int64_t* pre_all = srcpre + L * (N + 1);  // [N] sum_{e' < me*L} C[q][e']
   __shared__ int64_t tmp[33];
   const int tid = threadIdx.x, nt = blockDim.x;
   Flags* f = flags_of(region, s);
@@ -259,11 +262,12 @@ k_recv(txb_moe_shape s, void* region, int64_t* __restrict__ rows, int64_t* __res
   }
   for (int q = tid; q < N; q += nt) pre_all[q] = 0;
   __syncthreads();
-  for (int i = tid; i < N * me * L; i += nt) {
-    const int q = i / (me * L), e = i - q * (me * L);
-    atomicAdd((unsigned long long*)&pre_all[q], (unsigned long long)C[(size_t)q * E + e]);
+  if (me > 0) {
+    for (int i = tid; i < N * me * L; i += nt) {
+      const int q = i / (me * L), e = i - q * (me * L);
+      atomicAdd((unsigned long long*)&pre_all[q], (unsigned long long)C[(size_t)q * E + e]);
+    }
   }
-  // per-group sizes and per-source prefixes (L x N, thread per group)
   for (int le = tid; le < L; le += nt) {
     int64_t run = 0;
     for (int q = 0; q < N; ++q) {
@@ -274,30 +278,19 @@ k_recv(txb_moe_shape s, void* region, int64_t* __restrict__ rows, int64_t* __res
     gsize[le] = run;
     gstart[le] = pad_up(run);
   }
-  if (tid == 0) {
-    int64_t run = 0;
-    for (int q = 0; q < N; ++q) {
-      rstart[q] = run;
-      int64_t asg = 0;
-      for (int le = 0; le < L; ++le) asg += a[q * L + le];
-      run += asg;
-    }
-    rstart[N] = run;
-  }
   __syncthreads();
   const int64_t padded_total = block_excl_scan<int64_t>(gstart, L, tmp);
-  if (tid == 0) gstart[L] = padded_total;
-  block_excl_scan<int64_t>(rowbase, N * L, tmp);  // flattened [q][le] prefix
-  __syncthreads();
-  for (int i = tid; i < N * L; i += nt) {
-    const int q = i / L;
-    retbase[i] = rowbase[i] - rowbase[q * L];  // sum_{le'<le} a[q][le']
+  // recv slot base: recv_start[me][q] + sum_{le'<le} a[q][le'] is exactly the
+  // exclusive prefix of a[] flattened source-major (moe.py:178-184, 204-213)
+  const int64_t recv_total = block_excl_scan<int64_t>(rowbase, N * L, tmp);
+  if (tid == 0) {
+    gstart[L] = padded_total;
+    rowbase[N * L] = recv_total;
   }
   __syncthreads();
   for (int i = tid; i < N * L; i += nt) {
     const int q = i / L;
-    rowbase[i] = rstart[q] + retbase[i];
-    retbase[i] += pre_all[q];
+    retbase[i] = pre_all[q] + (rowbase[i] - rowbase[q * L]);
   }
   __syncthreads();
   if (blockIdx.x == 0) {
@@ -307,11 +300,13 @@ k_recv(txb_moe_shape s, void* region, int64_t* __restrict__ rows, int64_t* __res
     }
     if (tid == 0) {
       info[2 * L] = padded_total;
-      info[2 * L + 1] = rstart[N];
+      info[2 * L + 1] = recv_total;
     }
   }
-  // metadata per grouped row
-  for (int64_t g = (int64_t)blockIdx.x * nt + tid; g < padded_total; g += (int64_t)gridDim.x * nt) {
+  const int64_t P = s.payload_bytes;
+  uint8_t* G = grouped_of(region, s);
+  const int warp = tid >> 5, lane = tid & 31, nwarp = nt >> 5;
+  for (int64_t g = (int64_t)blockIdx.x * nwarp + warp; g < padded_total; g += (int64_t)gridDim.x * nwarp) {
     int lo = 0, hi = L - 1;  // last le with gstart[le] <= g
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
@@ -320,10 +315,13 @@ k_recv(txb_moe_shape s, void* region, int64_t* __restrict__ rows, int64_t* __res
     const int le = lo;
     const int64_t k = g - gstart[le];
     if (k >= gsize[le]) {
-      rows[g] = -1;
-      sources[g] = -1;
-      ret[g] = -1;
-    } else {
+      if (lane == 0) {
+        rows[g] = -1;
+        sources[g] = -1;
+        ret[g] = -1;
+      }
+      zero_row(G + g * P, P, lane, 32);  // padding rows are zero (moe.py:719)
+    } else if (lane == 0) {
       const int64_t* sp = srcpre + le * (N + 1);
       int q = 0;
       while (sp[q + 1] <= k) ++q;
@@ -332,15 +330,6 @@ k_recv(txb_moe_shape s, void* region, int64_t* __restrict__ rows, int64_t* __res
       sources[g] = q;
       ret[g] = (int32_t)(retbase[q * L + le] + kk);
     }
-  }
-  // zero padding rows (moe.py:719: data starts zeroed)
-  const int64_t P = s.payload_bytes;
-  uint8_t* G = grouped_of(region, s);
-  const int warp = tid >> 5, lane = tid & 31, nwarp = nt >> 5;
-  for (int le = 0; le < L; ++le) {
-    const int64_t p0 = gstart[le] + gsize[le], p1 = gstart[le + 1];
-    for (int64_t g = p0 + (int64_t)blockIdx.x * nwarp + warp; g < p1; g += (int64_t)gridDim.x * nwarp)
-      zero_row(G + g * P, P, lane, 32);
   }
   // acquire-wait for every expected row (token immediate count)
   if (blockIdx.x == 0 && tid == 0) {
@@ -390,7 +379,7 @@ k_comb_send(txb_moe_shape s, const uint8_t* __restrict__ out, int64_t ld, void* 
 
 // ------------------------------------------------------------ k_comb_recv
 
-constexpr int kCombRecvThreads = 256;
+constexpr int kCombRecvThreads = 512;
 
 template <int ELEM>
 __global__ void __launch_bounds__(kCombRecvThreads)
@@ -577,10 +566,11 @@ int txb_moe_dispatch_recv(const txb_moe_shape* s, void* region, int64_t* rows, i
   if (int rc = check_shape(s)) return rc;
   TXB_CUDA(cudaSetDevice(s->device));
   const int N = s->ranks, L = s->local_experts;
-  const size_t smem = (size_t)(3 * N * L + 2 * L + 1 + L * (N + 1) + N + 1 + N) * sizeof(int64_t);
+  const size_t smem = (size_t)(3 * N * L + 1 + 2 * L + 1 + L * (N + 1) + N) * sizeof(int64_t);
   if (smem > 48 * 1024) TXB_CUDA(cudaFuncSetAttribute(k_recv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t maxrows = s->grouped_rows;
-  int grid = (int)((maxrows + kRecvThreads - 1) / kRecvThreads);
+  const int64_t wpb = kRecvThreads / 32;
+  int grid = (int)((maxrows + wpb - 1) / wpb);
   if (grid > 2 * sm_count(s->device)) grid = 2 * sm_count(s->device);
   if (grid < 1) grid = 1;
   k_recv<<<grid, kRecvThreads, smem, (cudaStream_t)stream>>>(*s, region, rows, sources, ret_slot, info, timeout_ns);

@@ -9,6 +9,7 @@ namespace txb {
 
 constexpr int kMaxTopk = 64;
 
+// Load `cnt` (multiple of 4) consecutive source values as f32.
 template <int SRC>
 __device__ __forceinline__ void load_vals(const void* x, int64_t off, float* v, int cnt) {
   if constexpr (SRC == TXB_SRC_F32) {
@@ -18,8 +19,20 @@ __device__ __forceinline__ void load_vals(const void* x, int64_t off, float* v, 
       const float4 a = p[k];
       v[4 * k] = a.x; v[4 * k + 1] = a.y; v[4 * k + 2] = a.z; v[4 * k + 3] = a.w;
     }
-  } else {
+  } else if (cnt % 8 == 0) {
     // bf16 -> f32 is exact (kernels.bf16_decode, kernels.py:153-154)
+    const uint4* p = reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(x) + off);
+#pragma unroll
+    for (int k = 0; k < cnt / 8; ++k) {
+      const uint4 a = p[k];
+      const uint32_t w[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        v[8 * k + 2 * q] = __uint_as_float(w[q] << 16);
+        v[8 * k + 2 * q + 1] = __uint_as_float(w[q] & 0xFFFF0000u);
+      }
+    }
+  } else {
     const uint2* p = reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(x) + off);
 #pragma unroll
     for (int k = 0; k < cnt / 4; ++k) {
@@ -37,73 +50,110 @@ __device__ __forceinline__ float load_val(const void* x, int src, int64_t off) {
                             : bf16_to_f(reinterpret_cast<const uint16_t*>(x)[off]);
 }
 
+// Block-wide max of non-negative floats; every thread gets the result.
+__device__ __forceinline__ float block_max(float v, float* red) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((tid & 31) == 0) red[tid >> 5] = v;
+  __syncthreads();
+  if (tid < 32) {
+    float a = tid < ((nt + 31) >> 5) ? red[tid] : 0.f;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, o));
+    if (tid == 0) red[32] = a;
+  }
+  __syncthreads();
+  const float r = red[32];
+  __syncthreads();
+  return r;
+}
+
+// One 16-byte output chunk from EPC = 16/ELEM values.
+template <int ELEM>
+__device__ __forceinline__ uint4 encode_chunk(const float* v, float scale) {
+  uint4 o;
+  uint32_t* ow = reinterpret_cast<uint32_t*>(&o);
+  if constexpr (ELEM == 1) {
+    // x / f32(scale) with an IEEE division, then e4m3 RNE satfinite
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t lo = fp8x2(__fdiv_rn(v[4 * q], scale), __fdiv_rn(v[4 * q + 1], scale));
+      const uint32_t hi = fp8x2(__fdiv_rn(v[4 * q + 2], scale), __fdiv_rn(v[4 * q + 3], scale));
+      ow[q] = lo | (hi << 16);
+    }
+  } else if constexpr (ELEM == 2) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) ow[q] = (uint32_t)bf16_rne(v[2 * q]) | ((uint32_t)bf16_rne(v[2 * q + 1]) << 16);
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) ow[q] = __float_as_uint(v[q]);
+  }
+  return o;
+}
+
 // Encode one token row (values -> wire row) and store it to `nd` destination
-// rows.  ELEM: 1 fp8 (per-row scale), 2 bf16, 4 f32.  The data part is
-// produced in 16-byte chunks when hidden*ELEM is a multiple of 16 and the
-// source is 16-byte aligned; otherwise element by element.
+// rows.  ELEM: 1 fp8 (per-row scale), 2 bf16, 4 f32.
+//   fast path (hidden*ELEM % 16 == 0, 16-byte aligned rows, <= 2 chunks per
+//   thread): the row is read from HBM once into registers, the per-row amax
+//   is reduced across the block, and each 16-byte chunk is stored to all
+//   destinations;
+//   general path: element by element (arbitrary hidden / payload sizes).
 template <int SRC, int ELEM>
 __device__ void encode_store_row(const void* x, int64_t t, int H, int scales, int64_t P,
                                  uint8_t* const* dst, int nd, float* red) {
   const int tid = threadIdx.x, nt = blockDim.x;
   const int64_t rowoff = t * (int64_t)H;
-  float scale = 1.0f;
-  if (ELEM == 1) {
-    float amax = 0.f;
-    for (int h = tid; h < H; h += nt) {
-      const float v = load_val(x, SRC, rowoff + h);
-      if (isfinite(v)) amax = fmaxf(amax, fabsf(v));
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-    if ((tid & 31) == 0) red[tid >> 5] = amax;
-    __syncthreads();
-    if (tid < 32) {
-      float a = tid < (nt >> 5) ? red[tid] : 0.f;
-#pragma unroll
-      for (int o = 16; o; o >>= 1) a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, o));
-      if (tid == 0) red[32] = a;
-    }
-    __syncthreads();
-    amax = red[32];
-    scale = amax > 0.f ? __fdiv_rn(amax, 448.0f) : 1.0f;  // kernels.py:133-134
-  }
   constexpr int EPC = 16 / ELEM;  // elements per 16-byte output chunk
   const int64_t srcbytes = (SRC == TXB_SRC_F32 ? 4 : 2);
-  // 16-byte output chunks need 16-byte aligned destination rows (P % 16) and
-  // an aligned source chunk (4 or more source elements per load)
   const int64_t salign = (EPC * srcbytes) >= 16 ? 16 : EPC * srcbytes;
-  const bool vec = ((H * ELEM) % 16 == 0) && (P % 16 == 0) &&
+  const int nchunk = H / EPC;
+  const bool vec = ((H * ELEM) % 16 == 0) && (P % 16 == 0) && nchunk <= 2 * nt &&
                    (((reinterpret_cast<uintptr_t>(x) + rowoff * srcbytes) % salign) == 0);
+  float scale = 1.0f;
   if (vec) {
-    const int nchunk = H / EPC;
-    for (int c = tid; c < nchunk; c += nt) {
-      float v[EPC];
-      load_vals<SRC>(x, rowoff + (int64_t)c * EPC, v, EPC);
-      uint4 o;
-      uint32_t* ow = reinterpret_cast<uint32_t*>(&o);
-      if (ELEM == 1) {
+    float v[2][EPC];
+    float amax = 0.f;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const uint32_t lo = fp8x2(__fdiv_rn(v[4 * q], scale), __fdiv_rn(v[4 * q + 1], scale));
-          const uint32_t hi = fp8x2(__fdiv_rn(v[4 * q + 2], scale), __fdiv_rn(v[4 * q + 3], scale));
-          ow[q] = lo | (hi << 16);
+    for (int u = 0; u < 2; ++u) {
+      const int c = tid + u * nt;
+      if (c < nchunk) {
+        load_vals<SRC>(x, rowoff + (int64_t)c * EPC, v[u], EPC);
+        if constexpr (ELEM == 1) {
+#pragma unroll
+          for (int k = 0; k < EPC; ++k)
+            if (isfinite(v[u][k])) amax = fmaxf(amax, fabsf(v[u][k]));
         }
-      } else if (ELEM == 2) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) ow[q] = (uint32_t)bf16_rne(v[2 * q]) | ((uint32_t)bf16_rne(v[2 * q + 1]) << 16);
-      } else {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) ow[q] = __float_as_uint(v[q]);
       }
-      for (int j = 0; j < nd; ++j) reinterpret_cast<uint4*>(dst[j])[c] = o;
+    }
+    if constexpr (ELEM == 1) {
+      amax = block_max(amax, red);
+      scale = amax > 0.f ? __fdiv_rn(amax, 448.0f) : 1.0f;  // kernels.py:133-134
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int c = tid + u * nt;
+      if (c < nchunk) {
+        const uint4 o = encode_chunk<ELEM>(v[u], scale);
+        for (int j = 0; j < nd; ++j) reinterpret_cast<uint4*>(dst[j])[c] = o;
+      }
     }
   } else {
+    if constexpr (ELEM == 1) {
+      float amax = 0.f;
+      for (int h = tid; h < H; h += nt) {
+        const float v = load_val(x, SRC, rowoff + h);
+        if (isfinite(v)) amax = fmaxf(amax, fabsf(v));
+      }
+      amax = block_max(amax, red);
+      scale = amax > 0.f ? __fdiv_rn(amax, 448.0f) : 1.0f;
+    }
     for (int h = tid; h < H; h += nt) {
       const float v = load_val(x, SRC, rowoff + h);
       for (int j = 0; j < nd; ++j) {
-        if (ELEM == 1) {
+        if constexpr (ELEM == 1) {
           dst[j][h] = (uint8_t)(fp8x2(__fdiv_rn(v, scale), 0.f) & 0xFF);
-        } else if (ELEM == 2) {
+        } else if constexpr (ELEM == 2) {
           const uint16_t b = bf16_rne(v);
           dst[j][2 * h] = (uint8_t)(b & 0xFF);
           dst[j][2 * h + 1] = (uint8_t)(b >> 8);
@@ -119,45 +169,74 @@ __device__ void encode_store_row(const void* x, int64_t t, int H, int scales, in
   if (tailb) {
     const int64_t d0 = (int64_t)H * ELEM;
     const uint32_t sbits = ELEM == 1 ? __float_as_uint(scale) : 0u;
-    for (int b = tid; b < tailb; b += nt) {
-      const uint8_t val = b < 4 ? (uint8_t)(sbits >> (8 * b)) : (uint8_t)0;
-      for (int j = 0; j < nd; ++j) dst[j][d0 + b] = val;
+    if ((d0 & 3) == 0) {
+      for (int b = tid; b < scales; b += nt) {
+        const uint32_t val = b == 0 ? sbits : 0u;
+        for (int j = 0; j < nd; ++j) reinterpret_cast<uint32_t*>(dst[j] + d0)[b] = val;
+      }
+    } else {
+      for (int b = tid; b < tailb; b += nt) {
+        const uint8_t val = b < 4 ? (uint8_t)(sbits >> (8 * b)) : (uint8_t)0;
+        for (int j = 0; j < nd; ++j) dst[j][d0 + b] = val;
+      }
     }
   }
 }
 
+// ----------------------------------------------------------------- combine
+
+// Raw 8-element chunk of one wire row, loaded before any arithmetic so the
+// R loads of a chunk are in flight together.
 template <int ELEM>
-__device__ __forceinline__ void load8(const uint8_t* row, int64_t h0, float* v) {
-  if (ELEM == 1) {
-    const uint2 b = *reinterpret_cast<const uint2*>(row + h0);
-    const uint32_t w[2] = {b.x, b.y};
+struct Chunk8 {
+  uint4 a, b;  // ELEM 1: a.x,a.y; ELEM 2: a; ELEM 4: a,b
+};
+
+template <int ELEM>
+__device__ __forceinline__ Chunk8<ELEM> load_chunk8(const uint8_t* row, int64_t h0) {
+  Chunk8<ELEM> c;
+  if constexpr (ELEM == 1) {
+    const uint2 v = *reinterpret_cast<const uint2*>(row + h0);
+    c.a = make_uint4(v.x, v.y, 0, 0);
+  } else if constexpr (ELEM == 2) {
+    c.a = *reinterpret_cast<const uint4*>(row + 2 * h0);
+  } else {
+    c.a = *reinterpret_cast<const uint4*>(row + 4 * h0);
+    c.b = *reinterpret_cast<const uint4*>(row + 4 * h0 + 16);
+  }
+  return c;
+}
+
+template <int ELEM>
+__device__ __forceinline__ void unpack_chunk8(const Chunk8<ELEM>& c, float* v) {
+  if constexpr (ELEM == 1) {
+    const uint32_t w[2] = {c.a.x, c.a.y};
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
       const float2 lo = fp8x2_to_f2((uint16_t)(w[q] & 0xFFFF));
       const float2 hi = fp8x2_to_f2((uint16_t)(w[q] >> 16));
       v[4 * q] = lo.x; v[4 * q + 1] = lo.y; v[4 * q + 2] = hi.x; v[4 * q + 3] = hi.y;
     }
-  } else if (ELEM == 2) {
-    const uint4 b = *reinterpret_cast<const uint4*>(row + 2 * h0);
-    const uint32_t w[4] = {b.x, b.y, b.z, b.w};
+  } else if constexpr (ELEM == 2) {
+    const uint32_t w[4] = {c.a.x, c.a.y, c.a.z, c.a.w};
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       v[2 * q] = __uint_as_float(w[q] << 16);
       v[2 * q + 1] = __uint_as_float(w[q] & 0xFFFF0000u);
     }
   } else {
-    const float4 a = *reinterpret_cast<const float4*>(row + 4 * h0);
-    const float4 b = *reinterpret_cast<const float4*>(row + 4 * h0 + 16);
-    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    v[0] = __uint_as_float(c.a.x); v[1] = __uint_as_float(c.a.y);
+    v[2] = __uint_as_float(c.a.z); v[3] = __uint_as_float(c.a.w);
+    v[4] = __uint_as_float(c.b.x); v[5] = __uint_as_float(c.b.y);
+    v[6] = __uint_as_float(c.b.z); v[7] = __uint_as_float(c.b.w);
   }
 }
 
 template <int ELEM>
 __device__ __forceinline__ float load1(const uint8_t* row, int64_t h) {
-  if (ELEM == 1) {
-    const uint8_t b = row[h];
-    return fp8x2_to_f2((uint16_t)b).x;
-  } else if (ELEM == 2) {
+  if constexpr (ELEM == 1) {
+    return fp8x2_to_f2((uint16_t)row[h]).x;
+  } else if constexpr (ELEM == 2) {
     return bf16_to_f((uint16_t)(row[2 * h] | (row[2 * h + 1] << 8)));
   } else {
     uint32_t u = 0;
@@ -166,9 +245,13 @@ __device__ __forceinline__ float load1(const uint8_t* row, int64_t h) {
   }
 }
 
+constexpr int kCombBatch = 8;  // rows of one chunk loaded together
+
 // out[t] = sum_j w[t,j] * y[pos[t,j]], j ascending from 0.0, separately rounded
 // multiply and add (kernels.py:214-226); fp8 rows are dequantised first as
-// e4m3 * f32 scale (kernels.py:139-141).
+// e4m3 * f32 scale (kernels.py:139-141).  Each thread owns 8-element chunks;
+// the rows of a chunk are fetched in batches of kCombBatch before the
+// accumulation so their memory latencies overlap.
 template <int ELEM>
 __device__ void combine_rows(const uint8_t* base, int64_t Pc, int H, const int64_t* pos, const float* w,
                              int64_t n, int R, void* out, int out_bf16) {
@@ -176,6 +259,7 @@ __device__ void combine_rows(const uint8_t* base, int64_t Pc, int H, const int64
   __shared__ float ws[kMaxTopk];
   __shared__ float sc[kMaxTopk];
   const int tid = threadIdx.x, nt = blockDim.x;
+  const bool vec = (H % 8 == 0) && ((Pc & 15) == 0) && ((reinterpret_cast<uintptr_t>(base) & 15) == 0);
   for (int64_t t = blockIdx.x; t < n; t += gridDim.x) {
     if (tid < R) {
       const int64_t p = pos[t * R + tid];
@@ -190,20 +274,28 @@ __device__ void combine_rows(const uint8_t* base, int64_t Pc, int H, const int64
       sc[tid] = scale;
     }
     __syncthreads();
-    const bool vec = (H % 8 == 0) && ((Pc & 15) == 0) && ((reinterpret_cast<uintptr_t>(base) & 15) == 0);
     if (vec) {
       for (int c = tid; c < H / 8; c += nt) {
         float acc[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) acc[k] = 0.f;
-        for (int j = 0; j < R; ++j) {
-          float v[8];
-          load8<ELEM>(rowp[j], (int64_t)c * 8, v);
-          const float wj = ws[j], sj = sc[j];
+        for (int j0 = 0; j0 < R; j0 += kCombBatch) {
+          Chunk8<ELEM> raw[kCombBatch];
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const float y = ELEM == 1 ? __fmul_rn(v[k], sj) : v[k];
-            acc[k] = __fadd_rn(acc[k], __fmul_rn(wj, y));
+          for (int u = 0; u < kCombBatch; ++u)
+            if (j0 + u < R) raw[u] = load_chunk8<ELEM>(rowp[j0 + u], (int64_t)c * 8);
+#pragma unroll
+          for (int u = 0; u < kCombBatch; ++u) {
+            if (j0 + u < R) {
+              float v[8];
+              unpack_chunk8<ELEM>(raw[u], v);
+              const float wj = ws[j0 + u], sj = sc[j0 + u];
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                const float y = ELEM == 1 ? __fmul_rn(v[k], sj) : v[k];
+                acc[k] = __fadd_rn(acc[k], __fmul_rn(wj, y));
+              }
+            }
           }
         }
         if (out_bf16) {

@@ -522,7 +522,7 @@ class MoeRank:
 
     # ------------------------------------------------------------ dispatch
 
-    def dispatch_send(self, payload, routes, *, sync: bool = True, _mid_event=None) -> None:
+    def dispatch_send(self, payload, routes, *, sync: bool = True, _between=None) -> None:
         """Count, exchange route rows and store every token copy at its final
         grouped row on the owning rank (moe.py:470-497, 538-643)."""
         spec = self.spec
@@ -574,8 +574,8 @@ class MoeRank:
         _lib.call("txb_moe_route", self._shape_p, _sp(r_dev), i32, n, self._peer_table_p,
                   C.c_void_p(self.region.ptr), _sp(self._rank_scratch), _sp(self._pos),
                   self._tmo(None), sid)
-        if _mid_event is not None:
-            _mid_event.record(_stream(self.device))
+        if _between is not None:      # bench hook: split route / dispatch launches
+            _between()
         if self.host_gated:
             step = st.step
             self._gate(lambda c: all(v >= step for v in c["route_tag"][step & 1])

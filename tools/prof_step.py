@@ -1,0 +1,36 @@
+"""Eager DeepSeek-V3 decode steps at EP=1 for ncu captures (no graphs, no
+flush): python tools/prof_step.py [--steps N] [--tokens T]."""
+import argparse
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+import numpy as np
+import torch
+
+from paper_2510_27656_b200 import moe
+from paper_2510_27656_b200.engine import local_engines
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--steps", type=int, default=5)
+ap.add_argument("--tokens", type=int, default=128)
+ap.add_argument("--comb", type=int, default=2)
+a = ap.parse_args()
+T, H, E, R = a.tokens, 7168, 256, 8
+spec = moe.RoutingSpec(1, E, T, R, hidden=H, elem_size=1, scales=56, comb_elem_size=a.comb, comb_scales=0)
+rk = moe.build_mesh(local_engines([0]), spec)[0]
+rng = np.random.default_rng(0)
+x = torch.from_numpy(rng.standard_normal((T, H)).astype(np.float32)).cuda().to(torch.bfloat16)
+r = torch.from_numpy(np.argsort(rng.random((T, E)), axis=1)[:, :R].astype(np.int64)).cuda()
+w = torch.rand(T, R, device="cuda")
+y = torch.randn(int(rk._shape.grouped_rows), H, device="cuda").to(torch.bfloat16)
+for _ in range(a.steps):
+    rk.dispatch_send(x, r, sync=False)
+    rk.dispatch_recv(sync=False)
+    rk.combine_send(y)
+    rk.combine_recv(w, out_dtype=torch.bfloat16, sync=False)
+torch.cuda.synchronize()
+err, _ = rk.status()
+assert err == 0, hex(err)
+print("ok")
