@@ -192,27 +192,19 @@ def run_b200(a) -> None:
     graph = torch.cuda.CUDAGraph()
     with torch.cuda.graph(graph):
         step()
-    # one graph per kernel (route | dispatch | recv | comb_send | comb_recv)
-    # for the per-kernel event timing pass
+    # one graph per kernel: the fused dispatch (route + dispatch + receive
+    # metadata) and the fused combine (send + weighted reduce)
     pool = torch.cuda.graph_pool_handle()
-    gk = [torch.cuda.CUDAGraph() for _ in range(5)]
+    gk = [torch.cuda.CUDAGraph() for _ in range(2)]
     torch.cuda.synchronize()
-
-    def _switch():
-        gk[0].capture_end()
-        gk[1].capture_begin(pool=pool)
     gk[0].capture_begin(pool=pool)
-    rk.dispatch_send(xd, rd, sync=False, _between=_switch)
-    gk[1].capture_end()
-    gk[2].capture_begin(pool=pool)
+    rk.dispatch_send(xd, rd, sync=False)
     rk.dispatch_recv(sync=False)
-    gk[2].capture_end()
-    gk[3].capture_begin(pool=pool)
+    gk[0].capture_end()
+    gk[1].capture_begin(pool=pool)
     rk.combine_send(y)
-    gk[3].capture_end()
-    gk[4].capture_begin(pool=pool)
     rk.combine_recv(wd, out_dtype=torch.bfloat16, sync=False)
-    gk[4].capture_end()
+    gk[1].capture_end()
     for _ in range(max(3, a.warmup)):
         graph.replay()
     torch.cuda.synchronize()
@@ -240,23 +232,23 @@ def run_b200(a) -> None:
     tot = np.array([e0.elapsed_time(e1) * 1e3 for e0, e1 in ev])
 
     # -------- per-kernel durations: events between the kernels of the graph
-    names = ["route", "dispatch", "recv", "comb_send", "comb_recv"]
+    names = ["dispatch", "combine"]
     acc = {k: [] for k in names}
     for _ in range(max(20, K // 2)):
         flush.fill_(3)
         if world > 1:
             rk.barrier()
-        kev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+        kev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         kev[0].record(stream)
-        for i in range(5):
+        for i in range(2):
             gk[i].replay()
             kev[i + 1].record(stream)
         torch.cuda.synchronize()
         for i, k in enumerate(names):
             acc[k].append(kev[i].elapsed_time(kev[i + 1]) * 1e3)
     kt = {k: float(np.median(v)) for k, v in acc.items()}
-    dsp = np.array(acc["route"]) + np.array(acc["dispatch"]) + np.array(acc["recv"])
-    cmb = np.array(acc["comb_send"]) + np.array(acc["comb_recv"])
+    dsp = np.array(acc["dispatch"])
+    cmb = np.array(acc["combine"])
     if world > 1:
         import torch.distributed as dist
         t = torch.tensor(tot, device=dev)
@@ -275,21 +267,27 @@ def run_b200(a) -> None:
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     nvl_peak = 770.0
-    bytes_k = {
-        "dispatch": tokens * H * 2 + tokens * R * P if n_gpu == 1 else max(ex["out_rows"], ex["in_rows"]) * P,
-        "comb_send": 2 * ex["valid_rows"] * Pc if n_gpu == 1 else max(ex["valid_rows"] - ex["self_rows"], ex["out_rows"]) * Pc,
-        "comb_recv": tokens * R * Pc + tokens * H * 2,
-        "recv": ex["pad_rows"] * P,
-        "route": tokens * R * 8 * 2 + n_gpu * E * 4,
-    }
-    dom = max(("dispatch", "comb_send", "comb_recv"), key=lambda k: kt[k])
-    dom_local = dom == "comb_recv" or n_gpu == 1
-    peak = hbm_peak if dom_local else nvl_peak
+    # algorithmic bytes per launch: EP=1 moves
+    # everything through HBM; EP>1 is bounded by the NVLink egress/ingress
+    if n_gpu == 1:
+        bytes_k = {
+            "dispatch": tokens * H * 2 + tokens * R * P + ex["pad_rows"] * P,
+            "combine": tokens * R * Pc + tokens * H * 2,
+        }
+        bound = "hbm"
+    else:
+        bytes_k = {
+            "dispatch": max(ex["out_rows"], ex["in_rows"]) * P,
+            "combine": max(ex["valid_rows"] - ex["self_rows"], ex["out_rows"]) * Pc,
+        }
+        bound = "nvlink"
+    dom = max(names, key=lambda k: kt[k])
+    peak = hbm_peak if bound == "hbm" else nvl_peak
     achieved = bytes_k[dom] / (kt[dom] * 1e-6) / 1e9
-    roofline = {"bound": "hbm" if dom_local else "nvlink", "kernel": f"k_{dom}",
+    roofline = {"bound": bound, "kernel": f"k_{dom}_fused",
                 "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": None,
-                "peak_source": ("MEASURED_PEAKS.json hbm_gbs (burst copy)" if dom_local
+                "peak_source": ("MEASURED_PEAKS.json hbm_gbs (burst copy)" if bound == "hbm"
                                 else "B200_PROFILING.md measured peer copy 770 GB/s (fallback)"),
                 "algorithmic_bytes": int(bytes_k[dom]), "kernel_us": round(kt[dom], 2)}
     step_bytes = (tokens * R * P + tokens * R * Pc)
@@ -312,7 +310,7 @@ def run_b200(a) -> None:
         "kernel_us": {k: round(v, 2) for k, v in kt.items()},
         "roofline": roofline,
         "e2e": e2e,
-        "gpu_launches": 5 * K,
+        "gpu_launches": 2 * K,
         "clocks": clk,
     }
     if rank == 0 and n_gpu == 1 and not a.no_cpu_baseline:

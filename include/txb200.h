@@ -98,64 +98,71 @@ int txb_enable_peer(int device, int peer_device);
 
 /* ------------------------------------------------------- MoE hot path */
 
+/* Per-rank device buffers (all device pointers).  `region` is the rank's
+ * symmetric allocation (txb_moe_shape.region_bytes, laid out by
+ * txb_moe_plan); `peers` is a device array of `ranks` region base addresses
+ * as seen from this rank (own region at index `me`). */
+typedef struct txb_moe_bufs {
+  void* region;
+  void* const* peers;
+  int32_t* rank_scratch; /* [max_tokens*topk] stable rank of each copy in its expert */
+  int64_t* pos;          /* [max_tokens*topk] send slot of copy j of token t (moe.py:510-520) */
+  int32_t* gidx;         /* [max_tokens*topk] grouped row of copies served by this rank, else -1 */
+  int64_t* rows;         /* [grouped_rows] GroupedTokens.rows (moe.py:280) */
+  int64_t* sources;      /* [grouped_rows] GroupedTokens.sources (moe.py:281) */
+  int32_t* ret_slot;     /* [grouped_rows] combine return slot on the source */
+  int64_t* info;         /* [2L+3] group_sizes, group_starts, padded_total, recv_total, error word */
+} txb_moe_bufs;
+
 /* Validate a RoutingSpec (moe.py:52-70) and fill the derived fields. */
 int txb_moe_plan(txb_moe_shape* s);
 
-/* Route/count kernel: MoeRank._stage count row + _check_routes +
- * route-row scatter with the route immediate (moe.py:142-155, 499-523,
- * 538-553).  routes: i64 or i32 [n, R] device.  Writes pos[n, R] (i64,
- * moe.py:510-520) and the per-copy stable rank (i32 [n*R]) to scratch,
- * stores the own count row into every peer's route matrix and
- * release-publishes the step tag.  peers: device array of N region bases. */
-int txb_moe_route(const txb_moe_shape* s, const void* routes, int routes_i32, int64_t n,
-                  void* const* peers, void* region, int32_t* rank_scratch, int64_t* pos,
-                  uint64_t timeout_ns, void* stream);
+/* ---- fused path (one GPU per rank; cooperative launches) ---------------
+ * dispatch_fused = MoeRank.dispatch_send + dispatch_recv (moe.py:470-735):
+ * count the routes (_stage, moe.py:499-523; _check_routes 142-155), scatter
+ * the own count row to every peer with the route immediate (538-553), wait
+ * for all rows, derive the layout (compute_layout 200-225), store every
+ * token copy -- encoded on the fly for TXB_SRC_F32/BF16 (encode_tokens
+ * 231-246) -- straight into its final grouped row on the owner (the recv
+ * slab + pack_rows regroup of 556-722 in one peer store), release-add the
+ * row counts on the owners' token counters, build rows/sources/padding and
+ * wait for the expected token rows.  routes: i64 or i32 [n, R] device. */
+int txb_moe_dispatch_fused(const txb_moe_shape* s, const txb_moe_bufs* b, const void* x, int src_kind,
+                           int64_t n, const void* routes, int routes_i32, uint64_t timeout_ns,
+                           void* stream);
+/* combine_fused = combine_send + combine_recv (moe.py:739-833): every valid
+ * grouped row of `outputs` (row stride ld bytes, comb_bytes wide) returns to
+ * its source at the originating send slot, counts are release-added, then
+ * after the expected rows arrived out[t] = sum_j w[t,j] * row(t,j) in fp32,
+ * j ascending, no FMA (kernels.weighted_combine, kernels.py:206-242);
+ * out_bf16 selects bf16 RNE output (kernels.bf16_encode, kernels.py:144-150).
+ * The last CTA publishes the end-of-step barrier (moe.dbar) to every peer. */
+int txb_moe_combine_fused(const txb_moe_shape* s, const txb_moe_bufs* b, const void* outputs, int64_t ld,
+                          const float* weights, int64_t n, void* out, int out_bf16, uint64_t timeout_ns,
+                          void* stream);
 
-/* Dispatch kernel: waits for all route rows and for every peer's previous
- * step barrier, derives the layout (compute_layout, moe.py:200-225) and
- * writes each token copy straight to its final grouped row on the owning
- * peer (moe.py:556-643 + the pack_rows regroup at 699-722), encoding on
- * the fly for TXB_SRC_F32/BF16 (encode_tokens, moe.py:231-246).  Each CTA
- * release-adds the rows it wrote to every destination's token counter. */
-int txb_moe_dispatch(const txb_moe_shape* s, const void* x, int src_kind, int64_t n,
-                     const void* routes, int routes_i32, const int32_t* rank_scratch,
-                     void* const* peers, void* region, uint64_t timeout_ns, int grid,
-                     void* stream);
-
-/* Receive side (dispatch_recv, moe.py:665-735): fills rows/sources (i64
- * [grouped_rows]) and the combine return slot (i32), zeroes padding rows,
- * writes info = [group_sizes L][group_starts L][padded_total][recv_total]
- * [error word] (i64, 2L+3 entries) and acquire-waits until the token
- * counter reaches the expected receipts. */
-int txb_moe_dispatch_recv(const txb_moe_shape* s, void* region, int64_t* rows, int64_t* sources,
-                          int32_t* ret_slot, int64_t* info, uint64_t timeout_ns, void* stream);
-
-/* combine_send (moe.py:739-796): every valid grouped row g of `outputs`
- * (row stride ld bytes, comb_bytes wide) goes back to its source's combine
- * buffer at the originating copy's send slot; per-source release-add of
- * row counts, then the step barrier tag to every peer (moe.dbar). */
-int txb_moe_combine_send(const txb_moe_shape* s, const void* outputs, int64_t ld,
-                         void* const* peers, void* region, const int64_t* sources,
-                         const int32_t* ret_slot, const int64_t* info, int grid, void* stream);
-
-/* combine_recv (moe.py:802-833): acquire-wait for n*R returned rows, then
- * out[t] = sum_j w[t,j] * decode(row pos[t,j]) in fp32, j ascending, no FMA
- * (kernels.weighted_combine, kernels.py:206-242).  out_bf16: 0 -> f32 out,
- * 1 -> bf16 RNE out (kernels.bf16_encode, kernels.py:144-150). */
-int txb_moe_combine_recv(const txb_moe_shape* s, void* region, const int64_t* pos,
-                         const float* weights, int64_t n, void* out, int out_bf16,
-                         uint64_t timeout_ns, void* stream);
+/* ---- split path (same semantics, one phase per kernel; used when several
+ * ranks share one GPU and for batches above the fused limit) ------------- */
+int txb_moe_route(const txb_moe_shape* s, const txb_moe_bufs* b, const void* routes, int routes_i32,
+                  int64_t n, void* stream);
+int txb_moe_dispatch(const txb_moe_shape* s, const txb_moe_bufs* b, const void* x, int src_kind, int64_t n,
+                     const void* routes, int routes_i32, uint64_t timeout_ns, int grid, void* stream);
+int txb_moe_dispatch_recv(const txb_moe_shape* s, const txb_moe_bufs* b, uint64_t timeout_ns, void* stream);
+int txb_moe_combine_send(const txb_moe_shape* s, const txb_moe_bufs* b, const void* outputs, int64_t ld,
+                         int grid, void* stream);
+int txb_moe_combine_recv(const txb_moe_shape* s, const txb_moe_bufs* b, const void* outputs, int64_t ld,
+                         const float* weights, int64_t n, void* out, int out_bf16, uint64_t timeout_ns,
+                         void* stream);
 
 /* Device-side all-rank barrier over the mesh (engine submit_barrier,
  * engine.py:599-619): each rank release-stores its epoch into every peer,
  * then acquire-waits for every peer's epoch.  Used to align step starts. */
-int txb_moe_barrier(const txb_moe_shape* s, void* const* peers, void* region, uint64_t timeout_ns,
-                    void* stream);
+int txb_moe_barrier(const txb_moe_shape* s, const txb_moe_bufs* b, uint64_t timeout_ns, void* stream);
 
-/* Read the rank's latched error word and counters (synchronous, for the
- * host's ProtocolError diagnostics, moe.py:869-899).  counters receives
- * [step, tok_ctr, tok_target, comb_ctr, comb_target] followed by
- * route_tag[2][N] and done[N]; pass NULL to skip. */
+/* Read the rank's latched error word and counters (synchronous, on a
+ * private non-blocking stream; for the host's ProtocolError diagnostics,
+ * moe.py:869-899).  counters receives [step, tok_ctr, tok_target,
+ * comb_ctr, comb_target] then route_tag[2][N] and done[N]; NULL skips. */
 int txb_moe_status(const txb_moe_shape* s, void* region, uint32_t* err, uint64_t* counters,
                    int64_t ncounters);
 

@@ -51,6 +51,14 @@ class Shape(C.Structure):
     ]
 
 
+class Bufs(C.Structure):
+    """txb_moe_bufs (include/txb200.h)."""
+
+    _fields_ = [("region", C.c_void_p), ("peers", C.c_void_p), ("rank_scratch", C.c_void_p),
+                ("pos", C.c_void_p), ("gidx", C.c_void_p), ("rows", C.c_void_p),
+                ("sources", C.c_void_p), ("ret_slot", C.c_void_p), ("info", C.c_void_p)]
+
+
 _VP = C.c_void_p
 _I64 = C.c_int64
 _U64 = C.c_uint64
@@ -71,12 +79,14 @@ SIGNATURES: dict[str, list] = {
     "txb_ipc_close": [_INT, _VP],
     "txb_enable_peer": [_INT, _INT],
     "txb_moe_plan": [C.POINTER(Shape)],
-    "txb_moe_route": [C.POINTER(Shape), _VP, _INT, _I64, _VP, _VP, _VP, _VP, _U64, _VP],
-    "txb_moe_dispatch": [C.POINTER(Shape), _VP, _INT, _I64, _VP, _INT, _VP, _VP, _VP, _U64, _INT, _VP],
-    "txb_moe_dispatch_recv": [C.POINTER(Shape), _VP, _VP, _VP, _VP, _VP, _U64, _VP],
-    "txb_moe_combine_send": [C.POINTER(Shape), _VP, _I64, _VP, _VP, _VP, _VP, _VP, _INT, _VP],
-    "txb_moe_combine_recv": [C.POINTER(Shape), _VP, _VP, _VP, _I64, _VP, _INT, _U64, _VP],
-    "txb_moe_barrier": [C.POINTER(Shape), _VP, _VP, _U64, _VP],
+    "txb_moe_dispatch_fused": [C.POINTER(Shape), C.POINTER(Bufs), _VP, _INT, _I64, _VP, _INT, _U64, _VP],
+    "txb_moe_combine_fused": [C.POINTER(Shape), C.POINTER(Bufs), _VP, _I64, _VP, _I64, _VP, _INT, _U64, _VP],
+    "txb_moe_route": [C.POINTER(Shape), C.POINTER(Bufs), _VP, _INT, _I64, _VP],
+    "txb_moe_dispatch": [C.POINTER(Shape), C.POINTER(Bufs), _VP, _INT, _I64, _VP, _INT, _U64, _INT, _VP],
+    "txb_moe_dispatch_recv": [C.POINTER(Shape), C.POINTER(Bufs), _U64, _VP],
+    "txb_moe_combine_send": [C.POINTER(Shape), C.POINTER(Bufs), _VP, _I64, _INT, _VP],
+    "txb_moe_combine_recv": [C.POINTER(Shape), C.POINTER(Bufs), _VP, _I64, _VP, _I64, _VP, _INT, _U64, _VP],
+    "txb_moe_barrier": [C.POINTER(Shape), C.POINTER(Bufs), _U64, _VP],
     "txb_moe_status": [C.POINTER(Shape), _VP, C.POINTER(C.c_uint32), C.POINTER(_U64), _I64],
     "txb_encode_rows": [_VP, _INT, _I64, _I32, _I32, _I32, _VP, _VP],
     "txb_decode_rows": [_VP, _I64, _I32, _I32, _I32, _VP, _VP],

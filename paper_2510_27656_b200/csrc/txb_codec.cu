@@ -57,7 +57,8 @@ k_pack_rows(const uint8_t* __restrict__ src, int64_t width, const int64_t* __res
 __global__ void __launch_bounds__(256)
 k_weighted_combine(const float* __restrict__ y, int64_t hidden, const int64_t* __restrict__ pos,
                    const float* __restrict__ w, int64_t n, int topk, float* __restrict__ out) {
-  combine_rows<4>(reinterpret_cast<const uint8_t*>(y), hidden * 4, (int)hidden, pos, w, n, topk, out, 0);
+  combine_rows<4>(reinterpret_cast<const uint8_t*>(y), hidden * 4, nullptr, 0, (int)hidden, pos, nullptr, w, n,
+                  topk, out, 0, blockIdx.x, gridDim.x);
 }
 
 __global__ void k_fp8_encode(const float* __restrict__ x, int64_t n, uint8_t* __restrict__ out) {

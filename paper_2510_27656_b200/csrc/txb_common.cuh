@@ -48,6 +48,20 @@ __device__ __forceinline__ void red_release_sys_add(uint64_t* p, uint64_t v) {
   asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+__device__ __forceinline__ void red_relaxed_sys_add(uint64_t* p, uint64_t v) {
+  asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ void st_relaxed_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// One release fence for a batch of relaxed signals: fence.acq_rel.sys
+// followed by relaxed stores/reds forms the release pattern of the PTX
+// memory model, so N destination counters cost one system-scope MEMBAR
+// instead of one per red.release.
+__device__ __forceinline__ void fence_acqrel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+
 __device__ __forceinline__ void fence_sys() { asm volatile("fence.sc.sys;" ::: "memory"); }
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
@@ -77,11 +91,11 @@ struct Flags {
   uint64_t comb_ctr;                     // rows received (combine)
   uint64_t pad0[6];
   // local-only state (written by this rank's kernels, in stream order)
-  uint64_t step;         // current step number (1-based), bumped by route kernel
+  uint64_t step;         // last completed step (every kernel of step k reads k-1)
   uint64_t tok_target;   // cumulative expected tok_ctr
   uint64_t comb_target;  // cumulative expected comb_ctr
   uint32_t err;          // TXB_EV_* latch
-  uint32_t ticket;       // last-CTA detection in combine_send
+  uint32_t ticket;       // last-CTA detection at the end of a step
   uint64_t bar_epoch;    // local epoch of txb_moe_barrier
   uint64_t pad1[3];
   uint64_t bar[TXB_MAX_RANKS];  // [peer] = last barrier epoch peer reached

@@ -1,36 +1,49 @@
 // MoE expert-parallel dispatch/combine over one-sided peer stores and an
 // order-free completion counter (the WriteImm + ImmCounter design of
-// arXiv 2510.27656 section 6, reference: railtx/moe.py).
+// arXiv 2510.27656 section 6; reference: railtx/moe.py).
 //
-// One step on rank `me` is five stream-ordered kernels:
-//   k_route      count row + stable per-expert ranks + pos; the own count
-//                row is stored into every peer's route matrix and a step tag
-//                is release-published (reference: route scatter, imm_route).
-//   k_dispatch   acquire-waits for all route rows and for every peer's
-//                previous-step barrier, derives the layout and stores each
-//                token copy (optionally encoded: fp8 per-token scale / bf16)
-//                directly at its final grouped row on the owning rank, then
-//                release-adds the row count to that rank's token counter.
-//   k_recv       builds rows/sources/return-slot metadata and zero padding,
-//                then acquire-waits for the expected number of rows.
-//   k_comb_send  stores every valid grouped output row back into its
-//                source's combine buffer at the originating send slot,
-//                release-adds counts, and (last CTA) publishes the step
-//                barrier tag to every peer (buffer-reuse barrier, moe.dbar).
-//   k_comb_recv  acquire-waits for n*R rows, fp32 weighted sum per token.
+// A step is built from six phases (device functions below):
+//   P1 route    per-expert counts + stable per-copy ranks + pos; the own
+//               count row is stored into every peer's route matrix and a
+//               step tag is published (reference: route scatter, imm_route)
+//   P2 wait     acquire-wait for every route row of this step and for every
+//               peer's end-of-previous-step barrier (buffer reuse, moe.dbar)
+//   P3 layout   compute_layout + grouped order from the route matrix
+//   P4 tokens   each token copy is encoded (fp8 per-token scale / bf16 / raw)
+//               and stored straight into its final grouped row on the owner;
+//               per-destination row counts are added to the owner's token
+//               counter after one system-scope release fence (the ImmCounter)
+//   P5 recv     rows / sources / return-slot metadata, zeroed padding rows,
+//               then acquire-wait for the expected number of token rows
+//   C1 send     every valid grouped output row returns to its source's
+//               combine buffer at the originating send slot (rows whose
+//               source is this rank are read in place later)
+//   C2 combine  acquire-wait for the returned rows, fp32 weighted sum per
+//               token, last CTA publishes the end-of-step barrier tag
 //
-// Completion is counted, never ordered: a waiter only compares a monotone
+// Kernels:  split path  k_route(P1) k_dispatch(P2-P4) k_recv(P5)
+//                       k_comb_send(C1) k_comb_recv(C2)
+//           fused path  k_dispatch_fused(P1-P5) k_combine_fused(C1-C2),
+//                       cooperative launches (one wave, every CTA resident).
+// The split path is used when several ranks share one GPU (host-gated
+// emulation: no kernel may spin on a rank queued behind it) and for token
+// counts above the fused path's redundant-histogram limit.
+//
+// Completion is counted, never ordered: a waiter compares a monotone
 // counter with a cumulative threshold, so delivery order across NVLink is
-// irrelevant (engine.py:9-17 / ImmCounterTable engine.py:138-205).
+// irrelevant (engine.py:9-17, ImmCounterTable engine.py:138-205).
+#include <cstddef>
 #include <cstdio>
 
 #include "txb_rows.cuh"
 
 namespace txb {
 
-constexpr int kGroupPad = 8;     // moe.py:27
+constexpr int kGroupPad = 8;       // moe.py:27
+constexpr int kMaxExperts = 1536;  // shared-memory bound of the route phase
+constexpr int kThreads = 512;      // block size of the main kernels
 constexpr int kRouteThreads = 1024;
-constexpr int kMaxExperts = 1536;  // route-kernel shared-memory bound (33*E*4 B)
+constexpr int kFusedMaxCopies = 16384;  // n*R limit of the fused dispatch
 
 __device__ __forceinline__ int64_t load_route(const void* r, int i32, int64_t i) {
   return i32 ? (int64_t) reinterpret_cast<const int32_t*>(r)[i] : reinterpret_cast<const int64_t*>(r)[i];
@@ -38,25 +51,40 @@ __device__ __forceinline__ int64_t load_route(const void* r, int i32, int64_t i)
 
 __device__ __forceinline__ int64_t pad_up(int64_t x) { return (x + kGroupPad - 1) / kGroupPad * kGroupPad; }
 
-// ---------------------------------------------------------------- k_route
+__device__ __forceinline__ uint64_t cur_step(Flags* f) {
+  return *reinterpret_cast<volatile uint64_t*>(&f->step) + 1;
+}
 
-__global__ void __launch_bounds__(kRouteThreads)
-k_route(txb_moe_shape s, const void* __restrict__ routes, int i32, int64_t n,
-        void* const* __restrict__ peers, void* region, int32_t* __restrict__ rank_out,
-        int64_t* __restrict__ pos) {
-  extern __shared__ uint32_t sm[];
-  const int E = s.experts, R = s.topk, N = s.ranks;
-  uint32_t* hist = sm;       // [E]   running per-expert counts
-  uint32_t* wc = sm + E;     // [32][E] per-warp counts, then exclusive bases
-  __shared__ uint32_t bad;
-  __shared__ uint32_t tmp[33];
-  __shared__ uint64_t step_sh;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-  Flags* f = flags_of(region, s);
-  if (tid == 0) {
-    bad = 0;
-    step_sh = f->step + 1;
-  }
+// Shared-memory footprint of the phases (bytes), all carved from one
+// dynamic buffer and reused phase to phase.
+__host__ __device__ inline size_t smem_route(int E, int nwarps) { return (size_t)(1 + nwarps) * E * 4 + 16; }
+__host__ __device__ inline size_t smem_layout(int E) { return (size_t)(2 * E + 1) * 8; }
+__host__ __device__ inline size_t smem_recv(int N, int L) {
+  return (size_t)(3 * N * L + 1 + 2 * L + 1 + L * (N + 1) + N) * 8;
+}
+
+struct Shared {  // static shared state of one CTA
+  uint32_t bad, fail;
+  unsigned long long recv_me;
+  int64_t tmp[33];
+  float red[33];
+  uint32_t cnt[TXB_MAX_RANKS];
+  uint8_t* dstp[kMaxTopk];
+};
+
+// ------------------------------------------------------------------- P1
+
+// Counts and stable ranks of the n*R copies (stable = token order within an
+// expert, the (local_expert, t, j) slab order of moe.py:514-521).  Every
+// participating CTA scans all copies; copies of tokens t with
+// t % ncta == cta get their rank stored to rank_out.  Returns the
+// validation bits (moe.py:142-155).  hist[E] holds the counts afterwards.
+__device__ uint32_t route_counts(const txb_moe_shape& s, const void* routes, int i32, int64_t n,
+                                 uint32_t* hist, uint32_t* wc, int32_t* rank_out, int cta, int ncta,
+                                 Shared& sh) {
+  const int E = s.experts, R = s.topk;
+  const int tid = threadIdx.x, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  if (tid == 0) sh.bad = 0;
   for (int e = tid; e < E; e += blockDim.x) hist[e] = 0;
   __syncthreads();
   const int64_t M = n * R;
@@ -68,19 +96,18 @@ k_route(txb_moe_shape s, const void* __restrict__ routes, int i32, int64_t n,
     if (i < M) {
       const int64_t v = load_route(routes, i32, i);
       if (v < 0 || v >= E) {
-        atomicOr(&bad, TXB_EV_ROUTE_RANGE);
+        atomicOr(&sh.bad, TXB_EV_ROUTE_RANGE);
       } else {
         e = (int)v;
         const int64_t t = i / R;
         const int j = (int)(i - t * R);
         for (int jj = 0; jj < j; ++jj)
-          if (load_route(routes, i32, t * R + jj) == v) atomicOr(&bad, TXB_EV_ROUTE_DUP);
+          if (load_route(routes, i32, t * R + jj) == v) atomicOr(&sh.bad, TXB_EV_ROUTE_DUP);
       }
     }
-    // stable rank among equal experts inside the warp, then across warps
-    const uint32_t peers_mask = __match_any_sync(0xffffffffu, e);
-    const int lr = __popc(peers_mask & lanemask_lt());
-    if (e >= 0 && lr == 0) wc[warp * E + e] = __popc(peers_mask);
+    const uint32_t same = __match_any_sync(0xffffffffu, e);
+    const int lr = __popc(same & lanemask_lt());
+    if (e >= 0 && lr == 0) wc[warp * E + e] = __popc(same);
     __syncthreads();
     for (int x = tid; x < E; x += blockDim.x) {
       uint32_t run = hist[x];
@@ -92,82 +119,87 @@ k_route(txb_moe_shape s, const void* __restrict__ routes, int i32, int64_t n,
       hist[x] = run;
     }
     __syncthreads();
-    if (e >= 0) rank_out[i] = (int32_t)(wc[warp * E + e] + lr);
+    if (e >= 0 && (int)((i / R) % ncta) == cta) rank_out[i] = (int32_t)(wc[warp * E + e] + lr);
     __syncthreads();
   }
-  const uint32_t b = bad;
-  if (b) {
+  const uint32_t b = sh.bad;
+  if (b)
     for (int e = tid; e < E; e += blockDim.x) hist[e] = 0;  // publish an empty row
-  }
-  for (int e = tid; e < E; e += blockDim.x) wc[e] = hist[e];
   __syncthreads();
-  block_excl_scan<uint32_t>(wc, E, tmp);
-  // pos[t,j] = first send slot of expert e + stable rank (moe.py:514-521)
-  for (int64_t i = tid; i < M; i += blockDim.x) {
-    const int64_t v = load_route(routes, i32, i);
-    pos[i] = b ? -1 : (int64_t)wc[(int)v] + rank_out[i];
+  return b;
+}
+
+// pos[t,j] = first send slot of expert e + stable rank, for this CTA's
+// tokens (moe.py:510-520).  ex: int64 scratch of E entries.
+__device__ void route_positions(const txb_moe_shape& s, const void* routes, int i32, int64_t n,
+                                const uint32_t* hist, int64_t* ex, const int32_t* rank_in, int64_t* pos,
+                                uint32_t bad, int cta, int ncta, Shared& sh) {
+  const int E = s.experts, R = s.topk;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) ex[e] = hist[e];
+  __syncthreads();
+  block_excl_scan<int64_t>(ex, E, sh.tmp);
+  const int64_t nmine = n > cta ? (n - cta + ncta - 1) / ncta : 0;
+  for (int64_t k = threadIdx.x; k < nmine * R; k += blockDim.x) {
+    const int64_t t = cta + (k / R) * ncta;
+    const int64_t i = t * R + (k % R);
+    pos[i] = bad ? -1 : ex[(int)load_route(routes, i32, i)] + rank_in[i];
   }
-  // route-row scatter: own counts into every rank's matrix row `me`
-  const uint64_t step = step_sh;
+  __syncthreads();
+}
+
+// Route-row scatter: own counts into row `me` of every rank's matrix, one
+// release fence, then the step tag (single writer per slot).  Also books
+// the number of copies that will come back from other ranks.
+__device__ void route_publish(const txb_moe_shape& s, void* const* peers, Flags* f, const uint32_t* hist,
+                              uint64_t step, int64_t n, uint32_t bad) {
+  const int E = s.experts, N = s.ranks, L = s.local_experts;
   const int slot = (int)(step & 1);
-  for (int idx = tid; idx < N * E; idx += blockDim.x) {
+  for (int idx = threadIdx.x; idx < N * E; idx += blockDim.x) {
     const int d = idx / E, e = idx - d * E;
     route_of(peers[d], s, slot)[(size_t)s.me * E + e] = hist[e];
   }
   __syncthreads();
-  if (tid == 0) {
-    fence_sys();
-    for (int d = 0; d < N; ++d) st_release_sys(&flags_of(peers[d], s)->route_tag[slot][s.me], step);
-    f->step = step;
-    f->comb_target += b ? 0 : (uint64_t)M;
-    if (b) atomicOr(&f->err, b);
+  if (threadIdx.x == 0) {
+    uint64_t self = 0;
+    for (int le = 0; le < L; ++le) self += hist[s.me * L + le];
+    f->comb_target += bad ? 0 : (uint64_t)(n * s.topk) - self;
+    if (bad) atomicOr(&f->err, bad);
+    fence_acqrel_sys();
+    for (int d = 0; d < N; ++d) st_relaxed_sys(&flags_of(peers[d], s)->route_tag[slot][s.me], step);
   }
 }
 
-// ------------------------------------------------------------- k_dispatch
+// ------------------------------------------------------------------- P2
 
-constexpr int kDispThreads = 512;
-
-template <int SRC, int ELEM>
-__global__ void __launch_bounds__(kDispThreads)
-k_dispatch(txb_moe_shape s, const void* __restrict__ x, int64_t n, const void* __restrict__ routes,
-           int i32, const int32_t* __restrict__ rank_in, void* const* __restrict__ peers, void* region,
-           uint64_t timeout_ns) {
-  extern __shared__ int64_t dsm[];
-  const int N = s.ranks, E = s.experts, L = s.local_experts, R = s.topk;
-  int64_t* baseg = dsm;      // [E] grouped base row on the owner for (me, expert)
-  int64_t* padded = dsm + E; // [E+1] scan scratch
-  __shared__ int64_t tmp[33];
-  __shared__ uint32_t cnt[TXB_MAX_RANKS];
-  __shared__ uint8_t* dstp[kMaxTopk];
-  __shared__ uint32_t fail;
-  __shared__ float red[33];
-  __shared__ uint64_t recv_me;
-  const int tid = threadIdx.x;
-  Flags* f = flags_of(region, s);
-  const uint64_t step = *reinterpret_cast<volatile uint64_t*>(&f->step);
-  const int slot = (int)(step & 1);
-  if (tid == 0) {
-    fail = 0;
-    recv_me = 0;
-  }
-  for (int q = tid; q < N; q += blockDim.x) cnt[q] = 0;
+__device__ bool wait_routes(const txb_moe_shape& s, Flags* f, uint64_t step, uint64_t timeout_ns, Shared& sh) {
+  if (threadIdx.x == 0) sh.fail = 0;
   __syncthreads();
-  // wait: every route row of this step, every peer past the previous step
-  if (tid < 32) {
+  if (threadIdx.x < 32) {
+    const int slot = (int)(step & 1);
     const uint64_t dl = globaltimer() + timeout_ns;
-    for (int q = tid; q < N; q += 32) {
-      if (!spin_ge(&f->route_tag[slot][q], step, dl)) atomicOr(&fail, TXB_EV_WAIT_ROUTE);
-      if (!spin_ge(&f->done[q], step - 1, dl)) atomicOr(&fail, TXB_EV_WAIT_BARRIER);
+    for (int q = threadIdx.x; q < s.ranks; q += 32) {
+      if (!spin_ge(&f->route_tag[slot][q], step, dl)) atomicOr(&sh.fail, TXB_EV_WAIT_ROUTE);
+      if (!spin_ge(&f->done[q], step - 1, dl)) atomicOr(&sh.fail, TXB_EV_WAIT_BARRIER);
     }
   }
   __syncthreads();
-  if (fail) {
-    if (tid == 0) atomicOr(&f->err, fail);
-    return;
+  const uint32_t fl = sh.fail;
+  if (fl && threadIdx.x == 0) atomicOr(&f->err, fl);
+  return fl == 0;
+}
+
+// ------------------------------------------------------------------- P3
+
+// baseg[e] = grouped row on owner(e) where this rank's first copy for e
+// lands: group_starts[le] + sum_{s' < me} counts[s', e].
+__device__ bool dispatch_layout(const txb_moe_shape& s, const uint32_t* C, int64_t* baseg, int64_t* padded,
+                                Flags* f, bool book, Shared& sh) {
+  const int N = s.ranks, E = s.experts, L = s.local_experts, tid = threadIdx.x;
+  if (tid == 0) {
+    sh.recv_me = 0;
+    sh.fail = 0;
   }
-  // layout (compute_layout + grouped order, moe.py:200-225, 699-716)
-  const uint32_t* C = route_of(region, s, slot);
+  __syncthreads();
   for (int e = tid; e < E; e += blockDim.x) {
     int64_t col = 0, pre = 0;
     for (int q = 0; q < N; ++q) {
@@ -177,84 +209,97 @@ k_dispatch(txb_moe_shape s, const void* __restrict__ x, int64_t n, const void* _
     }
     padded[e] = pad_up(col);
     baseg[e] = pre;
-    if (blockIdx.x == 0 && e / L == s.me) atomicAdd((unsigned long long*)&recv_me, (unsigned long long)col);
+    if (book && e / L == s.me) atomicAdd(&sh.recv_me, (unsigned long long)col);
   }
   __syncthreads();
-  const int64_t tot = block_excl_scan<int64_t>(padded, E, tmp);
+  const int64_t tot = block_excl_scan<int64_t>(padded, E, sh.tmp);
   if (tid == 0) padded[E] = tot;
   __syncthreads();
   for (int e = tid; e < E; e += blockDim.x) baseg[e] += padded[e] - padded[(e / L) * L];
-  for (int d = tid; d < N; d += blockDim.x) {
-    const int64_t need = padded[(d + 1) * L] - padded[d * L];
-    if (need > s.grouped_rows) atomicOr(&fail, TXB_EV_CAPACITY);
-  }
+  for (int d = tid; d < N; d += blockDim.x)
+    if (padded[(d + 1) * L] - padded[d * L] > s.grouped_rows) atomicOr(&sh.fail, TXB_EV_CAPACITY);
   __syncthreads();
-  if (fail) {
-    if (tid == 0) atomicOr(&f->err, fail);
-    return;
+  const uint32_t fl = sh.fail;
+  if (fl) {
+    if (tid == 0) atomicOr(&f->err, fl);
+    return false;
   }
-  if (blockIdx.x == 0 && tid == 0) f->tok_target += recv_me;
+  if (book && tid == 0) f->tok_target += sh.recv_me;
+  return true;
+}
+
+// ------------------------------------------------------------------- P4
+
+template <int SRC, int ELEM>
+__device__ void dispatch_tokens(const txb_moe_shape& s, const void* x, int64_t n, const void* routes, int i32,
+                                const int32_t* rank_in, int32_t* gidx, void* const* peers, const int64_t* baseg,
+                                int cta, int ncta, Shared& sh) {
+  const int N = s.ranks, L = s.local_experts, R = s.topk, tid = threadIdx.x;
   const int64_t P = s.payload_bytes;
-  for (int64_t t = blockIdx.x; t < n; t += gridDim.x) {
+  for (int q = tid; q < N; q += blockDim.x) sh.cnt[q] = 0;
+  __syncthreads();
+  for (int64_t t = cta; t < n; t += ncta) {
     if (tid < R) {
       const int e = (int)load_route(routes, i32, t * R + tid);
       const int d = e / L;
       const int64_t g = baseg[e] + rank_in[t * R + tid];
-      dstp[tid] = grouped_of(peers[d], s) + g * P;
-      atomicAdd(&cnt[d], 1u);
+      sh.dstp[tid] = grouped_of(peers[d], s) + g * P;
+      gidx[t * R + tid] = d == s.me ? (int32_t)g : -1;
+      atomicAdd(&sh.cnt[d], 1u);
     }
     __syncthreads();
     if constexpr (SRC == TXB_SRC_ROWS) {
       const uint8_t* src = reinterpret_cast<const uint8_t*>(x) + t * P;
-      const int w = vec_width(src, dstp[0], P);
-      if (w == 16) {
-        const int64_t nv = P >> 4;
-        for (int64_t v = tid; v < nv; v += blockDim.x) {
+      if (vec_width(src, sh.dstp[0], P) == 16) {
+        for (int64_t v = tid; v < (P >> 4); v += blockDim.x) {
           const int4 val = reinterpret_cast<const int4*>(src)[v];
-          for (int j = 0; j < R; ++j) reinterpret_cast<int4*>(dstp[j])[v] = val;
+          for (int j = 0; j < R; ++j) reinterpret_cast<int4*>(sh.dstp[j])[v] = val;
         }
       } else {
-        for (int j = 0; j < R; ++j) copy_row(dstp[j], src, P, tid, blockDim.x);
+        for (int j = 0; j < R; ++j) copy_row(sh.dstp[j], src, P, tid, blockDim.x);
       }
     } else {
-      encode_store_row<SRC, ELEM>(x, t, s.hidden, s.scales, P, dstp, R, red);
+      encode_store_row<SRC, ELEM>(x, t, s.hidden, s.scales, P, sh.dstp, R, sh.red);
     }
     __syncthreads();
   }
-  // completion: per-destination release-add of the rows this CTA stored
-  if (tid == 0) {
-    fence_sys();
-    for (int d = 0; d < N; ++d)
-      if (cnt[d]) red_release_sys_add(&flags_of(peers[d], s)->tok_ctr, cnt[d]);
+}
+
+// Completion of this CTA's stores: one release fence, then a relaxed add of
+// the row count on every destination's counter at byte offset `field`.
+__device__ void signal_counts(const txb_moe_shape& s, void* const* peers, size_t field, Shared& sh) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    bool any = false;
+    for (int d = 0; d < s.ranks; ++d) any |= sh.cnt[d] != 0;
+    if (any) {
+      fence_acqrel_sys();
+      for (int d = 0; d < s.ranks; ++d)
+        if (sh.cnt[d])
+          red_relaxed_sys_add(reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(flags_of(peers[d], s)) + field),
+                              sh.cnt[d]);
+    }
   }
 }
 
-// ----------------------------------------------------------------- k_recv
+// ------------------------------------------------------------------- P5
 
-constexpr int kRecvThreads = 256;
-
-// Receive side: every CTA derives the (small) per-(source, local expert)
-// tables from the route matrix, then the grid walks the grouped rows with
-// one warp per row: metadata by lane 0, zero fill of padding rows by the
-// whole warp.  CTA 0 finally acquire-waits for the token receipts.
-__global__ void __launch_bounds__(kRecvThreads)
-k_recv(txb_moe_shape s, void* region, int64_t* __restrict__ rows, int64_t* __restrict__ sources,
-       int32_t* __restrict__ ret, int64_t* __restrict__ info, uint64_t timeout_ns) {
-  extern __shared__ int64_t rsm[];
+// Receive metadata for grouped rows (moe.py:699-722): every CTA derives the
+// per-(source, local expert) tables from the route matrix; the grid then
+// walks the grouped rows, one warp per row (lane 0 writes rows / sources /
+// return slot, the warp zero-fills padding rows).
+__device__ void recv_metadata(const txb_moe_shape& s, const uint32_t* C, int64_t* sm, int64_t* rows,
+                              int64_t* sources, int32_t* ret, int64_t* info, uint8_t* G, int cta, int ncta,
+                              Shared& sh) {
   const int N = s.ranks, E = s.experts, L = s.local_experts, me = s.me;
-  int64_t* a = rsm;                    // [N][L] counts into my experts
-  int64_t* rowbase = a + N * L;        // [N*L+1] flattened exclusive prefix = recv slot base
-  int64_t* retbase = rowbase + N * L + 1;  // [N][L] send slot base on the source
-  int64_t* gstart = retbase + N * L;   // [L+1] group starts (padded)
-  int64_t* gsize = gstart + L + 1;     // [L]
-  int64_t* srcpre = gsize + L;         // [L][N+1] prefix over sources within a group
-  int64_t* pre_all = srcpre + L * (N + 1);  // [N] sum_{e' < me*L} C[q][e']
-  __shared__ int64_t tmp[33];
   const int tid = threadIdx.x, nt = blockDim.x;
-  Flags* f = flags_of(region, s);
-  const uint64_t step = *reinterpret_cast<volatile uint64_t*>(&f->step);
-  const int slot = (int)(step & 1);
-  const uint32_t* C = route_of(region, s, slot);
+  int64_t* a = sm;                         // [N][L] counts into my experts
+  int64_t* rowbase = a + N * L;            // [N*L+1] flattened exclusive prefix = recv slot base
+  int64_t* retbase = rowbase + N * L + 1;  // [N][L] send slot base on the source
+  int64_t* gstart = retbase + N * L;       // [L+1]
+  int64_t* gsize = gstart + L + 1;         // [L]
+  int64_t* srcpre = gsize + L;             // [L][N+1]
+  int64_t* pre_all = srcpre + L * (N + 1); // [N] sum_{e' < me*L} C[q][e']
   for (int i = tid; i < N * L; i += nt) {
     const int q = i / L, le = i - q * L;
     a[i] = C[(size_t)q * E + me * L + le];
@@ -262,12 +307,11 @@ k_recv(txb_moe_shape s, void* region, int64_t* __restrict__ rows, int64_t* __res
   }
   for (int q = tid; q < N; q += nt) pre_all[q] = 0;
   __syncthreads();
-  if (me > 0) {
+  if (me > 0)
     for (int i = tid; i < N * me * L; i += nt) {
       const int q = i / (me * L), e = i - q * (me * L);
       atomicAdd((unsigned long long*)&pre_all[q], (unsigned long long)C[(size_t)q * E + e]);
     }
-  }
   for (int le = tid; le < L; le += nt) {
     int64_t run = 0;
     for (int q = 0; q < N; ++q) {
@@ -279,21 +323,18 @@ k_recv(txb_moe_shape s, void* region, int64_t* __restrict__ rows, int64_t* __res
     gstart[le] = pad_up(run);
   }
   __syncthreads();
-  const int64_t padded_total = block_excl_scan<int64_t>(gstart, L, tmp);
-  // recv slot base: recv_start[me][q] + sum_{le'<le} a[q][le'] is exactly the
-  // exclusive prefix of a[] flattened source-major (moe.py:178-184, 204-213)
-  const int64_t recv_total = block_excl_scan<int64_t>(rowbase, N * L, tmp);
+  const int64_t padded_total = block_excl_scan<int64_t>(gstart, L, sh.tmp);
+  // recv_start[me][q] + sum_{le'<le} a[q][le'] is the exclusive prefix of a[]
+  // flattened source-major (moe.py:178-184, 204-213)
+  const int64_t recv_total = block_excl_scan<int64_t>(rowbase, N * L, sh.tmp);
   if (tid == 0) {
     gstart[L] = padded_total;
     rowbase[N * L] = recv_total;
   }
   __syncthreads();
-  for (int i = tid; i < N * L; i += nt) {
-    const int q = i / L;
-    retbase[i] = pre_all[q] + (rowbase[i] - rowbase[q * L]);
-  }
+  for (int i = tid; i < N * L; i += nt) retbase[i] = pre_all[i / L] + (rowbase[i] - rowbase[(i / L) * L]);
   __syncthreads();
-  if (blockIdx.x == 0) {
+  if (cta == 0) {
     for (int le = tid; le < L; le += nt) {
       info[le] = gsize[le];
       info[L + le] = gstart[le];
@@ -304,9 +345,8 @@ k_recv(txb_moe_shape s, void* region, int64_t* __restrict__ rows, int64_t* __res
     }
   }
   const int64_t P = s.payload_bytes;
-  uint8_t* G = grouped_of(region, s);
   const int warp = tid >> 5, lane = tid & 31, nwarp = nt >> 5;
-  for (int64_t g = (int64_t)blockIdx.x * nwarp + warp; g < padded_total; g += (int64_t)gridDim.x * nwarp) {
+  for (int64_t g = (int64_t)cta * nwarp + warp; g < padded_total; g += (int64_t)ncta * nwarp) {
     int lo = 0, hi = L - 1;  // last le with gstart[le] <= g
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
@@ -331,79 +371,188 @@ k_recv(txb_moe_shape s, void* region, int64_t* __restrict__ rows, int64_t* __res
       ret[g] = (int32_t)(retbase[q * L + le] + kk);
     }
   }
-  // acquire-wait for every expected row (token immediate count)
-  if (blockIdx.x == 0 && tid == 0) {
+}
+
+__device__ void wait_tokens(Flags* f, int64_t* info, int L, uint64_t timeout_ns) {
+  if (threadIdx.x == 0) {
     const uint64_t dl = globaltimer() + timeout_ns;
     if (!spin_ge(&f->tok_ctr, f->tok_target, dl)) atomicOr(&f->err, TXB_EV_WAIT_TOKEN);
     info[2 * L + 2] = (int64_t)*reinterpret_cast<volatile uint32_t*>(&f->err);
   }
 }
 
-// ------------------------------------------------------------ k_comb_send
+// ------------------------------------------------------------------- C1
 
-constexpr int kCombThreads = 512;
-
-__global__ void __launch_bounds__(kCombThreads)
-k_comb_send(txb_moe_shape s, const uint8_t* __restrict__ out, int64_t ld, void* const* __restrict__ peers,
-            void* region, const int64_t* __restrict__ sources, const int32_t* __restrict__ ret,
-            const int64_t* __restrict__ info) {
-  __shared__ uint32_t cnt[TXB_MAX_RANKS];
+__device__ void combine_send_rows(const txb_moe_shape& s, const uint8_t* out, int64_t ld, void* const* peers,
+                                  const int64_t* sources, const int32_t* ret, const int64_t* info, int cta,
+                                  int ncta, Shared& sh) {
   const int N = s.ranks, L = s.local_experts, tid = threadIdx.x;
-  Flags* f = flags_of(region, s);
-  for (int q = tid; q < N; q += blockDim.x) cnt[q] = 0;
+  for (int q = tid; q < N; q += blockDim.x) sh.cnt[q] = 0;
   __syncthreads();
   const int64_t total = info[2 * L];
   const int64_t Pc = s.comb_bytes;
-  const int lane = tid & 31;
-  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (tid >> 5); g < total; g += nw) {
+  const int lane = tid & 31, nwarp = blockDim.x >> 5;
+  for (int64_t g = (int64_t)cta * nwarp + (tid >> 5); g < total; g += (int64_t)ncta * nwarp) {
     const int64_t q = sources[g];
-    if (q < 0) continue;
+    if (q < 0 || q == s.me) continue;  // padding, or read in place by C2
     copy_row(comb_of(peers[q], s) + (int64_t)ret[g] * Pc, out + g * ld, Pc, lane, 32);
-    if (lane == 0) atomicAdd(&cnt[q], 1u);
+    if (lane == 0) atomicAdd(&sh.cnt[q], 1u);
+  }
+}
+
+// ------------------------------------------------------------------- C2
+
+template <int ELEM>
+__device__ bool combine_reduce(const txb_moe_shape& s, Flags* f, const uint8_t* comb, const uint8_t* out,
+                               int64_t ld, const int64_t* pos, const int32_t* gidx, const float* w, int64_t n,
+                               void* dst, int out_bf16, uint64_t timeout_ns, int cta, int ncta, Shared& sh) {
+  if (threadIdx.x == 0) {
+    const uint64_t dl = globaltimer() + timeout_ns;
+    sh.fail = spin_ge(&f->comb_ctr, f->comb_target, dl) ? 0u : TXB_EV_WAIT_COMBINE;
+    if (sh.fail) atomicOr(&f->err, sh.fail);
   }
   __syncthreads();
-  if (tid == 0) {
-    fence_sys();
-    for (int q = 0; q < N; ++q)
-      if (cnt[q]) red_release_sys_add(&flags_of(peers[q], s)->comb_ctr, cnt[q]);
+  if (sh.fail) return false;
+  combine_rows<ELEM>(comb, s.comb_bytes, out, ld, s.hidden, pos, gidx, w, n, s.topk, dst, out_bf16, cta, ncta);
+  return true;
+}
+
+// End of step: the last CTA (ticket) publishes the barrier tag to every peer
+// ("all my reads of this step's buffers are done", moe.dbar) and advances
+// the local step counter.
+__device__ void end_of_step(const txb_moe_shape& s, void* const* peers, Flags* f, uint64_t step, int ncta) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
     const uint32_t t = atomicAdd(&f->ticket, 1u);
-    if (t == gridDim.x - 1) {
+    if (t == (uint32_t)ncta - 1) {
       f->ticket = 0;
-      fence_sys();
-      const uint64_t step = *reinterpret_cast<volatile uint64_t*>(&f->step);
-      for (int q = 0; q < N; ++q) st_release_sys(&flags_of(peers[q], s)->done[s.me], step);
+      *reinterpret_cast<volatile uint64_t*>(&f->step) = step;
+      fence_acqrel_sys();
+      for (int q = 0; q < s.ranks; ++q) st_relaxed_sys(&flags_of(peers[q], s)->done[s.me], step);
     }
   }
 }
 
-// ------------------------------------------------------------ k_comb_recv
+// ------------------------------------------------------------ split kernels
 
-constexpr int kCombRecvThreads = 512;
+__global__ void __launch_bounds__(kRouteThreads)
+k_route(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ routes, int i32, int64_t n) {
+  extern __shared__ __align__(16) uint8_t dsm[];
+  __shared__ Shared sh;
+  uint32_t* hist = reinterpret_cast<uint32_t*>(dsm);
+  uint32_t* wc = hist + ((s.experts + 3) & ~3);
+  Flags* f = flags_of(b.region, s);
+  const uint64_t step = cur_step(f);
+  const uint32_t bad = route_counts(s, routes, i32, n, hist, wc, b.rank_scratch, 0, 1, sh);
+  route_positions(s, routes, i32, n, hist, reinterpret_cast<int64_t*>(wc), b.rank_scratch, b.pos, bad, 0, 1, sh);
+  route_publish(s, b.peers, f, hist, step, n, bad);
+}
+
+template <int SRC, int ELEM>
+__global__ void __launch_bounds__(kThreads)
+k_dispatch(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, int64_t n, const void* __restrict__ routes,
+           int i32, uint64_t timeout_ns) {
+  extern __shared__ __align__(16) uint8_t dsm[];
+  __shared__ Shared sh;
+  Flags* f = flags_of(b.region, s);
+  const uint64_t step = cur_step(f);
+  if (!wait_routes(s, f, step, timeout_ns, sh)) return;
+  int64_t* baseg = reinterpret_cast<int64_t*>(dsm);
+  const uint32_t* C = route_of(b.region, s, (int)(step & 1));
+  if (!dispatch_layout(s, C, baseg, baseg + s.experts, f, blockIdx.x == 0, sh)) return;
+  dispatch_tokens<SRC, ELEM>(s, x, n, routes, i32, b.rank_scratch, b.gidx, b.peers, baseg, blockIdx.x,
+                             gridDim.x, sh);
+  signal_counts(s, b.peers, offsetof(Flags, tok_ctr), sh);
+}
+
+__global__ void __launch_bounds__(kThreads)
+k_recv(txb_moe_shape s, txb_moe_bufs b, uint64_t timeout_ns) {
+  extern __shared__ __align__(16) uint8_t dsm[];
+  __shared__ Shared sh;
+  Flags* f = flags_of(b.region, s);
+  const uint64_t step = cur_step(f);
+  recv_metadata(s, route_of(b.region, s, (int)(step & 1)), reinterpret_cast<int64_t*>(dsm), b.rows, b.sources,
+                b.ret_slot, b.info, grouped_of(b.region, s), blockIdx.x, gridDim.x, sh);
+  if (blockIdx.x == 0) wait_tokens(f, b.info, s.local_experts, timeout_ns);
+}
+
+__global__ void __launch_bounds__(kThreads)
+k_comb_send(txb_moe_shape s, txb_moe_bufs b, const uint8_t* __restrict__ out, int64_t ld) {
+  __shared__ Shared sh;
+  combine_send_rows(s, out, ld, b.peers, b.sources, b.ret_slot, b.info, blockIdx.x, gridDim.x, sh);
+  signal_counts(s, b.peers, offsetof(Flags, comb_ctr), sh);
+}
 
 template <int ELEM>
-__global__ void __launch_bounds__(kCombRecvThreads)
-k_comb_recv(txb_moe_shape s, void* region, const int64_t* __restrict__ pos, const float* __restrict__ w,
-            int64_t n, void* out, int out_bf16, uint64_t timeout_ns) {
-  __shared__ uint32_t ok;
-  Flags* f = flags_of(region, s);
-  if (threadIdx.x == 0) {
-    const uint64_t dl = globaltimer() + timeout_ns;
-    ok = spin_ge(&f->comb_ctr, f->comb_target, dl) ? 1u : 0u;
-    if (!ok) atomicOr(&f->err, TXB_EV_WAIT_COMBINE);
-  }
+__global__ void __launch_bounds__(kThreads)
+k_comb_recv(txb_moe_shape s, txb_moe_bufs b, const uint8_t* __restrict__ out, int64_t ld,
+            const float* __restrict__ w, int64_t n, void* dst, int out_bf16, uint64_t timeout_ns) {
+  __shared__ Shared sh;
+  Flags* f = flags_of(b.region, s);
+  const uint64_t step = cur_step(f);
+  combine_reduce<ELEM>(s, f, comb_of(b.region, s), out, ld, b.pos, b.gidx, w, n, dst, out_bf16, timeout_ns,
+                       blockIdx.x, gridDim.x, sh);
+  end_of_step(s, b.peers, f, step, gridDim.x);
+}
+
+// ------------------------------------------------------------ fused kernels
+
+// Route + dispatch + receive in one cooperative launch.  Every CTA counts
+// all n*R copies redundantly (no grid barrier needed; n*R is a decode-size
+// batch), CTA 0 publishes the count row, every CTA waits for the route rows,
+// derives the layout, stores its tokens, signals, then the grid fills the
+// receive metadata and CTA 0 waits for the incoming rows.
+template <int SRC, int ELEM>
+__global__ void __launch_bounds__(kThreads)
+k_dispatch_fused(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, int64_t n,
+                 const void* __restrict__ routes, int i32, uint64_t timeout_ns) {
+  extern __shared__ __align__(16) uint8_t dsm[];
+  __shared__ Shared sh;
+  Flags* f = flags_of(b.region, s);
+  const uint64_t step = cur_step(f);
+  const int cta = blockIdx.x, ncta = gridDim.x;
+  uint32_t* hist = reinterpret_cast<uint32_t*>(dsm);
+  uint32_t* wc = hist + ((s.experts + 3) & ~3);
+  const uint32_t bad = route_counts(s, routes, i32, n, hist, wc, b.rank_scratch, cta, ncta, sh);
+  if (cta == 0) route_publish(s, b.peers, f, hist, step, n, bad);
+  route_positions(s, routes, i32, n, hist, reinterpret_cast<int64_t*>(wc), b.rank_scratch, b.pos, bad, cta,
+                  ncta, sh);
+  if (!wait_routes(s, f, step, timeout_ns, sh)) return;
+  int64_t* baseg = reinterpret_cast<int64_t*>(dsm);
+  const uint32_t* C = route_of(b.region, s, (int)(step & 1));
+  if (!dispatch_layout(s, C, baseg, baseg + s.experts, f, cta == 0, sh)) return;
+  dispatch_tokens<SRC, ELEM>(s, x, n, routes, i32, b.rank_scratch, b.gidx, b.peers, baseg, cta, ncta, sh);
+  signal_counts(s, b.peers, offsetof(Flags, tok_ctr), sh);
   __syncthreads();
-  if (!ok) return;
-  combine_rows<ELEM>(comb_of(region, s), s.comb_bytes, s.hidden, pos, w, n, s.topk, out, out_bf16);
+  recv_metadata(s, C, reinterpret_cast<int64_t*>(dsm), b.rows, b.sources, b.ret_slot, b.info,
+                grouped_of(b.region, s), cta, ncta, sh);
+  if (cta == 0) wait_tokens(f, b.info, s.local_experts, timeout_ns);
+}
+
+// Combine send + reduce in one cooperative launch.
+template <int ELEM>
+__global__ void __launch_bounds__(kThreads)
+k_combine_fused(txb_moe_shape s, txb_moe_bufs b, const uint8_t* __restrict__ out, int64_t ld,
+                const float* __restrict__ w, int64_t n, void* dst, int out_bf16, uint64_t timeout_ns) {
+  __shared__ Shared sh;
+  Flags* f = flags_of(b.region, s);
+  const uint64_t step = cur_step(f);
+  combine_send_rows(s, out, ld, b.peers, b.sources, b.ret_slot, b.info, blockIdx.x, gridDim.x, sh);
+  signal_counts(s, b.peers, offsetof(Flags, comb_ctr), sh);
+  __syncthreads();
+  combine_reduce<ELEM>(s, f, comb_of(b.region, s), out, ld, b.pos, b.gidx, w, n, dst, out_bf16, timeout_ns,
+                       blockIdx.x, gridDim.x, sh);
+  end_of_step(s, b.peers, f, step, gridDim.x);
 }
 
 // -------------------------------------------------------------- k_barrier
 
-// All-rank device barrier (the reference's submit_barrier with one imm per
-// peer, engine.py:599-619): publish my epoch into every peer's slot, then
+// All-rank device barrier (submit_barrier with one imm per peer,
+// engine.py:599-619): publish my epoch into every peer's slot, then
 // acquire-wait until every peer's epoch has reached mine.
-__global__ void k_barrier(txb_moe_shape s, void* const* __restrict__ peers, void* region, uint64_t timeout_ns) {
-  Flags* f = flags_of(region, s);
+__global__ void k_barrier(txb_moe_shape s, txb_moe_bufs b, uint64_t timeout_ns) {
+  Flags* f = flags_of(b.region, s);
   __shared__ uint64_t ep;
   __shared__ uint32_t fail;
   if (threadIdx.x == 0) {
@@ -413,7 +562,7 @@ __global__ void k_barrier(txb_moe_shape s, void* const* __restrict__ peers, void
   }
   __syncthreads();
   const int N = s.ranks;
-  for (int q = threadIdx.x; q < N; q += blockDim.x) st_release_sys(&flags_of(peers[q], s)->bar[s.me], ep);
+  for (int q = threadIdx.x; q < N; q += blockDim.x) st_release_sys(&flags_of(b.peers[q], s)->bar[s.me], ep);
   const uint64_t dl = globaltimer() + timeout_ns;
   for (int q = threadIdx.x; q < N; q += blockDim.x)
     if (!spin_ge(&f->bar[q], ep, dl)) atomicOr(&fail, TXB_EV_WAIT_BARRIER);
@@ -436,16 +585,66 @@ static int sm_count(int dev) {
 
 static uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 
-static int check_shape(const txb_moe_shape* s) {
-  if (!s) {
-    set_error("null shape");
+static int check(const txb_moe_shape* s, const txb_moe_bufs* b) {
+  if (!s || !b) {
+    set_error("null shape or buffers");
     return TXB_ERR_PROTOCOL;
   }
   if (s->payload_bytes <= 0 || s->region_bytes == 0) {
     set_error("shape not planned (call txb_moe_plan)");
     return TXB_ERR_PROTOCOL;
   }
+  if (!b->region || !b->peers) {
+    set_error("buffers not wired (region / peer table missing)");
+    return TXB_ERR_REGION;
+  }
   return TXB_OK;
+}
+
+static size_t smem_main(const txb_moe_shape* s, bool route) {
+  size_t m = smem_layout(s->experts);
+  const size_t r = smem_recv(s->ranks, s->local_experts);
+  if (r > m) m = r;
+  if (route) {
+    const size_t q = smem_route(s->experts, kThreads / 32);
+    if (q > m) m = q;
+  }
+  return m;
+}
+
+template <typename K>
+static int set_smem(K kernel, size_t smem) {
+  if (smem > 48 * 1024) TXB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  return TXB_OK;
+}
+
+// Launch helper; `coop` requests a cooperative launch (all CTAs resident).
+template <typename... KArgs, typename... Args>
+static int launch(void (*kernel)(KArgs...), int grid, int block, size_t smem, cudaStream_t st, bool coop,
+                  Args... args) {
+  if (int rc = set_smem(kernel, smem)) return rc;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = coop ? 1 : 0;
+  TXB_CUDA(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
+  return TXB_OK;
+}
+
+// Largest cooperative grid for a kernel (one wave).
+template <typename K>
+static int coop_grid(K kernel, int dev, size_t smem, int want) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, smem);
+  const int cap = (per_sm > 0 ? per_sm : 1) * sm_count(dev);
+  if (want > cap) want = cap;
+  return want < 1 ? 1 : want;
 }
 
 }  // namespace txb
@@ -509,117 +708,153 @@ int txb_moe_plan(txb_moe_shape* s) {
   return TXB_OK;
 }
 
-int txb_moe_route(const txb_moe_shape* s, const void* routes, int routes_i32, int64_t n, void* const* peers,
-                  void* region, int32_t* rank_scratch, int64_t* pos, uint64_t timeout_ns, void* stream) {
-  (void)timeout_ns;
-  if (int rc = check_shape(s)) return rc;
+int txb_moe_route(const txb_moe_shape* s, const txb_moe_bufs* b, const void* routes, int routes_i32, int64_t n,
+                  void* stream) {
+  if (int rc = check(s, b)) return rc;
   if (n < 0 || n > s->max_tokens) {
     set_error("%lld tokens exceed the %d-token limit", (long long)n, s->max_tokens);
     return TXB_ERR_PROTOCOL;
   }
   TXB_CUDA(cudaSetDevice(s->device));
-  const size_t smem = (size_t)(1 + kRouteThreads / 32) * s->experts * sizeof(uint32_t);
-  if (smem > 48 * 1024) TXB_CUDA(cudaFuncSetAttribute(k_route, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_route<<<1, kRouteThreads, smem, (cudaStream_t)stream>>>(*s, routes, routes_i32, n, peers, region,
-                                                             rank_scratch, pos);
-  TXB_CUDA(cudaGetLastError());
-  return TXB_OK;
+  const size_t smem = smem_route(s->experts, kRouteThreads / 32);
+  return launch(k_route, 1, kRouteThreads, smem, (cudaStream_t)stream, false, *s, *b, routes, routes_i32, n);
 }
 
-int txb_moe_dispatch(const txb_moe_shape* s, const void* x, int src_kind, int64_t n, const void* routes,
-                     int routes_i32, const int32_t* rank_scratch, void* const* peers, void* region,
-                     uint64_t timeout_ns, int grid, void* stream) {
-  if (int rc = check_shape(s)) return rc;
+#define TXB_SWITCH_SRC_ELEM(KIND, ELEMSZ, MACRO)         \
+  do {                                                   \
+    if ((KIND) == TXB_SRC_ROWS) {                        \
+      MACRO(TXB_SRC_ROWS, 1);                            \
+    } else if ((KIND) == TXB_SRC_F32) {                  \
+      if ((ELEMSZ) == 1) MACRO(TXB_SRC_F32, 1);          \
+      else if ((ELEMSZ) == 2) MACRO(TXB_SRC_F32, 2);     \
+      else MACRO(TXB_SRC_F32, 4);                        \
+    } else if ((KIND) == TXB_SRC_BF16) {                 \
+      if ((ELEMSZ) == 1) MACRO(TXB_SRC_BF16, 1);         \
+      else if ((ELEMSZ) == 2) MACRO(TXB_SRC_BF16, 2);    \
+      else MACRO(TXB_SRC_BF16, 4);                       \
+    } else {                                             \
+      set_error("unknown source kind %d", (KIND));       \
+      return TXB_ERR_PROTOCOL;                           \
+    }                                                    \
+  } while (0)
+
+int txb_moe_dispatch(const txb_moe_shape* s, const txb_moe_bufs* b, const void* x, int src_kind, int64_t n,
+                     const void* routes, int routes_i32, uint64_t timeout_ns, int grid, void* stream) {
+  if (int rc = check(s, b)) return rc;
   TXB_CUDA(cudaSetDevice(s->device));
   if (grid <= 0) {
     const int64_t g = n < 1 ? 1 : n;
     grid = (int)(g < 4 * sm_count(s->device) ? g : 4 * sm_count(s->device));
   }
-  const size_t smem = (size_t)(2 * s->experts + 1) * sizeof(int64_t);
+  const size_t smem = smem_layout(s->experts);
   cudaStream_t st = (cudaStream_t)stream;
-#define TXB_LAUNCH_D(SRC, ELEM)                                                                   \
-  do {                                                                                            \
-    auto kfn = k_dispatch<SRC, ELEM>;                                                             \
-    if (smem > 48 * 1024) TXB_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-    kfn<<<grid, kDispThreads, smem, st>>>(*s, x, n, routes, routes_i32, rank_scratch, peers, region, timeout_ns); \
-  } while (0)
-  if (src_kind == TXB_SRC_ROWS) {
-    TXB_LAUNCH_D(TXB_SRC_ROWS, 1);
-  } else if (src_kind == TXB_SRC_F32 || src_kind == TXB_SRC_BF16) {
-    const bool f32 = src_kind == TXB_SRC_F32;
-    switch (s->elem_size) {
-      case 1: if (f32) TXB_LAUNCH_D(TXB_SRC_F32, 1); else TXB_LAUNCH_D(TXB_SRC_BF16, 1); break;
-      case 2: if (f32) TXB_LAUNCH_D(TXB_SRC_F32, 2); else TXB_LAUNCH_D(TXB_SRC_BF16, 2); break;
-      default: if (f32) TXB_LAUNCH_D(TXB_SRC_F32, 4); else TXB_LAUNCH_D(TXB_SRC_BF16, 4); break;
-    }
-  } else {
-    set_error("unknown source kind %d", src_kind);
-    return TXB_ERR_PROTOCOL;
-  }
-#undef TXB_LAUNCH_D
-  TXB_CUDA(cudaGetLastError());
+#define TXB_D(SRC, ELEM) \
+  return launch(k_dispatch<SRC, ELEM>, grid, kThreads, smem, st, false, *s, *b, x, n, routes, routes_i32, timeout_ns)
+  TXB_SWITCH_SRC_ELEM(src_kind, s->elem_size, TXB_D);
+#undef TXB_D
   return TXB_OK;
 }
 
-int txb_moe_dispatch_recv(const txb_moe_shape* s, void* region, int64_t* rows, int64_t* sources,
-                          int32_t* ret_slot, int64_t* info, uint64_t timeout_ns, void* stream) {
-  if (int rc = check_shape(s)) return rc;
+int txb_moe_dispatch_recv(const txb_moe_shape* s, const txb_moe_bufs* b, uint64_t timeout_ns, void* stream) {
+  if (int rc = check(s, b)) return rc;
   TXB_CUDA(cudaSetDevice(s->device));
-  const int N = s->ranks, L = s->local_experts;
-  const size_t smem = (size_t)(3 * N * L + 1 + 2 * L + 1 + L * (N + 1) + N) * sizeof(int64_t);
-  if (smem > 48 * 1024) TXB_CUDA(cudaFuncSetAttribute(k_recv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int64_t maxrows = s->grouped_rows;
-  const int64_t wpb = kRecvThreads / 32;
-  int grid = (int)((maxrows + wpb - 1) / wpb);
-  if (grid > 2 * sm_count(s->device)) grid = 2 * sm_count(s->device);
+  const size_t smem = smem_recv(s->ranks, s->local_experts);
+  const int64_t wpb = kThreads / 32;
+  int grid = (int)((s->grouped_rows + wpb - 1) / wpb);
+  if (grid > sm_count(s->device)) grid = sm_count(s->device);
   if (grid < 1) grid = 1;
-  k_recv<<<grid, kRecvThreads, smem, (cudaStream_t)stream>>>(*s, region, rows, sources, ret_slot, info, timeout_ns);
-  TXB_CUDA(cudaGetLastError());
-  return TXB_OK;
+  return launch(k_recv, grid, kThreads, smem, (cudaStream_t)stream, false, *s, *b, timeout_ns);
 }
 
-int txb_moe_combine_send(const txb_moe_shape* s, const void* outputs, int64_t ld, void* const* peers, void* region,
-                         const int64_t* sources, const int32_t* ret_slot, const int64_t* info, int grid,
+int txb_moe_combine_send(const txb_moe_shape* s, const txb_moe_bufs* b, const void* outputs, int64_t ld, int grid,
                          void* stream) {
-  if (int rc = check_shape(s)) return rc;
+  if (int rc = check(s, b)) return rc;
   TXB_CUDA(cudaSetDevice(s->device));
   if (grid <= 0) {
-    const int64_t rows = s->grouped_rows;
-    const int64_t want = (rows + (kCombThreads / 32) - 1) / (kCombThreads / 32);
+    const int64_t want = (s->grouped_rows + (kThreads / 32) - 1) / (kThreads / 32);
     const int cap = 2 * sm_count(s->device);
     grid = (int)(want < cap ? (want < 1 ? 1 : want) : cap);
   }
-  k_comb_send<<<grid, kCombThreads, 0, (cudaStream_t)stream>>>(*s, (const uint8_t*)outputs, ld, peers, region,
-                                                                 sources, ret_slot, info);
-  TXB_CUDA(cudaGetLastError());
-  return TXB_OK;
+  return launch(k_comb_send, grid, kThreads, 0, (cudaStream_t)stream, false, *s, *b, (const uint8_t*)outputs, ld);
 }
 
-int txb_moe_combine_recv(const txb_moe_shape* s, void* region, const int64_t* pos, const float* weights, int64_t n,
-                         void* out, int out_bf16, uint64_t timeout_ns, void* stream) {
-  if (int rc = check_shape(s)) return rc;
+int txb_moe_combine_recv(const txb_moe_shape* s, const txb_moe_bufs* b, const void* outputs, int64_t ld,
+                         const float* weights, int64_t n, void* out, int out_bf16, uint64_t timeout_ns,
+                         void* stream) {
+  if (int rc = check(s, b)) return rc;
   TXB_CUDA(cudaSetDevice(s->device));
-  int grid = (int)(n < 1 ? 1 : (n < 4 * sm_count(s->device) ? n : 4 * sm_count(s->device)));
+  const int grid = (int)(n < 1 ? 1 : (n < 2 * sm_count(s->device) ? n : 2 * sm_count(s->device)));
   cudaStream_t st = (cudaStream_t)stream;
+  const uint8_t* o = (const uint8_t*)outputs;
   switch (s->comb_elem_size) {
-    case 1: k_comb_recv<1><<<grid, kCombRecvThreads, 0, st>>>(*s, region, pos, weights, n, out, out_bf16, timeout_ns); break;
-    case 2: k_comb_recv<2><<<grid, kCombRecvThreads, 0, st>>>(*s, region, pos, weights, n, out, out_bf16, timeout_ns); break;
-    default: k_comb_recv<4><<<grid, kCombRecvThreads, 0, st>>>(*s, region, pos, weights, n, out, out_bf16, timeout_ns); break;
+    case 1: return launch(k_comb_recv<1>, grid, kThreads, 0, st, false, *s, *b, o, ld, weights, n, out, out_bf16, timeout_ns);
+    case 2: return launch(k_comb_recv<2>, grid, kThreads, 0, st, false, *s, *b, o, ld, weights, n, out, out_bf16, timeout_ns);
+    default: return launch(k_comb_recv<4>, grid, kThreads, 0, st, false, *s, *b, o, ld, weights, n, out, out_bf16, timeout_ns);
   }
-  TXB_CUDA(cudaGetLastError());
+}
+
+int txb_moe_dispatch_fused(const txb_moe_shape* s, const txb_moe_bufs* b, const void* x, int src_kind, int64_t n,
+                           const void* routes, int routes_i32, uint64_t timeout_ns, void* stream) {
+  if (int rc = check(s, b)) return rc;
+  if (n < 0 || n > s->max_tokens) {
+    set_error("%lld tokens exceed the %d-token limit", (long long)n, s->max_tokens);
+    return TXB_ERR_PROTOCOL;
+  }
+  if (n * s->topk > kFusedMaxCopies) {
+    set_error("fused dispatch handles at most %d copies per step (got %lld); use the split path",
+              kFusedMaxCopies, (long long)(n * s->topk));
+    return TXB_ERR_PROTOCOL;
+  }
+  TXB_CUDA(cudaSetDevice(s->device));
+  const size_t smem = smem_main(s, true);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int sms = sm_count(s->device);
+  const int want = (int)(n < 1 ? 1 : (n < sms ? n : sms));
+#define TXB_F(SRC, ELEM)                                                                          \
+  do {                                                                                            \
+    auto kfn = k_dispatch_fused<SRC, ELEM>;                                                       \
+    if (int rc = set_smem(kfn, smem)) return rc;                                                  \
+    const int grid = coop_grid(kfn, s->device, smem, want);                                       \
+    return launch(kfn, grid, kThreads, smem, st, true, *s, *b, x, n, routes, routes_i32, timeout_ns); \
+  } while (0)
+  TXB_SWITCH_SRC_ELEM(src_kind, s->elem_size, TXB_F);
+#undef TXB_F
   return TXB_OK;
 }
 
-int txb_moe_barrier(const txb_moe_shape* s, void* const* peers, void* region, uint64_t timeout_ns, void* stream) {
-  if (int rc = check_shape(s)) return rc;
+int txb_moe_combine_fused(const txb_moe_shape* s, const txb_moe_bufs* b, const void* outputs, int64_t ld,
+                          const float* weights, int64_t n, void* out, int out_bf16, uint64_t timeout_ns,
+                          void* stream) {
+  if (int rc = check(s, b)) return rc;
   TXB_CUDA(cudaSetDevice(s->device));
-  k_barrier<<<1, 128, 0, (cudaStream_t)stream>>>(*s, peers, region, timeout_ns);
-  TXB_CUDA(cudaGetLastError());
-  return TXB_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint8_t* o = (const uint8_t*)outputs;
+  const int sms = sm_count(s->device);
+#define TXB_C(ELEM)                                                                                   \
+  do {                                                                                                \
+    const int grid = coop_grid(k_combine_fused<ELEM>, s->device, 0, sms);                             \
+    return launch(k_combine_fused<ELEM>, grid, kThreads, 0, st, true, *s, *b, o, ld, weights, n, out, \
+                  out_bf16, timeout_ns);                                                              \
+  } while (0)
+  switch (s->comb_elem_size) {
+    case 1: TXB_C(1);
+    case 2: TXB_C(2);
+    default: TXB_C(4);
+  }
+#undef TXB_C
+}
+
+int txb_moe_barrier(const txb_moe_shape* s, const txb_moe_bufs* b, uint64_t timeout_ns, void* stream) {
+  if (int rc = check(s, b)) return rc;
+  TXB_CUDA(cudaSetDevice(s->device));
+  return launch(k_barrier, 1, 128, 0, (cudaStream_t)stream, false, *s, *b, timeout_ns);
 }
 
 int txb_moe_status(const txb_moe_shape* s, void* region, uint32_t* err, uint64_t* counters, int64_t ncounters) {
-  if (int rc = check_shape(s)) return rc;
+  if (!s || !region) {
+    set_error("null shape or region");
+    return TXB_ERR_PROTOCOL;
+  }
   TXB_CUDA(cudaSetDevice(s->device));
   // read on a private non-blocking stream so the snapshot never waits for
   // (or serialises with) kernels that are spinning on other streams

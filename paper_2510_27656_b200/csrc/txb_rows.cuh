@@ -247,27 +247,32 @@ __device__ __forceinline__ float load1(const uint8_t* row, int64_t h) {
 
 constexpr int kCombBatch = 8;  // rows of one chunk loaded together
 
-// out[t] = sum_j w[t,j] * y[pos[t,j]], j ascending from 0.0, separately rounded
+// out[t] = sum_j w[t,j] * y[t,j], j ascending from 0.0, separately rounded
 // multiply and add (kernels.py:214-226); fp8 rows are dequantised first as
-// e4m3 * f32 scale (kernels.py:139-141).  Each thread owns 8-element chunks;
-// the rows of a chunk are fetched in batches of kCombBatch before the
-// accumulation so their memory latencies overlap.
+// e4m3 * f32 scale (kernels.py:139-141).  Row y[t,j] is out_rows +
+// gidx[t,j]*ld when gidx[t,j] >= 0 (a copy this rank served itself, read in
+// place from the expert outputs) and comb + pos[t,j]*Pc otherwise.  Each
+// thread owns 8-element chunks; the rows of a chunk are fetched in batches
+// of kCombBatch before the accumulation so their memory latencies overlap.
 template <int ELEM>
-__device__ void combine_rows(const uint8_t* base, int64_t Pc, int H, const int64_t* pos, const float* w,
-                             int64_t n, int R, void* out, int out_bf16) {
+__device__ void combine_rows(const uint8_t* comb, int64_t Pc, const uint8_t* out_rows, int64_t ld, int H,
+                             const int64_t* pos, const int32_t* gidx, const float* w, int64_t n, int R,
+                             void* dst, int out_bf16, int cta, int ncta) {
   __shared__ const uint8_t* rowp[kMaxTopk];
   __shared__ float ws[kMaxTopk];
   __shared__ float sc[kMaxTopk];
   const int tid = threadIdx.x, nt = blockDim.x;
-  const bool vec = (H % 8 == 0) && ((Pc & 15) == 0) && ((reinterpret_cast<uintptr_t>(base) & 15) == 0);
-  for (int64_t t = blockIdx.x; t < n; t += gridDim.x) {
+  const bool vec = (H % 8 == 0) && ((Pc & 15) == 0) && ((reinterpret_cast<uintptr_t>(comb) & 15) == 0) &&
+                   (!gidx || (((ld & 15) == 0) && ((reinterpret_cast<uintptr_t>(out_rows) & 15) == 0)));
+  for (int64_t t = cta; t < n; t += ncta) {
     if (tid < R) {
-      const int64_t p = pos[t * R + tid];
-      rowp[tid] = base + p * Pc;
+      const int32_t gi = gidx ? gidx[t * R + tid] : -1;
+      const uint8_t* row = gi >= 0 ? out_rows + (int64_t)gi * ld : comb + pos[t * R + tid] * Pc;
+      rowp[tid] = row;
       ws[tid] = w[t * R + tid];
       float scale = 1.f;
       if (ELEM == 1) {
-        const uint8_t* sp = base + p * Pc + H;
+        const uint8_t* sp = row + H;
         uint32_t u = (uint32_t)sp[0] | ((uint32_t)sp[1] << 8) | ((uint32_t)sp[2] << 16) | ((uint32_t)sp[3] << 24);
         scale = __uint_as_float(u);
       }
@@ -303,9 +308,9 @@ __device__ void combine_rows(const uint8_t* base, int64_t Pc, int H, const int64
           uint32_t* ow = reinterpret_cast<uint32_t*>(&o);
 #pragma unroll
           for (int q = 0; q < 4; ++q) ow[q] = (uint32_t)bf16_rne(acc[2 * q]) | ((uint32_t)bf16_rne(acc[2 * q + 1]) << 16);
-          reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(out) + t * H)[c] = o;
+          reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(dst) + t * H)[c] = o;
         } else {
-          float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + t * H) + 2 * c;
+          float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(dst) + t * H) + 2 * c;
           o[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
           o[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
         }
@@ -318,8 +323,8 @@ __device__ void combine_rows(const uint8_t* base, int64_t Pc, int H, const int64
           const float y = ELEM == 1 ? __fmul_rn(v, sc[j]) : v;
           acc = __fadd_rn(acc, __fmul_rn(ws[j], y));
         }
-        if (out_bf16) reinterpret_cast<uint16_t*>(out)[t * H + h] = bf16_rne(acc);
-        else reinterpret_cast<float*>(out)[t * H + h] = acc;
+        if (out_bf16) reinterpret_cast<uint16_t*>(dst)[t * H + h] = bf16_rne(acc);
+        else reinterpret_cast<float*>(dst)[t * H + h] = acc;
       }
     }
     __syncthreads();

@@ -41,6 +41,7 @@ from .errors import ProtocolError
 from .memory import Region, enable_peer_access, view
 
 GROUP_PAD = 8           # moe.py:27
+FUSED_MAX_COPIES = 16384  # n*topk limit of the fused dispatch kernel (txb_moe.cu)
 DEFAULT_PRIVATE = 32    # moe.py:28
 
 
@@ -338,7 +339,7 @@ class StepStats:
 
 
 class _Step:
-    __slots__ = ("step", "n", "host", "grouped", "keep", "ev", "sync")
+    __slots__ = ("step", "n", "host", "grouped", "keep", "ev", "sync", "fused", "out", "ld")
 
     def __init__(self, step: int, n: int, host: bool) -> None:
         self.step = step
@@ -348,6 +349,9 @@ class _Step:
         self.keep: list = []
         self.ev: list = []
         self.sync = True
+        self.fused = False
+        self.out = None
+        self.ld = 0
 
 
 _WAIT_WHAT = (
@@ -395,6 +399,7 @@ class MoeRank:
         self._rows = torch.empty(G, dtype=torch.int64, device=dev)
         self._sources = torch.empty(G, dtype=torch.int64, device=dev)
         self._ret = torch.empty(G, dtype=torch.int32, device=dev)
+        self._gidx = torch.empty(max(1, T * R), dtype=torch.int32, device=dev)
         self._info = torch.zeros(2 * L + 3, dtype=torch.int64, device=dev)
         self._info_host = torch.zeros(2 * L + 3, dtype=torch.int64).pin_memory()
         self._grouped = self.region.tensor(int(sh.off_grouped), (G, int(sh.payload_bytes)), torch.uint8)
@@ -405,6 +410,9 @@ class MoeRank:
         self._peer_table: torch.Tensor | None = None
         self._peer_table_p = C.c_void_p(0)
         self.host_gated = False
+        self.fused = True           # fused kernels when one GPU per rank
+        self._bufs = _lib.Bufs()
+        self._bufs_p = C.byref(self._bufs)
         self._lock = threading.Lock()
         self._cur: _Step | None = None
         self._error: str | None = None
@@ -423,6 +431,16 @@ class MoeRank:
                                         device=torch.device("cuda", self.device))
         self._peer_table_p = C.c_void_p(self._peer_table.data_ptr())
         self.host_gated = gated
+        b = self._bufs
+        b.region = self.region.ptr
+        b.peers = self._peer_table.data_ptr()
+        b.rank_scratch = self._rank_scratch.data_ptr()
+        b.pos = self._pos.data_ptr()
+        b.gidx = self._gidx.data_ptr()
+        b.rows = self._rows.data_ptr()
+        b.sources = self._sources.data_ptr()
+        b.ret_slot = self._ret.data_ptr()
+        b.info = self._info.data_ptr()
 
     def _connect(self, mesh: Sequence["MoeRank"]) -> None:
         """In-process wiring: peers are addressed directly (peer access)."""
@@ -571,17 +589,21 @@ class MoeRank:
         st.keep = [r_dev, p]
         self._event(st)
         sid = self._sid()
-        _lib.call("txb_moe_route", self._shape_p, _sp(r_dev), i32, n, self._peer_table_p,
-                  C.c_void_p(self.region.ptr), _sp(self._rank_scratch), _sp(self._pos),
-                  self._tmo(None), sid)
+        st.fused = self.fused and not self.host_gated and n * spec.topk <= FUSED_MAX_COPIES \
+            and _between is None
+        if st.fused:
+            # route + dispatch + receive metadata in one cooperative kernel
+            _lib.call("txb_moe_dispatch_fused", self._shape_p, self._bufs_p, _sp(p), kind, n,
+                      _sp(r_dev), i32, self._tmo(None), sid)
+            return
+        _lib.call("txb_moe_route", self._shape_p, self._bufs_p, _sp(r_dev), i32, n, sid)
         if _between is not None:      # bench hook: split route / dispatch launches
             _between()
         if self.host_gated:
             step = st.step
             self._gate(lambda c: all(v >= step for v in c["route_tag"][step & 1])
                        and all(v >= step - 1 for v in c["done"]), step, "route counts", None)
-        _lib.call("txb_moe_dispatch", self._shape_p, _sp(p), kind, n, _sp(r_dev), i32,
-                  _sp(self._rank_scratch), self._peer_table_p, C.c_void_p(self.region.ptr),
+        _lib.call("txb_moe_dispatch", self._shape_p, self._bufs_p, _sp(p), kind, n, _sp(r_dev), i32,
                   self._tmo(None), 0, sid)
         if self.host_gated:
             torch.cuda.current_stream(self.device).synchronize()
@@ -595,11 +617,10 @@ class MoeRank:
             raise ProtocolError("no step in flight")
         self._raise_if_failed()
         sync = st.sync if sync is None else (sync or st.host)
-        if self.host_gated:
-            self._gate(lambda c: c["tok_ctr"] >= c["tok_target"], st.step, "token writes", timeout)
-        _lib.call("txb_moe_dispatch_recv", self._shape_p, C.c_void_p(self.region.ptr),
-                  _sp(self._rows), _sp(self._sources), _sp(self._ret), _sp(self._info),
-                  self._tmo(timeout), self._sid())
+        if not st.fused:
+            if self.host_gated:
+                self._gate(lambda c: c["tok_ctr"] >= c["tok_target"], st.step, "token writes", timeout)
+            _lib.call("txb_moe_dispatch_recv", self._shape_p, self._bufs_p, self._tmo(timeout), self._sid())
         L = self.spec.local_experts
         if not sync:
             st.grouped = GroupedTokens(self._grouped, self._info[:L], self._info[L:2 * L],
@@ -673,9 +694,10 @@ class MoeRank:
             raise ProtocolError(f"output rows {out.shape[0]} below the receive capacity {rows_needed}")
         ld = (out.stride(0) if out.numel() else width) * out.element_size()
         st.keep.append(out)
-        _lib.call("txb_moe_combine_send", self._shape_p, _sp(out), ld, self._peer_table_p,
-                  C.c_void_p(self.region.ptr), _sp(self._sources), _sp(self._ret), _sp(self._info),
-                  0, self._sid())
+        st.out, st.ld = out, ld
+        if st.fused:
+            return                    # sent by the fused combine kernel in combine_recv
+        _lib.call("txb_moe_combine_send", self._shape_p, self._bufs_p, _sp(out), ld, 0, self._sid())
         if self.host_gated:
             torch.cuda.current_stream(self.device).synchronize()
 
@@ -706,11 +728,17 @@ class MoeRank:
             raise ProtocolError(f"out_dtype {out_dtype} not in (float32, bfloat16)")
         out = torch.empty((st.n, spec.hidden), dtype=out_dtype, device=dev)
         sync = st.sync if sync is None else (sync or st.host)
-        if self.host_gated:
-            self._gate(lambda c: c["comb_ctr"] >= c["comb_target"], st.step, "combine writes", timeout)
-        _lib.call("txb_moe_combine_recv", self._shape_p, C.c_void_p(self.region.ptr), _sp(self._pos),
-                  _sp(w), st.n, _sp(out), 1 if out_dtype == torch.bfloat16 else 0,
-                  self._tmo(timeout), self._sid())
+        if st.out is None:
+            raise ProtocolError("combine_recv before combine_send")
+        bf = 1 if out_dtype == torch.bfloat16 else 0
+        if st.fused:
+            _lib.call("txb_moe_combine_fused", self._shape_p, self._bufs_p, _sp(st.out), st.ld, _sp(w),
+                      st.n, _sp(out), bf, self._tmo(timeout), self._sid())
+        else:
+            if self.host_gated:
+                self._gate(lambda c: c["comb_ctr"] >= c["comb_target"], st.step, "combine writes", timeout)
+            _lib.call("txb_moe_combine_recv", self._shape_p, self._bufs_p, _sp(st.out), st.ld, _sp(w),
+                      st.n, _sp(out), bf, self._tmo(timeout), self._sid())
         st.keep.append(w)
         if sync:
             self._event(st)
@@ -733,8 +761,7 @@ class MoeRank:
         (launch only; a later stream operation observes completion)."""
         if self.host_gated:
             raise ProtocolError("device barrier needs one device per rank")
-        _lib.call("txb_moe_barrier", self._shape_p, self._peer_table_p, C.c_void_p(self.region.ptr),
-                  self._tmo(timeout), self._sid())
+        _lib.call("txb_moe_barrier", self._shape_p, self._bufs_p, self._tmo(timeout), self._sid())
 
     @property
     def pos(self) -> torch.Tensor:

@@ -57,9 +57,10 @@ def _oracle_round(ospec, routes, values_or_payloads, encoded=False):
     return mo.dispatch(ospec, routes, payloads), payloads
 
 
+@pytest.mark.parametrize("fused", [True, False])
 @pytest.mark.parametrize("elem,src", [(1, torch.float32), (1, torch.bfloat16), (2, torch.float32),
                                       (2, torch.bfloat16), (4, torch.float32)])
-def test_fused_encode_dispatch_matches_oracle(elem, src):
+def test_fused_encode_dispatch_matches_oracle(elem, src, fused):
     """Device mode: f32/bf16 values encoded inside the dispatch kernel
     (fp8 per-token scale / bf16 RNE / f32) == encode_tokens then dispatch."""
     N = 1
@@ -74,6 +75,7 @@ def test_fused_encode_dispatch_matches_oracle(elem, src):
     mesh = moe.build_mesh(local_engines([0]), spec)
     try:
         rk = mesh[0]
+        rk.fused = fused
         rk.dispatch_send(vals[0].cuda(), torch.from_numpy(routes[0]).cuda())
         g = rk.dispatch_recv()
         want = res.ranks[0].grouped
@@ -87,7 +89,8 @@ def test_fused_encode_dispatch_matches_oracle(elem, src):
         close_mesh(mesh)
 
 
-def test_dsv3_decode_ep1_full_size():
+@pytest.mark.parametrize("fused", [True, False])
+def test_dsv3_decode_ep1_full_size(fused):
     """DeepSeek-V3 decode shape at EP=1 (128 tok, H=7168, E=256, top-8),
     fp8 dispatch from bf16 values, bf16 combine rows, bf16 out; several
     steps back to back on one mesh (counter epochs, buffer reuse)."""
@@ -97,6 +100,7 @@ def test_dsv3_decode_ep1_full_size():
     cs = mo.Spec(1, 256, 128, 8, hidden=7168, elem_size=2, scales=0)
     mesh = moe.build_mesh(local_engines([0]), spec)
     rk = mesh[0]
+    rk.fused = fused
     try:
         for step in range(3):
             rng = np.random.default_rng(100 + step)
