@@ -51,6 +51,11 @@ __device__ __forceinline__ int64_t load_route(const void* r, int i32, int64_t i)
 
 __device__ __forceinline__ int64_t pad_up(int64_t x) { return (x + kGroupPad - 1) / kGroupPad * kGroupPad; }
 
+// Optional phase stamps for profiling (txb_moe_bufs.prof).
+__device__ __forceinline__ void stamp(const txb_moe_bufs& b, int k) {
+  if (b.prof && threadIdx.x == 0) b.prof[blockIdx.x * 16 + k] = globaltimer();
+}
+
 __device__ __forceinline__ uint64_t cur_step(Flags* f) {
   return *reinterpret_cast<volatile uint64_t*>(&f->step) + 1;
 }
@@ -514,20 +519,29 @@ k_dispatch_fused(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
   const int cta = blockIdx.x, ncta = gridDim.x;
   uint32_t* hist = reinterpret_cast<uint32_t*>(dsm);
   uint32_t* wc = hist + ((s.experts + 3) & ~3);
+  stamp(b, 0);
   const uint32_t bad = route_counts(s, routes, i32, n, hist, wc, b.rank_scratch, cta, ncta, sh);
+  stamp(b, 1);
   if (cta == 0) route_publish(s, b.peers, f, hist, step, n, bad);
   route_positions(s, routes, i32, n, hist, reinterpret_cast<int64_t*>(wc), b.rank_scratch, b.pos, bad, cta,
                   ncta, sh);
+  stamp(b, 2);
   if (!wait_routes(s, f, step, timeout_ns, sh)) return;
+  stamp(b, 3);
   int64_t* baseg = reinterpret_cast<int64_t*>(dsm);
   const uint32_t* C = route_of(b.region, s, (int)(step & 1));
   if (!dispatch_layout(s, C, baseg, baseg + s.experts, f, cta == 0, sh)) return;
+  stamp(b, 4);
   dispatch_tokens<SRC, ELEM>(s, x, n, routes, i32, b.rank_scratch, b.gidx, b.peers, baseg, cta, ncta, sh);
+  stamp(b, 5);
   signal_counts(s, b.peers, offsetof(Flags, tok_ctr), sh);
   __syncthreads();
+  stamp(b, 6);
   recv_metadata(s, C, reinterpret_cast<int64_t*>(dsm), b.rows, b.sources, b.ret_slot, b.info,
                 grouped_of(b.region, s), cta, ncta, sh);
+  stamp(b, 7);
   if (cta == 0) wait_tokens(f, b.info, s.local_experts, timeout_ns);
+  stamp(b, 8);
 }
 
 // Combine send + reduce in one cooperative launch.
@@ -538,12 +552,17 @@ k_combine_fused(txb_moe_shape s, txb_moe_bufs b, const uint8_t* __restrict__ out
   __shared__ Shared sh;
   Flags* f = flags_of(b.region, s);
   const uint64_t step = cur_step(f);
+  stamp(b, 9);
   combine_send_rows(s, out, ld, b.peers, b.sources, b.ret_slot, b.info, blockIdx.x, gridDim.x, sh);
+  stamp(b, 10);
   signal_counts(s, b.peers, offsetof(Flags, comb_ctr), sh);
   __syncthreads();
+  stamp(b, 11);
   combine_reduce<ELEM>(s, f, comb_of(b.region, s), out, ld, b.pos, b.gidx, w, n, dst, out_bf16, timeout_ns,
                        blockIdx.x, gridDim.x, sh);
+  stamp(b, 12);
   end_of_step(s, b.peers, f, step, gridDim.x);
+  stamp(b, 13);
 }
 
 // -------------------------------------------------------------- k_barrier

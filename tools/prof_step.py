@@ -34,3 +34,25 @@ torch.cuda.synchronize()
 err, _ = rk.status()
 assert err == 0, hex(err)
 print("ok")
+
+# phase stamps of the fused kernels (%globaltimer, per CTA)
+prof = torch.zeros(148 * 16, dtype=torch.int64, device="cuda")
+rk._bufs.prof = prof.data_ptr()
+names = ["start", "counted", "positions", "routes-in", "layout", "stored", "signalled", "metadata",
+         "tokens-in", "c:start", "c:sent", "c:signalled", "c:reduced", "c:end"]
+for _ in range(3):
+    prof.zero_()
+    rk.dispatch_send(x, r, sync=False)
+    rk.dispatch_recv(sync=False)
+    rk.combine_send(y)
+    rk.combine_recv(w, out_dtype=torch.bfloat16, sync=False)
+    torch.cuda.synchronize()
+p = prof.view(148, 16).cpu().numpy().astype(np.float64)
+rk._bufs.prof = 0
+act = p[:, 0] > 0
+t0 = p[act, 0].min()
+for k, nm in enumerate(names):
+    col = p[:, k]
+    col = col[col > 0] - t0
+    if col.size:
+        print(f"{nm:12s} min {col.min()/1e3:8.2f}us  med {np.median(col)/1e3:8.2f}us  max {col.max()/1e3:8.2f}us  n={col.size}")
