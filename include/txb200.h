@@ -70,6 +70,8 @@ typedef struct txb_moe_shape {
   int32_t comb_elem_size, comb_scales;
   int32_t me;     /* this rank */
   int32_t device; /* CUDA device of this rank's region and stream */
+  int32_t single_device; /* 1 when every rank of the mesh lives on this device:
+                            completion fences drop from .sys to .gpu scope */
   /* derived by txb_moe_plan */
   int32_t local_experts;
   int64_t payload_bytes;  /* dispatch row bytes  = hidden*elem + 4*scales */

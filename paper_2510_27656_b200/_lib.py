@@ -43,7 +43,8 @@ class Shape(C.Structure):
         ("ranks", C.c_int32), ("experts", C.c_int32), ("max_tokens", C.c_int32),
         ("topk", C.c_int32), ("hidden", C.c_int32), ("elem_size", C.c_int32),
         ("scales", C.c_int32), ("comb_elem_size", C.c_int32), ("comb_scales", C.c_int32),
-        ("me", C.c_int32), ("device", C.c_int32), ("local_experts", C.c_int32),
+        ("me", C.c_int32), ("device", C.c_int32), ("single_device", C.c_int32),
+        ("local_experts", C.c_int32),
         ("payload_bytes", C.c_int64), ("comb_bytes", C.c_int64), ("capacity", C.c_int64),
         ("grouped_rows", C.c_int64), ("comb_rows", C.c_int64),
         ("off_flags", C.c_uint64), ("off_route", C.c_uint64), ("off_grouped", C.c_uint64),

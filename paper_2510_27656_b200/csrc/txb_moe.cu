@@ -63,18 +63,29 @@ __device__ __forceinline__ uint64_t cur_step(Flags* f) {
 // Shared-memory footprint of the phases (bytes), all carved from one
 // dynamic buffer and reused phase to phase.
 __host__ __device__ inline size_t smem_route(int E, int nwarps) { return (size_t)(1 + nwarps) * E * 4 + 16; }
+__host__ __device__ inline size_t smem_cmat(int N, int E) { return ((size_t)N * E * 4 + 15) / 16 * 16; }
+__host__ __device__ inline size_t smem_recv(int N, int L);
+__host__ __device__ inline size_t smem_layout(int E);
+// the route matrix copy (Cs) lives after the layout / recv scratch
+__host__ __device__ inline size_t cmat_offset(const txb_moe_shape& s) {
+  const size_t a = smem_layout(s.experts), b = smem_recv(s.ranks, s.local_experts);
+  return ((a > b ? a : b) + 15) / 16 * 16;
+}
 __host__ __device__ inline size_t smem_layout(int E) { return (size_t)(2 * E + 1) * 8; }
 __host__ __device__ inline size_t smem_recv(int N, int L) {
   return (size_t)(3 * N * L + 1 + 2 * L + 1 + L * (N + 1) + N) * 8;
 }
 
+constexpr int kMaxOwn = 64;  // copies per CTA handled by the direct-count rank path
+
 struct Shared {  // static shared state of one CTA
-  uint32_t bad, fail;
-  unsigned long long recv_me;
+  uint32_t bad, fail, recv_me;
   int64_t tmp[33];
   float red[33];
   uint32_t cnt[TXB_MAX_RANKS];
   uint8_t* dstp[kMaxTopk];
+  uint32_t own_rank[kMaxOwn];
+  int32_t own_e[kMaxOwn];
 };
 
 // ------------------------------------------------------------------- P1
@@ -91,8 +102,47 @@ __device__ uint32_t route_counts(const txb_moe_shape& s, const void* routes, int
   const int tid = threadIdx.x, warp = tid >> 5, nwarps = blockDim.x >> 5;
   if (tid == 0) sh.bad = 0;
   for (int e = tid; e < E; e += blockDim.x) hist[e] = 0;
-  __syncthreads();
   const int64_t M = n * R;
+  const int64_t nmine = n > cta ? (n - cta + ncta - 1) / ncta : 0;
+  const int64_t nown = nmine * R;
+  if (nown <= kMaxOwn) {
+    // Direct path: counts by shared atomics (order-free); the stable rank of
+    // each of this CTA's copies = number of earlier copies with its expert.
+    for (int k = tid; k < (int)nown; k += blockDim.x) {
+      const int64_t i = (cta + (int64_t)(k / R) * ncta) * R + (k % R);
+      const int64_t v = load_route(routes, i32, i);
+      sh.own_e[k] = (v >= 0 && v < E) ? (int)v : -1;
+      sh.own_rank[k] = 0;
+    }
+    __syncthreads();
+    for (int64_t i = tid; i < M; i += blockDim.x) {
+      const int64_t v = load_route(routes, i32, i);
+      if (v < 0 || v >= E) {
+        atomicOr(&sh.bad, TXB_EV_ROUTE_RANGE);
+        continue;
+      }
+      const int64_t t = i / R;
+      const int j = (int)(i - t * R);
+      for (int jj = 0; jj < j; ++jj)
+        if (load_route(routes, i32, t * R + jj) == v) atomicOr(&sh.bad, TXB_EV_ROUTE_DUP);
+      atomicAdd(&hist[(int)v], 1u);
+      for (int k = 0; k < (int)nown; ++k) {
+        const int64_t ik = (cta + (int64_t)(k / R) * ncta) * R + (k % R);
+        if (sh.own_e[k] == (int)v && i < ik) atomicAdd(&sh.own_rank[k], 1u);
+      }
+    }
+    __syncthreads();
+    for (int k = tid; k < (int)nown; k += blockDim.x) {
+      const int64_t i = (cta + (int64_t)(k / R) * ncta) * R + (k % R);
+      rank_out[i] = (int32_t)sh.own_rank[k];
+    }
+    const uint32_t b = sh.bad;
+    if (b)
+      for (int e = tid; e < E; e += blockDim.x) hist[e] = 0;
+    __syncthreads();
+    return b;
+  }
+  __syncthreads();
   for (int64_t base = 0; base < M; base += blockDim.x) {
     for (int i = tid; i < nwarps * E; i += blockDim.x) wc[i] = 0;
     __syncthreads();
@@ -159,9 +209,10 @@ __device__ void route_publish(const txb_moe_shape& s, void* const* peers, Flags*
                               uint64_t step, int64_t n, uint32_t bad) {
   const int E = s.experts, N = s.ranks, L = s.local_experts;
   const int slot = (int)(step & 1);
+  const uint64_t tag = (uint64_t)(uint32_t)step << 32;
   for (int idx = threadIdx.x; idx < N * E; idx += blockDim.x) {
     const int d = idx / E, e = idx - d * E;
-    route_of(peers[d], s, slot)[(size_t)s.me * E + e] = hist[e];
+    st_relaxed_sys(route_of(peers[d], s, slot) + (size_t)s.me * E + e, tag | hist[e]);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -169,23 +220,38 @@ __device__ void route_publish(const txb_moe_shape& s, void* const* peers, Flags*
     for (int le = 0; le < L; ++le) self += hist[s.me * L + le];
     f->comb_target += bad ? 0 : (uint64_t)(n * s.topk) - self;
     if (bad) atomicOr(&f->err, bad);
-    fence_acqrel_sys();
+    // per-source step tag for host-side gating/diagnostics only (the words
+    // above carry their own tags)
     for (int d = 0; d < N; ++d) st_relaxed_sys(&flags_of(peers[d], s)->route_tag[slot][s.me], step);
   }
 }
 
 // ------------------------------------------------------------------- P2
 
-__device__ bool wait_routes(const txb_moe_shape& s, Flags* f, uint64_t step, uint64_t timeout_ns, Shared& sh) {
+// Acquire every route word of this step (tag == step) into Cs[N*E] (shared
+// memory), and wait for every peer's end-of-previous-step barrier.
+__device__ bool wait_routes(const txb_moe_shape& s, Flags* f, const uint64_t* C, uint32_t* Cs, uint64_t step,
+                            uint64_t timeout_ns, Shared& sh) {
   if (threadIdx.x == 0) sh.fail = 0;
   __syncthreads();
-  if (threadIdx.x < 32) {
-    const int slot = (int)(step & 1);
-    const uint64_t dl = globaltimer() + timeout_ns;
-    for (int q = threadIdx.x; q < s.ranks; q += 32) {
-      if (!spin_ge(&f->route_tag[slot][q], step, dl)) atomicOr(&sh.fail, TXB_EV_WAIT_ROUTE);
-      if (!spin_ge(&f->done[q], step - 1, dl)) atomicOr(&sh.fail, TXB_EV_WAIT_BARRIER);
+  const uint64_t dl = globaltimer() + timeout_ns;
+  const uint32_t want = (uint32_t)step;
+  const int NE = s.ranks * s.experts;
+  for (int i = threadIdx.x; i < NE; i += blockDim.x) {
+    uint64_t v = ld_relaxed_sys(C + i);
+    uint32_t it = 0;
+    while ((uint32_t)(v >> 32) != want) {
+      if (((++it) & 255u) == 0 && globaltimer() > dl) {
+        atomicOr(&sh.fail, TXB_EV_WAIT_ROUTE);
+        break;
+      }
+      v = ld_relaxed_sys(C + i);
     }
+    Cs[i] = (uint32_t)v;
+  }
+  if (threadIdx.x < 32) {
+    for (int q = threadIdx.x; q < s.ranks; q += 32)
+      if (!spin_ge(&f->done[q], step - 1, dl)) atomicOr(&sh.fail, TXB_EV_WAIT_BARRIER);
   }
   __syncthreads();
   const uint32_t fl = sh.fail;
@@ -214,7 +280,7 @@ __device__ bool dispatch_layout(const txb_moe_shape& s, const uint32_t* C, int64
     }
     padded[e] = pad_up(col);
     baseg[e] = pre;
-    if (book && e / L == s.me) atomicAdd(&sh.recv_me, (unsigned long long)col);
+    if (book && e / L == s.me) atomicAdd(&sh.recv_me, (uint32_t)col);
   }
   __syncthreads();
   const int64_t tot = block_excl_scan<int64_t>(padded, E, sh.tmp);
@@ -278,7 +344,7 @@ __device__ void signal_counts(const txb_moe_shape& s, void* const* peers, size_t
     bool any = false;
     for (int d = 0; d < s.ranks; ++d) any |= sh.cnt[d] != 0;
     if (any) {
-      fence_acqrel_sys();
+      fence_release(s.single_device);
       for (int d = 0; d < s.ranks; ++d)
         if (sh.cnt[d])
           red_relaxed_sys_add(reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(flags_of(peers[d], s)) + field),
@@ -310,13 +376,17 @@ __device__ void recv_metadata(const txb_moe_shape& s, const uint32_t* C, int64_t
     a[i] = C[(size_t)q * E + me * L + le];
     rowbase[i] = a[i];
   }
-  for (int q = tid; q < N; q += nt) pre_all[q] = 0;
   __syncthreads();
-  if (me > 0)
-    for (int i = tid; i < N * me * L; i += nt) {
-      const int q = i / (me * L), e = i - q * (me * L);
-      atomicAdd((unsigned long long*)&pre_all[q], (unsigned long long)C[(size_t)q * E + e]);
+  {
+    const int warp = tid >> 5, lane = tid & 31, nwarp = nt >> 5;
+    for (int q = warp; q < N; q += nwarp) {
+      int64_t acc = 0;
+      for (int e = lane; e < me * L; e += 32) acc += C[(size_t)q * E + e];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) pre_all[q] = acc;
     }
+  }
   for (int le = tid; le < L; le += nt) {
     int64_t run = 0;
     for (int q = 0; q < N; ++q) {
@@ -433,7 +503,7 @@ __device__ void end_of_step(const txb_moe_shape& s, void* const* peers, Flags* f
     if (t == (uint32_t)ncta - 1) {
       f->ticket = 0;
       *reinterpret_cast<volatile uint64_t*>(&f->step) = step;
-      fence_acqrel_sys();
+      fence_release(s.single_device);
       for (int q = 0; q < s.ranks; ++q) st_relaxed_sys(&flags_of(peers[q], s)->done[s.me], step);
     }
   }
@@ -462,9 +532,9 @@ k_dispatch(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, int64_t 
   __shared__ Shared sh;
   Flags* f = flags_of(b.region, s);
   const uint64_t step = cur_step(f);
-  if (!wait_routes(s, f, step, timeout_ns, sh)) return;
+  uint32_t* C = reinterpret_cast<uint32_t*>(dsm + cmat_offset(s));
+  if (!wait_routes(s, f, route_of(b.region, s, (int)(step & 1)), C, step, timeout_ns, sh)) return;
   int64_t* baseg = reinterpret_cast<int64_t*>(dsm);
-  const uint32_t* C = route_of(b.region, s, (int)(step & 1));
   if (!dispatch_layout(s, C, baseg, baseg + s.experts, f, blockIdx.x == 0, sh)) return;
   dispatch_tokens<SRC, ELEM>(s, x, n, routes, i32, b.rank_scratch, b.gidx, b.peers, baseg, blockIdx.x,
                              gridDim.x, sh);
@@ -477,8 +547,10 @@ k_recv(txb_moe_shape s, txb_moe_bufs b, uint64_t timeout_ns) {
   __shared__ Shared sh;
   Flags* f = flags_of(b.region, s);
   const uint64_t step = cur_step(f);
-  recv_metadata(s, route_of(b.region, s, (int)(step & 1)), reinterpret_cast<int64_t*>(dsm), b.rows, b.sources,
-                b.ret_slot, b.info, grouped_of(b.region, s), blockIdx.x, gridDim.x, sh);
+  uint32_t* C = reinterpret_cast<uint32_t*>(dsm + cmat_offset(s));
+  if (!wait_routes(s, f, route_of(b.region, s, (int)(step & 1)), C, step, timeout_ns, sh)) return;
+  recv_metadata(s, C, reinterpret_cast<int64_t*>(dsm), b.rows, b.sources, b.ret_slot, b.info,
+                grouped_of(b.region, s), blockIdx.x, gridDim.x, sh);
   if (blockIdx.x == 0) wait_tokens(f, b.info, s.local_experts, timeout_ns);
 }
 
@@ -526,10 +598,10 @@ k_dispatch_fused(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
   route_positions(s, routes, i32, n, hist, reinterpret_cast<int64_t*>(wc), b.rank_scratch, b.pos, bad, cta,
                   ncta, sh);
   stamp(b, 2);
-  if (!wait_routes(s, f, step, timeout_ns, sh)) return;
+  uint32_t* C = reinterpret_cast<uint32_t*>(dsm + cmat_offset(s));
+  if (!wait_routes(s, f, route_of(b.region, s, (int)(step & 1)), C, step, timeout_ns, sh)) return;
   stamp(b, 3);
   int64_t* baseg = reinterpret_cast<int64_t*>(dsm);
-  const uint32_t* C = route_of(b.region, s, (int)(step & 1));
   if (!dispatch_layout(s, C, baseg, baseg + s.experts, f, cta == 0, sh)) return;
   stamp(b, 4);
   dispatch_tokens<SRC, ELEM>(s, x, n, routes, i32, b.rank_scratch, b.gidx, b.peers, baseg, cta, ncta, sh);
@@ -620,10 +692,10 @@ static int check(const txb_moe_shape* s, const txb_moe_bufs* b) {
   return TXB_OK;
 }
 
+// dynamic shared memory: [layout | recv scratch][route matrix copy], with
+// the route-count phase (before the matrix is loaded) overlapping both
 static size_t smem_main(const txb_moe_shape* s, bool route) {
-  size_t m = smem_layout(s->experts);
-  const size_t r = smem_recv(s->ranks, s->local_experts);
-  if (r > m) m = r;
+  size_t m = cmat_offset(*s) + smem_cmat(s->ranks, s->experts);
   if (route) {
     const size_t q = smem_route(s->experts, kThreads / 32);
     if (q > m) m = q;
@@ -704,6 +776,10 @@ int txb_moe_plan(txb_moe_shape* s) {
   }
   if (s->topk > kMaxTopk) { set_error("topk %d above the supported %d", s->topk, kMaxTopk); return TXB_ERR_PROTOCOL; }
   if (s->experts > kMaxExperts) { set_error("expert count %d above the supported %d", s->experts, kMaxExperts); return TXB_ERR_PROTOCOL; }
+  if ((int64_t)s->ranks * s->experts > 16384) {
+    set_error("ranks*experts %lld above the supported 16384", (long long)s->ranks * s->experts);
+    return TXB_ERR_PROTOCOL;
+  }
   if (s->me < 0 || s->me >= s->ranks) { set_error("rank %d outside 0..%d", s->me, s->ranks - 1); return TXB_ERR_PROTOCOL; }
   const int64_t N = s->ranks, T = s->max_tokens, R = s->topk;
   s->local_experts = s->experts / s->ranks;
@@ -718,7 +794,7 @@ int txb_moe_plan(txb_moe_shape* s) {
   s->off_flags = off;
   off = align_up(off + sizeof(Flags), 4096);
   s->off_route = off;
-  off = align_up(off + 2ull * N * s->experts * 4, 4096);
+  off = align_up(off + 2ull * N * s->experts * 8, 4096);
   s->off_grouped = off;
   off = align_up(off + (uint64_t)s->grouped_rows * s->payload_bytes, 4096);
   s->off_comb = off;
@@ -765,7 +841,7 @@ int txb_moe_dispatch(const txb_moe_shape* s, const txb_moe_bufs* b, const void* 
     const int64_t g = n < 1 ? 1 : n;
     grid = (int)(g < 4 * sm_count(s->device) ? g : 4 * sm_count(s->device));
   }
-  const size_t smem = smem_layout(s->experts);
+  const size_t smem = smem_main(s, false);
   cudaStream_t st = (cudaStream_t)stream;
 #define TXB_D(SRC, ELEM) \
   return launch(k_dispatch<SRC, ELEM>, grid, kThreads, smem, st, false, *s, *b, x, n, routes, routes_i32, timeout_ns)
@@ -777,7 +853,7 @@ int txb_moe_dispatch(const txb_moe_shape* s, const txb_moe_bufs* b, const void* 
 int txb_moe_dispatch_recv(const txb_moe_shape* s, const txb_moe_bufs* b, uint64_t timeout_ns, void* stream) {
   if (int rc = check(s, b)) return rc;
   TXB_CUDA(cudaSetDevice(s->device));
-  const size_t smem = smem_recv(s->ranks, s->local_experts);
+  const size_t smem = smem_main(s, false);
   const int64_t wpb = kThreads / 32;
   int grid = (int)((s->grouped_rows + wpb - 1) / wpb);
   if (grid > sm_count(s->device)) grid = sm_count(s->device);

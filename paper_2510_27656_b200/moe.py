@@ -403,8 +403,8 @@ class MoeRank:
         self._info = torch.zeros(2 * L + 3, dtype=torch.int64, device=dev)
         self._info_host = torch.zeros(2 * L + 3, dtype=torch.int64).pin_memory()
         self._grouped = self.region.tensor(int(sh.off_grouped), (G, int(sh.payload_bytes)), torch.uint8)
-        self._route_views = [self.region.tensor(int(sh.off_route) + k * spec.ranks * spec.experts * 4,
-                                                (spec.ranks, spec.experts), torch.int32) for k in (0, 1)]
+        self._route_views = [self.region.tensor(int(sh.off_route) + k * spec.ranks * spec.experts * 8,
+                                                (spec.ranks, spec.experts), torch.int64) for k in (0, 1)]
         self._peer_regions: list[Region] = []
         self._peer_ptrs: list[int] = []
         self._peer_table: torch.Tensor | None = None
@@ -425,12 +425,13 @@ class MoeRank:
 
     # -------------------------------------------------------------- wiring
 
-    def _set_peers(self, ptrs: Sequence[int], gated: bool) -> None:
+    def _set_peers(self, ptrs: Sequence[int], gated: bool, single_device: bool = False) -> None:
         self._peer_ptrs = [int(p) for p in ptrs]
         self._peer_table = torch.tensor(self._peer_ptrs, dtype=torch.int64,
                                         device=torch.device("cuda", self.device))
         self._peer_table_p = C.c_void_p(self._peer_table.data_ptr())
         self.host_gated = gated
+        self._shape.single_device = 1 if single_device else 0
         b = self._bufs
         b.region = self.region.ptr
         b.peers = self._peer_table.data_ptr()
@@ -446,7 +447,8 @@ class MoeRank:
         """In-process wiring: peers are addressed directly (peer access)."""
         devs = [m.device for m in mesh]
         gated = len(set(devs)) < len(devs)
-        self._set_peers([m.region.ptr for m in sorted(mesh, key=lambda m: m.rank)], gated)
+        self._set_peers([m.region.ptr for m in sorted(mesh, key=lambda m: m.rank)], gated,
+                        single_device=len(set(devs)) == 1)
 
     @property
     def peer_ptrs(self) -> list[int]:
@@ -652,7 +654,7 @@ class MoeRank:
         """Layout of the most recent step, from the device route matrix."""
         if self._step_no == 0:
             return None
-        m = self._route_views[self._step_no & 1].cpu().numpy().astype(np.int64)
+        m = self._route_views[self._step_no & 1].cpu().numpy() & 0xFFFFFFFF
         return compute_layout(self.spec, m)
 
     # ------------------------------------------------------------- combine

@@ -56,3 +56,8 @@ for k, nm in enumerate(names):
     col = col[col > 0] - t0
     if col.size:
         print(f"{nm:12s} min {col.min()/1e3:8.2f}us  med {np.median(col)/1e3:8.2f}us  max {col.max()/1e3:8.2f}us  n={col.size}")
+
+for k in (3, 4, 5, 6, 7, 8):
+    col = p[:, k] - t0
+    idx = np.argsort(-col)[:4]
+    print(names[k], "slowest CTAs", [(int(i), round(col[i] / 1e3, 2)) for i in idx])
