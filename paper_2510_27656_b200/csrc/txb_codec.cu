@@ -6,7 +6,7 @@
 namespace txb {
 
 template <int SRC, int ELEM>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 1)
 k_encode_rows(const void* __restrict__ x, int64_t n, int H, int scales, int64_t P, uint8_t* __restrict__ out) {
   __shared__ float red[33];
   __shared__ uint8_t* dst[1];
@@ -19,7 +19,7 @@ k_encode_rows(const void* __restrict__ x, int64_t n, int H, int scales, int64_t 
 }
 
 template <int ELEM>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 1)
 k_decode_rows(const uint8_t* __restrict__ rows, int64_t n, int H, int64_t P, float* __restrict__ out) {
   for (int64_t t = blockIdx.x; t < n; t += gridDim.x) {
     const uint8_t* r = rows + t * P;
@@ -45,7 +45,7 @@ k_decode_rows(const uint8_t* __restrict__ rows, int64_t n, int H, int64_t P, flo
   }
 }
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 1)
 k_pack_rows(const uint8_t* __restrict__ src, int64_t width, const int64_t* __restrict__ rows, int64_t k,
             uint8_t* __restrict__ out) {
   const int lane = threadIdx.x & 31;
@@ -54,7 +54,7 @@ k_pack_rows(const uint8_t* __restrict__ src, int64_t width, const int64_t* __res
     copy_row(out + i * width, src + rows[i] * width, width, lane, 32);
 }
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 1)
 k_weighted_combine(const float* __restrict__ y, int64_t hidden, const int64_t* __restrict__ pos,
                    const float* __restrict__ w, int64_t n, int topk, float* __restrict__ out) {
   combine_rows<4>(reinterpret_cast<const uint8_t*>(y), hidden * 4, nullptr, 0, (int)hidden, pos, nullptr, w, n,

@@ -79,13 +79,14 @@ __host__ __device__ inline size_t smem_recv(int N, int L) {
 constexpr int kMaxOwn = 64;  // copies per CTA handled by the direct-count rank path
 
 struct Shared {  // static shared state of one CTA
-  uint32_t bad, fail, recv_me;
+  uint32_t bad, fail, recv_me, direct;
   int64_t tmp[33];
   float red[33];
   uint32_t cnt[TXB_MAX_RANKS];
   uint8_t* dstp[kMaxTopk];
   uint32_t own_rank[kMaxOwn];
   int32_t own_e[kMaxOwn];
+  int32_t own_i[kMaxOwn];
 };
 
 // ------------------------------------------------------------------- P1
@@ -100,42 +101,42 @@ __device__ uint32_t route_counts(const txb_moe_shape& s, const void* routes, int
                                  Shared& sh) {
   const int E = s.experts, R = s.topk;
   const int tid = threadIdx.x, warp = tid >> 5, nwarps = blockDim.x >> 5;
-  if (tid == 0) sh.bad = 0;
+  if (tid == 0) {
+    sh.bad = 0;
+    sh.direct = 0;
+  }
   for (int e = tid; e < E; e += blockDim.x) hist[e] = 0;
   const int64_t M = n * R;
   const int64_t nmine = n > cta ? (n - cta + ncta - 1) / ncta : 0;
   const int64_t nown = nmine * R;
-  if (nown <= kMaxOwn) {
+  if (nown <= kMaxOwn && M < (1LL << 30)) {
     // Direct path: counts by shared atomics (order-free); the stable rank of
     // each of this CTA's copies = number of earlier copies with its expert.
-    for (int k = tid; k < (int)nown; k += blockDim.x) {
-      const int64_t i = (cta + (int64_t)(k / R) * ncta) * R + (k % R);
+    const int m = (int)M, nw = (int)nown;
+    for (int k = tid; k < nw; k += blockDim.x) {
+      const int i = (cta + (k / R) * ncta) * R + (k % R);
       const int64_t v = load_route(routes, i32, i);
       sh.own_e[k] = (v >= 0 && v < E) ? (int)v : -1;
+      sh.own_i[k] = i;
       sh.own_rank[k] = 0;
     }
     __syncthreads();
-    for (int64_t i = tid; i < M; i += blockDim.x) {
+    for (int i = tid; i < m; i += blockDim.x) {
       const int64_t v = load_route(routes, i32, i);
       if (v < 0 || v >= E) {
         atomicOr(&sh.bad, TXB_EV_ROUTE_RANGE);
         continue;
       }
-      const int64_t t = i / R;
-      const int j = (int)(i - t * R);
+      const int j = i % R, t0 = i - j;
       for (int jj = 0; jj < j; ++jj)
-        if (load_route(routes, i32, t * R + jj) == v) atomicOr(&sh.bad, TXB_EV_ROUTE_DUP);
+        if (load_route(routes, i32, t0 + jj) == v) atomicOr(&sh.bad, TXB_EV_ROUTE_DUP);
       atomicAdd(&hist[(int)v], 1u);
-      for (int k = 0; k < (int)nown; ++k) {
-        const int64_t ik = (cta + (int64_t)(k / R) * ncta) * R + (k % R);
-        if (sh.own_e[k] == (int)v && i < ik) atomicAdd(&sh.own_rank[k], 1u);
-      }
+      for (int k = 0; k < nw; ++k)
+        if (sh.own_e[k] == (int)v && i < sh.own_i[k]) atomicAdd(&sh.own_rank[k], 1u);
     }
     __syncthreads();
-    for (int k = tid; k < (int)nown; k += blockDim.x) {
-      const int64_t i = (cta + (int64_t)(k / R) * ncta) * R + (k % R);
-      rank_out[i] = (int32_t)sh.own_rank[k];
-    }
+    for (int k = tid; k < nw; k += blockDim.x) rank_out[sh.own_i[k]] = (int32_t)sh.own_rank[k];
+    if (tid == 0) sh.direct = 1;
     const uint32_t b = sh.bad;
     if (b)
       for (int e = tid; e < E; e += blockDim.x) hist[e] = 0;
@@ -206,14 +207,16 @@ __device__ void route_positions(const txb_moe_shape& s, const void* routes, int 
 // release fence, then the step tag (single writer per slot).  Also books
 // the number of copies that will come back from other ranks.
 __device__ void route_publish(const txb_moe_shape& s, void* const* peers, Flags* f, const uint32_t* hist,
-                              uint64_t step, int64_t n, uint32_t bad) {
+                              uint64_t step, int64_t n, uint32_t bad, int part, int nparts) {
   const int E = s.experts, N = s.ranks, L = s.local_experts;
   const int slot = (int)(step & 1);
   const uint64_t tag = (uint64_t)(uint32_t)step << 32;
-  for (int idx = threadIdx.x; idx < N * E; idx += blockDim.x) {
+  // every CTA holds the full histogram; CTA `part` stores its slice
+  for (int idx = part * blockDim.x + threadIdx.x; idx < N * E; idx += nparts * blockDim.x) {
     const int d = idx / E, e = idx - d * E;
     st_relaxed_sys(route_of(peers[d], s, slot) + (size_t)s.me * E + e, tag | hist[e]);
   }
+  if (part != 0) return;
   __syncthreads();
   if (threadIdx.x == 0) {
     uint64_t self = 0;
@@ -304,22 +307,34 @@ __device__ bool dispatch_layout(const txb_moe_shape& s, const uint32_t* C, int64
 template <int SRC, int ELEM>
 __device__ void dispatch_tokens(const txb_moe_shape& s, const void* x, int64_t n, const void* routes, int i32,
                                 const int32_t* rank_in, int32_t* gidx, void* const* peers, const int64_t* baseg,
-                                int cta, int ncta, Shared& sh) {
+                                int cta, int ncta, Shared& sh, const RowRegs* pre) {
   const int N = s.ranks, L = s.local_experts, R = s.topk, tid = threadIdx.x;
   const int64_t P = s.payload_bytes;
+  const bool direct = sh.direct != 0;
   for (int q = tid; q < N; q += blockDim.x) sh.cnt[q] = 0;
   __syncthreads();
-  for (int64_t t = cta; t < n; t += ncta) {
+  int kt = 0;
+  for (int64_t t = cta; t < n; t += ncta, ++kt) {
     if (tid < R) {
-      const int e = (int)load_route(routes, i32, t * R + tid);
+      int e;
+      int64_t rank;
+      if (direct) {  // ranks and experts of this CTA's copies are already in smem
+        e = sh.own_e[kt * R + tid];
+        rank = sh.own_rank[kt * R + tid];
+      } else {
+        e = (int)load_route(routes, i32, t * R + tid);
+        rank = rank_in[t * R + tid];
+      }
       const int d = e / L;
-      const int64_t g = baseg[e] + rank_in[t * R + tid];
+      const int64_t g = baseg[e] + rank;
       sh.dstp[tid] = grouped_of(peers[d], s) + g * P;
       gidx[t * R + tid] = d == s.me ? (int32_t)g : -1;
       atomicAdd(&sh.cnt[d], 1u);
     }
     __syncthreads();
-    if constexpr (SRC == TXB_SRC_ROWS) {
+    if (pre && pre->ok && kt == 0) {
+      store_row_regs<SRC, ELEM>(*pre, s.hidden, s.scales, sh.dstp, R);
+    } else if constexpr (SRC == TXB_SRC_ROWS) {
       const uint8_t* src = reinterpret_cast<const uint8_t*>(x) + t * P;
       if (vec_width(src, sh.dstp[0], P) == 16) {
         for (int64_t v = tid; v < (P >> 4); v += blockDim.x) {
@@ -521,11 +536,11 @@ k_route(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ routes, int i3
   const uint64_t step = cur_step(f);
   const uint32_t bad = route_counts(s, routes, i32, n, hist, wc, b.rank_scratch, 0, 1, sh);
   route_positions(s, routes, i32, n, hist, reinterpret_cast<int64_t*>(wc), b.rank_scratch, b.pos, bad, 0, 1, sh);
-  route_publish(s, b.peers, f, hist, step, n, bad);
+  route_publish(s, b.peers, f, hist, step, n, bad, 0, 1);
 }
 
 template <int SRC, int ELEM>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 1)
 k_dispatch(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, int64_t n, const void* __restrict__ routes,
            int i32, uint64_t timeout_ns) {
   extern __shared__ __align__(16) uint8_t dsm[];
@@ -536,12 +551,15 @@ k_dispatch(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, int64_t 
   if (!wait_routes(s, f, route_of(b.region, s, (int)(step & 1)), C, step, timeout_ns, sh)) return;
   int64_t* baseg = reinterpret_cast<int64_t*>(dsm);
   if (!dispatch_layout(s, C, baseg, baseg + s.experts, f, blockIdx.x == 0, sh)) return;
+  if (*reinterpret_cast<volatile uint32_t*>(&f->err) & (TXB_EV_ROUTE_RANGE | TXB_EV_ROUTE_DUP)) return;
+  if (threadIdx.x == 0) sh.direct = 0;
+  __syncthreads();
   dispatch_tokens<SRC, ELEM>(s, x, n, routes, i32, b.rank_scratch, b.gidx, b.peers, baseg, blockIdx.x,
-                             gridDim.x, sh);
+                             gridDim.x, sh, nullptr);
   signal_counts(s, b.peers, offsetof(Flags, tok_ctr), sh);
 }
 
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 1)
 k_recv(txb_moe_shape s, txb_moe_bufs b, uint64_t timeout_ns) {
   extern __shared__ __align__(16) uint8_t dsm[];
   __shared__ Shared sh;
@@ -554,7 +572,7 @@ k_recv(txb_moe_shape s, txb_moe_bufs b, uint64_t timeout_ns) {
   if (blockIdx.x == 0) wait_tokens(f, b.info, s.local_experts, timeout_ns);
 }
 
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 1)
 k_comb_send(txb_moe_shape s, txb_moe_bufs b, const uint8_t* __restrict__ out, int64_t ld) {
   __shared__ Shared sh;
   combine_send_rows(s, out, ld, b.peers, b.sources, b.ret_slot, b.info, blockIdx.x, gridDim.x, sh);
@@ -562,7 +580,7 @@ k_comb_send(txb_moe_shape s, txb_moe_bufs b, const uint8_t* __restrict__ out, in
 }
 
 template <int ELEM>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 1)
 k_comb_recv(txb_moe_shape s, txb_moe_bufs b, const uint8_t* __restrict__ out, int64_t ld,
             const float* __restrict__ w, int64_t n, void* dst, int out_bf16, uint64_t timeout_ns) {
   __shared__ Shared sh;
@@ -581,7 +599,7 @@ k_comb_recv(txb_moe_shape s, txb_moe_bufs b, const uint8_t* __restrict__ out, in
 // derives the layout, stores its tokens, signals, then the grid fills the
 // receive metadata and CTA 0 waits for the incoming rows.
 template <int SRC, int ELEM>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 1)
 k_dispatch_fused(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, int64_t n,
                  const void* __restrict__ routes, int i32, uint64_t timeout_ns) {
   extern __shared__ __align__(16) uint8_t dsm[];
@@ -592,9 +610,15 @@ k_dispatch_fused(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
   uint32_t* hist = reinterpret_cast<uint32_t*>(dsm);
   uint32_t* wc = hist + ((s.experts + 3) & ~3);
   stamp(b, 0);
+  // decode-sized batches (one token per CTA): read + encode the token now,
+  // before the route exchange, and keep it in registers until the layout
+  // is known
+  RowRegs pre;
+  pre.ok = false;
+  if (n == ncta) encode_row_regs<SRC, ELEM>(x, cta, s.hidden, s.payload_bytes, pre, sh.red);
   const uint32_t bad = route_counts(s, routes, i32, n, hist, wc, b.rank_scratch, cta, ncta, sh);
   stamp(b, 1);
-  if (cta == 0) route_publish(s, b.peers, f, hist, step, n, bad);
+  route_publish(s, b.peers, f, hist, step, n, bad, cta, ncta);
   route_positions(s, routes, i32, n, hist, reinterpret_cast<int64_t*>(wc), b.rank_scratch, b.pos, bad, cta,
                   ncta, sh);
   stamp(b, 2);
@@ -604,7 +628,8 @@ k_dispatch_fused(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
   int64_t* baseg = reinterpret_cast<int64_t*>(dsm);
   if (!dispatch_layout(s, C, baseg, baseg + s.experts, f, cta == 0, sh)) return;
   stamp(b, 4);
-  dispatch_tokens<SRC, ELEM>(s, x, n, routes, i32, b.rank_scratch, b.gidx, b.peers, baseg, cta, ncta, sh);
+  if (!bad) dispatch_tokens<SRC, ELEM>(s, x, n, routes, i32, b.rank_scratch, b.gidx, b.peers, baseg, cta, ncta, sh,
+                                       &pre);
   stamp(b, 5);
   signal_counts(s, b.peers, offsetof(Flags, tok_ctr), sh);
   __syncthreads();
@@ -618,7 +643,7 @@ k_dispatch_fused(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
 
 // Combine send + reduce in one cooperative launch.
 template <int ELEM>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 1)
 k_combine_fused(txb_moe_shape s, txb_moe_bufs b, const uint8_t* __restrict__ out, int64_t ld,
                 const float* __restrict__ w, int64_t n, void* dst, int out_bf16, uint64_t timeout_ns) {
   __shared__ Shared sh;

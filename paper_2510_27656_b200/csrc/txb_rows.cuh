@@ -183,6 +183,85 @@ __device__ void encode_store_row(const void* x, int64_t t, int H, int scales, in
   }
 }
 
+// Pre-encoded row held in registers: thread `tid` owns 16-byte chunks
+// c = tid and c = tid + blockDim.x of the wire row.  Lets a kernel read and
+// encode its token before the layout is known and store it afterwards.
+struct RowRegs {
+  uint4 c[2];
+  float scale;
+  int nchunk;  // chunks of the data part (values) or of the whole row (raw)
+  bool ok;     // false: shape not eligible, use encode_store_row later
+};
+
+template <int SRC, int ELEM>
+__device__ void encode_row_regs(const void* x, int64_t t, int H, int64_t P, RowRegs& r, float* red) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  r.ok = false;
+  r.scale = 1.0f;
+  if constexpr (SRC == TXB_SRC_ROWS) {
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(x) + t * P;
+    r.nchunk = (int)(P >> 4);
+    if ((P & 15) || (reinterpret_cast<uintptr_t>(src) & 15) || r.nchunk > 2 * nt) return;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int c = tid + u * nt;
+      if (c < r.nchunk) r.c[u] = reinterpret_cast<const uint4*>(src)[c];
+    }
+    r.ok = true;
+  } else {
+    constexpr int EPC = 16 / ELEM;
+    const int64_t rowoff = t * (int64_t)H;
+    const int64_t srcbytes = (SRC == TXB_SRC_F32 ? 4 : 2);
+    const int64_t salign = (EPC * srcbytes) >= 16 ? 16 : EPC * srcbytes;
+    r.nchunk = H / EPC;
+    if (((H * ELEM) % 16) || (P % 16) || r.nchunk > 2 * nt ||
+        ((reinterpret_cast<uintptr_t>(x) + rowoff * srcbytes) % salign))
+      return;
+    float v[2][EPC];
+    float amax = 0.f;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int c = tid + u * nt;
+      if (c < r.nchunk) {
+        load_vals<SRC>(x, rowoff + (int64_t)c * EPC, v[u], EPC);
+        if constexpr (ELEM == 1) {
+#pragma unroll
+          for (int k = 0; k < EPC; ++k)
+            if (isfinite(v[u][k])) amax = fmaxf(amax, fabsf(v[u][k]));
+        }
+      }
+    }
+    if constexpr (ELEM == 1) {
+      amax = block_max(amax, red);
+      r.scale = amax > 0.f ? __fdiv_rn(amax, 448.0f) : 1.0f;  // kernels.py:133-134
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int c = tid + u * nt;
+      if (c < r.nchunk) r.c[u] = encode_chunk<ELEM>(v[u], r.scale);
+    }
+    r.ok = true;
+  }
+}
+
+// Store a RowRegs row to nd destination rows (plus the scale slots).
+template <int SRC, int ELEM>
+__device__ void store_row_regs(const RowRegs& r, int H, int scales, uint8_t* const* dst, int nd) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int c = tid + u * nt;
+    if (c < r.nchunk)
+      for (int j = 0; j < nd; ++j) reinterpret_cast<uint4*>(dst[j])[c] = r.c[u];
+  }
+  if constexpr (SRC != TXB_SRC_ROWS) {
+    const int64_t d0 = (int64_t)H * ELEM;  // 16-byte aligned on this path
+    const uint32_t sbits = ELEM == 1 ? __float_as_uint(r.scale) : 0u;
+    for (int b = tid; b < scales; b += nt)
+      for (int j = 0; j < nd; ++j) reinterpret_cast<uint32_t*>(dst[j] + d0)[b] = b == 0 ? sbits : 0u;
+  }
+}
+
 // ----------------------------------------------------------------- combine
 
 // Raw 8-element chunk of one wire row, loaded before any arithmetic so the
