@@ -114,6 +114,7 @@ typedef struct txb_moe_bufs {
   int64_t* sources;      /* [grouped_rows] GroupedTokens.sources (moe.py:281) */
   int32_t* ret_slot;     /* [grouped_rows] combine return slot on the source */
   int64_t* info;         /* [2L+3] group_sizes, group_starts, padded_total, recv_total, error word */
+  uint8_t* dirty;        /* [grouped_rows] 1 = row may hold data (zeroed when it becomes padding) */
   uint64_t* prof;        /* optional [grid][16] %globaltimer phase stamps (NULL = off) */
 } txb_moe_bufs;
 

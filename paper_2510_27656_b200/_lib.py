@@ -58,7 +58,7 @@ class Bufs(C.Structure):
     _fields_ = [("region", C.c_void_p), ("peers", C.c_void_p), ("rank_scratch", C.c_void_p),
                 ("pos", C.c_void_p), ("gidx", C.c_void_p), ("rows", C.c_void_p),
                 ("sources", C.c_void_p), ("ret_slot", C.c_void_p), ("info", C.c_void_p),
-                ("prof", C.c_void_p)]
+                ("dirty", C.c_void_p), ("prof", C.c_void_p)]
 
 
 _VP = C.c_void_p

@@ -121,15 +121,29 @@ __device__ uint32_t route_counts(const txb_moe_shape& s, const void* routes, int
       sh.own_rank[k] = 0;
     }
     __syncthreads();
-    for (int i = tid; i < m; i += blockDim.x) {
-      const int64_t v = load_route(routes, i32, i);
+    // when R divides 32 a token's copies sit in consecutive lanes of one
+    // warp, so the duplicate check is R-1 shuffles instead of R-1 loads
+    const bool lanes = (32 % R) == 0;
+    for (int base = 0; base < m; base += blockDim.x) {
+      const int i = base + tid;
+      const bool valid = i < m;
+      const int64_t v = valid ? load_route(routes, i32, i) : -1;
+      const int j = i % R;
+      bool dup = false;
+      if (lanes) {
+        for (int jj = 1; jj < R; ++jj) {
+          const int64_t u = __shfl_up_sync(0xffffffffu, v, jj);
+          dup |= (jj <= j) && (u == v);
+        }
+      } else if (valid) {
+        for (int jj = 1; jj <= j; ++jj) dup |= load_route(routes, i32, i - jj) == v;
+      }
+      if (!valid) continue;
       if (v < 0 || v >= E) {
         atomicOr(&sh.bad, TXB_EV_ROUTE_RANGE);
         continue;
       }
-      const int j = i % R, t0 = i - j;
-      for (int jj = 0; jj < j; ++jj)
-        if (load_route(routes, i32, t0 + jj) == v) atomicOr(&sh.bad, TXB_EV_ROUTE_DUP);
+      if (dup) atomicOr(&sh.bad, TXB_EV_ROUTE_DUP);
       atomicAdd(&hist[(int)v], 1u);
       for (int k = 0; k < nw; ++k)
         if (sh.own_e[k] == (int)v && i < sh.own_i[k]) atomicAdd(&sh.own_rank[k], 1u);
@@ -375,8 +389,8 @@ __device__ void signal_counts(const txb_moe_shape& s, void* const* peers, size_t
 // walks the grouped rows, one warp per row (lane 0 writes rows / sources /
 // return slot, the warp zero-fills padding rows).
 __device__ void recv_metadata(const txb_moe_shape& s, const uint32_t* C, int64_t* sm, int64_t* rows,
-                              int64_t* sources, int32_t* ret, int64_t* info, uint8_t* G, int cta, int ncta,
-                              Shared& sh) {
+                              int64_t* sources, int32_t* ret, int64_t* info, uint8_t* G, uint8_t* dirty, int cta,
+                              int ncta, Shared& sh) {
   const int N = s.ranks, E = s.experts, L = s.local_experts, me = s.me;
   const int tid = threadIdx.x, nt = blockDim.x;
   int64_t* a = sm;                         // [N][L] counts into my experts
@@ -445,13 +459,18 @@ __device__ void recv_metadata(const txb_moe_shape& s, const uint32_t* C, int64_t
     const int le = lo;
     const int64_t k = g - gstart[le];
     if (k >= gsize[le]) {
+      // padding rows read as zero (moe.py:719); only rows that held data since
+      // they were last zeroed need the store
+      const bool d = dirty[g] != 0;
+      if (d) zero_row(G + g * P, P, lane, 32);
       if (lane == 0) {
         rows[g] = -1;
         sources[g] = -1;
         ret[g] = -1;
+        if (d) dirty[g] = 0;
       }
-      zero_row(G + g * P, P, lane, 32);  // padding rows are zero (moe.py:719)
     } else if (lane == 0) {
+      dirty[g] = 1;
       const int64_t* sp = srcpre + le * (N + 1);
       int q = 0;
       while (sp[q + 1] <= k) ++q;
@@ -568,7 +587,7 @@ k_recv(txb_moe_shape s, txb_moe_bufs b, uint64_t timeout_ns) {
   uint32_t* C = reinterpret_cast<uint32_t*>(dsm + cmat_offset(s));
   if (!wait_routes(s, f, route_of(b.region, s, (int)(step & 1)), C, step, timeout_ns, sh)) return;
   recv_metadata(s, C, reinterpret_cast<int64_t*>(dsm), b.rows, b.sources, b.ret_slot, b.info,
-                grouped_of(b.region, s), blockIdx.x, gridDim.x, sh);
+                grouped_of(b.region, s), b.dirty, blockIdx.x, gridDim.x, sh);
   if (blockIdx.x == 0) wait_tokens(f, b.info, s.local_experts, timeout_ns);
 }
 
@@ -616,6 +635,7 @@ k_dispatch_fused(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
   RowRegs pre;
   pre.ok = false;
   if (n == ncta) encode_row_regs<SRC, ELEM>(x, cta, s.hidden, s.payload_bytes, pre, sh.red);
+  stamp(b, 14);
   const uint32_t bad = route_counts(s, routes, i32, n, hist, wc, b.rank_scratch, cta, ncta, sh);
   stamp(b, 1);
   route_publish(s, b.peers, f, hist, step, n, bad, cta, ncta);
@@ -635,7 +655,7 @@ k_dispatch_fused(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
   __syncthreads();
   stamp(b, 6);
   recv_metadata(s, C, reinterpret_cast<int64_t*>(dsm), b.rows, b.sources, b.ret_slot, b.info,
-                grouped_of(b.region, s), cta, ncta, sh);
+                grouped_of(b.region, s), b.dirty, cta, ncta, sh);
   stamp(b, 7);
   if (cta == 0) wait_tokens(f, b.info, s.local_experts, timeout_ns);
   stamp(b, 8);

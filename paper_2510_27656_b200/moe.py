@@ -400,6 +400,8 @@ class MoeRank:
         self._sources = torch.empty(G, dtype=torch.int64, device=dev)
         self._ret = torch.empty(G, dtype=torch.int32, device=dev)
         self._gidx = torch.empty(max(1, T * R), dtype=torch.int32, device=dev)
+        # receive rows that may hold data (the region starts zeroed)
+        self._dirty = torch.zeros(G, dtype=torch.uint8, device=dev)
         self._info = torch.zeros(2 * L + 3, dtype=torch.int64, device=dev)
         self._info_host = torch.zeros(2 * L + 3, dtype=torch.int64).pin_memory()
         self._grouped = self.region.tensor(int(sh.off_grouped), (G, int(sh.payload_bytes)), torch.uint8)
@@ -442,6 +444,7 @@ class MoeRank:
         b.sources = self._sources.data_ptr()
         b.ret_slot = self._ret.data_ptr()
         b.info = self._info.data_ptr()
+        b.dirty = self._dirty.data_ptr()
 
     def _connect(self, mesh: Sequence["MoeRank"]) -> None:
         """In-process wiring: peers are addressed directly (peer access)."""
@@ -695,6 +698,12 @@ class MoeRank:
         if out.shape[0] < rows_needed and g.padded_total is not None:
             raise ProtocolError(f"output rows {out.shape[0]} below the receive capacity {rows_needed}")
         ld = (out.stride(0) if out.numel() else width) * out.element_size()
+        g0 = self.region.ptr + int(self._shape.off_grouped)
+        g1 = g0 + int(self._shape.grouped_rows) * int(self._shape.payload_bytes)
+        if out.numel() and g0 <= out.data_ptr() < g1:
+            # outputs written in place into the receive region: any row may now
+            # hold data, so the next step re-zeroes every padding row
+            self._dirty.fill_(1)
         st.keep.append(out)
         st.out, st.ld = out, ld
         if st.fused:

@@ -16,6 +16,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--steps", type=int, default=5)
 ap.add_argument("--tokens", type=int, default=128)
 ap.add_argument("--comb", type=int, default=2)
+ap.add_argument("--graph", action="store_true", help="stamps from CUDA-graph replays with an L2 flush")
 a = ap.parse_args()
 T, H, E, R = a.tokens, 7168, 256, 8
 spec = moe.RoutingSpec(1, E, T, R, hidden=H, elem_size=1, scales=56, comb_elem_size=a.comb, comb_scales=0)
@@ -40,18 +41,37 @@ prof = torch.zeros(148 * 16, dtype=torch.int64, device="cuda")
 rk._bufs.prof = prof.data_ptr()
 names = ["start", "counted", "positions", "routes-in", "layout", "stored", "signalled", "metadata",
          "tokens-in", "c:start", "c:sent", "c:signalled", "c:reduced", "c:end"]
-for _ in range(3):
-    prof.zero_()
+def one():
     rk.dispatch_send(x, r, sync=False)
     rk.dispatch_recv(sync=False)
     rk.combine_send(y)
     rk.combine_recv(w, out_dtype=torch.bfloat16, sync=False)
-    torch.cuda.synchronize()
+
+if a.graph:
+    side = torch.cuda.Stream()
+    torch.cuda.set_stream(side)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    one(); torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        one()
+    for _ in range(3):
+        flush.fill_(1)
+        prof.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(); g.replay(); e1.record()
+        torch.cuda.synchronize()
+    print(f"graph step {e0.elapsed_time(e1)*1e3:.2f} us (events)")
+else:
+    for _ in range(3):
+        prof.zero_()
+        one()
+        torch.cuda.synchronize()
 p = prof.view(148, 16).cpu().numpy().astype(np.float64)
 rk._bufs.prof = 0
 act = p[:, 0] > 0
 t0 = p[act, 0].min()
-for k, nm in enumerate(names):
+for k, nm in list(enumerate(names)) + [(14, "pre-encoded")]:
     col = p[:, k]
     col = col[col > 0] - t0
     if col.size:
