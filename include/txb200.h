@@ -130,10 +130,9 @@ int txb_moe_plan(txb_moe_shape* s);
  * 231-246) -- straight into its final grouped row on the owner (the recv
  * slab + pack_rows regroup of 556-722 in one peer store), release-add the
  * row counts on the owners' token counters, build rows/sources/padding and
- * wait for the expected token rows.  routes: i64 or i32 [n, R] device. */
+ * wait for the expected token rows.  routes: i64 [n, R] device (railtx's dtype). */
 int txb_moe_dispatch_fused(const txb_moe_shape* s, const txb_moe_bufs* b, const void* x, int src_kind,
-                           int64_t n, const void* routes, int routes_i32, uint64_t timeout_ns,
-                           void* stream);
+                           int64_t n, const int64_t* routes, uint64_t timeout_ns, void* stream);
 /* combine_fused = combine_send + combine_recv (moe.py:739-833): every valid
  * grouped row of `outputs` (row stride ld bytes, comb_bytes wide) returns to
  * its source at the originating send slot, counts are release-added, then
@@ -147,10 +146,10 @@ int txb_moe_combine_fused(const txb_moe_shape* s, const txb_moe_bufs* b, const v
 
 /* ---- split path (same semantics, one phase per kernel; used when several
  * ranks share one GPU and for batches above the fused limit) ------------- */
-int txb_moe_route(const txb_moe_shape* s, const txb_moe_bufs* b, const void* routes, int routes_i32,
-                  int64_t n, void* stream);
+int txb_moe_route(const txb_moe_shape* s, const txb_moe_bufs* b, const int64_t* routes, int64_t n,
+                  void* stream);
 int txb_moe_dispatch(const txb_moe_shape* s, const txb_moe_bufs* b, const void* x, int src_kind, int64_t n,
-                     const void* routes, int routes_i32, uint64_t timeout_ns, int grid, void* stream);
+                     const int64_t* routes, uint64_t timeout_ns, int grid, void* stream);
 int txb_moe_dispatch_recv(const txb_moe_shape* s, const txb_moe_bufs* b, uint64_t timeout_ns, void* stream);
 int txb_moe_combine_send(const txb_moe_shape* s, const txb_moe_bufs* b, const void* outputs, int64_t ld,
                          int grid, void* stream);

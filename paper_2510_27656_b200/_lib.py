@@ -81,10 +81,10 @@ SIGNATURES: dict[str, list] = {
     "txb_ipc_close": [_INT, _VP],
     "txb_enable_peer": [_INT, _INT],
     "txb_moe_plan": [C.POINTER(Shape)],
-    "txb_moe_dispatch_fused": [C.POINTER(Shape), C.POINTER(Bufs), _VP, _INT, _I64, _VP, _INT, _U64, _VP],
+    "txb_moe_dispatch_fused": [C.POINTER(Shape), C.POINTER(Bufs), _VP, _INT, _I64, _VP, _U64, _VP],
     "txb_moe_combine_fused": [C.POINTER(Shape), C.POINTER(Bufs), _VP, _I64, _VP, _I64, _VP, _INT, _U64, _VP],
-    "txb_moe_route": [C.POINTER(Shape), C.POINTER(Bufs), _VP, _INT, _I64, _VP],
-    "txb_moe_dispatch": [C.POINTER(Shape), C.POINTER(Bufs), _VP, _INT, _I64, _VP, _INT, _U64, _INT, _VP],
+    "txb_moe_route": [C.POINTER(Shape), C.POINTER(Bufs), _VP, _I64, _VP],
+    "txb_moe_dispatch": [C.POINTER(Shape), C.POINTER(Bufs), _VP, _INT, _I64, _VP, _U64, _INT, _VP],
     "txb_moe_dispatch_recv": [C.POINTER(Shape), C.POINTER(Bufs), _U64, _VP],
     "txb_moe_combine_send": [C.POINTER(Shape), C.POINTER(Bufs), _VP, _I64, _INT, _VP],
     "txb_moe_combine_recv": [C.POINTER(Shape), C.POINTER(Bufs), _VP, _I64, _VP, _I64, _VP, _INT, _U64, _VP],

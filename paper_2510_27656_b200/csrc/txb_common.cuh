@@ -133,52 +133,48 @@ __host__ __device__ inline uint8_t* comb_of(void* region, const txb_moe_shape& s
 
 // ------------------------------------------------------------- block scan
 
-// Exclusive prefix sum of a[0..len) in shared memory, in place; every thread
-// of the block must call it.  Returns the total.  `tmp` needs 33 ints.
-template <typename T>
-__device__ T block_excl_scan(T* a, int len, T* tmp) {
+// Exclusive prefix sum of a[0..len) (int32, shared memory) in place; every
+// thread of the block must call it.  Returns the total.  `tmp` needs 33
+// ints.  Out of line: one copy of the code serves every call site (the
+// fused kernels are instruction-fetch bound when the code balloons).
+static __device__ __noinline__ int block_scan_i32(int* a, int len, int* tmp) {
   const int nt = blockDim.x, tid = threadIdx.x;
   const int per = (len + nt - 1) / nt;
   const int lo = min(len, tid * per), hi = min(len, lo + per);
-  T sum = 0;
+  int sum = 0;
   for (int i = lo; i < hi; ++i) sum += a[i];
-  // warp inclusive scan of per-thread sums
   const int lane = tid & 31, warp = tid >> 5;
-  T x = sum;
-#pragma unroll
+  int x = sum;
   for (int o = 1; o < 32; o <<= 1) {
-    T y = __shfl_up_sync(0xffffffffu, x, o);
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
     if (lane >= o) x += y;
   }
   if (lane == 31) tmp[warp] = x;
   __syncthreads();
   if (warp == 0) {
     const int nw = (nt + 31) >> 5;
-    T w = lane < nw ? tmp[lane] : T(0);
-#pragma unroll
+    int w = lane < nw ? tmp[lane] : 0;
     for (int o = 1; o < 32; o <<= 1) {
-      T y = __shfl_up_sync(0xffffffffu, w, o);
+      const int y = __shfl_up_sync(0xffffffffu, w, o);
       if (lane >= o) w += y;
     }
     if (lane < nw) tmp[lane] = w;  // inclusive warp totals
     if (lane == nw - 1) tmp[32] = w;
   }
   __syncthreads();
-  T run = (x - sum) + (warp ? tmp[warp - 1] : T(0));
+  int run = (x - sum) + (warp ? tmp[warp - 1] : 0);
   for (int i = lo; i < hi; ++i) {
-    T v = a[i];
+    const int v = a[i];
     a[i] = run;
     run += v;
   }
-  T total = tmp[32];
+  const int total = tmp[32];
   __syncthreads();
   return total;
 }
 
 // ------------------------------------------------------------- row copy
 
-// Copy `bytes` from src to dst with the widest vector the alignment allows;
-// the calling group is `nthr` threads with index `t`.
 __device__ __forceinline__ int vec_width(const void* a, const void* b, int64_t bytes) {
   uintptr_t m = reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b) | (uintptr_t)bytes;
   if ((m & 15) == 0) return 16;
@@ -187,8 +183,10 @@ __device__ __forceinline__ int vec_width(const void* a, const void* b, int64_t b
   return 1;
 }
 
-__device__ __forceinline__ void copy_row(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src,
-                                         int64_t bytes, int t, int nthr) {
+// Copy `bytes` from src to dst with the widest vector the alignment allows;
+// the calling group is `nthr` threads with index `t`.
+static __device__ __noinline__ void copy_row(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src, int64_t bytes,
+                                      int t, int nthr) {
   const int w = vec_width(dst, src, bytes);
   if (w == 16) {
     const int4* s = reinterpret_cast<const int4*>(src);
@@ -196,15 +194,11 @@ __device__ __forceinline__ void copy_row(uint8_t* __restrict__ dst, const uint8_
     const int64_t nv = bytes >> 4;
     int64_t i = t;
     for (; i + 3 * nthr < nv; i += 4 * nthr) {
-      int4 a = s[i], b = s[i + nthr], c = s[i + 2 * nthr], e = s[i + 3 * nthr];
+      const int4 a = s[i], b = s[i + nthr], c = s[i + 2 * nthr], e = s[i + 3 * nthr];
       d[i] = a; d[i + nthr] = b; d[i + 2 * nthr] = c; d[i + 3 * nthr] = e;
     }
     for (; i < nv; i += nthr) d[i] = s[i];
-  } else if (w == 8) {
-    const int2* s = reinterpret_cast<const int2*>(src);
-    int2* d = reinterpret_cast<int2*>(dst);
-    for (int64_t i = t; i < (bytes >> 3); i += nthr) d[i] = s[i];
-  } else if (w == 4) {
+  } else if (w >= 4) {
     const int* s = reinterpret_cast<const int*>(src);
     int* d = reinterpret_cast<int*>(dst);
     for (int64_t i = t; i < (bytes >> 2); i += nthr) d[i] = s[i];
@@ -213,10 +207,10 @@ __device__ __forceinline__ void copy_row(uint8_t* __restrict__ dst, const uint8_
   }
 }
 
-__device__ __forceinline__ void zero_row(uint8_t* dst, int64_t bytes, int t, int nthr) {
+static __device__ __noinline__ void zero_row(uint8_t* dst, int64_t bytes, int t, int nthr) {
   const int w = vec_width(dst, dst, bytes);
   if (w == 16) {
-    int4 z = make_int4(0, 0, 0, 0);
+    const int4 z = make_int4(0, 0, 0, 0);
     for (int64_t i = t; i < (bytes >> 4); i += nthr) reinterpret_cast<int4*>(dst)[i] = z;
   } else if (w >= 4) {
     for (int64_t i = t; i < (bytes >> 2); i += nthr) reinterpret_cast<int*>(dst)[i] = 0;

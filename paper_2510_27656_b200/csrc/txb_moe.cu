@@ -4,20 +4,20 @@
 //
 // A step is built from six phases (device functions below):
 //   P1 route    per-expert counts + stable per-copy ranks + pos; the own
-//               count row is stored into every peer's route matrix and a
-//               step tag is published (reference: route scatter, imm_route)
-//   P2 wait     acquire-wait for every route row of this step and for every
-//               peer's end-of-previous-step barrier (buffer reuse, moe.dbar)
+//               count row is stored into every peer's route matrix as
+//               (step tag | count) words (reference: route scatter, imm_route)
+//   P2 wait     acquire every route word of this step and every peer's
+//               end-of-previous-step barrier (buffer reuse, moe.dbar)
 //   P3 layout   compute_layout + grouped order from the route matrix
 //   P4 tokens   each token copy is encoded (fp8 per-token scale / bf16 / raw)
 //               and stored straight into its final grouped row on the owner;
 //               per-destination row counts are added to the owner's token
-//               counter after one system-scope release fence (the ImmCounter)
+//               counter after one release fence (the ImmCounter)
 //   P5 recv     rows / sources / return-slot metadata, zeroed padding rows,
 //               then acquire-wait for the expected number of token rows
 //   C1 send     every valid grouped output row returns to its source's
 //               combine buffer at the originating send slot (rows whose
-//               source is this rank are read in place later)
+//               source is this rank are read in place by C2)
 //   C2 combine  acquire-wait for the returned rows, fp32 weighted sum per
 //               token, last CTA publishes the end-of-step barrier tag
 //
@@ -25,9 +25,12 @@
 //                       k_comb_send(C1) k_comb_recv(C2)
 //           fused path  k_dispatch_fused(P1-P5) k_combine_fused(C1-C2),
 //                       cooperative launches (one wave, every CTA resident).
+// k_dispatch_fused<..., DECODE=true> is the decode-batch specialisation (one
+// token per CTA, read and encoded before the route exchange, direct counts):
+// it carries only the code that path executes, because a once-per-SM kernel
+// of this kind is bound by instruction fetch when the code balloons.
 // The split path is used when several ranks share one GPU (host-gated
-// emulation: no kernel may spin on a rank queued behind it) and for token
-// counts above the fused path's redundant-histogram limit.
+// emulation: no kernel may spin on a rank queued behind it).
 //
 // Completion is counted, never ordered: a waiter compares a monotone
 // counter with a cumulative threshold, so delivery order across NVLink is
@@ -44,12 +47,9 @@ constexpr int kMaxExperts = 1536;  // shared-memory bound of the route phase
 constexpr int kThreads = 512;      // block size of the main kernels
 constexpr int kRouteThreads = 1024;
 constexpr int kFusedMaxCopies = 16384;  // n*R limit of the fused dispatch
+constexpr int kMaxOwn = 64;        // copies per CTA of the direct-count path
 
-__device__ __forceinline__ int64_t load_route(const void* r, int i32, int64_t i) {
-  return i32 ? (int64_t) reinterpret_cast<const int32_t*>(r)[i] : reinterpret_cast<const int64_t*>(r)[i];
-}
-
-__device__ __forceinline__ int64_t pad_up(int64_t x) { return (x + kGroupPad - 1) / kGroupPad * kGroupPad; }
+__device__ __forceinline__ int pad_up(int x) { return (x + kGroupPad - 1) / kGroupPad * kGroupPad; }
 
 // Optional phase stamps for profiling (txb_moe_bufs.prof).
 __device__ __forceinline__ void stamp(const txb_moe_bufs& b, int k) {
@@ -60,27 +60,23 @@ __device__ __forceinline__ uint64_t cur_step(Flags* f) {
   return *reinterpret_cast<volatile uint64_t*>(&f->step) + 1;
 }
 
-// Shared-memory footprint of the phases (bytes), all carved from one
-// dynamic buffer and reused phase to phase.
+// Shared-memory footprint of the phases (bytes), carved from one dynamic
+// buffer and reused phase to phase; all tables are int32.
 __host__ __device__ inline size_t smem_route(int E, int nwarps) { return (size_t)(1 + nwarps) * E * 4 + 16; }
+__host__ __device__ inline size_t smem_layout(int E) { return (size_t)(2 * E + 1) * 4; }
+__host__ __device__ inline size_t smem_recv(int N, int L) {
+  return (size_t)(3 * N * L + 1 + 2 * L + 1 + L * (N + 1) + N) * 4;
+}
 __host__ __device__ inline size_t smem_cmat(int N, int E) { return ((size_t)N * E * 4 + 15) / 16 * 16; }
-__host__ __device__ inline size_t smem_recv(int N, int L);
-__host__ __device__ inline size_t smem_layout(int E);
 // the route matrix copy (Cs) lives after the layout / recv scratch
 __host__ __device__ inline size_t cmat_offset(const txb_moe_shape& s) {
   const size_t a = smem_layout(s.experts), b = smem_recv(s.ranks, s.local_experts);
   return ((a > b ? a : b) + 15) / 16 * 16;
 }
-__host__ __device__ inline size_t smem_layout(int E) { return (size_t)(2 * E + 1) * 8; }
-__host__ __device__ inline size_t smem_recv(int N, int L) {
-  return (size_t)(3 * N * L + 1 + 2 * L + 1 + L * (N + 1) + N) * 8;
-}
-
-constexpr int kMaxOwn = 64;  // copies per CTA handled by the direct-count rank path
 
 struct Shared {  // static shared state of one CTA
   uint32_t bad, fail, recv_me, direct;
-  int64_t tmp[33];
+  int tmp[33];
   float red[33];
   uint32_t cnt[TXB_MAX_RANKS];
   uint8_t* dstp[kMaxTopk];
@@ -91,14 +87,71 @@ struct Shared {  // static shared state of one CTA
 
 // ------------------------------------------------------------------- P1
 
-// Counts and stable ranks of the n*R copies (stable = token order within an
-// expert, the (local_expert, t, j) slab order of moe.py:514-521).  Every
-// participating CTA scans all copies; copies of tokens t with
-// t % ncta == cta get their rank stored to rank_out.  Returns the
-// validation bits (moe.py:142-155).  hist[E] holds the counts afterwards.
-__device__ uint32_t route_counts(const txb_moe_shape& s, const void* routes, int i32, int64_t n,
-                                 uint32_t* hist, uint32_t* wc, int32_t* rank_out, int cta, int ncta,
-                                 Shared& sh) {
+// Direct counts: shared atomics (order-free) for the histogram; the stable
+// rank of each of this CTA's copies (token order within an expert, the
+// (local_expert, t, j) slab order of moe.py:514-521) is the number of
+// earlier copies with its expert.  Validation (moe.py:142-155): range, and
+// duplicates within a token -- R-1 shuffles when R divides 32 (a token's
+// copies sit in consecutive lanes), loads otherwise.
+__device__ uint32_t route_counts_direct(const txb_moe_shape& s, const int64_t* routes, int64_t n, uint32_t* hist,
+                                        int32_t* rank_out, int cta, int ncta, Shared& sh) {
+  const int E = s.experts, R = s.topk, tid = threadIdx.x;
+  const int m = (int)(n * R);
+  const int nmine = n > cta ? (int)((n - cta + ncta - 1) / ncta) : 0;
+  const int nw = nmine * R;
+  for (int e = tid; e < E; e += blockDim.x) hist[e] = 0;
+  for (int k = tid; k < nw; k += blockDim.x) {
+    const int i = (cta + (k / R) * ncta) * R + (k % R);
+    const int64_t v = routes[i];
+    sh.own_e[k] = (v >= 0 && v < E) ? (int)v : -1;
+    sh.own_i[k] = i;
+    sh.own_rank[k] = 0;
+  }
+  if (tid == 0) {
+    sh.bad = 0;
+    sh.direct = 1;
+  }
+  __syncthreads();
+  const bool lanes = (32 % R) == 0;
+  for (int base = 0; base < m; base += blockDim.x) {
+    const int i = base + tid;
+    const bool valid = i < m;
+    const int64_t v = valid ? routes[i] : -1;
+    const int j = i % R;
+    bool dup = false;
+    if (lanes) {
+      for (int jj = 1; jj < R; ++jj) {
+        const int64_t u = __shfl_up_sync(0xffffffffu, v, jj);
+        dup |= (jj <= j) && (u == v);
+      }
+    } else if (valid) {
+      for (int jj = 1; jj <= j; ++jj) dup |= routes[i - jj] == v;
+    }
+    if (!valid) continue;
+    if (v < 0 || v >= E) {
+      atomicOr(&sh.bad, TXB_EV_ROUTE_RANGE);
+      continue;
+    }
+    if (dup) atomicOr(&sh.bad, TXB_EV_ROUTE_DUP);
+    atomicAdd(&hist[(int)v], 1u);
+    for (int k = 0; k < nw; ++k)
+      if (sh.own_e[k] == (int)v && i < sh.own_i[k]) atomicAdd(&sh.own_rank[k], 1u);
+  }
+  __syncthreads();
+  for (int k = tid; k < nw; k += blockDim.x) rank_out[sh.own_i[k]] = (int32_t)sh.own_rank[k];
+  const uint32_t b = sh.bad;
+  if (b)
+    for (int e = tid; e < E; e += blockDim.x) hist[e] = 0;  // publish an empty row
+  __syncthreads();
+  return b;
+}
+
+// Chunked counts for large batches: per chunk of blockDim copies a warp
+// match + per-warp counts + a scan over warps per expert give the stable
+// ranks; copies of tokens t with t % ncta == cta get their rank stored.
+__device__ __noinline__ uint32_t route_counts_chunked(const txb_moe_shape& s, const int64_t* routes, int64_t n,
+                                                     uint32_t* hist, uint32_t* wc, int32_t* rank_out, int cta,
+                                                     int ncta, Shared& sh) {
   const int E = s.experts, R = s.topk;
   const int tid = threadIdx.x, warp = tid >> 5, nwarps = blockDim.x >> 5;
   if (tid == 0) {
@@ -106,73 +159,22 @@ __device__ uint32_t route_counts(const txb_moe_shape& s, const void* routes, int
     sh.direct = 0;
   }
   for (int e = tid; e < E; e += blockDim.x) hist[e] = 0;
-  const int64_t M = n * R;
-  const int64_t nmine = n > cta ? (n - cta + ncta - 1) / ncta : 0;
-  const int64_t nown = nmine * R;
-  if (nown <= kMaxOwn && M < (1LL << 30)) {
-    // Direct path: counts by shared atomics (order-free); the stable rank of
-    // each of this CTA's copies = number of earlier copies with its expert.
-    const int m = (int)M, nw = (int)nown;
-    for (int k = tid; k < nw; k += blockDim.x) {
-      const int i = (cta + (k / R) * ncta) * R + (k % R);
-      const int64_t v = load_route(routes, i32, i);
-      sh.own_e[k] = (v >= 0 && v < E) ? (int)v : -1;
-      sh.own_i[k] = i;
-      sh.own_rank[k] = 0;
-    }
-    __syncthreads();
-    // when R divides 32 a token's copies sit in consecutive lanes of one
-    // warp, so the duplicate check is R-1 shuffles instead of R-1 loads
-    const bool lanes = (32 % R) == 0;
-    for (int base = 0; base < m; base += blockDim.x) {
-      const int i = base + tid;
-      const bool valid = i < m;
-      const int64_t v = valid ? load_route(routes, i32, i) : -1;
-      const int j = i % R;
-      bool dup = false;
-      if (lanes) {
-        for (int jj = 1; jj < R; ++jj) {
-          const int64_t u = __shfl_up_sync(0xffffffffu, v, jj);
-          dup |= (jj <= j) && (u == v);
-        }
-      } else if (valid) {
-        for (int jj = 1; jj <= j; ++jj) dup |= load_route(routes, i32, i - jj) == v;
-      }
-      if (!valid) continue;
-      if (v < 0 || v >= E) {
-        atomicOr(&sh.bad, TXB_EV_ROUTE_RANGE);
-        continue;
-      }
-      if (dup) atomicOr(&sh.bad, TXB_EV_ROUTE_DUP);
-      atomicAdd(&hist[(int)v], 1u);
-      for (int k = 0; k < nw; ++k)
-        if (sh.own_e[k] == (int)v && i < sh.own_i[k]) atomicAdd(&sh.own_rank[k], 1u);
-    }
-    __syncthreads();
-    for (int k = tid; k < nw; k += blockDim.x) rank_out[sh.own_i[k]] = (int32_t)sh.own_rank[k];
-    if (tid == 0) sh.direct = 1;
-    const uint32_t b = sh.bad;
-    if (b)
-      for (int e = tid; e < E; e += blockDim.x) hist[e] = 0;
-    __syncthreads();
-    return b;
-  }
   __syncthreads();
+  const int64_t M = n * R;
   for (int64_t base = 0; base < M; base += blockDim.x) {
     for (int i = tid; i < nwarps * E; i += blockDim.x) wc[i] = 0;
     __syncthreads();
     const int64_t i = base + tid;
     int e = -1;
     if (i < M) {
-      const int64_t v = load_route(routes, i32, i);
+      const int64_t v = routes[i];
       if (v < 0 || v >= E) {
         atomicOr(&sh.bad, TXB_EV_ROUTE_RANGE);
       } else {
         e = (int)v;
         const int64_t t = i / R;
-        const int j = (int)(i - t * R);
-        for (int jj = 0; jj < j; ++jj)
-          if (load_route(routes, i32, t * R + jj) == v) atomicOr(&sh.bad, TXB_EV_ROUTE_DUP);
+        for (int64_t q = t * R; q < i; ++q)
+          if (routes[q] == v) atomicOr(&sh.bad, TXB_EV_ROUTE_DUP);
       }
     }
     const uint32_t same = __match_any_sync(0xffffffffu, e);
@@ -194,51 +196,47 @@ __device__ uint32_t route_counts(const txb_moe_shape& s, const void* routes, int
   }
   const uint32_t b = sh.bad;
   if (b)
-    for (int e = tid; e < E; e += blockDim.x) hist[e] = 0;  // publish an empty row
+    for (int e = tid; e < E; e += blockDim.x) hist[e] = 0;
   __syncthreads();
   return b;
 }
 
 // pos[t,j] = first send slot of expert e + stable rank, for this CTA's
-// tokens (moe.py:510-520).  ex: int64 scratch of E entries.
-__device__ void route_positions(const txb_moe_shape& s, const void* routes, int i32, int64_t n,
-                                const uint32_t* hist, int64_t* ex, const int32_t* rank_in, int64_t* pos,
-                                uint32_t bad, int cta, int ncta, Shared& sh) {
+// tokens (moe.py:510-520).  ex: int32 scratch of E entries.
+__device__ void route_positions(const txb_moe_shape& s, const int64_t* routes, int64_t n, const uint32_t* hist,
+                                int* ex, const int32_t* rank_in, int64_t* pos, uint32_t bad, int cta, int ncta,
+                                Shared& sh) {
   const int E = s.experts, R = s.topk;
-  for (int e = threadIdx.x; e < E; e += blockDim.x) ex[e] = hist[e];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) ex[e] = (int)hist[e];
   __syncthreads();
-  block_excl_scan<int64_t>(ex, E, sh.tmp);
+  block_scan_i32(ex, E, sh.tmp);
   const int64_t nmine = n > cta ? (n - cta + ncta - 1) / ncta : 0;
   for (int64_t k = threadIdx.x; k < nmine * R; k += blockDim.x) {
-    const int64_t t = cta + (k / R) * ncta;
-    const int64_t i = t * R + (k % R);
-    pos[i] = bad ? -1 : ex[(int)load_route(routes, i32, i)] + rank_in[i];
+    const int64_t i = (cta + (k / R) * ncta) * R + (k % R);
+    pos[i] = bad ? -1 : (int64_t)ex[(int)routes[i]] + rank_in[i];
   }
   __syncthreads();
 }
 
-// Route-row scatter: own counts into row `me` of every rank's matrix, one
-// release fence, then the step tag (single writer per slot).  Also books
-// the number of copies that will come back from other ranks.
+// Route-row scatter: own counts into row `me` of every rank's matrix as
+// (step tag << 32 | count) words -- single-copy atomic, so no fence.  Every
+// CTA holds the full histogram; CTA `part` of `nparts` stores its slice.
+// Part 0 also books the copies that will come back from other ranks.
 __device__ void route_publish(const txb_moe_shape& s, void* const* peers, Flags* f, const uint32_t* hist,
                               uint64_t step, int64_t n, uint32_t bad, int part, int nparts) {
   const int E = s.experts, N = s.ranks, L = s.local_experts;
   const int slot = (int)(step & 1);
   const uint64_t tag = (uint64_t)(uint32_t)step << 32;
-  // every CTA holds the full histogram; CTA `part` stores its slice
   for (int idx = part * blockDim.x + threadIdx.x; idx < N * E; idx += nparts * blockDim.x) {
     const int d = idx / E, e = idx - d * E;
     st_relaxed_sys(route_of(peers[d], s, slot) + (size_t)s.me * E + e, tag | hist[e]);
   }
-  if (part != 0) return;
-  __syncthreads();
-  if (threadIdx.x == 0) {
+  if (part == 0 && threadIdx.x == 0) {
     uint64_t self = 0;
     for (int le = 0; le < L; ++le) self += hist[s.me * L + le];
     f->comb_target += bad ? 0 : (uint64_t)(n * s.topk) - self;
     if (bad) atomicOr(&f->err, bad);
-    // per-source step tag for host-side gating/diagnostics only (the words
-    // above carry their own tags)
+    // per-source step tags for host-side gating / diagnostics only
     for (int d = 0; d < N; ++d) st_relaxed_sys(&flags_of(peers[d], s)->route_tag[slot][s.me], step);
   }
 }
@@ -246,7 +244,7 @@ __device__ void route_publish(const txb_moe_shape& s, void* const* peers, Flags*
 // ------------------------------------------------------------------- P2
 
 // Acquire every route word of this step (tag == step) into Cs[N*E] (shared
-// memory), and wait for every peer's end-of-previous-step barrier.
+// memory) and wait for every peer's end-of-previous-step barrier.
 __device__ bool wait_routes(const txb_moe_shape& s, Flags* f, const uint64_t* C, uint32_t* Cs, uint64_t step,
                             uint64_t timeout_ns, Shared& sh) {
   if (threadIdx.x == 0) sh.fail = 0;
@@ -266,10 +264,9 @@ __device__ bool wait_routes(const txb_moe_shape& s, Flags* f, const uint64_t* C,
     }
     Cs[i] = (uint32_t)v;
   }
-  if (threadIdx.x < 32) {
+  if (threadIdx.x < 32)
     for (int q = threadIdx.x; q < s.ranks; q += 32)
       if (!spin_ge(&f->done[q], step - 1, dl)) atomicOr(&sh.fail, TXB_EV_WAIT_BARRIER);
-  }
   __syncthreads();
   const uint32_t fl = sh.fail;
   if (fl && threadIdx.x == 0) atomicOr(&f->err, fl);
@@ -280,8 +277,8 @@ __device__ bool wait_routes(const txb_moe_shape& s, Flags* f, const uint64_t* C,
 
 // baseg[e] = grouped row on owner(e) where this rank's first copy for e
 // lands: group_starts[le] + sum_{s' < me} counts[s', e].
-__device__ bool dispatch_layout(const txb_moe_shape& s, const uint32_t* C, int64_t* baseg, int64_t* padded,
-                                Flags* f, bool book, Shared& sh) {
+__device__ bool dispatch_layout(const txb_moe_shape& s, const uint32_t* C, int* baseg, int* padded, Flags* f,
+                                bool book, Shared& sh) {
   const int N = s.ranks, E = s.experts, L = s.local_experts, tid = threadIdx.x;
   if (tid == 0) {
     sh.recv_me = 0;
@@ -289,9 +286,9 @@ __device__ bool dispatch_layout(const txb_moe_shape& s, const uint32_t* C, int64
   }
   __syncthreads();
   for (int e = tid; e < E; e += blockDim.x) {
-    int64_t col = 0, pre = 0;
+    int col = 0, pre = 0;
     for (int q = 0; q < N; ++q) {
-      const uint32_t c = C[(size_t)q * E + e];
+      const int c = (int)C[q * E + e];
       col += c;
       if (q < s.me) pre += c;
     }
@@ -300,7 +297,7 @@ __device__ bool dispatch_layout(const txb_moe_shape& s, const uint32_t* C, int64
     if (book && e / L == s.me) atomicAdd(&sh.recv_me, (uint32_t)col);
   }
   __syncthreads();
-  const int64_t tot = block_excl_scan<int64_t>(padded, E, sh.tmp);
+  const int tot = block_scan_i32(padded, E, sh.tmp);
   if (tid == 0) padded[E] = tot;
   __syncthreads();
   for (int e = tid; e < E; e += blockDim.x) baseg[e] += padded[e] - padded[(e / L) * L];
@@ -318,37 +315,52 @@ __device__ bool dispatch_layout(const txb_moe_shape& s, const uint32_t* C, int64
 
 // ------------------------------------------------------------------- P4
 
-template <int SRC, int ELEM>
-__device__ void dispatch_tokens(const txb_moe_shape& s, const void* x, int64_t n, const void* routes, int i32,
-                                const int32_t* rank_in, int32_t* gidx, void* const* peers, const int64_t* baseg,
-                                int cta, int ncta, Shared& sh, const RowRegs* pre) {
-  const int N = s.ranks, L = s.local_experts, R = s.topk, tid = threadIdx.x;
-  const int64_t P = s.payload_bytes;
-  const bool direct = sh.direct != 0;
-  for (int q = tid; q < N; q += blockDim.x) sh.cnt[q] = 0;
+// Destination rows of token t's copies (kt-th token of this CTA) into
+// sh.dstp; books gidx and per-destination counts.
+__device__ __forceinline__ void token_dests(const txb_moe_shape& s, const int64_t* routes, const int32_t* rank_in,
+                                            int32_t* gidx, void* const* peers, const int* baseg, int64_t t, int kt,
+                                            Shared& sh) {
+  const int R = s.topk, L = s.local_experts, tid = threadIdx.x;
+  if (tid < R) {
+    int e, rank;
+    if (sh.direct) {  // experts and ranks of this CTA's copies are in smem
+      e = sh.own_e[kt * R + tid];
+      rank = (int)sh.own_rank[kt * R + tid];
+    } else {
+      e = (int)routes[t * R + tid];
+      rank = rank_in[t * R + tid];
+    }
+    const int d = e / L;
+    const int64_t g = (int64_t)baseg[e] + rank;
+    sh.dstp[tid] = grouped_of(peers[d], s) + g * s.payload_bytes;
+    gidx[t * R + tid] = d == s.me ? (int32_t)g : -1;
+    atomicAdd(&sh.cnt[d], 1u);
+  }
   __syncthreads();
+}
+
+// Out-of-line copy/encode of one token row to sh.dstp (general shapes).
+template <int SRC, int ELEM>
+__device__ __noinline__ void dispatch_row_slow(const txb_moe_shape& s, const void* x, int64_t t, Shared& sh) {
+  const int64_t P = s.payload_bytes;
+  if constexpr (SRC == TXB_SRC_ROWS) {
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(x) + t * P;
+    for (int j = 0; j < s.topk; ++j) copy_row(sh.dstp[j], src, P, threadIdx.x, blockDim.x);
+  } else {
+    encode_store_row<SRC, ELEM>(x, t, s.hidden, s.scales, P, sh.dstp, s.topk, sh.red);
+  }
+}
+
+template <int SRC, int ELEM>
+__device__ __noinline__ void dispatch_tokens(const txb_moe_shape& s, const void* x, int64_t n,
+                                             const int64_t* routes, const int32_t* rank_in, int32_t* gidx,
+                                             void* const* peers, const int* baseg, int cta, int ncta, Shared& sh) {
+  const int R = s.topk, tid = threadIdx.x;
+  const int64_t P = s.payload_bytes;
   int kt = 0;
   for (int64_t t = cta; t < n; t += ncta, ++kt) {
-    if (tid < R) {
-      int e;
-      int64_t rank;
-      if (direct) {  // ranks and experts of this CTA's copies are already in smem
-        e = sh.own_e[kt * R + tid];
-        rank = sh.own_rank[kt * R + tid];
-      } else {
-        e = (int)load_route(routes, i32, t * R + tid);
-        rank = rank_in[t * R + tid];
-      }
-      const int d = e / L;
-      const int64_t g = baseg[e] + rank;
-      sh.dstp[tid] = grouped_of(peers[d], s) + g * P;
-      gidx[t * R + tid] = d == s.me ? (int32_t)g : -1;
-      atomicAdd(&sh.cnt[d], 1u);
-    }
-    __syncthreads();
-    if (pre && pre->ok && kt == 0) {
-      store_row_regs<SRC, ELEM>(*pre, s.hidden, s.scales, sh.dstp, R);
-    } else if constexpr (SRC == TXB_SRC_ROWS) {
+    token_dests(s, routes, rank_in, gidx, peers, baseg, t, kt, sh);
+    if constexpr (SRC == TXB_SRC_ROWS) {
       const uint8_t* src = reinterpret_cast<const uint8_t*>(x) + t * P;
       if (vec_width(src, sh.dstp[0], P) == 16) {
         for (int64_t v = tid; v < (P >> 4); v += blockDim.x) {
@@ -356,7 +368,7 @@ __device__ void dispatch_tokens(const txb_moe_shape& s, const void* x, int64_t n
           for (int j = 0; j < R; ++j) reinterpret_cast<int4*>(sh.dstp[j])[v] = val;
         }
       } else {
-        for (int j = 0; j < R; ++j) copy_row(sh.dstp[j], src, P, tid, blockDim.x);
+        dispatch_row_slow<SRC, ELEM>(s, x, t, sh);
       }
     } else {
       encode_store_row<SRC, ELEM>(x, t, s.hidden, s.scales, P, sh.dstp, R, sh.red);
@@ -387,37 +399,36 @@ __device__ void signal_counts(const txb_moe_shape& s, void* const* peers, size_t
 // Receive metadata for grouped rows (moe.py:699-722): every CTA derives the
 // per-(source, local expert) tables from the route matrix; the grid then
 // walks the grouped rows, one warp per row (lane 0 writes rows / sources /
-// return slot, the warp zero-fills padding rows).
-__device__ void recv_metadata(const txb_moe_shape& s, const uint32_t* C, int64_t* sm, int64_t* rows,
-                              int64_t* sources, int32_t* ret, int64_t* info, uint8_t* G, uint8_t* dirty, int cta,
-                              int ncta, Shared& sh) {
+// return slot; the warp zero-fills padding rows that may hold stale data).
+__device__ __noinline__ void recv_metadata(const txb_moe_shape& s, const uint32_t* C, int* sm, int64_t* rows,
+                                           int64_t* sources, int32_t* ret, int64_t* info, uint8_t* G,
+                                           uint8_t* dirty, int cta, int ncta, Shared& sh) {
   const int N = s.ranks, E = s.experts, L = s.local_experts, me = s.me;
   const int tid = threadIdx.x, nt = blockDim.x;
-  int64_t* a = sm;                         // [N][L] counts into my experts
-  int64_t* rowbase = a + N * L;            // [N*L+1] flattened exclusive prefix = recv slot base
-  int64_t* retbase = rowbase + N * L + 1;  // [N][L] send slot base on the source
-  int64_t* gstart = retbase + N * L;       // [L+1]
-  int64_t* gsize = gstart + L + 1;         // [L]
-  int64_t* srcpre = gsize + L;             // [L][N+1]
-  int64_t* pre_all = srcpre + L * (N + 1); // [N] sum_{e' < me*L} C[q][e']
+  int* a = sm;                         // [N][L] counts into my experts
+  int* rowbase = a + N * L;            // [N*L+1] flattened exclusive prefix = recv slot base
+  int* retbase = rowbase + N * L + 1;  // [N][L] send slot base on the source
+  int* gstart = retbase + N * L;       // [L+1]
+  int* gsize = gstart + L + 1;         // [L]
+  int* srcpre = gsize + L;             // [L][N+1]
+  int* pre_all = srcpre + L * (N + 1); // [N] sum_{e' < me*L} C[q][e']
   for (int i = tid; i < N * L; i += nt) {
     const int q = i / L, le = i - q * L;
-    a[i] = C[(size_t)q * E + me * L + le];
+    a[i] = (int)C[q * E + me * L + le];
     rowbase[i] = a[i];
   }
-  __syncthreads();
   {
     const int warp = tid >> 5, lane = tid & 31, nwarp = nt >> 5;
     for (int q = warp; q < N; q += nwarp) {
-      int64_t acc = 0;
-      for (int e = lane; e < me * L; e += 32) acc += C[(size_t)q * E + e];
-#pragma unroll
+      int acc = 0;
+      for (int e = lane; e < me * L; e += 32) acc += (int)C[q * E + e];
       for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
       if (lane == 0) pre_all[q] = acc;
     }
   }
+  __syncthreads();
   for (int le = tid; le < L; le += nt) {
-    int64_t run = 0;
+    int run = 0;
     for (int q = 0; q < N; ++q) {
       srcpre[le * (N + 1) + q] = run;
       run += a[q * L + le];
@@ -427,10 +438,10 @@ __device__ void recv_metadata(const txb_moe_shape& s, const uint32_t* C, int64_t
     gstart[le] = pad_up(run);
   }
   __syncthreads();
-  const int64_t padded_total = block_excl_scan<int64_t>(gstart, L, sh.tmp);
+  const int padded_total = block_scan_i32(gstart, L, sh.tmp);
   // recv_start[me][q] + sum_{le'<le} a[q][le'] is the exclusive prefix of a[]
   // flattened source-major (moe.py:178-184, 204-213)
-  const int64_t recv_total = block_excl_scan<int64_t>(rowbase, N * L, sh.tmp);
+  const int recv_total = block_scan_i32(rowbase, N * L, sh.tmp);
   if (tid == 0) {
     gstart[L] = padded_total;
     rowbase[N * L] = recv_total;
@@ -450,19 +461,19 @@ __device__ void recv_metadata(const txb_moe_shape& s, const uint32_t* C, int64_t
   }
   const int64_t P = s.payload_bytes;
   const int warp = tid >> 5, lane = tid & 31, nwarp = nt >> 5;
-  for (int64_t g = (int64_t)cta * nwarp + warp; g < padded_total; g += (int64_t)ncta * nwarp) {
+  for (int g = cta * nwarp + warp; g < padded_total; g += ncta * nwarp) {
     int lo = 0, hi = L - 1;  // last le with gstart[le] <= g
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
       if (gstart[mid] <= g) lo = mid; else hi = mid - 1;
     }
     const int le = lo;
-    const int64_t k = g - gstart[le];
+    const int k = g - gstart[le];
     if (k >= gsize[le]) {
-      // padding rows read as zero (moe.py:719); only rows that held data since
-      // they were last zeroed need the store
+      // padding rows read as zero (moe.py:719); only rows that held data
+      // since they were last zeroed need the store
       const bool d = dirty[g] != 0;
-      if (d) zero_row(G + g * P, P, lane, 32);
+      if (d) zero_row(G + (int64_t)g * P, P, lane, 32);
       if (lane == 0) {
         rows[g] = -1;
         sources[g] = -1;
@@ -471,13 +482,13 @@ __device__ void recv_metadata(const txb_moe_shape& s, const uint32_t* C, int64_t
       }
     } else if (lane == 0) {
       dirty[g] = 1;
-      const int64_t* sp = srcpre + le * (N + 1);
+      const int* sp = srcpre + le * (N + 1);
       int q = 0;
       while (sp[q + 1] <= k) ++q;
-      const int64_t kk = k - sp[q];
+      const int kk = k - sp[q];
       rows[g] = rowbase[q * L + le] + kk;
       sources[g] = q;
-      ret[g] = (int32_t)(retbase[q * L + le] + kk);
+      ret[g] = retbase[q * L + le] + kk;
     }
   }
 }
@@ -498,13 +509,14 @@ __device__ void combine_send_rows(const txb_moe_shape& s, const uint8_t* out, in
   const int N = s.ranks, L = s.local_experts, tid = threadIdx.x;
   for (int q = tid; q < N; q += blockDim.x) sh.cnt[q] = 0;
   __syncthreads();
-  const int64_t total = info[2 * L];
+  if (N == 1) return;  // every row is this rank's own: read in place by C2
+  const int total = (int)info[2 * L];
   const int64_t Pc = s.comb_bytes;
   const int lane = tid & 31, nwarp = blockDim.x >> 5;
-  for (int64_t g = (int64_t)cta * nwarp + (tid >> 5); g < total; g += (int64_t)ncta * nwarp) {
-    const int64_t q = sources[g];
+  for (int g = cta * nwarp + (tid >> 5); g < total; g += ncta * nwarp) {
+    const int q = (int)sources[g];
     if (q < 0 || q == s.me) continue;  // padding, or read in place by C2
-    copy_row(comb_of(peers[q], s) + (int64_t)ret[g] * Pc, out + g * ld, Pc, lane, 32);
+    copy_row(comb_of(peers[q], s) + (int64_t)ret[g] * Pc, out + (int64_t)g * ld, Pc, lane, 32);
     if (lane == 0) atomicAdd(&sh.cnt[q], 1u);
   }
 }
@@ -546,35 +558,35 @@ __device__ void end_of_step(const txb_moe_shape& s, void* const* peers, Flags* f
 // ------------------------------------------------------------ split kernels
 
 __global__ void __launch_bounds__(kRouteThreads)
-k_route(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ routes, int i32, int64_t n) {
+k_route(txb_moe_shape s, txb_moe_bufs b, const int64_t* __restrict__ routes, int64_t n) {
   extern __shared__ __align__(16) uint8_t dsm[];
   __shared__ Shared sh;
   uint32_t* hist = reinterpret_cast<uint32_t*>(dsm);
   uint32_t* wc = hist + ((s.experts + 3) & ~3);
   Flags* f = flags_of(b.region, s);
   const uint64_t step = cur_step(f);
-  const uint32_t bad = route_counts(s, routes, i32, n, hist, wc, b.rank_scratch, 0, 1, sh);
-  route_positions(s, routes, i32, n, hist, reinterpret_cast<int64_t*>(wc), b.rank_scratch, b.pos, bad, 0, 1, sh);
+  const uint32_t bad = route_counts_chunked(s, routes, n, hist, wc, b.rank_scratch, 0, 1, sh);
+  route_positions(s, routes, n, hist, reinterpret_cast<int*>(wc), b.rank_scratch, b.pos, bad, 0, 1, sh);
   route_publish(s, b.peers, f, hist, step, n, bad, 0, 1);
 }
 
 template <int SRC, int ELEM>
 __global__ void __launch_bounds__(kThreads, 1)
-k_dispatch(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, int64_t n, const void* __restrict__ routes,
-           int i32, uint64_t timeout_ns) {
+k_dispatch(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, int64_t n,
+           const int64_t* __restrict__ routes, uint64_t timeout_ns) {
   extern __shared__ __align__(16) uint8_t dsm[];
   __shared__ Shared sh;
   Flags* f = flags_of(b.region, s);
   const uint64_t step = cur_step(f);
   uint32_t* C = reinterpret_cast<uint32_t*>(dsm + cmat_offset(s));
   if (!wait_routes(s, f, route_of(b.region, s, (int)(step & 1)), C, step, timeout_ns, sh)) return;
-  int64_t* baseg = reinterpret_cast<int64_t*>(dsm);
+  int* baseg = reinterpret_cast<int*>(dsm);
   if (!dispatch_layout(s, C, baseg, baseg + s.experts, f, blockIdx.x == 0, sh)) return;
   if (*reinterpret_cast<volatile uint32_t*>(&f->err) & (TXB_EV_ROUTE_RANGE | TXB_EV_ROUTE_DUP)) return;
+  for (int q = threadIdx.x; q < s.ranks; q += blockDim.x) sh.cnt[q] = 0;
   if (threadIdx.x == 0) sh.direct = 0;
   __syncthreads();
-  dispatch_tokens<SRC, ELEM>(s, x, n, routes, i32, b.rank_scratch, b.gidx, b.peers, baseg, blockIdx.x,
-                             gridDim.x, sh, nullptr);
+  dispatch_tokens<SRC, ELEM>(s, x, n, routes, b.rank_scratch, b.gidx, b.peers, baseg, blockIdx.x, gridDim.x, sh);
   signal_counts(s, b.peers, offsetof(Flags, tok_ctr), sh);
 }
 
@@ -586,7 +598,7 @@ k_recv(txb_moe_shape s, txb_moe_bufs b, uint64_t timeout_ns) {
   const uint64_t step = cur_step(f);
   uint32_t* C = reinterpret_cast<uint32_t*>(dsm + cmat_offset(s));
   if (!wait_routes(s, f, route_of(b.region, s, (int)(step & 1)), C, step, timeout_ns, sh)) return;
-  recv_metadata(s, C, reinterpret_cast<int64_t*>(dsm), b.rows, b.sources, b.ret_slot, b.info,
+  recv_metadata(s, C, reinterpret_cast<int*>(dsm), b.rows, b.sources, b.ret_slot, b.info,
                 grouped_of(b.region, s), b.dirty, blockIdx.x, gridDim.x, sh);
   if (blockIdx.x == 0) wait_tokens(f, b.info, s.local_experts, timeout_ns);
 }
@@ -613,14 +625,17 @@ k_comb_recv(txb_moe_shape s, txb_moe_bufs b, const uint8_t* __restrict__ out, in
 // ------------------------------------------------------------ fused kernels
 
 // Route + dispatch + receive in one cooperative launch.  Every CTA counts
-// all n*R copies redundantly (no grid barrier needed; n*R is a decode-size
-// batch), CTA 0 publishes the count row, every CTA waits for the route rows,
-// derives the layout, stores its tokens, signals, then the grid fills the
-// receive metadata and CTA 0 waits for the incoming rows.
-template <int SRC, int ELEM>
+// all n*R copies redundantly (no grid barrier), the CTAs publish slices of
+// the count row, every CTA acquires the route matrix, derives the layout,
+// stores its tokens and signals; then the grid fills the receive metadata
+// and CTA 0 waits for the incoming rows.
+// DECODE (n == grid, vectorisable rows, R | 32, <= kMaxOwn copies per CTA):
+// the CTA's single token is read and encoded into registers before the
+// route exchange and stored once the layout is known.
+template <int SRC, int ELEM, bool DECODE>
 __global__ void __launch_bounds__(kThreads, 1)
 k_dispatch_fused(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, int64_t n,
-                 const void* __restrict__ routes, int i32, uint64_t timeout_ns) {
+                 const int64_t* __restrict__ routes, uint64_t timeout_ns) {
   extern __shared__ __align__(16) uint8_t dsm[];
   __shared__ Shared sh;
   Flags* f = flags_of(b.region, s);
@@ -629,32 +644,38 @@ k_dispatch_fused(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
   uint32_t* hist = reinterpret_cast<uint32_t*>(dsm);
   uint32_t* wc = hist + ((s.experts + 3) & ~3);
   stamp(b, 0);
-  // decode-sized batches (one token per CTA): read + encode the token now,
-  // before the route exchange, and keep it in registers until the layout
-  // is known
   RowRegs pre;
-  pre.ok = false;
-  if (n == ncta) encode_row_regs<SRC, ELEM>(x, cta, s.hidden, s.payload_bytes, pre, sh.red);
+  if constexpr (DECODE) encode_row_regs<SRC, ELEM>(x, cta, s.hidden, s.payload_bytes, pre, sh.red);
   stamp(b, 14);
-  const uint32_t bad = route_counts(s, routes, i32, n, hist, wc, b.rank_scratch, cta, ncta, sh);
+  uint32_t bad;
+  if constexpr (DECODE) bad = route_counts_direct(s, routes, n, hist, b.rank_scratch, cta, ncta, sh);
+  else bad = route_counts_chunked(s, routes, n, hist, wc, b.rank_scratch, cta, ncta, sh);
   stamp(b, 1);
   route_publish(s, b.peers, f, hist, step, n, bad, cta, ncta);
-  route_positions(s, routes, i32, n, hist, reinterpret_cast<int64_t*>(wc), b.rank_scratch, b.pos, bad, cta,
-                  ncta, sh);
+  route_positions(s, routes, n, hist, reinterpret_cast<int*>(wc), b.rank_scratch, b.pos, bad, cta, ncta, sh);
   stamp(b, 2);
   uint32_t* C = reinterpret_cast<uint32_t*>(dsm + cmat_offset(s));
   if (!wait_routes(s, f, route_of(b.region, s, (int)(step & 1)), C, step, timeout_ns, sh)) return;
   stamp(b, 3);
-  int64_t* baseg = reinterpret_cast<int64_t*>(dsm);
+  int* baseg = reinterpret_cast<int*>(dsm);
   if (!dispatch_layout(s, C, baseg, baseg + s.experts, f, cta == 0, sh)) return;
+  for (int q = threadIdx.x; q < s.ranks; q += blockDim.x) sh.cnt[q] = 0;
+  __syncthreads();
   stamp(b, 4);
-  if (!bad) dispatch_tokens<SRC, ELEM>(s, x, n, routes, i32, b.rank_scratch, b.gidx, b.peers, baseg, cta, ncta, sh,
-                                       &pre);
+  if (!bad) {
+    if constexpr (DECODE) {
+      token_dests(s, routes, b.rank_scratch, b.gidx, b.peers, baseg, cta, 0, sh);
+      if (pre.ok) store_row_regs<SRC, ELEM>(pre, s.hidden, s.scales, sh.dstp, s.topk);
+      else dispatch_row_slow<SRC, ELEM>(s, x, cta, sh);
+    } else {
+      dispatch_tokens<SRC, ELEM>(s, x, n, routes, b.rank_scratch, b.gidx, b.peers, baseg, cta, ncta, sh);
+    }
+  }
   stamp(b, 5);
   signal_counts(s, b.peers, offsetof(Flags, tok_ctr), sh);
   __syncthreads();
   stamp(b, 6);
-  recv_metadata(s, C, reinterpret_cast<int64_t*>(dsm), b.rows, b.sources, b.ret_slot, b.info,
+  recv_metadata(s, C, reinterpret_cast<int*>(dsm), b.rows, b.sources, b.ret_slot, b.info,
                 grouped_of(b.region, s), b.dirty, cta, ncta, sh);
   stamp(b, 7);
   if (cta == 0) wait_tokens(f, b.info, s.local_experts, timeout_ns);
@@ -848,8 +869,7 @@ int txb_moe_plan(txb_moe_shape* s) {
   return TXB_OK;
 }
 
-int txb_moe_route(const txb_moe_shape* s, const txb_moe_bufs* b, const void* routes, int routes_i32, int64_t n,
-                  void* stream) {
+int txb_moe_route(const txb_moe_shape* s, const txb_moe_bufs* b, const int64_t* routes, int64_t n, void* stream) {
   if (int rc = check(s, b)) return rc;
   if (n < 0 || n > s->max_tokens) {
     set_error("%lld tokens exceed the %d-token limit", (long long)n, s->max_tokens);
@@ -857,7 +877,7 @@ int txb_moe_route(const txb_moe_shape* s, const txb_moe_bufs* b, const void* rou
   }
   TXB_CUDA(cudaSetDevice(s->device));
   const size_t smem = smem_route(s->experts, kRouteThreads / 32);
-  return launch(k_route, 1, kRouteThreads, smem, (cudaStream_t)stream, false, *s, *b, routes, routes_i32, n);
+  return launch(k_route, 1, kRouteThreads, smem, (cudaStream_t)stream, false, *s, *b, routes, n);
 }
 
 #define TXB_SWITCH_SRC_ELEM(KIND, ELEMSZ, MACRO)         \
@@ -879,7 +899,7 @@ int txb_moe_route(const txb_moe_shape* s, const txb_moe_bufs* b, const void* rou
   } while (0)
 
 int txb_moe_dispatch(const txb_moe_shape* s, const txb_moe_bufs* b, const void* x, int src_kind, int64_t n,
-                     const void* routes, int routes_i32, uint64_t timeout_ns, int grid, void* stream) {
+                     const int64_t* routes, uint64_t timeout_ns, int grid, void* stream) {
   if (int rc = check(s, b)) return rc;
   TXB_CUDA(cudaSetDevice(s->device));
   if (grid <= 0) {
@@ -889,7 +909,7 @@ int txb_moe_dispatch(const txb_moe_shape* s, const txb_moe_bufs* b, const void* 
   const size_t smem = smem_main(s, false);
   cudaStream_t st = (cudaStream_t)stream;
 #define TXB_D(SRC, ELEM) \
-  return launch(k_dispatch<SRC, ELEM>, grid, kThreads, smem, st, false, *s, *b, x, n, routes, routes_i32, timeout_ns)
+  return launch(k_dispatch<SRC, ELEM>, grid, kThreads, smem, st, false, *s, *b, x, n, routes, timeout_ns)
   TXB_SWITCH_SRC_ELEM(src_kind, s->elem_size, TXB_D);
 #undef TXB_D
   return TXB_OK;
@@ -934,7 +954,7 @@ int txb_moe_combine_recv(const txb_moe_shape* s, const txb_moe_bufs* b, const vo
 }
 
 int txb_moe_dispatch_fused(const txb_moe_shape* s, const txb_moe_bufs* b, const void* x, int src_kind, int64_t n,
-                           const void* routes, int routes_i32, uint64_t timeout_ns, void* stream) {
+                           const int64_t* routes, uint64_t timeout_ns, void* stream) {
   if (int rc = check(s, b)) return rc;
   if (n < 0 || n > s->max_tokens) {
     set_error("%lld tokens exceed the %d-token limit", (long long)n, s->max_tokens);
@@ -949,13 +969,32 @@ int txb_moe_dispatch_fused(const txb_moe_shape* s, const txb_moe_bufs* b, const 
   const size_t smem = smem_main(s, true);
   cudaStream_t st = (cudaStream_t)stream;
   const int sms = sm_count(s->device);
+  // decode specialisation: one token per CTA, row vectorisable in registers
+  const int64_t srcb = src_kind == TXB_SRC_F32 ? 4 : 2;
+  const int epc = src_kind == TXB_SRC_ROWS ? 16 : 16 / s->elem_size;
+  const int64_t nchunk = src_kind == TXB_SRC_ROWS ? s->payload_bytes / 16 : s->hidden / epc;
+  bool vec;
+  if (src_kind == TXB_SRC_ROWS)
+    vec = (s->payload_bytes % 16 == 0) && ((uintptr_t)x % 16 == 0);
+  else {
+    const int64_t salign = epc * srcb >= 16 ? 16 : epc * srcb;
+    vec = ((int64_t)s->hidden * s->elem_size % 16 == 0) && (s->payload_bytes % 16 == 0) &&
+          ((uintptr_t)x % salign == 0) && ((int64_t)s->hidden * srcb % salign == 0);
+  }
+  const bool decode = n >= 1 && n <= sms && s->topk <= kMaxOwn && vec && nchunk <= 2 * kThreads;
   const int want = (int)(n < 1 ? 1 : (n < sms ? n : sms));
-#define TXB_F(SRC, ELEM)                                                                          \
-  do {                                                                                            \
-    auto kfn = k_dispatch_fused<SRC, ELEM>;                                                       \
-    if (int rc = set_smem(kfn, smem)) return rc;                                                  \
-    const int grid = coop_grid(kfn, s->device, smem, want);                                       \
-    return launch(kfn, grid, kThreads, smem, st, true, *s, *b, x, n, routes, routes_i32, timeout_ns); \
+#define TXB_F(SRC, ELEM)                                                                            \
+  do {                                                                                              \
+    if (decode) {                                                                                   \
+      auto kd = k_dispatch_fused<SRC, ELEM, true>;                                                  \
+      if (int rc = set_smem(kd, smem)) return rc;                                                   \
+      if (coop_grid(kd, s->device, smem, want) == want)                                             \
+        return launch(kd, want, kThreads, smem, st, true, *s, *b, x, n, routes, timeout_ns);        \
+    }                                                                                               \
+    auto kg = k_dispatch_fused<SRC, ELEM, false>;                                                   \
+    if (int rc = set_smem(kg, smem)) return rc;                                                     \
+    const int grid = coop_grid(kg, s->device, smem, want);                                          \
+    return launch(kg, grid, kThreads, smem, st, true, *s, *b, x, n, routes, timeout_ns);            \
   } while (0)
   TXB_SWITCH_SRC_ELEM(src_kind, s->elem_size, TXB_F);
 #undef TXB_F

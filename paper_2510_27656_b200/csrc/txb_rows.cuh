@@ -100,7 +100,7 @@ __device__ __forceinline__ uint4 encode_chunk(const float* v, float scale) {
 //   destinations;
 //   general path: element by element (arbitrary hidden / payload sizes).
 template <int SRC, int ELEM>
-__device__ void encode_store_row(const void* x, int64_t t, int H, int scales, int64_t P,
+__device__ __noinline__ void encode_store_row(const void* x, int64_t t, int H, int scales, int64_t P,
                                  uint8_t* const* dst, int nd, float* red) {
   const int tid = threadIdx.x, nt = blockDim.x;
   const int64_t rowoff = t * (int64_t)H;

@@ -556,14 +556,11 @@ class MoeRank:
                 raise ProtocolError(f"route array shape {tuple(routes.shape)} is not (tokens, {spec.topk})")
             if routes.shape[0] > spec.max_tokens:
                 raise ProtocolError(f"{routes.shape[0]} tokens exceed the {spec.max_tokens}-token limit")
-            if routes.dtype not in (torch.int64, torch.int32):
-                routes = routes.long()
-            r_dev = routes.contiguous()
+            r_dev = routes.long().contiguous()   # int64, like railtx
         else:
             r = _check_routes(spec, routes.cpu().numpy() if isinstance(routes, torch.Tensor) else routes)
             r_dev = torch.from_numpy(np.ascontiguousarray(r)).to(dev)
         n = int(r_dev.shape[0])
-        i32 = 1 if r_dev.dtype == torch.int32 else 0
         if isinstance(payload, torch.Tensor) and payload.is_cuda:
             p = payload.contiguous()
             if p.dtype == torch.uint8:
@@ -599,16 +596,16 @@ class MoeRank:
         if st.fused:
             # route + dispatch + receive metadata in one cooperative kernel
             _lib.call("txb_moe_dispatch_fused", self._shape_p, self._bufs_p, _sp(p), kind, n,
-                      _sp(r_dev), i32, self._tmo(None), sid)
+                      _sp(r_dev), self._tmo(None), sid)
             return
-        _lib.call("txb_moe_route", self._shape_p, self._bufs_p, _sp(r_dev), i32, n, sid)
+        _lib.call("txb_moe_route", self._shape_p, self._bufs_p, _sp(r_dev), n, sid)
         if _between is not None:      # bench hook: split route / dispatch launches
             _between()
         if self.host_gated:
             step = st.step
             self._gate(lambda c: all(v >= step for v in c["route_tag"][step & 1])
                        and all(v >= step - 1 for v in c["done"]), step, "route counts", None)
-        _lib.call("txb_moe_dispatch", self._shape_p, self._bufs_p, _sp(p), kind, n, _sp(r_dev), i32,
+        _lib.call("txb_moe_dispatch", self._shape_p, self._bufs_p, _sp(p), kind, n, _sp(r_dev),
                   self._tmo(None), 0, sid)
         if self.host_gated:
             torch.cuda.current_stream(self.device).synchronize()
