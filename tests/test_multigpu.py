@@ -1,0 +1,127 @@
+"""Multi-GPU parity: one rank per GPU in one process (threads, peer access)
+and one rank per process (torchrun, CUDA IPC).  Skipped with fewer GPUs
+than ranks; run with `gpurun --gpus N`."""
+
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+
+from golden_io import load_moe
+from oracle import moe_oracle as mo
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+NGPU = torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+if NGPU:
+    from moe_driver import close_mesh, ospec_of, run_moe_round
+    from paper_2510_27656_b200 import moe
+    from paper_2510_27656_b200.engine import local_engines
+
+
+def _np(x):
+    return x.cpu().numpy() if isinstance(x, torch.Tensor) else np.asarray(x)
+
+
+@pytest.mark.parametrize("name", ["cfg1_full", "cfg1_rand", "check_moe", "n4_e16_t9_r4", "n4_e8_t5_r1",
+                                  "n8_e16_t7_r3", "fp8_n4_h64_s1", "fp8_dsv3ish", "empty"])
+def test_golden_one_rank_per_gpu(name):
+    case = load_moe(name)
+    spec = moe.RoutingSpec(**case.spec_args)
+    if NGPU < spec.ranks:
+        pytest.skip(f"needs {spec.ranks} GPUs")
+    mesh = moe.build_mesh(local_engines(list(range(spec.ranks))), spec, timeout=20.0)
+    assert not mesh[0].host_gated
+    try:
+        for st in case.steps:
+            res = run_moe_round(mesh, spec, st.routes, st.values, st.weights, timeout=20.0)
+            for q in range(spec.ranks):
+                g, comb, pos = res[q]
+                assert np.array_equal(pos, st.pos[q])
+                assert np.array_equal(_np(g.rows), st.rows[q])
+                assert np.array_equal(_np(g.sources), st.sources[q])
+                assert np.array_equal(_np(g.data), st.data[q])
+                assert np.array_equal(comb, st.combined[q])
+    finally:
+        close_mesh(mesh)
+
+
+@pytest.mark.parametrize("ranks", [2, 4, 8])
+def test_dsv3_decode_device_mode(ranks):
+    """DeepSeek-V3 decode shape, EP=ranks over NVLink, fused fp8 encode in the
+    dispatch kernel, bf16 combine rows; several steps back to back."""
+    if NGPU < ranks:
+        pytest.skip(f"needs {ranks} GPUs")
+    import threading
+    spec = moe.RoutingSpec(ranks=ranks, experts=256, max_tokens=128, topk=8, hidden=7168,
+                           elem_size=1, scales=56, comb_elem_size=2, comb_scales=0)
+    os_ = ospec_of(spec)
+    cs = mo.Spec(ranks, 256, 128, 8, hidden=7168, elem_size=2, scales=0)
+    mesh = moe.build_mesh(local_engines(list(range(ranks))), spec, timeout=20.0)
+    try:
+        for step in range(3):
+            rng = np.random.default_rng(200 + step)
+            routes, values, weights = mo.random_step(os_, rng, tokens=128)
+            xb = [torch.from_numpy(v).to(torch.bfloat16) for v in values]
+            ref = mo.dispatch(os_, routes, [mo.encode_tokens(os_, x.float().numpy()) for x in xb])
+            got = [None] * ranks
+            outs_np = [None] * ranks
+            errs = []
+
+            def worker(r):
+                try:
+                    torch.cuda.set_device(r)
+                    rk = mesh[r]
+                    rk.dispatch_send(xb[r].cuda(r), torch.from_numpy(routes[r]).cuda(r))
+                    g = rk.dispatch_recv()
+                    dec = moe.decode_tokens(spec, g.data)
+                    y = (dec * 0.5).to(torch.bfloat16)
+                    outs_np[r] = (g.data.cpu().numpy(), y.float().cpu().numpy())
+                    rk.combine_send(y)
+                    got[r] = rk.combine_recv(torch.from_numpy(weights[r]).cuda(r), out_dtype=torch.bfloat16)
+                    torch.cuda.synchronize(r)
+                except Exception as e:  # noqa: BLE001
+                    errs.append(e)
+
+            th = [threading.Thread(target=worker, args=(r,)) for r in range(ranks)]
+            for t in th:
+                t.start()
+            for t in th:
+                t.join(120)
+            if errs:
+                raise errs[0]
+            for r in range(ranks):
+                assert np.array_equal(outs_np[r][0], ref.ranks[r].grouped.data)
+            outs = [mo.bf16_encode(outs_np[r][1]).view(np.uint8).reshape(outs_np[r][1].shape[0], -1)
+                    for r in range(ranks)]
+            comb = mo.combine(os_, ref, outs, weights, comb_spec=cs)
+            for r in range(ranks):
+                want = mo.bf16_encode(comb[r])
+                assert np.array_equal(got[r].view(torch.int16).cpu().numpy().view(np.uint16), want)
+    finally:
+        close_mesh(mesh)
+
+
+@pytest.mark.parametrize("ranks", [2])
+def test_torchrun_ipc_bench_smoke(ranks, tmp_path):
+    """One rank per process over CUDA IPC (connect_process_group): a short
+    bench run under torchrun must finish and print one JSON line."""
+    if NGPU < ranks:
+        pytest.skip(f"needs {ranks} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={ranks}",
+           "--master-addr", "127.0.0.1", "--master-port", "29531", str(ROOT / "bench.py"),
+           "--gpus", str(ranks), "--steps", "5", "--warmup", "3", "--no-cpu-baseline"]
+    env = dict(os.environ)
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
+    assert p.returncode == 0, p.stderr[-4000:]
+    import json
+    line = [x for x in p.stdout.splitlines() if x.startswith("{")][-1]
+    d = json.loads(line)
+    assert d["n_gpus"] == ranks and d["value"] > 0
