@@ -68,10 +68,13 @@ __host__ __device__ inline size_t smem_recv(int N, int L) {
   return (size_t)(3 * N * L + 1 + 2 * L + 1 + L * (N + 1) + N) * 4;
 }
 __host__ __device__ inline size_t smem_cmat(int N, int E) { return ((size_t)N * E * 4 + 15) / 16 * 16; }
-// the route matrix copy (Cs) lives after the layout / recv scratch
+// layout scratch [0, recv_offset), receive tables [recv_offset, cmat_offset),
+// route matrix copy (Cs) after them; the route-count phase overlaps all
+__host__ __device__ inline size_t recv_offset(const txb_moe_shape& s) {
+  return (smem_layout(s.experts) + 15) / 16 * 16;
+}
 __host__ __device__ inline size_t cmat_offset(const txb_moe_shape& s) {
-  const size_t a = smem_layout(s.experts), b = smem_recv(s.ranks, s.local_experts);
-  return ((a > b ? a : b) + 15) / 16 * 16;
+  return recv_offset(s) + (smem_recv(s.ranks, s.local_experts) + 15) / 16 * 16;
 }
 
 struct Shared {  // static shared state of one CTA
@@ -396,26 +399,44 @@ __device__ void signal_counts(const txb_moe_shape& s, void* const* peers, size_t
 
 // ------------------------------------------------------------------- P5
 
-// Receive metadata for grouped rows (moe.py:699-722): every CTA derives the
-// per-(source, local expert) tables from the route matrix; the grid then
-// walks the grouped rows, one warp per row (lane 0 writes rows / sources /
-// return slot; the warp zero-fills padding rows that may hold stale data).
-__device__ __noinline__ void recv_metadata(const txb_moe_shape& s, const uint32_t* C, int* sm, int64_t* rows,
-                                           int64_t* sources, int32_t* ret, int64_t* info, uint8_t* G,
-                                           uint8_t* dirty, int cta, int ncta, Shared& sh) {
+// Receive metadata for grouped rows (moe.py:699-722), in two parts:
+// recv_tables (block barriers) derives the per-(source, local expert) tables
+// from the route matrix into shared memory; recv_rows (no barriers) walks
+// the grouped rows, one warp per row: lane 0 writes rows / sources / return
+// slot, the warp zero-fills padding rows that may hold stale data.
+struct RecvTables {
+  int* a;        // [N][L] counts into my experts
+  int* rowbase;  // [N*L+1] flattened exclusive prefix = recv slot base
+  int* retbase;  // [N][L] send slot base on the source
+  int* gstart;   // [L+1]
+  int* gsize;    // [L]
+  int* srcpre;   // [L][N+1]
+  int* pre_all;  // [N] sum_{e' < me*L} C[q][e']
+  int padded_total, recv_total;
+};
+
+__device__ __forceinline__ RecvTables recv_carve(const txb_moe_shape& s, int* sm) {
+  const int N = s.ranks, L = s.local_experts;
+  RecvTables t;
+  t.a = sm;
+  t.rowbase = t.a + N * L;
+  t.retbase = t.rowbase + N * L + 1;
+  t.gstart = t.retbase + N * L;
+  t.gsize = t.gstart + L + 1;
+  t.srcpre = t.gsize + L;
+  t.pre_all = t.srcpre + L * (N + 1);
+  return t;
+}
+
+__device__ __noinline__ void recv_tables(const txb_moe_shape& s, const uint32_t* C, int* sm, int64_t* info,
+                                         int cta, Shared& sh) {
   const int N = s.ranks, E = s.experts, L = s.local_experts, me = s.me;
   const int tid = threadIdx.x, nt = blockDim.x;
-  int* a = sm;                         // [N][L] counts into my experts
-  int* rowbase = a + N * L;            // [N*L+1] flattened exclusive prefix = recv slot base
-  int* retbase = rowbase + N * L + 1;  // [N][L] send slot base on the source
-  int* gstart = retbase + N * L;       // [L+1]
-  int* gsize = gstart + L + 1;         // [L]
-  int* srcpre = gsize + L;             // [L][N+1]
-  int* pre_all = srcpre + L * (N + 1); // [N] sum_{e' < me*L} C[q][e']
+  RecvTables t = recv_carve(s, sm);
   for (int i = tid; i < N * L; i += nt) {
     const int q = i / L, le = i - q * L;
-    a[i] = (int)C[q * E + me * L + le];
-    rowbase[i] = a[i];
+    t.a[i] = (int)C[q * E + me * L + le];
+    t.rowbase[i] = t.a[i];
   }
   {
     const int warp = tid >> 5, lane = tid & 31, nwarp = nt >> 5;
@@ -423,53 +444,60 @@ __device__ __noinline__ void recv_metadata(const txb_moe_shape& s, const uint32_
       int acc = 0;
       for (int e = lane; e < me * L; e += 32) acc += (int)C[q * E + e];
       for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (lane == 0) pre_all[q] = acc;
+      if (lane == 0) t.pre_all[q] = acc;
     }
   }
   __syncthreads();
   for (int le = tid; le < L; le += nt) {
     int run = 0;
     for (int q = 0; q < N; ++q) {
-      srcpre[le * (N + 1) + q] = run;
-      run += a[q * L + le];
+      t.srcpre[le * (N + 1) + q] = run;
+      run += t.a[q * L + le];
     }
-    srcpre[le * (N + 1) + N] = run;
-    gsize[le] = run;
-    gstart[le] = pad_up(run);
+    t.srcpre[le * (N + 1) + N] = run;
+    t.gsize[le] = run;
+    t.gstart[le] = pad_up(run);
   }
   __syncthreads();
-  const int padded_total = block_scan_i32(gstart, L, sh.tmp);
+  const int padded_total = block_scan_i32(t.gstart, L, sh.tmp);
   // recv_start[me][q] + sum_{le'<le} a[q][le'] is the exclusive prefix of a[]
   // flattened source-major (moe.py:178-184, 204-213)
-  const int recv_total = block_scan_i32(rowbase, N * L, sh.tmp);
+  const int recv_total = block_scan_i32(t.rowbase, N * L, sh.tmp);
   if (tid == 0) {
-    gstart[L] = padded_total;
-    rowbase[N * L] = recv_total;
+    t.gstart[L] = padded_total;
+    t.rowbase[N * L] = recv_total;
   }
   __syncthreads();
-  for (int i = tid; i < N * L; i += nt) retbase[i] = pre_all[i / L] + (rowbase[i] - rowbase[(i / L) * L]);
+  for (int i = tid; i < N * L; i += nt) t.retbase[i] = t.pre_all[i / L] + (t.rowbase[i] - t.rowbase[(i / L) * L]);
   __syncthreads();
   if (cta == 0) {
     for (int le = tid; le < L; le += nt) {
-      info[le] = gsize[le];
-      info[L + le] = gstart[le];
+      info[le] = t.gsize[le];
+      info[L + le] = t.gstart[le];
     }
     if (tid == 0) {
       info[2 * L] = padded_total;
       info[2 * L + 1] = recv_total;
     }
   }
+}
+
+__device__ __noinline__ void recv_rows(const txb_moe_shape& s, int* sm, int64_t* rows, int64_t* sources,
+                                       int32_t* ret, uint8_t* G, uint8_t* dirty, int cta, int ncta) {
+  const int N = s.ranks, L = s.local_experts;
+  const RecvTables t = recv_carve(s, sm);
+  const int padded_total = t.gstart[L];
   const int64_t P = s.payload_bytes;
-  const int warp = tid >> 5, lane = tid & 31, nwarp = nt >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
   for (int g = cta * nwarp + warp; g < padded_total; g += ncta * nwarp) {
     int lo = 0, hi = L - 1;  // last le with gstart[le] <= g
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
-      if (gstart[mid] <= g) lo = mid; else hi = mid - 1;
+      if (t.gstart[mid] <= g) lo = mid; else hi = mid - 1;
     }
     const int le = lo;
-    const int k = g - gstart[le];
-    if (k >= gsize[le]) {
+    const int k = g - t.gstart[le];
+    if (k >= t.gsize[le]) {
       // padding rows read as zero (moe.py:719); only rows that held data
       // since they were last zeroed need the store
       const bool d = dirty[g] != 0;
@@ -482,13 +510,13 @@ __device__ __noinline__ void recv_metadata(const txb_moe_shape& s, const uint32_
       }
     } else if (lane == 0) {
       dirty[g] = 1;
-      const int* sp = srcpre + le * (N + 1);
+      const int* sp = t.srcpre + le * (N + 1);
       int q = 0;
       while (sp[q + 1] <= k) ++q;
       const int kk = k - sp[q];
-      rows[g] = rowbase[q * L + le] + kk;
+      rows[g] = t.rowbase[q * L + le] + kk;
       sources[g] = q;
-      ret[g] = retbase[q * L + le] + kk;
+      ret[g] = t.retbase[q * L + le] + kk;
     }
   }
 }
@@ -503,6 +531,11 @@ __device__ void wait_tokens(Flags* f, int64_t* info, int L, uint64_t timeout_ns)
 
 // ------------------------------------------------------------------- C1
 
+// Rows are moved in 2 KiB chunks (one warp, four 16-byte loads per lane in
+// flight before the four peer stores) so a step's return traffic spreads
+// over every warp of the grid instead of one warp per 14 KiB row.
+constexpr int kChunk = 2048;
+
 __device__ void combine_send_rows(const txb_moe_shape& s, const uint8_t* out, int64_t ld, void* const* peers,
                                   const int64_t* sources, const int32_t* ret, const int64_t* info, int cta,
                                   int ncta, Shared& sh) {
@@ -512,10 +545,32 @@ __device__ void combine_send_rows(const txb_moe_shape& s, const uint8_t* out, in
   if (N == 1) return;  // every row is this rank's own: read in place by C2
   const int total = (int)info[2 * L];
   const int64_t Pc = s.comb_bytes;
-  const int lane = tid & 31, nwarp = blockDim.x >> 5;
-  for (int g = cta * nwarp + (tid >> 5); g < total; g += ncta * nwarp) {
+  const int lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
+  const bool vec = (Pc % 16 == 0) && (ld % 16 == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+  if (vec) {
+    const int cpr = (int)((Pc + kChunk - 1) / kChunk);
+    const int items = total * cpr;
+    for (int it = cta * nwarp + warp; it < items; it += ncta * nwarp) {
+      const int g = it / cpr, c = it - g * cpr;
+      const int q = (int)sources[g];
+      if (q < 0 || q == s.me) continue;  // padding, or read in place by C2
+      const int4* src = reinterpret_cast<const int4*>(out + (int64_t)g * ld + (int64_t)c * kChunk);
+      int4* dst = reinterpret_cast<int4*>(comb_of(peers[q], s) + (int64_t)ret[g] * Pc + (int64_t)c * kChunk);
+      const int n16 = (int)(min((int64_t)kChunk, Pc - (int64_t)c * kChunk) >> 4);
+      int4 v[kChunk / 512];
+#pragma unroll
+      for (int u = 0; u < kChunk / 512; ++u)
+        if (lane + 32 * u < n16) v[u] = src[lane + 32 * u];
+#pragma unroll
+      for (int u = 0; u < kChunk / 512; ++u)
+        if (lane + 32 * u < n16) dst[lane + 32 * u] = v[u];
+      if (c == 0 && lane == 0) atomicAdd(&sh.cnt[q], 1u);
+    }
+    return;
+  }
+  for (int g = cta * nwarp + warp; g < total; g += ncta * nwarp) {
     const int q = (int)sources[g];
-    if (q < 0 || q == s.me) continue;  // padding, or read in place by C2
+    if (q < 0 || q == s.me) continue;
     copy_row(comb_of(peers[q], s) + (int64_t)ret[g] * Pc, out + (int64_t)g * ld, Pc, lane, 32);
     if (lane == 0) atomicAdd(&sh.cnt[q], 1u);
   }
@@ -598,8 +653,9 @@ k_recv(txb_moe_shape s, txb_moe_bufs b, uint64_t timeout_ns) {
   const uint64_t step = cur_step(f);
   uint32_t* C = reinterpret_cast<uint32_t*>(dsm + cmat_offset(s));
   if (!wait_routes(s, f, route_of(b.region, s, (int)(step & 1)), C, step, timeout_ns, sh)) return;
-  recv_metadata(s, C, reinterpret_cast<int*>(dsm), b.rows, b.sources, b.ret_slot, b.info,
-                grouped_of(b.region, s), b.dirty, blockIdx.x, gridDim.x, sh);
+  int* rt = reinterpret_cast<int*>(dsm + recv_offset(s));
+  recv_tables(s, C, rt, b.info, blockIdx.x, sh);
+  recv_rows(s, rt, b.rows, b.sources, b.ret_slot, grouped_of(b.region, s), b.dirty, blockIdx.x, gridDim.x);
   if (blockIdx.x == 0) wait_tokens(f, b.info, s.local_experts, timeout_ns);
 }
 
@@ -659,6 +715,8 @@ k_dispatch_fused(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
   stamp(b, 3);
   int* baseg = reinterpret_cast<int*>(dsm);
   if (!dispatch_layout(s, C, baseg, baseg + s.experts, f, cta == 0, sh)) return;
+  int* rt = reinterpret_cast<int*>(dsm + recv_offset(s));
+  recv_tables(s, C, rt, b.info, cta, sh);
   for (int q = threadIdx.x; q < s.ranks; q += blockDim.x) sh.cnt[q] = 0;
   __syncthreads();
   stamp(b, 4);
@@ -672,11 +730,10 @@ k_dispatch_fused(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
     }
   }
   stamp(b, 5);
+  // thread 0 fences and signals while the other warps fill the metadata
   signal_counts(s, b.peers, offsetof(Flags, tok_ctr), sh);
-  __syncthreads();
   stamp(b, 6);
-  recv_metadata(s, C, reinterpret_cast<int*>(dsm), b.rows, b.sources, b.ret_slot, b.info,
-                grouped_of(b.region, s), b.dirty, cta, ncta, sh);
+  recv_rows(s, rt, b.rows, b.sources, b.ret_slot, grouped_of(b.region, s), b.dirty, cta, ncta);
   stamp(b, 7);
   if (cta == 0) wait_tokens(f, b.info, s.local_experts, timeout_ns);
   stamp(b, 8);
