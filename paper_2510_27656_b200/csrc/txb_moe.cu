@@ -51,9 +51,14 @@ constexpr int kMaxOwn = 64;        // copies per CTA of the direct-count path
 
 __device__ __forceinline__ int pad_up(int x) { return (x + kGroupPad - 1) / kGroupPad * kGroupPad; }
 
-// Optional phase stamps for profiling (txb_moe_bufs.prof).
+// Optional phase stamps for profiling (txb_moe_bufs.prof, [grid][32]).
+__device__ uint64_t* g_prof = nullptr;
+__device__ __forceinline__ void substamp(int k) {
+  uint64_t* p = g_prof;
+  if (p && threadIdx.x == 0) p[blockIdx.x * 32 + k] = globaltimer();
+}
 __device__ __forceinline__ void stamp(const txb_moe_bufs& b, int k) {
-  if (b.prof && threadIdx.x == 0) b.prof[blockIdx.x * 16 + k] = globaltimer();
+  if (b.prof && threadIdx.x == 0) b.prof[blockIdx.x * 32 + k] = globaltimer();
 }
 
 __device__ __forceinline__ uint64_t cur_step(Flags* f) {
@@ -115,6 +120,7 @@ __device__ uint32_t route_counts_direct(const txb_moe_shape& s, const int64_t* r
     sh.direct = 1;
   }
   __syncthreads();
+  substamp(21);
   const bool lanes = (32 % R) == 0;
   for (int base = 0; base < m; base += blockDim.x) {
     const int i = base + tid;
@@ -141,6 +147,7 @@ __device__ uint32_t route_counts_direct(const txb_moe_shape& s, const int64_t* r
       if (sh.own_e[k] == (int)v && i < sh.own_i[k]) atomicAdd(&sh.own_rank[k], 1u);
   }
   __syncthreads();
+  substamp(22);
   for (int k = tid; k < nw; k += blockDim.x) rank_out[sh.own_i[k]] = (int32_t)sh.own_rank[k];
   const uint32_t b = sh.bad;
   if (b)
@@ -300,7 +307,9 @@ __device__ bool dispatch_layout(const txb_moe_shape& s, const uint32_t* C, int* 
     if (book && e / L == s.me) atomicAdd(&sh.recv_me, (uint32_t)col);
   }
   __syncthreads();
+  substamp(16);
   const int tot = block_scan_i32(padded, E, sh.tmp);
+  substamp(17);
   if (tid == 0) padded[E] = tot;
   __syncthreads();
   for (int e = tid; e < E; e += blockDim.x) baseg[e] += padded[e] - padded[(e / L) * L];
@@ -448,6 +457,7 @@ __device__ __noinline__ void recv_tables(const txb_moe_shape& s, const uint32_t*
     }
   }
   __syncthreads();
+  substamp(18);
   for (int le = tid; le < L; le += nt) {
     int run = 0;
     for (int q = 0; q < N; ++q) {
@@ -459,10 +469,12 @@ __device__ __noinline__ void recv_tables(const txb_moe_shape& s, const uint32_t*
     t.gstart[le] = pad_up(run);
   }
   __syncthreads();
+  substamp(19);
   const int padded_total = block_scan_i32(t.gstart, L, sh.tmp);
   // recv_start[me][q] + sum_{le'<le} a[q][le'] is the exclusive prefix of a[]
   // flattened source-major (moe.py:178-184, 204-213)
   const int recv_total = block_scan_i32(t.rowbase, N * L, sh.tmp);
+  substamp(20);
   if (tid == 0) {
     t.gstart[L] = padded_total;
     t.rowbase[N * L] = recv_total;
@@ -699,6 +711,8 @@ k_dispatch_fused(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
   const int cta = blockIdx.x, ncta = gridDim.x;
   uint32_t* hist = reinterpret_cast<uint32_t*>(dsm);
   uint32_t* wc = hist + ((s.experts + 3) & ~3);
+  if (threadIdx.x == 0 && blockIdx.x == 0) g_prof = b.prof;
+  __syncthreads();
   stamp(b, 0);
   RowRegs pre;
   if constexpr (DECODE) encode_row_regs<SRC, ELEM>(x, cta, s.hidden, s.payload_bytes, pre, sh.red);
@@ -715,6 +729,7 @@ k_dispatch_fused(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
   stamp(b, 3);
   int* baseg = reinterpret_cast<int*>(dsm);
   if (!dispatch_layout(s, C, baseg, baseg + s.experts, f, cta == 0, sh)) return;
+  stamp(b, 15);
   int* rt = reinterpret_cast<int*>(dsm + recv_offset(s));
   recv_tables(s, C, rt, b.info, cta, sh);
   for (int q = threadIdx.x; q < s.ranks; q += blockDim.x) sh.cnt[q] = 0;

@@ -20,16 +20,19 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--ranks", type=int, default=torch.cuda.device_count())
 ap.add_argument("--tokens", type=int, default=128)
 ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--noflush", action="store_true")
 a = ap.parse_args()
 N, T, H, E, R = a.ranks, a.tokens, 7168, 256, 8
 spec = moe.RoutingSpec(N, E, T, R, hidden=H, elem_size=1, scales=56, comb_elem_size=2, comb_scales=0)
 mesh = moe.build_mesh(local_engines(list(range(N))), spec, timeout=20.0)
-names = ["start", "counted", "positions", "routes-in", "layout", "stored", "signalled", "metadata",
-         "tokens-in", "c:start", "c:sent", "c:signalled", "c:reduced", "c:end", "pre-encoded"]
-order = [0, 14, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13]
+names = ["start", "counted", "positions", "routes-in", "tables", "stored", "signalled", "metadata",
+         "tokens-in", "c:start", "c:sent", "c:signalled", "c:reduced", "c:end", "pre-encoded", "layout",
+         "L:col-done", "L:scan-done", "T:loaded", "T:srcpre", "T:scans", "RC:owned", "RC:counted"]
+order = [0, 14, 21, 22, 1, 2, 3, 16, 17, 15, 18, 19, 20, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13]
 stamps = [None] * N
 times = [None] * N
 bar = threading.Barrier(N)
+CAPTURE = threading.Lock()
 
 
 def worker(r):
@@ -43,7 +46,7 @@ def worker(r):
     side = torch.cuda.Stream()
     torch.cuda.set_stream(side)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
-    prof = torch.zeros(148 * 16, dtype=torch.int64, device="cuda")
+    prof = torch.zeros(148 * 32, dtype=torch.int64, device="cuda")
 
     def one():
         rk.dispatch_send(x, rt, sync=False)
@@ -56,16 +59,14 @@ def worker(r):
     torch.cuda.synchronize()
     bar.wait()
     g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g):
-        one()
     rk._bufs.prof = prof.data_ptr()
-    # re-capture so the graph carries the stamp pointer
-    g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g):
-        one()
+    with CAPTURE:
+        with torch.cuda.graph(g, stream=side, capture_error_mode="thread_local"):
+            one()
     res, ts = [], []
     for _ in range(a.reps):
-        flush.fill_(1)
+        if not a.noflush:
+            flush.fill_(1)
         prof.zero_()
         torch.cuda.synchronize()
         bar.wait()
@@ -75,7 +76,7 @@ def worker(r):
         g.replay()
         e1.record()
         torch.cuda.synchronize()
-        res.append(prof.view(148, 16).cpu().numpy().astype(np.float64))
+        res.append(prof.view(148, 32).cpu().numpy().astype(np.float64))
         ts.append(e0.elapsed_time(e1) * 1e3)
     rk._bufs.prof = 0
     stamps[r] = res[-1]
