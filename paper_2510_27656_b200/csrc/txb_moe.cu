@@ -715,11 +715,14 @@ k_dispatch_fused(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
   __syncthreads();
   stamp(b, 0);
   RowRegs pre;
-  if constexpr (DECODE) encode_row_regs<SRC, ELEM>(x, cta, s.hidden, s.payload_bytes, pre, sh.red);
-  stamp(b, 14);
+  RowRaw raw;
+  // issue the token's loads first; route counting runs while they land
+  if constexpr (DECODE) load_row_raw<SRC, ELEM>(x, cta, s.hidden, s.payload_bytes, raw);
   uint32_t bad;
   if constexpr (DECODE) bad = route_counts_direct(s, routes, n, hist, b.rank_scratch, cta, ncta, sh);
   else bad = route_counts_chunked(s, routes, n, hist, wc, b.rank_scratch, cta, ncta, sh);
+  stamp(b, 14);
+  if constexpr (DECODE) finish_row_regs<SRC, ELEM>(raw, pre, sh.red);
   stamp(b, 1);
   route_publish(s, b.peers, f, hist, step, n, bad, cta, ncta);
   route_positions(s, routes, n, hist, reinterpret_cast<int*>(wc), b.rank_scratch, b.pos, bad, cta, ncta, sh);

@@ -193,38 +193,80 @@ struct RowRegs {
   bool ok;     // false: shape not eligible, use encode_store_row later
 };
 
+// Raw source bytes of a thread's (up to) two chunks, loaded before they are
+// needed so the HBM latency overlaps other work (route counting).
+struct RowRaw {
+  uint4 r[2][4];
+  int nchunk;
+  bool ok;
+};
+
 template <int SRC, int ELEM>
-__device__ void encode_row_regs(const void* x, int64_t t, int H, int64_t P, RowRegs& r, float* red) {
+__device__ __forceinline__ void load_row_raw(const void* x, int64_t t, int H, int64_t P, RowRaw& rr) {
   const int tid = threadIdx.x, nt = blockDim.x;
-  r.ok = false;
-  r.scale = 1.0f;
+  rr.ok = false;
   if constexpr (SRC == TXB_SRC_ROWS) {
     const uint8_t* src = reinterpret_cast<const uint8_t*>(x) + t * P;
-    r.nchunk = (int)(P >> 4);
-    if ((P & 15) || (reinterpret_cast<uintptr_t>(src) & 15) || r.nchunk > 2 * nt) return;
+    rr.nchunk = (int)(P >> 4);
+    if ((P & 15) || (reinterpret_cast<uintptr_t>(src) & 15) || rr.nchunk > 2 * nt) return;
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const int c = tid + u * nt;
-      if (c < r.nchunk) r.c[u] = reinterpret_cast<const uint4*>(src)[c];
+      if (c < rr.nchunk) rr.r[u][0] = reinterpret_cast<const uint4*>(src)[c];
     }
-    r.ok = true;
   } else {
     constexpr int EPC = 16 / ELEM;
+    constexpr int SB = SRC == TXB_SRC_F32 ? 4 : 2;  // source bytes per element
+    constexpr int CB = EPC * SB;                     // source bytes per chunk (8..64)
     const int64_t rowoff = t * (int64_t)H;
-    const int64_t srcbytes = (SRC == TXB_SRC_F32 ? 4 : 2);
-    const int64_t salign = (EPC * srcbytes) >= 16 ? 16 : EPC * srcbytes;
-    r.nchunk = H / EPC;
-    if (((H * ELEM) % 16) || (P % 16) || r.nchunk > 2 * nt ||
-        ((reinterpret_cast<uintptr_t>(x) + rowoff * srcbytes) % salign))
+    const int64_t salign = CB >= 16 ? 16 : CB;
+    rr.nchunk = H / EPC;
+    if (((H * ELEM) % 16) || (P % 16) || rr.nchunk > 2 * nt ||
+        ((reinterpret_cast<uintptr_t>(x) + rowoff * SB) % salign))
       return;
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(x) + rowoff * SB;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int c = tid + u * nt;
+      if (c < rr.nchunk) {
+        if constexpr (CB >= 16) {
+#pragma unroll
+          for (int k = 0; k < CB / 16; ++k) rr.r[u][k] = reinterpret_cast<const uint4*>(src + (int64_t)c * CB)[k];
+        } else {
+          const uint2 v = *reinterpret_cast<const uint2*>(src + (int64_t)c * CB);
+          rr.r[u][0] = make_uint4(v.x, v.y, 0, 0);
+        }
+      }
+    }
+  }
+  rr.ok = true;
+}
+
+// Finish a raw row into encoded chunks (per-row amax reduce for fp8).
+template <int SRC, int ELEM>
+__device__ void finish_row_regs(const RowRaw& rr, RowRegs& r, float* red) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  r.ok = rr.ok;
+  r.nchunk = rr.nchunk;
+  r.scale = 1.0f;
+  if (!rr.ok) return;
+  if constexpr (SRC == TXB_SRC_ROWS) {
+    r.c[0] = rr.r[0][0];
+    r.c[1] = rr.r[1][0];
+  } else {
+    constexpr int EPC = 16 / ELEM;
     float v[2][EPC];
     float amax = 0.f;
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
-      const int c = tid + u * nt;
-      if (c < r.nchunk) {
-        load_vals<SRC>(x, rowoff + (int64_t)c * EPC, v[u], EPC);
-        if constexpr (ELEM == 1) {
+      const uint32_t* w = reinterpret_cast<const uint32_t*>(&rr.r[u][0]);
+#pragma unroll
+      for (int k = 0; k < EPC; ++k) {
+        if constexpr (SRC == TXB_SRC_F32) v[u][k] = __uint_as_float(w[k]);
+        else v[u][k] = __uint_as_float((k & 1) ? (w[k >> 1] & 0xFFFF0000u) : (w[k >> 1] << 16));
+      }
+      if constexpr (ELEM == 1) {
+        if (tid + u * nt < rr.nchunk) {
 #pragma unroll
           for (int k = 0; k < EPC; ++k)
             if (isfinite(v[u][k])) amax = fmaxf(amax, fabsf(v[u][k]));
@@ -236,11 +278,8 @@ __device__ void encode_row_regs(const void* x, int64_t t, int H, int64_t P, RowR
       r.scale = amax > 0.f ? __fdiv_rn(amax, 448.0f) : 1.0f;  // kernels.py:133-134
     }
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int c = tid + u * nt;
-      if (c < r.nchunk) r.c[u] = encode_chunk<ELEM>(v[u], r.scale);
-    }
-    r.ok = true;
+    for (int u = 0; u < 2; ++u)
+      if (tid + u * nt < rr.nchunk) r.c[u] = encode_chunk<ELEM>(v[u], r.scale);
   }
 }
 
@@ -359,39 +398,55 @@ __device__ void combine_rows(const uint8_t* comb, int64_t Pc, const uint8_t* out
     }
     __syncthreads();
     if (vec) {
-      for (int c = tid; c < H / 8; c += nt) {
-        float acc[8];
+      // two 8-element chunks per thread per pass (c, c + nt) for 1- and
+      // 2-byte rows: 2*kCombBatch independent loads in flight per thread
+      constexpr int CPT = ELEM == 4 ? 1 : 2;
+      for (int c0 = tid; c0 < H / 8; c0 += CPT * nt) {
+        float acc[CPT][8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) acc[k] = 0.f;
+        for (int p = 0; p < CPT; ++p)
+#pragma unroll
+          for (int k = 0; k < 8; ++k) acc[p][k] = 0.f;
         for (int j0 = 0; j0 < R; j0 += kCombBatch) {
-          Chunk8<ELEM> raw[kCombBatch];
+          Chunk8<ELEM> raw[CPT][kCombBatch];
 #pragma unroll
-          for (int u = 0; u < kCombBatch; ++u)
-            if (j0 + u < R) raw[u] = load_chunk8<ELEM>(rowp[j0 + u], (int64_t)c * 8);
+          for (int p = 0; p < CPT; ++p)
 #pragma unroll
-          for (int u = 0; u < kCombBatch; ++u) {
-            if (j0 + u < R) {
-              float v[8];
-              unpack_chunk8<ELEM>(raw[u], v);
-              const float wj = ws[j0 + u], sj = sc[j0 + u];
+            for (int u = 0; u < kCombBatch; ++u)
+              if (j0 + u < R && c0 + p * nt < H / 8)
+                raw[p][u] = load_chunk8<ELEM>(rowp[j0 + u], (int64_t)(c0 + p * nt) * 8);
 #pragma unroll
-              for (int k = 0; k < 8; ++k) {
-                const float y = ELEM == 1 ? __fmul_rn(v[k], sj) : v[k];
-                acc[k] = __fadd_rn(acc[k], __fmul_rn(wj, y));
+          for (int p = 0; p < CPT; ++p)
+#pragma unroll
+            for (int u = 0; u < kCombBatch; ++u) {
+              if (j0 + u < R) {
+                float v[8];
+                unpack_chunk8<ELEM>(raw[p][u], v);
+                const float wj = ws[j0 + u], sj = sc[j0 + u];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                  const float y = ELEM == 1 ? __fmul_rn(v[k], sj) : v[k];
+                  acc[p][k] = __fadd_rn(acc[p][k], __fmul_rn(wj, y));
+                }
               }
             }
-          }
         }
-        if (out_bf16) {
-          uint4 o;
-          uint32_t* ow = reinterpret_cast<uint32_t*>(&o);
 #pragma unroll
-          for (int q = 0; q < 4; ++q) ow[q] = (uint32_t)bf16_rne(acc[2 * q]) | ((uint32_t)bf16_rne(acc[2 * q + 1]) << 16);
-          reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(dst) + t * H)[c] = o;
-        } else {
-          float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(dst) + t * H) + 2 * c;
-          o[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
-          o[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+        for (int p = 0; p < CPT; ++p) {
+          const int c = c0 + p * nt;
+          if (c >= H / 8) continue;
+          if (out_bf16) {
+            uint4 o;
+            uint32_t* ow = reinterpret_cast<uint32_t*>(&o);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              ow[q] = (uint32_t)bf16_rne(acc[p][2 * q]) | ((uint32_t)bf16_rne(acc[p][2 * q + 1]) << 16);
+            reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(dst) + t * H)[c] = o;
+          } else {
+            float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(dst) + t * H) + 2 * c;
+            o[0] = make_float4(acc[p][0], acc[p][1], acc[p][2], acc[p][3]);
+            o[1] = make_float4(acc[p][4], acc[p][5], acc[p][6], acc[p][7]);
+          }
         }
       }
     } else {

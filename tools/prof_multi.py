@@ -25,10 +25,10 @@ a = ap.parse_args()
 N, T, H, E, R = a.ranks, a.tokens, 7168, 256, 8
 spec = moe.RoutingSpec(N, E, T, R, hidden=H, elem_size=1, scales=56, comb_elem_size=2, comb_scales=0)
 mesh = moe.build_mesh(local_engines(list(range(N))), spec, timeout=20.0)
-names = ["start", "counted", "positions", "routes-in", "tables", "stored", "signalled", "metadata",
-         "tokens-in", "c:start", "c:sent", "c:signalled", "c:reduced", "c:end", "pre-encoded", "layout",
+names = ["start", "encoded", "positions", "routes-in", "tables", "stored", "signalled", "metadata",
+         "tokens-in", "c:start", "c:sent", "c:signalled", "c:reduced", "c:end", "counted(+loads)", "layout",
          "L:col-done", "L:scan-done", "T:loaded", "T:srcpre", "T:scans", "RC:owned", "RC:counted"]
-order = [0, 14, 21, 22, 1, 2, 3, 16, 17, 15, 18, 19, 20, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13]
+order = [0, 21, 22, 14, 1, 2, 3, 16, 17, 15, 18, 19, 20, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13]
 stamps = [None] * N
 times = [None] * N
 bar = threading.Barrier(N)
