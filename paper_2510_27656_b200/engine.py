@@ -14,7 +14,7 @@ is no host proxy and no worker thread.
 from __future__ import annotations
 
 import itertools
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 from typing import Sequence
 
 import torch
@@ -34,6 +34,43 @@ class NetAddr:
     @property
     def data(self) -> bytes:
         return f"{self.host}/{self.proc}/{self.device}".encode()
+
+
+@dataclass(frozen=True)
+class RegionDesc:
+    """What a peer needs to reach one rank's symmetric region (the MrDesc
+    analog, wire.py:64-87): owner rank, host, device, the 64-byte CUDA IPC
+    handle, the region size and a key of the spec that laid it out."""
+
+    rank: int
+    host: str
+    device: int
+    handle: bytes
+    nbytes: int
+    spec_key: tuple = ()
+
+
+def check_descs(descs: Sequence[RegionDesc], world: int) -> list[RegionDesc]:
+    """Validate an all-gathered descriptor set (sorted by rank): ranks
+    0..world-1 exactly once, one spec and region size for everyone, and no
+    two ranks on one GPU (ranks that wait on each other must not be separate
+    processes on one device)."""
+    ds = sorted(descs, key=lambda d: d.rank)
+    if [d.rank for d in ds] != list(range(world)):
+        raise RegionError(f"region descriptors for ranks {[d.rank for d in ds]}, expected 0..{world - 1}")
+    if len({d.spec_key for d in ds}) != 1:
+        raise RegionError("ranks disagree on the routing spec: "
+                          + "; ".join(f"rank {d.rank}: {d.spec_key}" for d in ds))
+    if len({d.nbytes for d in ds}) != 1:
+        raise RegionError("ranks disagree on the region size")
+    seen: dict = {}
+    for d in ds:
+        k = (d.host, d.device)
+        if k in seen:
+            raise RegionError(f"ranks {seen[k]} and {d.rank} share GPU {d.device} on {d.host}: "
+                              "use build_mesh in one process for several ranks per GPU")
+        seen[k] = d.rank
+    return ds
 
 
 class NvlinkFabric:
@@ -66,6 +103,11 @@ class NvlinkFabric:
         out = [None] * world
         dist.all_gather_object(out, obj, group=self.group)
         return out
+
+    def exchange(self, mine: RegionDesc) -> list[RegionDesc]:
+        """All-gather every rank's region descriptor and validate the set."""
+        import torch.distributed as dist
+        return check_descs(self.all_gather(mine), dist.get_world_size(self.group))
 
     def barrier(self) -> None:
         import torch.distributed as dist

@@ -26,6 +26,7 @@ payload may also be f32/bf16 values, encoded inside the dispatch kernel).
 
 from __future__ import annotations
 
+import dataclasses
 import threading
 import time
 from dataclasses import dataclass
@@ -36,7 +37,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .engine import TransferEngine
+from .engine import RegionDesc, TransferEngine
 from .errors import ProtocolError
 from .memory import Region, enable_peer_access, view
 
@@ -832,22 +833,16 @@ def connect_process_group(engine: TransferEngine, spec: RoutingSpec, *,
         private = PrivateBufferConfig(min(DEFAULT_PRIVATE, spec.max_tokens))
     me = MoeRank(rank, engine, spec, private, node=rank // max(1, ranks_per_node), timeout=timeout)
     import socket
-    mine = (rank, socket.gethostname(), engine.device, me.region.ipc_handle(), me.region.nbytes)
-    allinfo = sorted(engine.fabric.all_gather(mine), key=lambda x: x[0])
+    mine = RegionDesc(rank, socket.gethostname(), engine.device, me.region.ipc_handle(),
+                      me.region.nbytes, spec_key=dataclasses.astuple(spec))
     ptrs = []
-    same_dev = False
-    for (q, host, dev, handle, nbytes) in allinfo:
-        if q == rank:
+    for d in engine.fabric.exchange(mine):
+        if d.rank == rank:
             ptrs.append(me.region.ptr)
             continue
-        if host == mine[1] and dev == engine.device:
-            same_dev = True
-        reg = Region.open_ipc(engine.device, handle, nbytes)
+        reg = Region.open_ipc(engine.device, d.handle, d.nbytes)
         me._peer_regions.append(reg)
         ptrs.append(reg.ptr)
-    if same_dev:
-        raise ProtocolError("two processes share one GPU: ranks waiting on each other as separate "
-                            "processes on one device are not supported; use build_mesh in one process")
     me._set_peers(ptrs, gated=False)
     engine.fabric.barrier()
     return me
