@@ -52,11 +52,6 @@ constexpr int kMaxOwn = 64;        // copies per CTA of the direct-count path
 __device__ __forceinline__ int pad_up(int x) { return (x + kGroupPad - 1) / kGroupPad * kGroupPad; }
 
 // Optional phase stamps for profiling (txb_moe_bufs.prof, [grid][32]).
-__device__ uint64_t* g_prof = nullptr;
-__device__ __forceinline__ void substamp(int k) {
-  uint64_t* p = g_prof;
-  if (p && threadIdx.x == 0) p[blockIdx.x * 32 + k] = globaltimer();
-}
 __device__ __forceinline__ void stamp(const txb_moe_bufs& b, int k) {
   if (b.prof && threadIdx.x == 0) b.prof[blockIdx.x * 32 + k] = globaltimer();
 }
@@ -70,7 +65,7 @@ __device__ __forceinline__ uint64_t cur_step(Flags* f) {
 __host__ __device__ inline size_t smem_route(int E, int nwarps) { return (size_t)(1 + nwarps) * E * 4 + 16; }
 __host__ __device__ inline size_t smem_layout(int E) { return (size_t)(2 * E + 1) * 4; }
 __host__ __device__ inline size_t smem_recv(int N, int L) {
-  return (size_t)(3 * N * L + 1 + 2 * L + 1 + L * (N + 1) + N) * 4;
+  return (size_t)(3 * N * L + 2 + 2 * L + L * (N + 1) + N) * 4;
 }
 __host__ __device__ inline size_t smem_cmat(int N, int E) { return ((size_t)N * E * 4 + 15) / 16 * 16; }
 // layout scratch [0, recv_offset), receive tables [recv_offset, cmat_offset),
@@ -120,7 +115,6 @@ __device__ uint32_t route_counts_direct(const txb_moe_shape& s, const int64_t* r
     sh.direct = 1;
   }
   __syncthreads();
-  substamp(21);
   const bool lanes = (32 % R) == 0;
   for (int base = 0; base < m; base += blockDim.x) {
     const int i = base + tid;
@@ -147,7 +141,6 @@ __device__ uint32_t route_counts_direct(const txb_moe_shape& s, const int64_t* r
       if (sh.own_e[k] == (int)v && i < sh.own_i[k]) atomicAdd(&sh.own_rank[k], 1u);
   }
   __syncthreads();
-  substamp(22);
   for (int k = tid; k < nw; k += blockDim.x) rank_out[sh.own_i[k]] = (int32_t)sh.own_rank[k];
   const uint32_t b = sh.bad;
   if (b)
@@ -307,9 +300,7 @@ __device__ bool dispatch_layout(const txb_moe_shape& s, const uint32_t* C, int* 
     if (book && e / L == s.me) atomicAdd(&sh.recv_me, (uint32_t)col);
   }
   __syncthreads();
-  substamp(16);
   const int tot = block_scan_i32(padded, E, sh.tmp);
-  substamp(17);
   if (tid == 0) padded[E] = tot;
   __syncthreads();
   for (int e = tid; e < E; e += blockDim.x) baseg[e] += padded[e] - padded[(e / L) * L];
@@ -323,6 +314,48 @@ __device__ bool dispatch_layout(const txb_moe_shape& s, const uint32_t* C, int* 
   }
   if (book && tid == 0) f->tok_target += sh.recv_me;
   return true;
+}
+
+// DECODE layout: this CTA's single token needs only its own R copies'
+// send slots and destination rows, so each comes from one warp reduction
+// instead of block-wide scans (one warp per copy, no block barrier).
+// pos = sum_{e' < e} hist[e'] + rank (moe.py:514-521).
+__device__ void own_positions(const txb_moe_shape& s, const uint32_t* hist, int64_t* pos, uint32_t bad,
+                              Shared& sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  for (int k = warp; k < s.topk; k += nwarp) {
+    const int e = sh.own_e[k];
+    int acc = 0;
+    for (int x = lane; x < e; x += 32) acc += (int)hist[x];
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) pos[sh.own_i[k]] = bad ? -1 : (int64_t)acc + sh.own_rank[k];
+  }
+}
+
+// grouped row on owner d of copy k: group_starts_d[le] + sum_{s' < me}
+// counts[s', e] + rank; books gidx and the counts.
+__device__ void own_dests(const txb_moe_shape& s, const uint32_t* C, void* const* peers, int32_t* gidx,
+                          Shared& sh) {
+  const int N = s.ranks, E = s.experts, L = s.local_experts;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  for (int k = warp; k < s.topk; k += nwarp) {
+    const int e = sh.own_e[k], d = e / L, le = e - d * L;
+    int acc = 0;
+    for (int x = lane; x < le; x += 32) {
+      int col = 0;
+      for (int q = 0; q < N; ++q) col += (int)C[q * E + d * L + x];
+      acc += pad_up(col);
+    }
+    for (int q = lane; q < s.me; q += 32) acc += (int)C[q * E + e];
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) {
+      const int g = acc + (int)sh.own_rank[k];
+      sh.dstp[k] = grouped_of(peers[d], s) + (int64_t)g * s.payload_bytes;
+      gidx[sh.own_i[k]] = d == s.me ? g : -1;
+      atomicAdd(&sh.cnt[d], 1u);
+    }
+  }
+  __syncthreads();
 }
 
 // ------------------------------------------------------------------- P4
@@ -415,23 +448,24 @@ __device__ void signal_counts(const txb_moe_shape& s, void* const* peers, size_t
 // slot, the warp zero-fills padding rows that may hold stale data.
 struct RecvTables {
   int* a;        // [N][L] counts into my experts
-  int* rowbase;  // [N*L+1] flattened exclusive prefix = recv slot base
+  int* gstart;   // [L] group starts (padded) -- followed directly by rowbase,
+  int* rowbase;  // [N*L] flattened exclusive prefix = recv slot base
+  int* tot;      // [2] padded_total, recv_total
   int* retbase;  // [N][L] send slot base on the source
-  int* gstart;   // [L+1]
   int* gsize;    // [L]
   int* srcpre;   // [L][N+1]
   int* pre_all;  // [N] sum_{e' < me*L} C[q][e']
-  int padded_total, recv_total;
 };
 
 __device__ __forceinline__ RecvTables recv_carve(const txb_moe_shape& s, int* sm) {
   const int N = s.ranks, L = s.local_experts;
   RecvTables t;
   t.a = sm;
-  t.rowbase = t.a + N * L;
-  t.retbase = t.rowbase + N * L + 1;
-  t.gstart = t.retbase + N * L;
-  t.gsize = t.gstart + L + 1;
+  t.gstart = t.a + N * L;
+  t.rowbase = t.gstart + L;
+  t.tot = t.rowbase + N * L;
+  t.retbase = t.tot + 2;
+  t.gsize = t.retbase + N * L;
   t.srcpre = t.gsize + L;
   t.pre_all = t.srcpre + L * (N + 1);
   return t;
@@ -457,7 +491,6 @@ __device__ __noinline__ void recv_tables(const txb_moe_shape& s, const uint32_t*
     }
   }
   __syncthreads();
-  substamp(18);
   for (int le = tid; le < L; le += nt) {
     int run = 0;
     for (int q = 0; q < N; ++q) {
@@ -469,15 +502,15 @@ __device__ __noinline__ void recv_tables(const txb_moe_shape& s, const uint32_t*
     t.gstart[le] = pad_up(run);
   }
   __syncthreads();
-  substamp(19);
-  const int padded_total = block_scan_i32(t.gstart, L, sh.tmp);
-  // recv_start[me][q] + sum_{le'<le} a[q][le'] is the exclusive prefix of a[]
-  // flattened source-major (moe.py:178-184, 204-213)
-  const int recv_total = block_scan_i32(t.rowbase, N * L, sh.tmp);
-  substamp(20);
+  // one scan over [padded group sizes (L) | counts flattened source-major
+  // (N*L)]: the first part gives group_starts, the second (minus the padded
+  // total) recv_start[me][q] + sum_{le'<le} a[q][le'] (moe.py:178-184, 204-213)
+  const int all = block_scan_i32(t.gstart, L + N * L, sh.tmp);
+  const int padded_total = N * L ? t.rowbase[0] : all;
+  for (int i = tid; i < N * L; i += nt) t.rowbase[i] -= padded_total;
   if (tid == 0) {
-    t.gstart[L] = padded_total;
-    t.rowbase[N * L] = recv_total;
+    t.tot[0] = padded_total;
+    t.tot[1] = all - padded_total;
   }
   __syncthreads();
   for (int i = tid; i < N * L; i += nt) t.retbase[i] = t.pre_all[i / L] + (t.rowbase[i] - t.rowbase[(i / L) * L]);
@@ -488,8 +521,8 @@ __device__ __noinline__ void recv_tables(const txb_moe_shape& s, const uint32_t*
       info[L + le] = t.gstart[le];
     }
     if (tid == 0) {
-      info[2 * L] = padded_total;
-      info[2 * L + 1] = recv_total;
+      info[2 * L] = t.tot[0];
+      info[2 * L + 1] = t.tot[1];
     }
   }
 }
@@ -498,7 +531,7 @@ __device__ __noinline__ void recv_rows(const txb_moe_shape& s, int* sm, int64_t*
                                        int32_t* ret, uint8_t* G, uint8_t* dirty, int cta, int ncta) {
   const int N = s.ranks, L = s.local_experts;
   const RecvTables t = recv_carve(s, sm);
-  const int padded_total = t.gstart[L];
+  const int padded_total = t.tot[0];
   const int64_t P = s.payload_bytes;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
   for (int g = cta * nwarp + warp; g < padded_total; g += ncta * nwarp) {
@@ -711,45 +744,56 @@ k_dispatch_fused(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
   const int cta = blockIdx.x, ncta = gridDim.x;
   uint32_t* hist = reinterpret_cast<uint32_t*>(dsm);
   uint32_t* wc = hist + ((s.experts + 3) & ~3);
-  if (threadIdx.x == 0 && blockIdx.x == 0) g_prof = b.prof;
-  __syncthreads();
-  stamp(b, 0);
-  RowRegs pre;
-  RowRaw raw;
-  // issue the token's loads first; route counting runs while they land
-  if constexpr (DECODE) load_row_raw<SRC, ELEM>(x, cta, s.hidden, s.payload_bytes, raw);
-  uint32_t bad;
-  if constexpr (DECODE) bad = route_counts_direct(s, routes, n, hist, b.rank_scratch, cta, ncta, sh);
-  else bad = route_counts_chunked(s, routes, n, hist, wc, b.rank_scratch, cta, ncta, sh);
-  stamp(b, 14);
-  if constexpr (DECODE) finish_row_regs<SRC, ELEM>(raw, pre, sh.red);
-  stamp(b, 1);
-  route_publish(s, b.peers, f, hist, step, n, bad, cta, ncta);
-  route_positions(s, routes, n, hist, reinterpret_cast<int*>(wc), b.rank_scratch, b.pos, bad, cta, ncta, sh);
-  stamp(b, 2);
   uint32_t* C = reinterpret_cast<uint32_t*>(dsm + cmat_offset(s));
-  if (!wait_routes(s, f, route_of(b.region, s, (int)(step & 1)), C, step, timeout_ns, sh)) return;
-  stamp(b, 3);
-  int* baseg = reinterpret_cast<int*>(dsm);
-  if (!dispatch_layout(s, C, baseg, baseg + s.experts, f, cta == 0, sh)) return;
-  stamp(b, 15);
   int* rt = reinterpret_cast<int*>(dsm + recv_offset(s));
-  recv_tables(s, C, rt, b.info, cta, sh);
-  for (int q = threadIdx.x; q < s.ranks; q += blockDim.x) sh.cnt[q] = 0;
-  __syncthreads();
-  stamp(b, 4);
-  if (!bad) {
-    if constexpr (DECODE) {
-      token_dests(s, routes, b.rank_scratch, b.gidx, b.peers, baseg, cta, 0, sh);
+  stamp(b, 0);
+  if constexpr (DECODE) {
+    RowRegs pre;
+    RowRaw raw;
+    // issue the token's loads first; route counting runs while they land
+    load_row_raw<SRC, ELEM>(x, cta, s.hidden, s.payload_bytes, raw);
+    const uint32_t bad = route_counts_direct(s, routes, n, hist, b.rank_scratch, cta, ncta, sh);
+    stamp(b, 14);
+    finish_row_regs<SRC, ELEM>(raw, pre, sh.red);
+    stamp(b, 1);
+    route_publish(s, b.peers, f, hist, step, n, bad, cta, ncta);
+    own_positions(s, hist, b.pos, bad, sh);
+    for (int q = threadIdx.x; q < s.ranks; q += blockDim.x) sh.cnt[q] = 0;
+    stamp(b, 2);
+    if (!wait_routes(s, f, route_of(b.region, s, (int)(step & 1)), C, step, timeout_ns, sh)) return;
+    stamp(b, 3);
+    if (!bad) {
+      own_dests(s, C, b.peers, b.gidx, sh);
+      stamp(b, 15);
       if (pre.ok) store_row_regs<SRC, ELEM>(pre, s.hidden, s.scales, sh.dstp, s.topk);
       else dispatch_row_slow<SRC, ELEM>(s, x, cta, sh);
-    } else {
-      dispatch_tokens<SRC, ELEM>(s, x, n, routes, b.rank_scratch, b.gidx, b.peers, baseg, cta, ncta, sh);
     }
+    stamp(b, 5);
+    // the receive tables overlap the stores in flight; the fence follows
+    recv_tables(s, C, rt, b.info, cta, sh);
+    stamp(b, 4);
+    if (cta == 0 && threadIdx.x == 0) f->tok_target += (uint64_t)recv_carve(s, rt).tot[1];
+    signal_counts(s, b.peers, offsetof(Flags, tok_ctr), sh);
+  } else {
+    const uint32_t bad = route_counts_chunked(s, routes, n, hist, wc, b.rank_scratch, cta, ncta, sh);
+    stamp(b, 1);
+    route_publish(s, b.peers, f, hist, step, n, bad, cta, ncta);
+    route_positions(s, routes, n, hist, reinterpret_cast<int*>(wc), b.rank_scratch, b.pos, bad, cta, ncta, sh);
+    stamp(b, 2);
+    if (!wait_routes(s, f, route_of(b.region, s, (int)(step & 1)), C, step, timeout_ns, sh)) return;
+    stamp(b, 3);
+    int* baseg = reinterpret_cast<int*>(dsm);
+    if (!dispatch_layout(s, C, baseg, baseg + s.experts, f, cta == 0, sh)) return;
+    recv_tables(s, C, rt, b.info, cta, sh);
+    for (int q = threadIdx.x; q < s.ranks; q += blockDim.x) sh.cnt[q] = 0;
+    __syncthreads();
+    stamp(b, 4);
+    if (!bad)
+      dispatch_tokens<SRC, ELEM>(s, x, n, routes, b.rank_scratch, b.gidx, b.peers, baseg, cta, ncta, sh);
+    stamp(b, 5);
+    signal_counts(s, b.peers, offsetof(Flags, tok_ctr), sh);
   }
-  stamp(b, 5);
   // thread 0 fences and signals while the other warps fill the metadata
-  signal_counts(s, b.peers, offsetof(Flags, tok_ctr), sh);
   stamp(b, 6);
   recv_rows(s, rt, b.rows, b.sources, b.ret_slot, grouped_of(b.region, s), b.dirty, cta, ncta);
   stamp(b, 7);

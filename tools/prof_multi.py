@@ -25,10 +25,10 @@ a = ap.parse_args()
 N, T, H, E, R = a.ranks, a.tokens, 7168, 256, 8
 spec = moe.RoutingSpec(N, E, T, R, hidden=H, elem_size=1, scales=56, comb_elem_size=2, comb_scales=0)
 mesh = moe.build_mesh(local_engines(list(range(N))), spec, timeout=20.0)
-names = ["start", "encoded", "positions", "routes-in", "tables", "stored", "signalled", "metadata",
-         "tokens-in", "c:start", "c:sent", "c:signalled", "c:reduced", "c:end", "counted(+loads)", "layout",
-         "L:col-done", "L:scan-done", "T:loaded", "T:srcpre", "T:scans", "RC:owned", "RC:counted"]
-order = [0, 21, 22, 14, 1, 2, 3, 16, 17, 15, 18, 19, 20, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13]
+names = {0: "start", 14: "counted(+loads)", 1: "encoded", 2: "published+pos", 3: "routes-in",
+         15: "dests", 5: "stored", 4: "tables", 6: "signalled", 7: "metadata", 8: "tokens-in",
+         9: "c:start", 10: "c:sent", 11: "c:signalled", 12: "c:reduced", 13: "c:end"}
+order = [0, 14, 1, 2, 3, 15, 5, 4, 6, 7, 8, 9, 10, 11, 12, 13]
 stamps = [None] * N
 times = [None] * N
 bar = threading.Barrier(N)
