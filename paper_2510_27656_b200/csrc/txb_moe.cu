@@ -234,13 +234,18 @@ __device__ void route_publish(const txb_moe_shape& s, void* const* peers, Flags*
     const int d = idx / E, e = idx - d * E;
     st_relaxed_sys(route_of(peers[d], s, slot) + (size_t)s.me * E + e, tag | hist[e]);
   }
-  if (part == 0 && threadIdx.x == 0) {
-    uint64_t self = 0;
-    for (int le = 0; le < L; ++le) self += hist[s.me * L + le];
-    f->comb_target += bad ? 0 : (uint64_t)(n * s.topk) - self;
-    if (bad) atomicOr(&f->err, bad);
+  if (part == 0 && threadIdx.x < 32) {
+    // copies this rank serves itself do not come back through the counter
+    const int lane = threadIdx.x;
+    uint32_t self = 0;
+    for (int le = lane; le < L; le += 32) self += hist[s.me * L + le];
+    for (int o = 16; o; o >>= 1) self += __shfl_xor_sync(0xffffffffu, self, o);
     // per-source step tags for host-side gating / diagnostics only
-    for (int d = 0; d < N; ++d) st_relaxed_sys(&flags_of(peers[d], s)->route_tag[slot][s.me], step);
+    for (int d = lane; d < N; d += 32) st_relaxed_sys(&flags_of(peers[d], s)->route_tag[slot][s.me], step);
+    if (lane == 0) {
+      f->comb_target += bad ? 0 : (uint64_t)(n * s.topk) - self;
+      if (bad) atomicOr(&f->err, bad);
+    }
   }
 }
 
@@ -623,10 +628,17 @@ __device__ void combine_send_rows(const txb_moe_shape& s, const uint8_t* out, in
 
 // ------------------------------------------------------------------- C2
 
+// Wait for the returned rows, then reduce this CTA's tokens.  The first
+// token's row pointers and weights are staged before the wait.
 template <int ELEM>
 __device__ bool combine_reduce(const txb_moe_shape& s, Flags* f, const uint8_t* comb, const uint8_t* out,
                                int64_t ld, const int64_t* pos, const int32_t* gidx, const float* w, int64_t n,
                                void* dst, int out_bf16, uint64_t timeout_ns, int cta, int ncta, Shared& sh) {
+  __shared__ CombTok ct;
+  const int64_t Pc = s.comb_bytes;
+  const int H = s.hidden, R = s.topk;
+  const bool vec = combine_vec<ELEM>(Pc, comb, out, ld, H, gidx);
+  if (cta < n) combine_prep(ct, comb, Pc, out, ld, pos, gidx, w, cta, R);
   if (threadIdx.x == 0) {
     const uint64_t dl = globaltimer() + timeout_ns;
     sh.fail = spin_ge(&f->comb_ctr, f->comb_target, dl) ? 0u : TXB_EV_WAIT_COMBINE;
@@ -634,7 +646,14 @@ __device__ bool combine_reduce(const txb_moe_shape& s, Flags* f, const uint8_t* 
   }
   __syncthreads();
   if (sh.fail) return false;
-  combine_rows<ELEM>(comb, s.comb_bytes, out, ld, s.hidden, pos, gidx, w, n, s.topk, dst, out_bf16, cta, ncta);
+  for (int64_t t = cta; t < n; t += ncta) {
+    if (t != cta) {
+      combine_prep(ct, comb, Pc, out, ld, pos, gidx, w, t, R);
+      __syncthreads();
+    }
+    combine_token<ELEM>(ct, Pc, comb, H, R, t, dst, out_bf16, vec);
+    __syncthreads();
+  }
   return true;
 }
 

@@ -372,95 +372,131 @@ constexpr int kCombBatch = 8;  // rows of one chunk loaded together
 // place from the expert outputs) and comb + pos[t,j]*Pc otherwise.  Each
 // thread owns 8-element chunks; the rows of a chunk are fetched in batches
 // of kCombBatch before the accumulation so their memory latencies overlap.
+// Per-token row pointers, weights and (fp8) scales, staged in shared memory.
+struct CombTok {
+  const uint8_t* rowp[kMaxTopk];
+  float ws[kMaxTopk];
+  float sc[kMaxTopk];
+};
+
+// Row of copy j of token t: out_rows + gidx*ld when this rank served it
+// (read in place), else comb + pos*Pc.  Needs only metadata, so it can run
+// before the rows have arrived.
+__device__ __forceinline__ void combine_prep(CombTok& ct, const uint8_t* comb, int64_t Pc, const uint8_t* out_rows,
+                                             int64_t ld, const int64_t* pos, const int32_t* gidx, const float* w,
+                                             int64_t t, int R) {
+  const int tid = threadIdx.x;
+  if (tid < R) {
+    const int32_t gi = gidx ? gidx[t * R + tid] : -1;
+    ct.rowp[tid] = gi >= 0 ? out_rows + (int64_t)gi * ld : comb + pos[t * R + tid] * Pc;
+    ct.ws[tid] = w[t * R + tid];
+  }
+}
+
+// out[t] = sum_j w[t,j] * y[t,j], j ascending from 0.0, separately rounded
+// multiply and add (kernels.py:214-226); fp8 rows are dequantised first as
+// e4m3 * f32 scale (kernels.py:139-141).  Each thread owns 8-element chunks;
+// the rows of a chunk are fetched in batches of kCombBatch before the
+// accumulation so their memory latencies overlap.  Expects combine_prep(t)
+// and a barrier before the call.
+template <int ELEM>
+__device__ void combine_token(CombTok& ct, int64_t Pc, const uint8_t* comb, int H, int R, int64_t t, void* dst,
+                              int out_bf16, bool vec) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  if (ELEM == 1) {
+    if (tid < R) {
+      const uint8_t* sp = ct.rowp[tid] + H;
+      const uint32_t u = (uint32_t)sp[0] | ((uint32_t)sp[1] << 8) | ((uint32_t)sp[2] << 16) | ((uint32_t)sp[3] << 24);
+      ct.sc[tid] = __uint_as_float(u);
+    }
+    __syncthreads();
+  }
+  const uint8_t* const* rowp = ct.rowp;
+  const float* ws = ct.ws;
+  const float* sc = ct.sc;
+  if (vec) {
+    // two 8-element chunks per thread per pass (c, c + nt) for 1- and
+    // 2-byte rows: 2*kCombBatch independent loads in flight per thread
+    constexpr int CPT = ELEM == 4 ? 1 : 2;
+    for (int c0 = tid; c0 < H / 8; c0 += CPT * nt) {
+      float acc[CPT][8];
+#pragma unroll
+      for (int p = 0; p < CPT; ++p)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[p][k] = 0.f;
+      for (int j0 = 0; j0 < R; j0 += kCombBatch) {
+        Chunk8<ELEM> raw[CPT][kCombBatch];
+#pragma unroll
+        for (int p = 0; p < CPT; ++p)
+#pragma unroll
+          for (int u = 0; u < kCombBatch; ++u)
+            if (j0 + u < R && c0 + p * nt < H / 8)
+              raw[p][u] = load_chunk8<ELEM>(rowp[j0 + u], (int64_t)(c0 + p * nt) * 8);
+#pragma unroll
+        for (int p = 0; p < CPT; ++p)
+#pragma unroll
+          for (int u = 0; u < kCombBatch; ++u) {
+            if (j0 + u < R) {
+              float v[8];
+              unpack_chunk8<ELEM>(raw[p][u], v);
+              const float wj = ws[j0 + u], sj = sc[j0 + u];
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                const float y = ELEM == 1 ? __fmul_rn(v[k], sj) : v[k];
+                acc[p][k] = __fadd_rn(acc[p][k], __fmul_rn(wj, y));
+              }
+            }
+          }
+      }
+#pragma unroll
+      for (int p = 0; p < CPT; ++p) {
+        const int c = c0 + p * nt;
+        if (c >= H / 8) continue;
+        if (out_bf16) {
+          uint4 o;
+          uint32_t* ow = reinterpret_cast<uint32_t*>(&o);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            ow[q] = (uint32_t)bf16_rne(acc[p][2 * q]) | ((uint32_t)bf16_rne(acc[p][2 * q + 1]) << 16);
+          reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(dst) + t * H)[c] = o;
+        } else {
+          float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(dst) + t * H) + 2 * c;
+          o[0] = make_float4(acc[p][0], acc[p][1], acc[p][2], acc[p][3]);
+          o[1] = make_float4(acc[p][4], acc[p][5], acc[p][6], acc[p][7]);
+        }
+      }
+    }
+  } else {
+    for (int h = tid; h < H; h += nt) {
+      float acc = 0.f;
+      for (int j = 0; j < R; ++j) {
+        const float v = load1<ELEM>(rowp[j], h);
+        const float y = ELEM == 1 ? __fmul_rn(v, sc[j]) : v;
+        acc = __fadd_rn(acc, __fmul_rn(ws[j], y));
+      }
+      if (out_bf16) reinterpret_cast<uint16_t*>(dst)[t * H + h] = bf16_rne(acc);
+      else reinterpret_cast<float*>(dst)[t * H + h] = acc;
+    }
+  }
+}
+
+template <int ELEM>
+__device__ bool combine_vec(int64_t Pc, const uint8_t* comb, const uint8_t* out_rows, int64_t ld, int H,
+                            const int32_t* gidx) {
+  return (H % 8 == 0) && ((Pc & 15) == 0) && ((reinterpret_cast<uintptr_t>(comb) & 15) == 0) &&
+         (!gidx || (((ld & 15) == 0) && ((reinterpret_cast<uintptr_t>(out_rows) & 15) == 0)));
+}
+
 template <int ELEM>
 __device__ void combine_rows(const uint8_t* comb, int64_t Pc, const uint8_t* out_rows, int64_t ld, int H,
                              const int64_t* pos, const int32_t* gidx, const float* w, int64_t n, int R,
                              void* dst, int out_bf16, int cta, int ncta) {
-  __shared__ const uint8_t* rowp[kMaxTopk];
-  __shared__ float ws[kMaxTopk];
-  __shared__ float sc[kMaxTopk];
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const bool vec = (H % 8 == 0) && ((Pc & 15) == 0) && ((reinterpret_cast<uintptr_t>(comb) & 15) == 0) &&
-                   (!gidx || (((ld & 15) == 0) && ((reinterpret_cast<uintptr_t>(out_rows) & 15) == 0)));
+  __shared__ CombTok ct;
+  const bool vec = combine_vec<ELEM>(Pc, comb, out_rows, ld, H, gidx);
   for (int64_t t = cta; t < n; t += ncta) {
-    if (tid < R) {
-      const int32_t gi = gidx ? gidx[t * R + tid] : -1;
-      const uint8_t* row = gi >= 0 ? out_rows + (int64_t)gi * ld : comb + pos[t * R + tid] * Pc;
-      rowp[tid] = row;
-      ws[tid] = w[t * R + tid];
-      float scale = 1.f;
-      if (ELEM == 1) {
-        const uint8_t* sp = row + H;
-        uint32_t u = (uint32_t)sp[0] | ((uint32_t)sp[1] << 8) | ((uint32_t)sp[2] << 16) | ((uint32_t)sp[3] << 24);
-        scale = __uint_as_float(u);
-      }
-      sc[tid] = scale;
-    }
+    combine_prep(ct, comb, Pc, out_rows, ld, pos, gidx, w, t, R);
     __syncthreads();
-    if (vec) {
-      // two 8-element chunks per thread per pass (c, c + nt) for 1- and
-      // 2-byte rows: 2*kCombBatch independent loads in flight per thread
-      constexpr int CPT = ELEM == 4 ? 1 : 2;
-      for (int c0 = tid; c0 < H / 8; c0 += CPT * nt) {
-        float acc[CPT][8];
-#pragma unroll
-        for (int p = 0; p < CPT; ++p)
-#pragma unroll
-          for (int k = 0; k < 8; ++k) acc[p][k] = 0.f;
-        for (int j0 = 0; j0 < R; j0 += kCombBatch) {
-          Chunk8<ELEM> raw[CPT][kCombBatch];
-#pragma unroll
-          for (int p = 0; p < CPT; ++p)
-#pragma unroll
-            for (int u = 0; u < kCombBatch; ++u)
-              if (j0 + u < R && c0 + p * nt < H / 8)
-                raw[p][u] = load_chunk8<ELEM>(rowp[j0 + u], (int64_t)(c0 + p * nt) * 8);
-#pragma unroll
-          for (int p = 0; p < CPT; ++p)
-#pragma unroll
-            for (int u = 0; u < kCombBatch; ++u) {
-              if (j0 + u < R) {
-                float v[8];
-                unpack_chunk8<ELEM>(raw[p][u], v);
-                const float wj = ws[j0 + u], sj = sc[j0 + u];
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                  const float y = ELEM == 1 ? __fmul_rn(v[k], sj) : v[k];
-                  acc[p][k] = __fadd_rn(acc[p][k], __fmul_rn(wj, y));
-                }
-              }
-            }
-        }
-#pragma unroll
-        for (int p = 0; p < CPT; ++p) {
-          const int c = c0 + p * nt;
-          if (c >= H / 8) continue;
-          if (out_bf16) {
-            uint4 o;
-            uint32_t* ow = reinterpret_cast<uint32_t*>(&o);
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              ow[q] = (uint32_t)bf16_rne(acc[p][2 * q]) | ((uint32_t)bf16_rne(acc[p][2 * q + 1]) << 16);
-            reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(dst) + t * H)[c] = o;
-          } else {
-            float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(dst) + t * H) + 2 * c;
-            o[0] = make_float4(acc[p][0], acc[p][1], acc[p][2], acc[p][3]);
-            o[1] = make_float4(acc[p][4], acc[p][5], acc[p][6], acc[p][7]);
-          }
-        }
-      }
-    } else {
-      for (int h = tid; h < H; h += nt) {
-        float acc = 0.f;
-        for (int j = 0; j < R; ++j) {
-          const float v = load1<ELEM>(rowp[j], h);
-          const float y = ELEM == 1 ? __fmul_rn(v, sc[j]) : v;
-          acc = __fadd_rn(acc, __fmul_rn(ws[j], y));
-        }
-        if (out_bf16) reinterpret_cast<uint16_t*>(dst)[t * H + h] = bf16_rne(acc);
-        else reinterpret_cast<float*>(dst)[t * H + h] = acc;
-      }
-    }
+    combine_token<ELEM>(ct, Pc, comb, H, R, t, dst, out_bf16, vec);
     __syncthreads();
   }
 }

@@ -103,3 +103,10 @@ for k in order:
               f"  max {max(v[1] for v in vals)/1e3:8.2f}us")
 for m in mesh:
     m.close()
+# slowest CTAs per phase on rank 0 (relative to rank 0's earliest start)
+p0 = stamps[0]
+t00 = p0[p0[:, 0] > 0, 0].min()
+for k in (6, 7, 8, 12, 13):
+    col = p0[:, k]
+    idx = np.argsort(-col)[:5]
+    print(names[k], "slowest CTAs (rank 0)", [(int(i), round((col[i] - t00) / 1e3, 2)) for i in idx if col[i] > 0])
