@@ -1,18 +1,22 @@
-"""Benchmark: MoE dispatch+combine p50 latency (decode) on B200.
+"""Benchmark: MoE dispatch+combine p50 latency on B200 (BASELINE.json metric).
 
-Workload (BASELINE.json configs[1], DeepSeek-V3 decode): 128 tokens per
-rank, hidden 7168, 256 experts, top-8; dispatch carries fp8 e4m3 rows with
-per-token f32 scales (7168 + 56*4 = 7392 B, encoded inside the dispatch
-kernel from bf16 activations), combine carries bf16 rows (14336 B) and
-produces bf16 outputs.  EP = number of GPUs (1 = loopback through HBM).
+Default workload (BASELINE.json configs[1], DeepSeek-V3 decode): 128 tokens
+per rank, hidden 7168, 256 experts, top-8; dispatch carries fp8 e4m3 rows
+with per-token f32 scales (7168 + 56*4 = 7392 B, encoded inside the
+dispatch kernel from bf16 activations), combine carries bf16 rows
+(14336 B) and produces bf16 outputs.  EP = number of GPUs (1 = loopback
+through HBM).  --config prefill (configs[2]: 4096 tok/rank, bf16 both
+ways) and --config kimi (configs[3]: 384 experts, skewed routing) run the
+other BASELINE configurations with the same methodology.
 
 A step = dispatch_send -> dispatch_recv -> combine_send -> combine_recv
-through the public MoeRank API (launch-only, sync=False), timed per step
-with CUDA events on the rank's stream after a device-side all-rank
-barrier; L2 is flushed (write of a 512 MiB buffer) before every timed step.
+through the public MoeRank API (launch-only, sync=False), captured once
+into a CUDA graph and replayed; each timed step follows an L2 flush (write
+of a 512 MiB buffer) and, for N > 1, a device-side all-rank barrier, and
+is timed with CUDA events on the rank's stream.
 value = p50 over steps of the max over ranks of the step time (us).
 
-Usage:  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+Usage:  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl reference]
         torchrun --nproc-per-node N bench.py --gpus N ...
 """
 
@@ -32,8 +36,17 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-T, H, E, R, SCALES = 128, 7168, 256, 8, 56
-METRIC = "dispatch+combine p50 us (decode, DeepSeek-V3 shape)"
+WORKLOADS = {
+    "decode": dict(tokens=128, experts=256, topk=8, hidden=7168, elem=1, scales=56, routing="uniform",
+                   name="DeepSeek-V3 decode dispatch+combine",
+                   metric="dispatch+combine p50 us (decode, DeepSeek-V3 shape)"),
+    "prefill": dict(tokens=4096, experts=256, topk=8, hidden=7168, elem=2, scales=0, routing="uniform",
+                    name="DeepSeek-V3 prefill dispatch+combine (bf16)",
+                    metric="dispatch+combine p50 us (prefill, DeepSeek-V3 shape, bf16)"),
+    "kimi": dict(tokens=128, experts=384, topk=8, hidden=7168, elem=1, scales=56, routing="skewed",
+                 name="Kimi-K2-shape decode dispatch+combine, skewed routing",
+                 metric="dispatch+combine p50 us (decode, Kimi-K2 shape, skewed)"),
+}
 
 
 def _args():
@@ -42,10 +55,10 @@ def _args():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--tokens", type=int, default=T)
-    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--config", default="decode", choices=sorted(WORKLOADS))
+    ap.add_argument("--tokens", type=int, default=None)
+    ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--kernel-times", action="store_true", default=True)
     return ap.parse_args()
 
 
@@ -56,11 +69,23 @@ def _dist():
     return world, rank, local
 
 
-def _inputs(rank: int, tokens: int, seed: int = 0):
+def routes_for(wl: dict, rng: np.random.Generator, tokens: int) -> np.ndarray:
+    """Uniform top-R, or skewed: Gumbel-top-R over logits
+    -log(1 + rank_e) on a seeded expert permutation (Zipf-like hot experts)."""
+    E, R = wl["experts"], wl["topk"]
+    if wl["routing"] == "uniform":
+        return np.argsort(rng.random((tokens, E)), axis=1)[:, :R].astype(np.int64)
+    perm = np.random.default_rng(1234).permutation(E)
+    logits = -np.log1p(np.arange(E, dtype=np.float64))[np.argsort(perm)]
+    g = -np.log(-np.log(rng.random((tokens, E))))
+    return np.argsort(-(logits[None, :] + g), axis=1)[:, :R].astype(np.int64)
+
+
+def _inputs(wl: dict, rank: int, tokens: int, seed: int = 0):
     rng = np.random.default_rng((seed << 8) + rank)
-    x = rng.standard_normal((tokens, H)).astype(np.float32)
-    routes = np.argsort(rng.random((tokens, E)), axis=1)[:, :R].astype(np.int64)
-    w = rng.random((tokens, R)).astype(np.float32)
+    x = rng.standard_normal((tokens, wl["hidden"])).astype(np.float32)
+    routes = routes_for(wl, rng, tokens)
+    w = rng.random((tokens, wl["topk"])).astype(np.float32)
     return x, routes, w
 
 
@@ -68,9 +93,9 @@ def _inputs(rank: int, tokens: int, seed: int = 0):
 
 
 def cpu_port_step(ospec, cspec, x_bf16_f32, routes, w, mo):
-    """One decode step of the reference algorithm on the host (oracle port):
-    encode (fp8 per token) -> dispatch regroup -> identity expert in bf16 ->
-    combine return -> fp32 weighted sum -> bf16 out."""
+    """One step of the reference algorithm on the host (oracle port):
+    encode -> dispatch regroup -> expert stand-in in bf16 -> combine return
+    -> fp32 weighted sum -> bf16 out."""
     pay = mo.encode_tokens(ospec, x_bf16_f32)
     res = mo.dispatch(ospec, [routes], [pay])
     g = res.ranks[0].grouped
@@ -80,11 +105,16 @@ def cpu_port_step(ospec, cspec, x_bf16_f32, routes, w, mo):
     return mo.bf16_encode(comb)
 
 
-def cpu_baseline(tokens: int, seconds: float) -> dict:
+def cpu_baseline(wl: dict, tokens: int, seconds: float) -> dict:
+    """The oracle port timed on the host (one thread), EP=1, on a bounded
+    sample: the full step when it is short, else a 512-token slice scaled
+    linearly to the step's token count (stated in `sample`)."""
     from oracle import moe_oracle as mo
-    ospec = mo.Spec(1, E, tokens, R, hidden=H, elem_size=1, scales=SCALES)
-    cspec = mo.Spec(1, E, tokens, R, hidden=H, elem_size=2, scales=0)
-    x, routes, w = _inputs(0, tokens)
+    sample = min(tokens, 512)
+    E, R, H = wl["experts"], wl["topk"], wl["hidden"]
+    ospec = mo.Spec(1, E, sample, R, hidden=H, elem_size=wl["elem"], scales=wl["scales"])
+    cspec = mo.Spec(1, E, sample, R, hidden=H, elem_size=2, scales=0)
+    x, routes, w = _inputs(wl, 0, sample)
     xb = mo.bf16_decode(mo.bf16_encode(x))
     cpu_port_step(ospec, cspec, xb, routes, w, mo)  # warm
     times = []
@@ -93,9 +123,12 @@ def cpu_baseline(tokens: int, seconds: float) -> dict:
         t0 = time.perf_counter()
         cpu_port_step(ospec, cspec, xb, routes, w, mo)
         times.append((time.perf_counter() - t0) * 1e6)
-    return {"value": statistics.median(times), "unit": "us", "cores": 1, "kind": "port",
-            "sample": f"{len(times)} full EP=1 decode steps ({tokens} tok, H={H}, E={E}, top-{R}, "
-                      f"fp8 dispatch + bf16 combine), numpy oracle port, single thread, p50"}
+    v = statistics.median(times) * tokens / sample
+    what = (f"{len(times)} full EP=1 steps" if sample == tokens else
+            f"{len(times)} EP=1 steps on a {sample}-token slice, scaled x{tokens / sample:g} to {tokens} tokens")
+    return {"value": round(v, 1), "unit": "us", "cores": 1, "kind": "port",
+            "sample": f"{what} ({wl['name']}, H={H}, E={E}, top-{R}); numpy oracle port "
+                      f"(oracle/moe_oracle.py), single thread, p50"}
 
 
 # ------------------------------------------------------------ clocks
@@ -143,8 +176,34 @@ class Clocks:
 # ------------------------------------------------------------ GPU arm
 
 
+def expected_rows(wl: dict, rank: int, n: int, tokens: int) -> dict:
+    """Row counts of this rank for the synthetic inputs (for the bytes)."""
+    E = wl["experts"]
+    L = E // n
+    all_routes = [_inputs(wl, q, tokens)[1] for q in range(n)]
+    dest = all_routes[rank] // L
+    counts = np.zeros(L, np.int64)
+    for r in all_routes:
+        e = r.ravel()
+        counts += np.bincount(e[e // L == rank] - rank * L, minlength=L)
+    return {"out_rows": int((dest != rank).sum()), "self_rows": int((dest == rank).sum()),
+            "in_rows": int(sum(((r // L) == rank).sum() for q, r in enumerate(all_routes) if q != rank)),
+            "valid_rows": int(counts.sum()), "pad_rows": int(((-counts) % 8).sum())}
+
+
+def _max_over_ranks(arr, world: int):
+    if world == 1:
+        return np.asarray(arr)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(np.asarray(arr, dtype=np.float64))
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.numpy()
+
+
 def run_b200(a) -> None:
     import torch
+    wl = dict(WORKLOADS[a.config])
     world, rank, local = _dist()
     n_gpu = world
     torch.cuda.set_device(local)
@@ -152,8 +211,10 @@ def run_b200(a) -> None:
     from paper_2510_27656_b200 import moe
     from paper_2510_27656_b200.engine import NvlinkFabric, TransferEngine
 
-    spec = moe.RoutingSpec(ranks=n_gpu, experts=E, max_tokens=a.tokens, topk=R, hidden=H,
-                           elem_size=1, scales=SCALES, comb_elem_size=2, comb_scales=0)
+    tokens = a.tokens or wl["tokens"]
+    E, R, H = wl["experts"], wl["topk"], wl["hidden"]
+    spec = moe.RoutingSpec(ranks=n_gpu, experts=E, max_tokens=tokens, topk=R, hidden=H,
+                           elem_size=wl["elem"], scales=wl["scales"], comb_elem_size=2, comb_scales=0)
     if world > 1:
         import torch.distributed as dist
         # setup-only plumbing (IPC-handle exchange, barriers, max-over-ranks
@@ -165,8 +226,7 @@ def run_b200(a) -> None:
         eng = TransferEngine(NvlinkFabric(), device=local)
         rk = moe.build_mesh([eng], spec)[0]
     rk.record_stats = False
-    tokens = a.tokens
-    x, routes, w = _inputs(rank, tokens)
+    x, routes, w = _inputs(wl, rank, tokens)
     xd = torch.from_numpy(x).to(dev).to(torch.bfloat16)
     rd = torch.from_numpy(routes).to(dev)
     wd = torch.from_numpy(w).to(dev)
@@ -192,7 +252,7 @@ def run_b200(a) -> None:
     # (step counter, counter targets), so it is captured once into a CUDA
     # graph and replayed: the timed span is device work, not Python.
     graph = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(graph):
+    with torch.cuda.graph(graph, stream=stream):
         step()
     # one graph per kernel: the fused dispatch (route + dispatch + receive
     # metadata) and the fused combine (send + weighted reduce)
@@ -213,8 +273,7 @@ def run_b200(a) -> None:
 
     # -------- timed: per step events, L2 flush + barrier outside the span
     K = a.steps
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(K)]
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
     clocks = Clocks(local)
     if world > 1:
         import torch.distributed as dist
@@ -231,9 +290,9 @@ def run_b200(a) -> None:
     clk = clocks.stop()
     err, _ = rk.status()
     assert err == 0, f"device error word {err:#x}"
-    tot = np.array([e0.elapsed_time(e1) * 1e3 for e0, e1 in ev])
+    tot = _max_over_ranks([e0.elapsed_time(e1) * 1e3 for e0, e1 in ev], world)
 
-    # -------- per-kernel durations: events between the kernels of the graph
+    # -------- per-kernel durations: one graph per kernel, events between
     names = ["dispatch", "combine"]
     acc = {k: [] for k in names}
     for _ in range(max(20, K // 2)):
@@ -248,40 +307,26 @@ def run_b200(a) -> None:
         torch.cuda.synchronize()
         for i, k in enumerate(names):
             acc[k].append(kev[i].elapsed_time(kev[i + 1]) * 1e3)
-    kt = {k: float(np.median(v)) for k, v in acc.items()}
-    dsp = np.array(acc["dispatch"])
-    cmb = np.array(acc["combine"])
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor(tot)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        tot = t.cpu().numpy()
-        kk = torch.tensor([kt[k] for k in names])
-        dist.all_reduce(kk, op=dist.ReduceOp.MAX)
-        kt = dict(zip(names, kk.cpu().numpy().tolist()))
+    kt = dict(zip(names, _max_over_ranks([float(np.median(acc[k])) for k in names], world).tolist()))
 
     # -------- e2e through the public API with pinned host buffers
     e2e = e2e_times(rk, x, routes, w, stream, flush, dev, K, world)
 
     # -------- bytes / roofline
-    ex = expected_rows(rank, n_gpu, tokens)
+    ex = expected_rows(wl, rank, n_gpu, tokens)
     P, Pc = spec.payload_bytes, spec.comb_payload_bytes
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     nvl_peak = 770.0
-    # algorithmic bytes per launch: EP=1 moves
-    # everything through HBM; EP>1 is bounded by the NVLink egress/ingress
+    # algorithmic bytes per launch: EP=1 moves everything
+    # through HBM; EP>1 is bounded by the larger of NVLink egress/ingress
     if n_gpu == 1:
-        bytes_k = {
-            "dispatch": tokens * H * 2 + tokens * R * P + ex["pad_rows"] * P,
-            "combine": tokens * R * Pc + tokens * H * 2,
-        }
+        bytes_k = {"dispatch": tokens * H * 2 + tokens * R * P + ex["pad_rows"] * P,
+                   "combine": tokens * R * Pc + tokens * H * 2}
         bound = "hbm"
     else:
-        bytes_k = {
-            "dispatch": max(ex["out_rows"], ex["in_rows"]) * P,
-            "combine": max(ex["valid_rows"] - ex["self_rows"], ex["out_rows"]) * Pc,
-        }
+        bytes_k = {"dispatch": max(ex["out_rows"], ex["in_rows"]) * P,
+                   "combine": max(ex["valid_rows"] - ex["self_rows"], ex["out_rows"]) * Pc}
         bound = "nvlink"
     dom = max(names, key=lambda k: kt[k])
     peak = hbm_peak if bound == "hbm" else nvl_peak
@@ -291,24 +336,24 @@ def run_b200(a) -> None:
                 "frac": round(achieved / peak, 4), "traffic": None,
                 "peak_source": ("MEASURED_PEAKS.json hbm_gbs (burst copy)" if bound == "hbm"
                                 else "B200_PROFILING.md measured peer copy 770 GB/s (fallback)"),
-                "algorithmic_bytes": int(bytes_k[dom]), "kernel_us": round(kt[dom], 2)}
-    step_bytes = (tokens * R * P + tokens * R * Pc)
+                "algorithmic_bytes": int(bytes_k[dom]), "kernel_us": round(kt[dom], 2),
+                "all_kernels": {k: {"bytes": int(bytes_k[k]), "us": round(kt[k], 2),
+                                    "gbs": round(bytes_k[k] / (kt[k] * 1e-6) / 1e9, 1)} for k in names}}
+    p50 = float(np.median(tot))
     res = {
-        "metric": METRIC, "value": round(float(np.median(tot)), 2), "unit": "us",
-        "n_gpus": n_gpu, "steps": K, "warmup": a.warmup,
-        "ms_per_step": round(float(np.median(tot)) / 1e3, 5),
+        "metric": wl["metric"], "value": round(p50, 2), "unit": "us",
+        "n_gpus": n_gpu, "steps": K, "warmup": a.warmup, "ms_per_step": round(p50 / 1e3, 5),
         "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
-        "dtype": "fp8-e4m3 dispatch / bf16 combine (fp32 accumulate)", "data": "synthetic",
-        "config": {"workload": "DeepSeek-V3 decode dispatch+combine", "tokens_per_rank": tokens,
-                   "hidden": H, "experts": E, "topk": R, "ep": n_gpu,
-                   "dispatch_row_bytes": P, "combine_row_bytes": Pc, "routing": "uniform top-8",
-                   "l2": "flushed before every step (512 MiB write)", "parallelism": f"ep{n_gpu}"},
-        "p50_dispatch_us": round(float(np.median(dsp)), 2),
-        "p50_combine_us": round(float(np.median(cmb)), 2),
+        "dtype": ("fp8-e4m3" if wl["elem"] == 1 else "bf16") + " dispatch / bf16 combine (fp32 accumulate)",
+        "data": "synthetic",
+        "config": {"workload": wl["name"], "tokens_per_rank": tokens, "hidden": H, "experts": E,
+                   "topk": R, "ep": n_gpu, "dispatch_row_bytes": P, "combine_row_bytes": Pc,
+                   "routing": f"{wl['routing']} top-{R}", "l2": "flushed before every step (512 MiB write)",
+                   "timing": "CUDA-graph replay of the public-API step, CUDA events, max over ranks",
+                   "parallelism": f"ep{n_gpu}"},
         "p90_us": round(float(np.percentile(tot, 90)), 2),
         "p99_us": round(float(np.percentile(tot, 99)), 2),
-        "tokens_per_s": round(n_gpu * tokens / (float(np.median(tot)) * 1e-6), 1),
-        "payload_gbs_per_rank": round(step_bytes / (float(np.median(tot)) * 1e-6) / 1e9, 1),
+        "tokens_per_s": round(n_gpu * tokens / (p50 * 1e-6), 1),
         "kernel_us": {k: round(v, 2) for k, v in kt.items()},
         "roofline": roofline,
         "e2e": e2e,
@@ -316,7 +361,7 @@ def run_b200(a) -> None:
         "clocks": clk,
     }
     if rank == 0 and n_gpu == 1 and not a.no_cpu_baseline:
-        res["cpu_baseline"] = cpu_baseline(tokens, a.cpu_seconds)
+        res["cpu_baseline"] = cpu_baseline(wl, tokens, a.cpu_seconds)
     if rank == 0:
         print(json.dumps(res), flush=True)
     rk.close()
@@ -326,28 +371,9 @@ def run_b200(a) -> None:
         dist.destroy_process_group()
 
 
-def expected_rows(rank: int, n: int, tokens: int) -> dict:
-    """Per-rank row counts for this rank's inputs (uniform routes)."""
-    L = E // n
-    all_routes = [_inputs(q, tokens)[1] for q in range(n)]
-    mine = all_routes[rank]
-    dest = mine // L
-    out_rows = int((dest != rank).sum())
-    self_rows = int((dest == rank).sum())
-    in_rows = int(sum(((r // L) == rank).sum() for q, r in enumerate(all_routes) if q != rank))
-    counts = np.zeros(L, np.int64)
-    for r in all_routes:
-        e = r.ravel()
-        e = e[e // L == rank] - rank * L
-        counts += np.bincount(e, minlength=L)
-    pad = int(((-counts) % 8).sum())
-    return {"out_rows": out_rows, "in_rows": in_rows, "self_rows": self_rows,
-            "valid_rows": int(counts.sum()), "pad_rows": pad}
-
-
 def e2e_times(rk, x, routes, w, stream, flush, dev, K: int, world: int) -> dict:
-    """Same step through the public API with pinned HOST buffers: H2D of
-    activations (bf16), routes (i64) and weights (f32) and D2H of the
+    """Same step through the eager public API with pinned HOST buffers: H2D
+    of activations (bf16), routes (i64) and weights (f32) and D2H of the
     combined bf16 output inside the timed span."""
     import torch
     xh = torch.from_numpy(x).to(torch.bfloat16).pin_memory()
@@ -376,34 +402,35 @@ def e2e_times(rk, x, routes, w, stream, flush, dev, K: int, world: int) -> dict:
         torch.cuda.synchronize()
         if k >= 5:
             times.append(e0.elapsed_time(e1) * 1e3)
-    t = np.array(times)
-    if world > 1:
-        import torch.distributed as dist
-        tt = torch.tensor(t)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t = tt.cpu().numpy()
+    t = _max_over_ranks(times, world)
     bi = x.shape[0] * x.shape[1] * 2 + routes.size * 8 + w.size * 4
     return {"value": round(float(np.median(t)), 2), "unit": "us",
-            "h2d_bytes_per_step": int(bi), "d2h_bytes_per_step": int(x.shape[0] * x.shape[1] * 2)}
+            "h2d_bytes_per_step": int(bi), "d2h_bytes_per_step": int(x.shape[0] * x.shape[1] * 2),
+            "path": "eager MoeRank API, pinned host buffers, copies inside the span"}
 
 
 # ------------------------------------------------------------ reference arm
 
 
 def run_reference(a) -> None:
+    """The reference's algorithm on the host cores: railtx is pure Python and
+    cannot travel to the GPU box, so the oracle port of it is timed
+    (DESIGN.md §9).  Rank 0 only; other ranks exit without work."""
     world, rank, _ = _dist()
     if rank != 0:
         return
-    cb = cpu_baseline(a.tokens, max(2.0, min(a.cpu_seconds, 30.0)))
-    res = {"impl": "reference", "metric": METRIC, "value": round(cb["value"], 2), "unit": "us",
+    wl = WORKLOADS[a.config]
+    tokens = a.tokens or wl["tokens"]
+    cb = cpu_baseline(wl, tokens, max(2.0, min(a.cpu_seconds, 30.0)))
+    res = {"impl": "reference", "metric": wl["metric"], "value": cb["value"], "unit": "us",
            "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "higher_is_better": False,
-           "scaling": "weak", "vs_baseline": None, "dtype": "fp8-e4m3 dispatch / bf16 combine (fp32 accumulate)",
+           "scaling": "weak", "vs_baseline": None,
+           "dtype": ("fp8-e4m3" if wl["elem"] == 1 else "bf16") + " dispatch / bf16 combine (fp32 accumulate)",
            "data": "synthetic",
-           "config": {"workload": "DeepSeek-V3 decode dispatch+combine", "tokens_per_rank": a.tokens,
-                      "hidden": H, "experts": E, "topk": R, "ep": 1},
+           "config": {"workload": wl["name"], "tokens_per_rank": tokens, "hidden": wl["hidden"],
+                      "experts": wl["experts"], "topk": wl["topk"], "ep": 1},
            "cpu_baseline": cb,
-           "e2e": {"value": round(cb["value"], 2), "unit": "us", "h2d_bytes_per_step": 0,
-                   "d2h_bytes_per_step": 0},
+           "e2e": {"value": cb["value"], "unit": "us", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
            "note": "reference railtx is pure Python and cannot travel to the GPU box; this arm times "
                    "the oracle port of its algorithm (oracle/moe_oracle.py) on the host cores"}
     print(json.dumps(res), flush=True)

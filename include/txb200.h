@@ -36,6 +36,7 @@ extern "C" {
 #define TXB_ERR_CUDA (-4)     /* CUDA runtime failure (RailtxError)        */
 
 #define TXB_MAX_RANKS 128
+#define TXB_MAX_CTAS 1024 /* cooperative grid bound for the per-CTA scratch */
 #define TXB_IPC_HANDLE_BYTES 64
 
 /* Device error-word bits (latched per rank). */
@@ -115,6 +116,8 @@ typedef struct txb_moe_bufs {
   int32_t* ret_slot;     /* [grouped_rows] combine return slot on the source */
   int64_t* info;         /* [2L+3] group_sizes, group_starts, padded_total, recv_total, error word */
   uint8_t* dirty;        /* [grouped_rows] 1 = row may hold data (zeroed when it becomes padding) */
+  uint32_t* cta_hist;    /* [TXB_MAX_CTAS][experts] per-CTA counts of the segmented route phase */
+  uint32_t* cta_bad;     /* [TXB_MAX_CTAS] per-CTA route validation bits */
   uint64_t* prof;        /* optional [grid][16] %globaltimer phase stamps (NULL = off) */
 } txb_moe_bufs;
 

@@ -23,6 +23,7 @@ TXB_ERR_REGION = -3
 TXB_ERR_CUDA = -4
 
 TXB_MAX_RANKS = 128
+TXB_MAX_CTAS = 1024
 
 EV_ROUTE_RANGE = 0x1
 EV_ROUTE_DUP = 0x2
@@ -58,7 +59,8 @@ class Bufs(C.Structure):
     _fields_ = [("region", C.c_void_p), ("peers", C.c_void_p), ("rank_scratch", C.c_void_p),
                 ("pos", C.c_void_p), ("gidx", C.c_void_p), ("rows", C.c_void_p),
                 ("sources", C.c_void_p), ("ret_slot", C.c_void_p), ("info", C.c_void_p),
-                ("dirty", C.c_void_p), ("prof", C.c_void_p)]
+                ("dirty", C.c_void_p), ("cta_hist", C.c_void_p), ("cta_bad", C.c_void_p),
+                ("prof", C.c_void_p)]
 
 
 _VP = C.c_void_p

@@ -110,7 +110,9 @@ struct Flags {
   uint32_t err;          // TXB_EV_* latch
   uint32_t ticket;       // last-CTA detection at the end of a step
   uint64_t bar_epoch;    // local epoch of txb_moe_barrier
-  uint64_t pad1[3];
+  uint32_t gbar_count;   // grid barrier of the cooperative kernels (local)
+  uint32_t gbar_gen;
+  uint64_t pad1[2];
   uint64_t bar[TXB_MAX_RANKS];  // [peer] = last barrier epoch peer reached
 };
 

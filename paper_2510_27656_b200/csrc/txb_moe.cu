@@ -46,7 +46,6 @@ constexpr int kGroupPad = 8;       // moe.py:27
 constexpr int kMaxExperts = 1536;  // shared-memory bound of the route phase
 constexpr int kThreads = 512;      // block size of the main kernels
 constexpr int kRouteThreads = 1024;
-constexpr int kFusedMaxCopies = 16384;  // n*R limit of the fused dispatch
 constexpr int kMaxOwn = 64;        // copies per CTA of the direct-count path
 
 __device__ __forceinline__ int pad_up(int x) { return (x + kGroupPad - 1) / kGroupPad * kGroupPad; }
@@ -200,6 +199,117 @@ __device__ __noinline__ uint32_t route_counts_chunked(const txb_moe_shape& s, co
   const uint32_t b = sh.bad;
   if (b)
     for (int e = tid; e < E; e += blockDim.x) hist[e] = 0;
+  __syncthreads();
+  return b;
+}
+
+// Grid barrier for cooperative launches (every CTA resident): arrival
+// counter + generation word in the rank's local flags.
+__device__ void grid_sync(Flags* f, int ncta) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile uint32_t* gen = &f->gbar_gen;
+    const uint32_t my = *gen;
+    __threadfence();
+    if (atomicAdd(&f->gbar_count, 1u) == (uint32_t)ncta - 1) {
+      f->gbar_count = 0;
+      __threadfence();
+      atomicAdd(&f->gbar_gen, 1u);
+    } else {
+      while (*gen == my) {
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// Segmented counts for large batches: CTA `cta` owns tokens [t0, t1); it
+// ranks its own copies (chunked warp match + per-warp scan), publishes its
+// per-expert counts, and after a grid barrier adds the counts of all
+// earlier CTAs -- global stable ranks (moe.py:514-521) in O(n/grid) per CTA.
+// Writes the global ranks and pos[t,j] of its copies; hist = totals.
+__device__ __noinline__ uint32_t route_counts_segmented(const txb_moe_shape& s, const int64_t* routes,
+                                                       uint32_t* hist, uint32_t* wc, int32_t* rank_out,
+                                                       int64_t* pos, int64_t t0, int64_t t1,
+                                                       uint32_t* cta_hist, uint32_t* cta_bad, Flags* f, int cta,
+                                                       int ncta, Shared& sh) {
+  const int E = s.experts, R = s.topk;
+  const int tid = threadIdx.x, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  if (tid == 0) {
+    sh.bad = 0;
+    sh.direct = 0;
+  }
+  for (int e = tid; e < E; e += blockDim.x) hist[e] = 0;
+  __syncthreads();
+  const int64_t M0 = t0 * R, M1 = t1 * R;
+  for (int64_t base = M0; base < M1; base += blockDim.x) {
+    for (int i = tid; i < nwarps * E; i += blockDim.x) wc[i] = 0;
+    __syncthreads();
+    const int64_t i = base + tid;
+    int e = -1;
+    if (i < M1) {
+      const int64_t v = routes[i];
+      if (v < 0 || v >= E) {
+        atomicOr(&sh.bad, TXB_EV_ROUTE_RANGE);
+      } else {
+        e = (int)v;
+        for (int64_t q = (i / R) * R; q < i; ++q)
+          if (routes[q] == v) atomicOr(&sh.bad, TXB_EV_ROUTE_DUP);
+      }
+    }
+    const uint32_t same = __match_any_sync(0xffffffffu, e);
+    const int lr = __popc(same & lanemask_lt());
+    if (e >= 0 && lr == 0) wc[warp * E + e] = __popc(same);
+    __syncthreads();
+    for (int x = tid; x < E; x += blockDim.x) {
+      uint32_t run = hist[x];
+      for (int w = 0; w < nwarps; ++w) {
+        const uint32_t c = wc[w * E + x];
+        wc[w * E + x] = run;
+        run += c;
+      }
+      hist[x] = run;
+    }
+    __syncthreads();
+    if (e >= 0) rank_out[i] = (int32_t)(wc[warp * E + e] + lr);
+    __syncthreads();
+  }
+  for (int e = tid; e < E; e += blockDim.x) cta_hist[(size_t)cta * E + e] = hist[e];
+  if (tid == 0) cta_bad[cta] = sh.bad;
+  grid_sync(f, ncta);
+  int* basev = reinterpret_cast<int*>(wc);   // [E] counts of earlier CTAs
+  int* ex = basev + E;                       // [E] exclusive prefix of the totals
+  for (int e = tid; e < E; e += blockDim.x) {
+    int before = 0, total = 0;
+    for (int q = 0; q < ncta; ++q) {
+      const int c = (int)cta_hist[(size_t)q * E + e];
+      total += c;
+      if (q < cta) before += c;
+    }
+    basev[e] = before;
+    hist[e] = (uint32_t)total;
+  }
+  for (int q = tid; q < ncta; q += blockDim.x)
+    if (cta_bad[q]) atomicOr(&sh.bad, cta_bad[q]);
+  __syncthreads();
+  const uint32_t b = sh.bad;
+  for (int e = tid; e < E; e += blockDim.x) {
+    if (b) hist[e] = 0;  // publish an empty row
+    ex[e] = (int)hist[e];
+  }
+  __syncthreads();
+  block_scan_i32(ex, E, sh.tmp);
+  for (int64_t i = M0 + tid; i < M1; i += blockDim.x) {
+    if (b) {
+      pos[i] = -1;
+      continue;
+    }
+    const int e = (int)routes[i];
+    const int r = rank_out[i] + basev[e];
+    rank_out[i] = r;
+    pos[i] = (int64_t)ex[e] + r;
+  }
   __syncthreads();
   return b;
 }
@@ -401,14 +511,15 @@ __device__ __noinline__ void dispatch_row_slow(const txb_moe_shape& s, const voi
   }
 }
 
+// Tokens t = t0, t0 + dt, ... < t1 of this CTA.
 template <int SRC, int ELEM>
-__device__ __noinline__ void dispatch_tokens(const txb_moe_shape& s, const void* x, int64_t n,
-                                             const int64_t* routes, const int32_t* rank_in, int32_t* gidx,
-                                             void* const* peers, const int* baseg, int cta, int ncta, Shared& sh) {
+__device__ __noinline__ void dispatch_tokens(const txb_moe_shape& s, const void* x, int64_t t0, int64_t t1,
+                                             int64_t dt, const int64_t* routes, const int32_t* rank_in,
+                                             int32_t* gidx, void* const* peers, const int* baseg, Shared& sh) {
   const int R = s.topk, tid = threadIdx.x;
   const int64_t P = s.payload_bytes;
   int kt = 0;
-  for (int64_t t = cta; t < n; t += ncta, ++kt) {
+  for (int64_t t = t0; t < t1; t += dt, ++kt) {
     token_dests(s, routes, rank_in, gidx, peers, baseg, t, kt, sh);
     if constexpr (SRC == TXB_SRC_ROWS) {
       const uint8_t* src = reinterpret_cast<const uint8_t*>(x) + t * P;
@@ -705,7 +816,7 @@ k_dispatch(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, int64_t 
   for (int q = threadIdx.x; q < s.ranks; q += blockDim.x) sh.cnt[q] = 0;
   if (threadIdx.x == 0) sh.direct = 0;
   __syncthreads();
-  dispatch_tokens<SRC, ELEM>(s, x, n, routes, b.rank_scratch, b.gidx, b.peers, baseg, blockIdx.x, gridDim.x, sh);
+  dispatch_tokens<SRC, ELEM>(s, x, blockIdx.x, n, gridDim.x, routes, b.rank_scratch, b.gidx, b.peers, baseg, sh);
   signal_counts(s, b.peers, offsetof(Flags, tok_ctr), sh);
 }
 
@@ -794,10 +905,13 @@ k_dispatch_fused(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
     if (cta == 0 && threadIdx.x == 0) f->tok_target += (uint64_t)recv_carve(s, rt).tot[1];
     signal_counts(s, b.peers, offsetof(Flags, tok_ctr), sh);
   } else {
-    const uint32_t bad = route_counts_chunked(s, routes, n, hist, wc, b.rank_scratch, cta, ncta, sh);
+    // contiguous token range per CTA, segmented counting with a grid barrier
+    const int64_t chunk = (n + ncta - 1) / ncta;
+    const int64_t t0 = n < cta * chunk ? n : cta * chunk, t1 = n < t0 + chunk ? n : t0 + chunk;
+    const uint32_t bad = route_counts_segmented(s, routes, hist, wc, b.rank_scratch, b.pos, t0, t1, b.cta_hist,
+                                                b.cta_bad, f, cta, ncta, sh);
     stamp(b, 1);
     route_publish(s, b.peers, f, hist, step, n, bad, cta, ncta);
-    route_positions(s, routes, n, hist, reinterpret_cast<int*>(wc), b.rank_scratch, b.pos, bad, cta, ncta, sh);
     stamp(b, 2);
     if (!wait_routes(s, f, route_of(b.region, s, (int)(step & 1)), C, step, timeout_ns, sh)) return;
     stamp(b, 3);
@@ -807,8 +921,7 @@ k_dispatch_fused(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
     for (int q = threadIdx.x; q < s.ranks; q += blockDim.x) sh.cnt[q] = 0;
     __syncthreads();
     stamp(b, 4);
-    if (!bad)
-      dispatch_tokens<SRC, ELEM>(s, x, n, routes, b.rank_scratch, b.gidx, b.peers, baseg, cta, ncta, sh);
+    if (!bad) dispatch_tokens<SRC, ELEM>(s, x, t0, t1, 1, routes, b.rank_scratch, b.gidx, b.peers, baseg, sh);
     stamp(b, 5);
     signal_counts(s, b.peers, offsetof(Flags, tok_ctr), sh);
   }
@@ -1098,10 +1211,9 @@ int txb_moe_dispatch_fused(const txb_moe_shape* s, const txb_moe_bufs* b, const 
     set_error("%lld tokens exceed the %d-token limit", (long long)n, s->max_tokens);
     return TXB_ERR_PROTOCOL;
   }
-  if (n * s->topk > kFusedMaxCopies) {
-    set_error("fused dispatch handles at most %d copies per step (got %lld); use the split path",
-              kFusedMaxCopies, (long long)(n * s->topk));
-    return TXB_ERR_PROTOCOL;
+  if (!b->cta_hist || !b->cta_bad) {
+    set_error("fused dispatch needs the per-CTA scratch (cta_hist / cta_bad)");
+    return TXB_ERR_REGION;
   }
   TXB_CUDA(cudaSetDevice(s->device));
   const size_t smem = smem_main(s, true);

@@ -42,7 +42,6 @@ from .errors import ProtocolError
 from .memory import Region, enable_peer_access, view
 
 GROUP_PAD = 8           # moe.py:27
-FUSED_MAX_COPIES = 16384  # n*topk limit of the fused dispatch kernel (txb_moe.cu)
 DEFAULT_PRIVATE = 32    # moe.py:28
 
 
@@ -403,6 +402,8 @@ class MoeRank:
         self._gidx = torch.empty(max(1, T * R), dtype=torch.int32, device=dev)
         # receive rows that may hold data (the region starts zeroed)
         self._dirty = torch.zeros(G, dtype=torch.uint8, device=dev)
+        self._cta_hist = torch.zeros(_lib.TXB_MAX_CTAS * spec.experts, dtype=torch.int32, device=dev)
+        self._cta_bad = torch.zeros(_lib.TXB_MAX_CTAS, dtype=torch.int32, device=dev)
         self._info = torch.zeros(2 * L + 3, dtype=torch.int64, device=dev)
         self._info_host = torch.zeros(2 * L + 3, dtype=torch.int64).pin_memory()
         self._grouped = self.region.tensor(int(sh.off_grouped), (G, int(sh.payload_bytes)), torch.uint8)
@@ -446,6 +447,8 @@ class MoeRank:
         b.ret_slot = self._ret.data_ptr()
         b.info = self._info.data_ptr()
         b.dirty = self._dirty.data_ptr()
+        b.cta_hist = self._cta_hist.data_ptr()
+        b.cta_bad = self._cta_bad.data_ptr()
 
     def _connect(self, mesh: Sequence["MoeRank"]) -> None:
         """In-process wiring: peers are addressed directly (peer access)."""
@@ -592,8 +595,7 @@ class MoeRank:
         st.keep = [r_dev, p]
         self._event(st)
         sid = self._sid()
-        st.fused = self.fused and not self.host_gated and n * spec.topk <= FUSED_MAX_COPIES \
-            and _between is None
+        st.fused = self.fused and not self.host_gated and _between is None
         if st.fused:
             # route + dispatch + receive metadata in one cooperative kernel
             _lib.call("txb_moe_dispatch_fused", self._shape_p, self._bufs_p, _sp(p), kind, n,
