@@ -172,6 +172,47 @@ int txb_moe_barrier(const txb_moe_shape* s, const txb_moe_bufs* b, uint64_t time
 int txb_moe_status(const txb_moe_shape* s, void* region, uint32_t* err, uint64_t* counters,
                    int64_t ncounters);
 
+/* ------------------------------------------- engine primitives (phase 2) */
+
+/* ImmCounter table: one u64 receipt counter per slot, slot = imm % TXB_IMM_SLOTS
+ * (ImmCounterTable, engine.py:138-205; receipts are counted on the device,
+ * the host keeps `consumed` per imm so a value can be re-armed). */
+#define TXB_IMM_SLOTS 65536
+
+/* One paged write (submit_paged_writes, engine.py:438-466; a single write is
+ * one page).  Page i: src_base + src_offset + src_idx[i]*src_stride ->
+ * dst_base + dst_offset + dst_idx[i]*dst_stride, page_len bytes (wire.py
+ * Pages:100-112).  idx arrays are device i64 (NULL = identity).  imm_ctr:
+ * the destination's ImmCounter slot (peer-mapped) or NULL; incremented once,
+ * after the whole payload is visible.  ticket: a zeroed device u32 used for
+ * last-CTA detection (operations sharing a ticket must be stream-ordered). */
+typedef struct txb_pages {
+  const void* src_base;
+  int64_t src_offset, src_stride;
+  const int64_t* src_idx;
+  void* dst_base;
+  int64_t dst_offset, dst_stride;
+  const int64_t* dst_idx;
+  int64_t npages, page_len;
+  uint64_t* imm_ctr;
+  uint32_t* ticket;
+  int32_t use_tma;       /* 1: TMA bulk copies (16-byte aligned pages), 0: vector copies */
+  int32_t single_device; /* 1: every party on this device (.gpu-scope fences) */
+} txb_pages;
+
+int txb_imm_table_slots(void);
+/* Move the pages and release one increment on *imm_ctr (engine.py:480-508, 759-782). */
+int txb_copy_pages(const txb_pages* job, int grid, void* stream);
+/* Zero-length writes carrying an immediate: +value on each of n counters
+ * (ctrs: device array of peer-mapped counter pointers) (submit_barrier). */
+int txb_imm_add(uint64_t* const* ctrs, int n, uint64_t value, int single_device, void* stream);
+/* Block `stream` until *ctr >= threshold (device-side ImmFlag wait); on
+ * timeout sets TXB_EV_WAIT_IMM in *err (may be NULL). */
+int txb_imm_wait(const uint64_t* ctr, uint64_t threshold, uint64_t timeout_ns, uint32_t* err, void* stream);
+/* Per-tensor fp8 narrowing of bf16 words (weights.prepare, weights.py:383-387):
+ * out = e4m3(x / f32(amax/448)) bytes followed by the f32 scale (n + 4 bytes). */
+int txb_fp8_quantize_tensor(const uint16_t* x, int64_t n, uint32_t* amax_scratch, uint8_t* out, void* stream);
+
 /* ----------------------------------- codecs (kernels.py registry "cuda") */
 
 /* encode_tokens (moe.py:231-246): values (f32 or bf16 [n, hidden]) ->

@@ -63,6 +63,18 @@ class Bufs(C.Structure):
                 ("prof", C.c_void_p)]
 
 
+class Pages(C.Structure):
+    """txb_pages (include/txb200.h)."""
+
+    _fields_ = [("src_base", C.c_void_p), ("src_offset", C.c_int64), ("src_stride", C.c_int64),
+                ("src_idx", C.c_void_p), ("dst_base", C.c_void_p), ("dst_offset", C.c_int64),
+                ("dst_stride", C.c_int64), ("dst_idx", C.c_void_p), ("npages", C.c_int64),
+                ("page_len", C.c_int64), ("imm_ctr", C.c_void_p), ("ticket", C.c_void_p),
+                ("use_tma", C.c_int32), ("single_device", C.c_int32)]
+
+
+TXB_IMM_SLOTS = 65536
+
 _VP = C.c_void_p
 _I64 = C.c_int64
 _U64 = C.c_uint64
@@ -92,6 +104,11 @@ SIGNATURES: dict[str, list] = {
     "txb_moe_combine_recv": [C.POINTER(Shape), C.POINTER(Bufs), _VP, _I64, _VP, _I64, _VP, _INT, _U64, _VP],
     "txb_moe_barrier": [C.POINTER(Shape), C.POINTER(Bufs), _U64, _VP],
     "txb_moe_status": [C.POINTER(Shape), _VP, C.POINTER(C.c_uint32), C.POINTER(_U64), _I64],
+    "txb_imm_table_slots": [],
+    "txb_copy_pages": [C.POINTER(Pages), _INT, _VP],
+    "txb_imm_add": [_VP, _INT, _U64, _INT, _VP],
+    "txb_imm_wait": [_VP, _U64, _U64, _VP, _VP],
+    "txb_fp8_quantize_tensor": [_VP, _I64, _VP, _VP, _VP],
     "txb_encode_rows": [_VP, _INT, _I64, _I32, _I32, _I32, _VP, _VP],
     "txb_decode_rows": [_VP, _I64, _I32, _I32, _I32, _VP, _VP],
     "txb_pack_rows": [_VP, _I64, _VP, _I64, _VP, _VP],

@@ -13,14 +13,18 @@ is no host proxy and no worker thread.
 
 from __future__ import annotations
 
+import ctypes as C
 import itertools
+import os
+import threading
+import time
 from dataclasses import dataclass
-from typing import Sequence
+from typing import Callable, Sequence
 
 import torch
 
-from . import memory
-from .errors import RegionError, TransferError
+from . import _lib, memory
+from .errors import ProtocolError, RegionError, TransferError
 
 
 @dataclass(frozen=True)
@@ -115,8 +119,161 @@ class NvlinkFabric:
             dist.barrier(group=self.group)
 
 
+# ------------------------------------------------------------- wire types
+
+
+@dataclass(frozen=True)
+class MrHandle:
+    """Local handle of a registered region (wire.py:90-97)."""
+
+    region_id: int
+    base: int          # device address
+    length: int
+    device: int
+
+
+@dataclass(frozen=True)
+class MrDesc:
+    """What a peer needs to write into a region and count receipts
+    (wire.py:64-87): the owner engine, the region's device address and
+    length, and the owner's ImmCounter table.  `ipc`/`imm_ipc` carry CUDA
+    IPC handles for peers in other processes (regions allocated by the
+    engine); in-process peers use the addresses directly."""
+
+    owner: str
+    device: int
+    base: int
+    length: int
+    imm_base: int
+    pid: int
+    ipc: bytes | None = None
+    ipc_offset: int = 0
+    imm_ipc: bytes | None = None
+
+
+@dataclass(frozen=True)
+class Pages:
+    """Indirect page addressing: page i lives at offset + indices[i] * stride
+    (wire.py:100-112)."""
+
+    indices: tuple
+    stride: int
+    offset: int = 0
+
+    def __post_init__(self) -> None:
+        object.__setattr__(self, "indices", tuple(int(i) for i in self.indices))
+
+    def page_offset(self, i: int) -> int:
+        return self.offset + self.indices[i] * self.stride
+
+
+@dataclass(frozen=True)
+class ScatterDst:
+    """One peer's slice in a scatter: src offset -> (desc, offset), `length`
+    bytes (wire.py:115-122)."""
+
+    length: int
+    src: int
+    desc: MrDesc
+    offset: int
+
+
+class CompletionFlag:
+    """Completion of one submitted operation (engine.py:48-77): a CUDA event
+    recorded after the operation's kernel on the engine's stream."""
+
+    def __init__(self, event=None, ok: bool = True, error: str | None = None) -> None:
+        self._ev = event
+        self.ok = ok
+        self.error = error
+        self.vtime = 0.0
+
+    def done(self) -> bool:
+        return self._ev is None or self._ev.query()
+
+    def wait(self, timeout: float | None = None) -> bool:
+        if self._ev is None:
+            return True
+        if timeout is None:
+            self._ev.synchronize()
+            return True
+        deadline = time.monotonic() + timeout
+        while not self._ev.query():
+            if time.monotonic() > deadline:
+                return False
+            time.sleep(2e-5)
+        return True
+
+    def result(self, timeout: float | None = None) -> float:
+        if not self.wait(timeout):
+            raise TransferError("timed out waiting for completion")
+        if not self.ok:
+            raise TransferError(self.error or "operation failed")
+        return self.vtime
+
+
+class ImmFlag:
+    """Fires when an armed immediate count is reached (engine.py:80-103).
+
+    Receipts are counted on the device (one u64 slot per imm value); the
+    flag holds the threshold `consumed + count` fixed when it was armed.
+    `wait_device(stream)` makes GPU work queued behind it wait on the device
+    instead of the host."""
+
+    def __init__(self, engine: "TransferEngine", imm: int, threshold: int,
+                 cb: Callable | None = None) -> None:
+        self.engine = engine
+        self.imm = imm
+        self.threshold = threshold
+        self.cb = cb
+        self.vtime = 0.0
+        self._fired = False
+
+    def _check(self) -> bool:
+        if not self._fired and self.engine.imm_received_total(self.imm) >= self.threshold:
+            self._fired = True
+            self.engine._disarm(self.imm, self)
+            if self.cb is not None:
+                self.cb(self)
+        return self._fired
+
+    def done(self) -> bool:
+        return self._check()
+
+    def wait(self, timeout: float | None = None) -> bool:
+        deadline = None if timeout is None else time.monotonic() + timeout
+        sleep = 1e-5
+        while not self._check():
+            if deadline is not None and time.monotonic() > deadline:
+                return False
+            time.sleep(sleep)
+            sleep = min(2 * sleep, 1e-3)
+        return True
+
+    def result(self, timeout: float | None = None) -> float:
+        if not self.wait(timeout):
+            raise TransferError(f"timed out waiting for imm {self.imm}")
+        return self.vtime
+
+    def wait_device(self, stream=None, timeout: float = 30.0) -> None:
+        st = stream or torch.cuda.current_stream(self.engine.device)
+        _lib.call("txb_imm_wait", C.c_void_p(self.engine._imm_slot_ptr(self.imm)), self.threshold,
+                  int(timeout * 1e9), C.c_void_p(self.engine._err.data_ptr()), C.c_void_p(st.cuda_stream))
+
+
 class TransferEngine:
-    """One rank's endpoint on one CUDA device."""
+    """One rank's endpoint on one CUDA device.
+
+    Mirrors the submission API of railtx.engine.TransferEngine
+    (engine.py:260-850): reg_mr / dereg_mr, submit_single_write,
+    submit_paged_writes, submit_scatter, submit_barrier, expect_imm_count,
+    add_peer_group.  Every submission is one sm_100a kernel on the engine's
+    stream that moves the bytes with device-initiated stores (TMA bulk copies
+    for aligned pages) and releases one increment on the destination's
+    ImmCounter slot after the payload is visible.  There are no rails, no
+    worker thread and no host proxy."""
+
+    _TICKETS = 64
 
     def __init__(self, fabric: NvlinkFabric | None = None, *, device: int = 0,
                  name: str | None = None, rails: int = 1, engine_id: int | None = None) -> None:
@@ -128,7 +285,16 @@ class TransferEngine:
         self.device = int(device)
         self.fabric.engines.append(self)
         self._regions: dict[int, memory.Region] = {}
+        self._mrs: dict[int, tuple[MrHandle, MrDesc, object]] = {}
+        self._ids = itertools.count(1)
+        self._lock = threading.Lock()
         self._closed = False
+        self._imm = None           # lazily: ImmCounter table region
+        self._stream = None
+        self._consumed: dict[int, int] = {}
+        self._armed: dict[int, ImmFlag] = {}
+        self._groups: dict[int, tuple] = {}
+        self._opened: dict[tuple, memory.Region] = {}
 
     def main_address(self) -> NetAddr:
         import socket
@@ -151,9 +317,313 @@ class TransferEngine:
             raise RegionError("region not registered with this engine")
         region.close()
 
+    def _ensure_imm(self) -> None:
+        if self._imm is None:
+            self._imm = self.alloc_region(_lib.TXB_IMM_SLOTS * 8 + 4096)
+            dev = torch.device("cuda", self.device)
+            self._tickets = torch.zeros(self._TICKETS, dtype=torch.int32, device=dev)
+            self._ticket_i = 0
+            self._err = torch.zeros(1, dtype=torch.int32, device=dev)
+            self._stream = torch.cuda.Stream(dev)
+            self._read_stream = torch.cuda.Stream(dev)   # counter snapshots
+
+    @property
+    def stream(self):
+        self._ensure_imm()
+        return self._stream
+
+    def alloc_buffer(self, nbytes: int) -> torch.Tensor:
+        """A uint8 device buffer whose region can be exported to peers in
+        other processes (CUDA IPC); register it with reg_mr."""
+        r = self.alloc_region(nbytes)
+        t = r.tensor(0, (nbytes,), torch.uint8)
+        t._txb_region = r  # keep the region reachable from the tensor
+        return t
+
+    def reg_mr(self, buf, device: int | None = None) -> tuple[MrHandle, MrDesc]:
+        """Register a writable contiguous CUDA tensor (engine.py:314-341)."""
+        self._ensure_imm()
+        if device is not None and device != self.device:
+            raise RegionError(f"unknown device {device}")
+        if not isinstance(buf, torch.Tensor) or not buf.is_cuda:
+            raise RegionError("region must be a CUDA tensor on the engine's device")
+        if buf.device.index != self.device:
+            raise RegionError(f"region lives on cuda:{buf.device.index}, engine on cuda:{self.device}")
+        if not buf.is_contiguous():
+            raise RegionError("region must be contiguous")
+        base, length = buf.data_ptr(), buf.numel() * buf.element_size()
+        with self._lock:
+            if any(h.base == base for h, _, _ in self._mrs.values()):
+                raise RegionError("buffer already registered")
+            rid = next(self._ids)
+        ipc, ipc_off = None, 0
+        reg = getattr(buf, "_txb_region", None)
+        if reg is not None:
+            ipc, ipc_off = reg.ipc_handle(), base - reg.ptr
+        h = MrHandle(rid, base, length, self.device)
+        d = MrDesc(self.name, self.device, base, length, self._imm.ptr, os.getpid(), ipc, ipc_off,
+                   self._imm.ipc_handle())
+        with self._lock:
+            self._mrs[rid] = (h, d, buf)
+        return h, d
+
+    def dereg_mr(self, handle: MrHandle) -> None:
+        with self._lock:
+            if self._mrs.pop(handle.region_id, None) is None:
+                raise RegionError(f"region {handle.region_id} not registered")
+
+    def desc_of(self, handle: MrHandle) -> MrDesc:
+        with self._lock:
+            rec = self._mrs.get(handle.region_id)
+        if rec is None:
+            raise RegionError(f"region {handle.region_id} not registered")
+        return rec[1]
+
+    def _get(self, handle: MrHandle) -> MrHandle:
+        with self._lock:
+            rec = self._mrs.get(handle.region_id)
+        if rec is None:
+            raise RegionError(f"region {handle.region_id} not registered")
+        return rec[0]
+
+    def _peer_base(self, desc: MrDesc) -> tuple[int, int]:
+        """(region address, ImmCounter table address) of `desc` as seen from
+        this process."""
+        if desc.pid == os.getpid():
+            return desc.base, desc.imm_base
+        if desc.ipc is None or desc.imm_ipc is None:
+            raise RegionError("remote region was not allocated with alloc_buffer (no IPC handle)")
+        key = (desc.pid, desc.ipc, desc.imm_ipc)
+        with self._lock:
+            got = self._opened.get(key)
+            if got is None:
+                reg = memory.Region.open_ipc(self.device, desc.ipc, desc.ipc_offset + desc.length)
+                imm = memory.Region.open_ipc(self.device, desc.imm_ipc, _lib.TXB_IMM_SLOTS * 8)
+                got = self._opened[key] = (reg, imm)
+        return got[0].ptr + desc.ipc_offset, got[1].ptr
+
+    def _imm_slot_ptr(self, imm: int, imm_base: int | None = None) -> int:
+        base = self._imm.ptr if imm_base is None else imm_base
+        return base + (imm % _lib.TXB_IMM_SLOTS) * 8
+
+    # --------------------------------------------------------- submissions
+
+    def _single_device(self, desc: MrDesc) -> int:
+        return 1 if desc.pid == os.getpid() and desc.device == self.device else 0
+
+    def _launch_pages(self, src_base: int, src_pages: Pages, desc: MrDesc, dst_pages: Pages,
+                      page_len: int, npages: int, imm: int | None,
+                      idx: tuple | None = None) -> CompletionFlag:
+        self._ensure_imm()
+        dst_base, dst_imm = self._peer_base(desc)
+        dev = torch.device("cuda", self.device)
+        j = _lib.Pages()
+        j.src_base, j.src_offset, j.src_stride = src_base, src_pages.offset, src_pages.stride
+        j.dst_base, j.dst_offset, j.dst_stride = dst_base, dst_pages.offset, dst_pages.stride
+        keep = []
+        if idx is not None:
+            si = torch.tensor(src_pages.indices, dtype=torch.int64).to(dev, non_blocking=True)
+            di = torch.tensor(dst_pages.indices, dtype=torch.int64).to(dev, non_blocking=True)
+            keep = [si, di]
+            j.src_idx, j.dst_idx = si.data_ptr(), di.data_ptr()
+        j.npages, j.page_len = npages, page_len
+        j.imm_ctr = self._imm_slot_ptr(imm, dst_imm) if imm is not None else None
+        with self._lock:
+            t = self._ticket_i
+            self._ticket_i = (t + 1) % self._TICKETS
+        j.ticket = self._tickets.data_ptr() + 4 * t
+        aligned = all(v % 16 == 0 for v in (src_base + src_pages.offset, dst_base + dst_pages.offset,
+                                            src_pages.stride, dst_pages.stride, page_len))
+        j.use_tma = 1 if aligned and page_len >= 1024 else 0
+        j.single_device = self._single_device(desc)
+        with torch.cuda.device(self.device):
+            # the payload was produced on the caller's stream
+            self._stream.wait_stream(torch.cuda.current_stream(self.device))
+            with torch.cuda.stream(self._stream):
+                for k in keep:
+                    k.record_stream(self._stream)
+                _lib.call("txb_copy_pages", C.byref(j), 0, C.c_void_p(self._stream.cuda_stream))
+                ev = torch.cuda.Event()
+                ev.record(self._stream)
+        return CompletionFlag(ev)
+
+    @staticmethod
+    def _check_imm(imm) -> None:
+        if imm is not None and not 0 <= imm < (1 << 32):
+            raise TransferError(f"imm {imm} is not a u32")
+
+    def submit_single_write(self, length: int, src: tuple, dst: tuple, imm: int | None = None,
+                            on_done: Callable | None = None, not_before: float = 0.0,
+                            label: str = "") -> CompletionFlag:
+        """engine.py:397-436 -- bounds, then one device copy + one receipt."""
+        handle, src_off = src
+        desc, dst_off = dst
+        rec = self._get(handle)
+        if length < 0 or src_off < 0 or dst_off < 0:
+            raise TransferError("negative length or offset")
+        if src_off + length > rec.length:
+            raise TransferError(f"source range [{src_off},{src_off + length}) outside region of {rec.length}")
+        if dst_off + length > desc.length:
+            raise TransferError(f"destination range [{dst_off},{dst_off + length}) outside region of {desc.length}")
+        if length == 0 and imm is None:
+            raise TransferError("zero-length write requires an immediate")
+        self._check_imm(imm)
+        flag = self._launch_pages(rec.base, Pages((0,), 0, src_off), desc, Pages((0,), 0, dst_off),
+                                  length, 1 if length else 0, imm)
+        return self._done(flag, on_done)
+
+    def submit_paged_writes(self, page_len: int, src: tuple, dst: tuple, imm: int | None = None,
+                            on_done: Callable | None = None, not_before: float = 0.0,
+                            label: str = "") -> CompletionFlag:
+        """engine.py:438-466 -- one kernel moves every page, one receipt."""
+        handle, src_pages = src
+        desc, dst_pages = dst
+        rec = self._get(handle)
+        if len(src_pages.indices) != len(dst_pages.indices):
+            raise TransferError(f"{len(src_pages.indices)} source pages vs "
+                                f"{len(dst_pages.indices)} destination pages")
+        if page_len <= 0:
+            raise TransferError("page length must be positive")
+        self._check_pages(src_pages, page_len, rec.length, "source")
+        self._check_pages(dst_pages, page_len, desc.length, "destination")
+        self._check_imm(imm)
+        flag = self._launch_pages(rec.base, src_pages, desc, dst_pages, page_len,
+                                  len(src_pages.indices), imm, idx=(True,))
+        return self._done(flag, on_done)
+
+    @staticmethod
+    def _check_pages(pages: Pages, page_len: int, region_len: int, side: str) -> None:
+        for i in pages.indices:
+            if not 0 <= i < (1 << 32):
+                raise TransferError(f"{side} page index {i} is not a u32")
+        if pages.indices:
+            worst = pages.offset + max(pages.indices) * pages.stride + page_len
+            if worst > region_len:
+                raise TransferError(f"{side} page ends at {worst}, outside region of {region_len}")
+
+    def add_peer_group(self, addrs: Sequence) -> int:
+        if not addrs:
+            raise TransferError("empty peer group")
+        with self._lock:
+            h = next(self._ids)
+            self._groups[h] = tuple(addrs)
+        return h
+
+    def _group(self, group: int, n: int, what: str) -> tuple:
+        with self._lock:
+            peers = self._groups.get(group)
+        if peers is None:
+            raise TransferError(f"unknown peer group {group}")
+        if n != len(peers):
+            raise TransferError(f"{what} carries {n} entries for a group of {len(peers)}")
+        return peers
+
+    def submit_scatter(self, group: int, src: MrHandle, dsts: Sequence[ScatterDst], imm: int | None = None,
+                       on_done: Callable | None = None, not_before: float = 0.0,
+                       label: str = "") -> CompletionFlag:
+        """engine.py:563-597 -- one slice per peer, each carrying the imm."""
+        self._group(group, len(dsts), "scatter")
+        rec = self._get(src)
+        self._check_imm(imm)
+        flag = CompletionFlag()
+        for i, d in enumerate(dsts):
+            if d.length < 0 or d.src < 0 or d.offset < 0:
+                raise TransferError("negative length or offset in scatter entry")
+            if d.src + d.length > rec.length:
+                raise TransferError(f"scatter source slice {i} out of bounds")
+            if d.offset + d.length > d.desc.length:
+                raise TransferError(f"scatter destination slice {i} out of bounds")
+        for d in dsts:
+            if d.length == 0 and imm is None:
+                continue
+            flag = self._launch_pages(rec.base, Pages((0,), 0, d.src), d.desc, Pages((0,), 0, d.offset),
+                                      d.length, 1 if d.length else 0, imm)
+        return self._done(flag, on_done)
+
+    def submit_barrier(self, group: int, imm: int, dsts: Sequence[tuple], on_done: Callable | None = None,
+                       not_before: float = 0.0, label: str = "") -> CompletionFlag:
+        """engine.py:599-619 -- a zero-length write with the imm per peer."""
+        self._group(group, len(dsts), "barrier")
+        if not 0 <= imm < (1 << 32):
+            raise TransferError(f"imm {imm} is not a u32")
+        self._ensure_imm()
+        ptrs = []
+        for desc, off in dsts:
+            if not 0 <= off <= desc.length:
+                raise TransferError(f"barrier offset {off} out of bounds")
+            ptrs.append(self._imm_slot_ptr(imm, self._peer_base(desc)[1]))
+        dev = torch.device("cuda", self.device)
+        tab = torch.tensor(ptrs, dtype=torch.int64).to(dev, non_blocking=True)
+        sd = 1 if all(self._single_device(d) for d, _ in dsts) else 0
+        with torch.cuda.device(self.device):
+            self._stream.wait_stream(torch.cuda.current_stream(self.device))
+            with torch.cuda.stream(self._stream):
+                tab.record_stream(self._stream)
+                _lib.call("txb_imm_add", C.c_void_p(tab.data_ptr()), len(ptrs), 1, sd,
+                          C.c_void_p(self._stream.cuda_stream))
+                ev = torch.cuda.Event()
+                ev.record(self._stream)
+        return self._done(CompletionFlag(ev), on_done)
+
+    def _done(self, flag: CompletionFlag, on_done: Callable | None) -> CompletionFlag:
+        if on_done is not None:
+            flag.wait()
+            on_done(flag)
+        return flag
+
+    # ----------------------------------------------------------- ImmCounter
+
+    def imm_received_total(self, imm: int) -> int:
+        """Receipts counted for `imm` so far (ImmCounterTable.received_total)."""
+        self._ensure_imm()
+        out = torch.empty(1, dtype=torch.int64)
+        with torch.cuda.device(self.device), torch.cuda.stream(self._read_stream):
+            out.copy_(self._imm.tensor((imm % _lib.TXB_IMM_SLOTS) * 8, (1,), torch.int64))
+        return int(out[0])
+
+    def expect_imm_count(self, imm: int, count: int, cb: Callable | None = None) -> ImmFlag:
+        """Arm a threshold (engine.py:527-543 / ImmCounterTable.arm): fires
+        once `count` receipts beyond those already consumed have arrived and
+        consumes them, so the same imm can be re-armed round after round."""
+        if not 0 <= imm < (1 << 32):
+            raise TransferError(f"imm {imm} is not a u32")
+        if count < 0:
+            raise ProtocolError("negative imm count")
+        self._ensure_imm()
+        with self._lock:
+            if imm in self._armed:
+                raise ProtocolError(f"imm {imm} already armed")
+            base = self._consumed.get(imm, 0)
+            self._consumed[imm] = base + count
+            flag = ImmFlag(self, imm, base + count, cb)
+            self._armed[imm] = flag
+        flag._check()
+        return flag
+
+    def _disarm(self, imm: int, flag: ImmFlag) -> None:
+        with self._lock:
+            if self._armed.get(imm) is flag:
+                del self._armed[imm]
+
+    def cancel_imm(self, imm: int) -> None:
+        """ImmCounterTable.cancel: drop the expectation and realign the
+        consumed count with the receipts seen so far."""
+        total = self.imm_received_total(imm)
+        with self._lock:
+            self._armed.pop(imm, None)
+            self._consumed[imm] = total
+
+    # ---------------------------------------------------------------- close
+
     def close(self) -> None:
         if self._closed:
             return
+        if self._stream is not None:
+            self._stream.synchronize()
+        for reg, imm in self._opened.values():
+            reg.close()
+            imm.close()
+        self._opened.clear()
         for r in list(self._regions.values()):
             r.close()
         self._regions.clear()

@@ -166,12 +166,47 @@ def make_codecs(ref: Path) -> None:
     print("codecs.npz")
 
 
+def make_weights(ref: Path) -> None:
+    """weights.prepare outputs for the reference's small topology and a
+    larger fp8 tensor (per-tensor quantisation incl. NaN/inf/zero words)."""
+    _import_ref(ref)
+    import struct
+    from railtx import kernels
+    from railtx.weights import build_schedule, fill_store, prepare
+    import _invariants as inv
+    train, infer = inv.small_topology()
+    sched = build_schedule(train, infer)
+    store = fill_store(train, 7)
+    blob: dict[str, np.ndarray] = {}
+    for k, t in enumerate(sched.tasks):
+        full = np.concatenate([store.get(t.sources[0], i) for i in range(64)
+                               if (t.sources[0], i) in store._data], axis=t.axis)
+        width = t.full_shape[t.axis] // t.shard_count
+        sl = [slice(None)] * len(t.full_shape)
+        sl[t.axis] = slice(t.shard_index * width, (t.shard_index + 1) * width)
+        words = np.ascontiguousarray(full[tuple(sl)]).reshape(-1)
+        blob[f"t{k}_words"] = words
+        blob[f"t{k}_dtype"] = np.array([0 if t.dtype == "bf16" else 1])
+        blob[f"t{k}_prepared"] = np.frombuffer(prepare(t, store), np.uint8)
+    rng = np.random.default_rng(77)
+    x = (rng.standard_normal(1 << 16) * 3).astype(np.float32)
+    x[5], x[6], x[7], x[8] = np.nan, np.inf, -np.inf, 0.0
+    w = kernels.bf16_encode(x)
+    q, scale = kernels.fp8_quantize(kernels.bf16_decode(w))
+    blob["big_words"] = w
+    blob["big_prepared"] = np.frombuffer(q.tobytes() + struct.pack("<f", scale), np.uint8)
+    blob["ntasks"] = np.array([len(sched.tasks)])
+    np.savez_compressed(HERE / "weights.npz", **blob)
+    print("weights.npz", len(sched.tasks), "tasks")
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--ref", default="/root/reference")
     a = ap.parse_args()
     ref = Path(a.ref)
     make_codecs(ref)
+    make_weights(ref)
     make_moe(ref)
 
 

@@ -116,3 +116,13 @@ def test_oracle_vs_live_reference_random_grid():
             assert np.array_equal(g.data, res.ranks[q].grouped.data)
             assert np.array_equal(g.rows, res.ranks[q].grouped.rows)
             assert np.array_equal(results[q][1], comb[q])
+
+
+def test_weights_prepare_matches_reference():
+    from oracle import transfer_oracle as to
+    from golden_io import GOLDEN
+    z = np.load(GOLDEN / "weights.npz")
+    for k in range(int(z["ntasks"][0])):
+        dt = "bf16" if int(z[f"t{k}_dtype"][0]) == 0 else "fp8"
+        assert np.array_equal(to.prepare_words(z[f"t{k}_words"], dt), z[f"t{k}_prepared"]), k
+    assert np.array_equal(to.prepare_words(z["big_words"], "fp8"), z["big_prepared"])
