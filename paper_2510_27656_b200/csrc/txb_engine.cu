@@ -19,7 +19,7 @@ namespace txb {
 
 constexpr int kCopyThreads = 256;
 constexpr int kPiece = 32 * 1024;  // bytes per TMA piece (one smem stage)
-constexpr int kStages = 2;
+constexpr int kStages = 4;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(kCopyThreads, 1) k_copy_pages(txb_pages j) {
     __syncthreads();
     // thread 0 drives a kStages-deep TMA pipeline over this CTA's pieces
     if (threadIdx.x == 0) {
-      uint32_t phase[kStages] = {0, 0};
+      uint32_t phase[kStages] = {0, 0, 0, 0};
       const int64_t k0 = blockIdx.x;
       // prologue: fill the stages
       for (int s = 0; s < kStages && k0 + (int64_t)s * gridDim.x < total; ++s) {

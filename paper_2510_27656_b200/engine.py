@@ -21,6 +21,7 @@ import time
 from dataclasses import dataclass
 from typing import Callable, Sequence
 
+import numpy as np
 import torch
 
 from . import _lib, memory
@@ -295,6 +296,7 @@ class TransferEngine:
         self._armed: dict[int, ImmFlag] = {}
         self._groups: dict[int, tuple] = {}
         self._opened: dict[tuple, memory.Region] = {}
+        self.use_tma = True        # TMA bulk copies for 16-byte aligned pages
 
     def main_address(self) -> NetAddr:
         import socket
@@ -411,19 +413,23 @@ class TransferEngine:
     def _single_device(self, desc: MrDesc) -> int:
         return 1 if desc.pid == os.getpid() and desc.device == self.device else 0
 
+    def page_indices(self, pages: Pages) -> torch.Tensor:
+        """Device copy of a page index list (reusable across submissions)."""
+        t = torch.from_numpy(np.asarray(pages.indices, dtype=np.int64)).pin_memory()
+        return t.to(torch.device("cuda", self.device), non_blocking=True)
+
     def _launch_pages(self, src_base: int, src_pages: Pages, desc: MrDesc, dst_pages: Pages,
                       page_len: int, npages: int, imm: int | None,
                       idx: tuple | None = None) -> CompletionFlag:
         self._ensure_imm()
         dst_base, dst_imm = self._peer_base(desc)
-        dev = torch.device("cuda", self.device)
         j = _lib.Pages()
         j.src_base, j.src_offset, j.src_stride = src_base, src_pages.offset, src_pages.stride
         j.dst_base, j.dst_offset, j.dst_stride = dst_base, dst_pages.offset, dst_pages.stride
         keep = []
         if idx is not None:
-            si = torch.tensor(src_pages.indices, dtype=torch.int64).to(dev, non_blocking=True)
-            di = torch.tensor(dst_pages.indices, dtype=torch.int64).to(dev, non_blocking=True)
+            si, di = idx if isinstance(idx[0], torch.Tensor) else \
+                (self.page_indices(src_pages), self.page_indices(dst_pages))
             keep = [si, di]
             j.src_idx, j.dst_idx = si.data_ptr(), di.data_ptr()
         j.npages, j.page_len = npages, page_len
@@ -434,7 +440,7 @@ class TransferEngine:
         j.ticket = self._tickets.data_ptr() + 4 * t
         aligned = all(v % 16 == 0 for v in (src_base + src_pages.offset, dst_base + dst_pages.offset,
                                             src_pages.stride, dst_pages.stride, page_len))
-        j.use_tma = 1 if aligned and page_len >= 1024 else 0
+        j.use_tma = 1 if aligned and page_len >= 1024 and self.use_tma else 0
         j.single_device = self._single_device(desc)
         with torch.cuda.device(self.device):
             # the payload was produced on the caller's stream
@@ -474,8 +480,10 @@ class TransferEngine:
 
     def submit_paged_writes(self, page_len: int, src: tuple, dst: tuple, imm: int | None = None,
                             on_done: Callable | None = None, not_before: float = 0.0,
-                            label: str = "") -> CompletionFlag:
-        """engine.py:438-466 -- one kernel moves every page, one receipt."""
+                            label: str = "", device_indices: tuple | None = None) -> CompletionFlag:
+        """engine.py:438-466 -- one kernel moves every page, one receipt.
+        `device_indices` = (src, dst) int64 CUDA tensors equal to the Pages
+        indices (from page_indices) skip the per-call index upload."""
         handle, src_pages = src
         desc, dst_pages = dst
         rec = self._get(handle)
@@ -488,18 +496,20 @@ class TransferEngine:
         self._check_pages(dst_pages, page_len, desc.length, "destination")
         self._check_imm(imm)
         flag = self._launch_pages(rec.base, src_pages, desc, dst_pages, page_len,
-                                  len(src_pages.indices), imm, idx=(True,))
+                                  len(src_pages.indices), imm, idx=device_indices or (True,))
         return self._done(flag, on_done)
 
     @staticmethod
     def _check_pages(pages: Pages, page_len: int, region_len: int, side: str) -> None:
-        for i in pages.indices:
-            if not 0 <= i < (1 << 32):
-                raise TransferError(f"{side} page index {i} is not a u32")
-        if pages.indices:
-            worst = pages.offset + max(pages.indices) * pages.stride + page_len
-            if worst > region_len:
-                raise TransferError(f"{side} page ends at {worst}, outside region of {region_len}")
+        if not pages.indices:
+            return
+        idx = np.asarray(pages.indices, dtype=np.int64)
+        lo, hi = int(idx.min()), int(idx.max())
+        if lo < 0 or hi >= (1 << 32):
+            raise TransferError(f"{side} page index {lo if lo < 0 else hi} is not a u32")
+        worst = pages.offset + hi * pages.stride + page_len
+        if worst > region_len:
+            raise TransferError(f"{side} page ends at {worst}, outside region of {region_len}")
 
     def add_peer_group(self, addrs: Sequence) -> int:
         if not addrs:

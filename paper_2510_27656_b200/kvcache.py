@@ -192,8 +192,9 @@ class KvSender:
         self.kv_handle, _ = engine.reg_mr(kv)
         self.ctx_handle = engine.reg_mr(ctx)[0] if ctx is not None else None
 
-    def send_step(self, req: KvRequest, step: int):
-        """Step in 1..layout.steps: chunk, layer = divmod(step - 1, layers)."""
+    def step_pages(self, req: KvRequest, step: int) -> tuple[Pages, Pages]:
+        """Source and destination pages of one (chunk, layer) step
+        (kvcache.py:484-498)."""
         layout = req.layout
         if not 1 <= step <= layout.steps:
             raise ProtocolError(f"step {step} outside 1..{layout.steps}")
@@ -204,9 +205,26 @@ class KvSender:
             for slot in layout.chunk_slots(chunk):
                 src.append(layout.page_index(nh, layout.slots, layer, j, slot))
                 dst.append((layer * req.dst_heads + j) * req.dst_slots + req.slot_list[slot])
+        return Pages(tuple(src), layout.page_len), Pages(tuple(dst), layout.page_len)
+
+    def prepare(self, req: KvRequest) -> None:
+        """Precompute every step's page lists and upload their indices once,
+        so each layer step is a single kernel launch."""
+        self._plan = {}
+        for k in range(1, req.layout.steps + 1):
+            sp, dp = self.step_pages(req, k)
+            self._plan[(req.request_id, k)] = (sp, dp, (self.engine.page_indices(sp), self.engine.page_indices(dp)))
+
+    def send_step(self, req: KvRequest, step: int):
+        """Step in 1..layout.steps: chunk, layer = divmod(step - 1, layers)."""
+        plan = getattr(self, "_plan", {}).get((req.request_id, step))
+        if plan is None:
+            sp, dp = self.step_pages(req, step)
+            dev = None
+        else:
+            sp, dp, dev = plan
         return self.engine.submit_paged_writes(
-            layout.page_len, (self.kv_handle, Pages(tuple(src), layout.page_len)),
-            (req.kv_desc, Pages(tuple(dst), layout.page_len)), imm=req.imm)
+            req.layout.page_len, (self.kv_handle, sp), (req.kv_desc, dp), imm=req.imm, device_indices=dev)
 
     def send_context(self, req: KvRequest):
         if self.ctx_handle is None:

@@ -30,6 +30,7 @@ ap.add_argument("--heads", type=int, default=8)
 ap.add_argument("--slots", type=int, default=2048)
 ap.add_argument("--page", type=int, default=8192)
 ap.add_argument("--steps", type=int, default=40)
+ap.add_argument("--no-tma", action="store_true")
 a = ap.parse_args()
 
 ngpu = torch.cuda.device_count()
@@ -48,6 +49,9 @@ kv = pre.alloc_buffer(layout.region_bytes(a.heads, layout.slots))
 kv.fill_(7)
 ctx = pre.alloc_buffer(4096)
 send = kvcache.KvSender(pre, kv, ctx)
+pre.use_tma = not a.no_tma
+send.prepare(t.request)
+torch.cuda.synchronize()
 step_bytes = a.heads * ppc * a.page
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda:0")
 st = pre.stream
@@ -79,7 +83,8 @@ res = {"metric": "paged KV layer transfer GB/s (Llama-3-70B shape)", "value": ro
        "peak": 770.0 if d1 else 6555.2,
        "frac": round(step_bytes / (med * 1e-6) / 1e9 / (770.0 if d1 else 6555.2), 3),
        "pages_per_step": a.heads * ppc, "page_bytes": a.page, "layers": a.layers, "chunks": a.chunks,
-       "copy": "TMA bulk (cp.async.bulk) 32 KiB pieces, double-buffered, one ImmCounter receipt per step"}
+       "copy": ("TMA bulk (cp.async.bulk) pieces <= 32 KiB, 4 stages per CTA" if not a.no_tma else
+                "16-byte vector copies, one warp per page piece") + ", one ImmCounter receipt per step"}
 assert t.wait(60.0), "KV request did not complete"
 res["request_completed"] = True
 print(json.dumps(res))
