@@ -297,6 +297,7 @@ class TransferEngine:
         self._groups: dict[int, tuple] = {}
         self._opened: dict[tuple, memory.Region] = {}
         self.use_tma = True        # TMA bulk copies for 16-byte aligned pages
+        self.timing: list | None = None
 
     def main_address(self) -> NetAddr:
         import socket
@@ -448,7 +449,14 @@ class TransferEngine:
             with torch.cuda.stream(self._stream):
                 for k in keep:
                     k.record_stream(self._stream)
+                if self.timing is not None:          # bench hook: device time of the copy kernel
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e0.record(self._stream)
                 _lib.call("txb_copy_pages", C.byref(j), 0, C.c_void_p(self._stream.cuda_stream))
+                if self.timing is not None:
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e1.record(self._stream)
+                    self.timing.append((e0, e1))
                 ev = torch.cuda.Event()
                 ev.record(self._stream)
         return CompletionFlag(ev)
