@@ -18,8 +18,8 @@
 namespace txb {
 
 constexpr int kCopyThreads = 256;
-constexpr int kPiece = 32 * 1024;  // bytes per TMA piece (one smem stage)
-constexpr int kStages = 4;
+constexpr int kPiece = 16 * 1024;  // bytes per TMA piece (one smem stage)
+constexpr int kStages = 8;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -63,8 +63,10 @@ __device__ __forceinline__ void tma_store(void* gmem, const void* smem, uint32_t
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
 
-__device__ __forceinline__ void tma_store_wait_read() {  // smem may be reused
-  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+// at most kStages-1 stores may still be reading shared memory: the oldest
+// stage is free again
+__device__ __forceinline__ void tma_store_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kStages - 1) : "memory");
 }
 
 __device__ __forceinline__ void tma_store_wait_all() {  // writes performed
@@ -107,7 +109,7 @@ __global__ void __launch_bounds__(kCopyThreads, 1) k_copy_pages(txb_pages j) {
     __syncthreads();
     // thread 0 drives a kStages-deep TMA pipeline over this CTA's pieces
     if (threadIdx.x == 0) {
-      uint32_t phase[kStages] = {0, 0, 0, 0};
+      uint32_t phase[kStages] = {};
       const int64_t k0 = blockIdx.x;
       // prologue: fill the stages
       for (int s = 0; s < kStages && k0 + (int64_t)s * gridDim.x < total; ++s) {
@@ -123,7 +125,7 @@ __global__ void __launch_bounds__(kCopyThreads, 1) k_copy_pages(txb_pages j) {
         tma_store(p.dst, stage + s * kPiece, p.bytes);
         const int64_t kn = k + (int64_t)kStages * gridDim.x;
         if (kn < total) {
-          tma_store_wait_read();  // stage s is free again
+          tma_store_wait_read();  // the stage stored kStages-1 pieces ago is free
           const PieceRef q = piece_of(j, kn, per_page);
           mbar_expect_tx(&bars[s], q.bytes);
           tma_load(stage + s * kPiece, q.src, q.bytes, &bars[s]);
@@ -139,18 +141,19 @@ __global__ void __launch_bounds__(kCopyThreads, 1) k_copy_pages(txb_pages j) {
       const PieceRef p = piece_of(j, k, per_page);
       const int w = vec_width(p.src, p.dst, p.bytes);
       if (w == 16) {
+        // a whole 16-KiB piece is 32 int4 per lane: all loads in flight
+        // before the first store
         const int4* s = reinterpret_cast<const int4*>(p.src);
         int4* d = reinterpret_cast<int4*>(p.dst);
         const int nv = (int)(p.bytes >> 4);
-        for (int i = lane; i < nv; i += 128) {
-          int4 v[4];
+        constexpr int U = kPiece / 512;
+        int4 v[U];
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (i + 32 * u < nv) v[u] = s[i + 32 * u];
+        for (int u = 0; u < U; ++u)
+          if (lane + 32 * u < nv) v[u] = s[lane + 32 * u];
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (i + 32 * u < nv) d[i + 32 * u] = v[u];
-        }
+        for (int u = 0; u < U; ++u)
+          if (lane + 32 * u < nv) d[lane + 32 * u] = v[u];
       } else {
         copy_row(p.dst, p.src, p.bytes, lane, 32);
       }
