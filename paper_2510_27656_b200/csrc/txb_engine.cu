@@ -216,10 +216,16 @@ __global__ void k_quant_bf16_fp8(const uint16_t* __restrict__ x, int64_t n, cons
 }
 
 static int sms(int) {
-  int dev = 0, v = 0;
+  static int cache[64] = {0};
+  int dev = 0;
   cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-  return v > 0 ? v : 148;
+  if (dev < 0 || dev >= 64) return 148;
+  if (!cache[dev]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = v > 0 ? v : 148;
+  }
+  return cache[dev];
 }
 
 }  // namespace txb
@@ -249,7 +255,13 @@ int txb_copy_pages(const txb_pages* j, int grid, void* stream) {
   }
   if (total == 0) job.npages = 0;
   const size_t smem = job.use_tma ? (size_t)kStages * kPiece : 0;
-  if (smem > 48 * 1024) TXB_CUDA(cudaFuncSetAttribute(k_copy_pages, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  static bool attr_set[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (smem > 48 * 1024 && (dev < 0 || dev >= 64 || !attr_set[dev])) {
+    TXB_CUDA(cudaFuncSetAttribute(k_copy_pages, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kStages * kPiece)));
+    if (dev >= 0 && dev < 64) attr_set[dev] = true;
+  }
   k_copy_pages<<<grid, kCopyThreads, smem, (cudaStream_t)stream>>>(job);
   TXB_CUDA(cudaGetLastError());
   return TXB_OK;

@@ -1020,9 +1020,24 @@ static size_t smem_main(const txb_moe_shape* s, bool route) {
   return m;
 }
 
+// Raise a kernel's dynamic shared-memory limit once per (kernel, device);
+// cudaFuncSetAttribute on every launch costs microseconds of host time.
 template <typename K>
 static int set_smem(K kernel, size_t smem) {
-  if (smem > 48 * 1024) TXB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (smem <= 48 * 1024) return TXB_OK;
+  struct Entry {
+    const void* fn;
+    int dev;
+    size_t smem;
+  };
+  static thread_local Entry seen[64];
+  static thread_local int nseen = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  for (int i = 0; i < nseen; ++i)
+    if (seen[i].fn == (const void*)kernel && seen[i].dev == dev && seen[i].smem >= smem) return TXB_OK;
+  TXB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (nseen < 64) seen[nseen++] = Entry{(const void*)kernel, dev, smem};
   return TXB_OK;
 }
 

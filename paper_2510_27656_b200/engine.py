@@ -450,6 +450,7 @@ class TransferEngine:
                 for k in keep:
                     k.record_stream(self._stream)
                 if self.timing is not None:          # bench hook: device time of the copy kernel
+                    torch.cuda._sleep(200000)         # keep the GPU busy past the host launch
                     e0 = torch.cuda.Event(enable_timing=True)
                     e0.record(self._stream)
                 _lib.call("txb_copy_pages", C.byref(j), 0, C.c_void_p(self._stream.cuda_stream))

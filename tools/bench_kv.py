@@ -58,8 +58,8 @@ st = pre.stream
 times = []
 pre.timing = []
 for k in range(1, min(layout.steps, a.steps) + 5):
-    flush.fill_(1)
     torch.cuda.synchronize(0)
+    flush.fill_(1)            # still running while the step is enqueued behind it
     send.send_step(t.request, k)
     torch.cuda.synchronize(0)
     e0, e1 = pre.timing[-1]
