@@ -118,6 +118,7 @@ typedef struct txb_moe_bufs {
   uint8_t* dirty;        /* [grouped_rows] 1 = row may hold data (zeroed when it becomes padding) */
   uint32_t* cta_hist;    /* [TXB_MAX_CTAS][experts] per-CTA counts of the segmented route phase */
   uint32_t* cta_bad;     /* [TXB_MAX_CTAS] per-CTA route validation bits */
+  int32_t* send_list;    /* [grouped_rows] grouped rows whose source is another rank */
   uint64_t* prof;        /* optional [grid][16] %globaltimer phase stamps (NULL = off) */
 } txb_moe_bufs;
 

@@ -60,7 +60,7 @@ class Bufs(C.Structure):
                 ("pos", C.c_void_p), ("gidx", C.c_void_p), ("rows", C.c_void_p),
                 ("sources", C.c_void_p), ("ret_slot", C.c_void_p), ("info", C.c_void_p),
                 ("dirty", C.c_void_p), ("cta_hist", C.c_void_p), ("cta_bad", C.c_void_p),
-                ("prof", C.c_void_p)]
+                ("send_list", C.c_void_p), ("prof", C.c_void_p)]
 
 
 class Pages(C.Structure):

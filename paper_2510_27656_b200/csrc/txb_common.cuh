@@ -112,7 +112,9 @@ struct Flags {
   uint64_t bar_epoch;    // local epoch of txb_moe_barrier
   uint32_t gbar_count;   // grid barrier of the cooperative kernels (local)
   uint32_t gbar_gen;
-  uint64_t pad1[2];
+  uint32_t send_cnt;     // grouped rows to return to other ranks (this step)
+  uint32_t pad2;
+  uint64_t pad1[1];
   uint64_t bar[TXB_MAX_RANKS];  // [peer] = last barrier epoch peer reached
 };
 

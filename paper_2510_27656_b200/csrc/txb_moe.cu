@@ -644,7 +644,8 @@ __device__ __noinline__ void recv_tables(const txb_moe_shape& s, const uint32_t*
 }
 
 __device__ __noinline__ void recv_rows(const txb_moe_shape& s, int* sm, int64_t* rows, int64_t* sources,
-                                       int32_t* ret, uint8_t* G, uint8_t* dirty, int cta, int ncta) {
+                                       int32_t* ret, uint8_t* G, uint8_t* dirty, int32_t* send_list,
+                                       uint32_t* send_cnt, int cta, int ncta) {
   const int N = s.ranks, L = s.local_experts;
   const RecvTables t = recv_carve(s, sm);
   const int padded_total = t.tot[0];
@@ -678,6 +679,8 @@ __device__ __noinline__ void recv_rows(const txb_moe_shape& s, int* sm, int64_t*
       rows[g] = t.rowbase[q * L + le] + kk;
       sources[g] = q;
       ret[g] = t.retbase[q * L + le] + kk;
+      // rows that go back over the fabric, compacted (order is irrelevant)
+      if (q != s.me) send_list[atomicAdd(send_cnt, 1u)] = g;
     }
   }
 }
@@ -697,14 +700,15 @@ __device__ void wait_tokens(Flags* f, int64_t* info, int L, uint64_t timeout_ns)
 // over every warp of the grid instead of one warp per 14 KiB row.
 constexpr int kChunk = 2048;
 
-__device__ void combine_send_rows(const txb_moe_shape& s, const uint8_t* out, int64_t ld, void* const* peers,
-                                  const int64_t* sources, const int32_t* ret, const int64_t* info, int cta,
-                                  int ncta, Shared& sh) {
-  const int N = s.ranks, L = s.local_experts, tid = threadIdx.x;
+__device__ void combine_send_rows(const txb_moe_shape& s, Flags* f, const uint8_t* out, int64_t ld,
+                                  void* const* peers, const int64_t* sources, const int32_t* ret,
+                                  const int32_t* send_list, int cta, int ncta, Shared& sh) {
+  const int N = s.ranks, tid = threadIdx.x;
   for (int q = tid; q < N; q += blockDim.x) sh.cnt[q] = 0;
   __syncthreads();
   if (N == 1) return;  // every row is this rank's own: read in place by C2
-  const int total = (int)info[2 * L];
+  // rows that return over the fabric (compacted by the receive phase)
+  const int total = (int)*reinterpret_cast<volatile uint32_t*>(&f->send_cnt);
   const int64_t Pc = s.comb_bytes;
   const int lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
   const bool vec = (Pc % 16 == 0) && (ld % 16 == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
@@ -712,9 +716,9 @@ __device__ void combine_send_rows(const txb_moe_shape& s, const uint8_t* out, in
     const int cpr = (int)((Pc + kChunk - 1) / kChunk);
     const int items = total * cpr;
     for (int it = cta * nwarp + warp; it < items; it += ncta * nwarp) {
-      const int g = it / cpr, c = it - g * cpr;
+      const int r = it / cpr, c = it - r * cpr;
+      const int g = send_list[r];
       const int q = (int)sources[g];
-      if (q < 0 || q == s.me) continue;  // padding, or read in place by C2
       const int4* src = reinterpret_cast<const int4*>(out + (int64_t)g * ld + (int64_t)c * kChunk);
       int4* dst = reinterpret_cast<int4*>(comb_of(peers[q], s) + (int64_t)ret[g] * Pc + (int64_t)c * kChunk);
       const int n16 = (int)(min((int64_t)kChunk, Pc - (int64_t)c * kChunk) >> 4);
@@ -729,9 +733,9 @@ __device__ void combine_send_rows(const txb_moe_shape& s, const uint8_t* out, in
     }
     return;
   }
-  for (int g = cta * nwarp + warp; g < total; g += ncta * nwarp) {
+  for (int r = cta * nwarp + warp; r < total; r += ncta * nwarp) {
+    const int g = send_list[r];
     const int q = (int)sources[g];
-    if (q < 0 || q == s.me) continue;
     copy_row(comb_of(peers[q], s) + (int64_t)ret[g] * Pc, out + (int64_t)g * ld, Pc, lane, 32);
     if (lane == 0) atomicAdd(&sh.cnt[q], 1u);
   }
@@ -778,6 +782,7 @@ __device__ void end_of_step(const txb_moe_shape& s, void* const* peers, Flags* f
     const uint32_t t = atomicAdd(&f->ticket, 1u);
     if (t == (uint32_t)ncta - 1) {
       f->ticket = 0;
+      f->send_cnt = 0;
       *reinterpret_cast<volatile uint64_t*>(&f->step) = step;
       fence_release(s.single_device);
       for (int q = 0; q < s.ranks; ++q) st_relaxed_sys(&flags_of(peers[q], s)->done[s.me], step);
@@ -830,14 +835,16 @@ k_recv(txb_moe_shape s, txb_moe_bufs b, uint64_t timeout_ns) {
   if (!wait_routes(s, f, route_of(b.region, s, (int)(step & 1)), C, step, timeout_ns, sh)) return;
   int* rt = reinterpret_cast<int*>(dsm + recv_offset(s));
   recv_tables(s, C, rt, b.info, blockIdx.x, sh);
-  recv_rows(s, rt, b.rows, b.sources, b.ret_slot, grouped_of(b.region, s), b.dirty, blockIdx.x, gridDim.x);
+  recv_rows(s, rt, b.rows, b.sources, b.ret_slot, grouped_of(b.region, s), b.dirty, b.send_list, &f->send_cnt,
+            blockIdx.x, gridDim.x);
   if (blockIdx.x == 0) wait_tokens(f, b.info, s.local_experts, timeout_ns);
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
 k_comb_send(txb_moe_shape s, txb_moe_bufs b, const uint8_t* __restrict__ out, int64_t ld) {
   __shared__ Shared sh;
-  combine_send_rows(s, out, ld, b.peers, b.sources, b.ret_slot, b.info, blockIdx.x, gridDim.x, sh);
+  combine_send_rows(s, flags_of(b.region, s), out, ld, b.peers, b.sources, b.ret_slot, b.send_list, blockIdx.x,
+                    gridDim.x, sh);
   signal_counts(s, b.peers, offsetof(Flags, comb_ctr), sh);
 }
 
@@ -927,7 +934,8 @@ k_dispatch_fused(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
   }
   // thread 0 fences and signals while the other warps fill the metadata
   stamp(b, 6);
-  recv_rows(s, rt, b.rows, b.sources, b.ret_slot, grouped_of(b.region, s), b.dirty, cta, ncta);
+  recv_rows(s, rt, b.rows, b.sources, b.ret_slot, grouped_of(b.region, s), b.dirty, b.send_list, &f->send_cnt,
+            cta, ncta);
   stamp(b, 7);
   if (cta == 0) wait_tokens(f, b.info, s.local_experts, timeout_ns);
   stamp(b, 8);
@@ -942,7 +950,8 @@ k_combine_fused(txb_moe_shape s, txb_moe_bufs b, const uint8_t* __restrict__ out
   Flags* f = flags_of(b.region, s);
   const uint64_t step = cur_step(f);
   stamp(b, 9);
-  combine_send_rows(s, out, ld, b.peers, b.sources, b.ret_slot, b.info, blockIdx.x, gridDim.x, sh);
+  combine_send_rows(s, flags_of(b.region, s), out, ld, b.peers, b.sources, b.ret_slot, b.send_list, blockIdx.x,
+                    gridDim.x, sh);
   stamp(b, 10);
   signal_counts(s, b.peers, offsetof(Flags, comb_ctr), sh);
   __syncthreads();

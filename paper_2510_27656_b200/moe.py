@@ -404,6 +404,7 @@ class MoeRank:
         self._dirty = torch.zeros(G, dtype=torch.uint8, device=dev)
         self._cta_hist = torch.zeros(_lib.TXB_MAX_CTAS * spec.experts, dtype=torch.int32, device=dev)
         self._cta_bad = torch.zeros(_lib.TXB_MAX_CTAS, dtype=torch.int32, device=dev)
+        self._send_list = torch.zeros(G, dtype=torch.int32, device=dev)
         self._info = torch.zeros(2 * L + 3, dtype=torch.int64, device=dev)
         self._info_host = torch.zeros(2 * L + 3, dtype=torch.int64).pin_memory()
         self._grouped = self.region.tensor(int(sh.off_grouped), (G, int(sh.payload_bytes)), torch.uint8)
@@ -449,6 +450,7 @@ class MoeRank:
         b.dirty = self._dirty.data_ptr()
         b.cta_hist = self._cta_hist.data_ptr()
         b.cta_bad = self._cta_bad.data_ptr()
+        b.send_list = self._send_list.data_ptr()
 
     def _connect(self, mesh: Sequence["MoeRank"]) -> None:
         """In-process wiring: peers are addressed directly (peer access)."""
