@@ -101,6 +101,14 @@ __device__ uint32_t route_counts_direct(const txb_moe_shape& s, const int64_t* r
   const int m = (int)(n * R);
   const int nmine = n > cta ? (int)((n - cta + ncta - 1) / ncta) : 0;
   const int nw = nmine * R;
+  // issue every route load this thread needs (its own copies and up to
+  // kPre entries of the batch) before the first barrier
+  constexpr int kPre = 4;
+  const int nt = blockDim.x;
+  const bool pre_ok = m <= kPre * nt;
+  int64_t pre[kPre];
+#pragma unroll
+  for (int u = 0; u < kPre; ++u) pre[u] = (pre_ok && u * nt + tid < m) ? routes[u * nt + tid] : -1;
   for (int e = tid; e < E; e += blockDim.x) hist[e] = 0;
   for (int k = tid; k < nw; k += blockDim.x) {
     const int i = (cta + (k / R) * ncta) * R + (k % R);
@@ -115,10 +123,17 @@ __device__ uint32_t route_counts_direct(const txb_moe_shape& s, const int64_t* r
   }
   __syncthreads();
   const bool lanes = (32 % R) == 0;
-  for (int base = 0; base < m; base += blockDim.x) {
+  for (int base = 0, u = 0; base < m; base += blockDim.x, ++u) {
     const int i = base + tid;
     const bool valid = i < m;
-    const int64_t v = valid ? routes[i] : -1;
+    int64_t v = -1;
+    if (pre_ok) {
+#pragma unroll
+      for (int q = 0; q < kPre; ++q)
+        if (q == u) v = pre[q];
+    } else if (valid) {
+      v = routes[i];
+    }
     const int j = i % R;
     bool dup = false;
     if (lanes) {
@@ -745,6 +760,10 @@ __device__ void combine_send_rows(const txb_moe_shape& s, Flags* f, const uint8_
 
 // Wait for the returned rows, then reduce this CTA's tokens.  The first
 // token's row pointers and weights are staged before the wait.
+// Wait for the returned rows, then reduce this CTA's tokens.  The first
+// token's row pointers and weights are staged before the wait; on the
+// decode path (one token per CTA, R <= 8, H % 8 == 0 rows) the rows this
+// rank served itself are already loaded into registers when the wait ends.
 template <int ELEM>
 __device__ bool combine_reduce(const txb_moe_shape& s, Flags* f, const uint8_t* comb, const uint8_t* out,
                                int64_t ld, const int64_t* pos, const int32_t* gidx, const float* w, int64_t n,
@@ -754,13 +773,23 @@ __device__ bool combine_reduce(const txb_moe_shape& s, Flags* f, const uint8_t* 
   const int H = s.hidden, R = s.topk;
   const bool vec = combine_vec<ELEM>(Pc, comb, out, ld, H, gidx);
   if (cta < n) combine_prep(ct, comb, Pc, out, ld, pos, gidx, w, cta, R);
-  if (threadIdx.x == 0) {
-    const uint64_t dl = globaltimer() + timeout_ns;
-    sh.fail = spin_ge(&f->comb_ctr, f->comb_target, dl) ? 0u : TXB_EV_WAIT_COMBINE;
-    if (sh.fail) atomicOr(&f->err, sh.fail);
+  auto wait = [&]() -> bool {
+    if (threadIdx.x == 0) {
+      const uint64_t dl = globaltimer() + timeout_ns;
+      sh.fail = spin_ge(&f->comb_ctr, f->comb_target, dl) ? 0u : TXB_EV_WAIT_COMBINE;
+      if (sh.fail) atomicOr(&f->err, sh.fail);
+    }
+    __syncthreads();
+    return sh.fail == 0;
+  };
+  const bool split = vec && R <= kCombBatch && cta < n && H / 8 <= 2 * (int)blockDim.x && n <= ncta;
+  if (split) {
+    __syncthreads();  // ct staged
+    if (!combine_token_split<ELEM>(ct, H, R, cta, dst, out_bf16, wait)) return false;
+    __syncthreads();
+    return true;
   }
-  __syncthreads();
-  if (sh.fail) return false;
+  if (!wait()) return false;
   for (int64_t t = cta; t < n; t += ncta) {
     if (t != cta) {
       combine_prep(ct, comb, Pc, out, ld, pos, gidx, w, t, R);

@@ -377,6 +377,7 @@ struct CombTok {
   const uint8_t* rowp[kMaxTopk];
   float ws[kMaxTopk];
   float sc[kMaxTopk];
+  bool local[kMaxTopk];  // row served by this rank (readable before the wait)
 };
 
 // Row of copy j of token t: out_rows + gidx*ld when this rank served it
@@ -390,6 +391,7 @@ __device__ __forceinline__ void combine_prep(CombTok& ct, const uint8_t* comb, i
     const int32_t gi = gidx ? gidx[t * R + tid] : -1;
     ct.rowp[tid] = gi >= 0 ? out_rows + (int64_t)gi * ld : comb + pos[t * R + tid] * Pc;
     ct.ws[tid] = w[t * R + tid];
+    ct.local[tid] = gi >= 0;
   }
 }
 
@@ -478,6 +480,72 @@ __device__ void combine_token(CombTok& ct, int64_t Pc, const uint8_t* comb, int 
       else reinterpret_cast<float*>(dst)[t * H + h] = acc;
     }
   }
+}
+
+// Decode fast path (R <= kCombBatch, 8-element chunks vectorisable): the
+// rows this rank served itself are loaded BEFORE the completion wait, the
+// returned rows after it; the sum then runs in the reference order.  The
+// wait itself is done by `wait_fn` (thread 0 spins, then a barrier).
+template <int ELEM, typename Wait>
+__device__ bool combine_token_split(CombTok& ct, int H, int R, int64_t t, void* dst, int out_bf16, Wait wait_fn) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  constexpr int CPT = ELEM == 4 ? 1 : 2;
+  const int c0 = tid;
+  Chunk8<ELEM> raw[CPT][kCombBatch];
+#pragma unroll
+  for (int p = 0; p < CPT; ++p)
+#pragma unroll
+    for (int u = 0; u < kCombBatch; ++u)
+      if (u < R && ct.local[u] && c0 + p * nt < H / 8)
+        raw[p][u] = load_chunk8<ELEM>(ct.rowp[u], (int64_t)(c0 + p * nt) * 8);
+  if (!wait_fn()) return false;
+#pragma unroll
+  for (int p = 0; p < CPT; ++p)
+#pragma unroll
+    for (int u = 0; u < kCombBatch; ++u)
+      if (u < R && !ct.local[u] && c0 + p * nt < H / 8)
+        raw[p][u] = load_chunk8<ELEM>(ct.rowp[u], (int64_t)(c0 + p * nt) * 8);
+  if (ELEM == 1) {
+    if (tid < R) {
+      const uint8_t* sp = ct.rowp[tid] + H;
+      const uint32_t v = (uint32_t)sp[0] | ((uint32_t)sp[1] << 8) | ((uint32_t)sp[2] << 16) | ((uint32_t)sp[3] << 24);
+      ct.sc[tid] = __uint_as_float(v);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int p = 0; p < CPT; ++p) {
+    const int c = c0 + p * nt;
+    if (c >= H / 8) continue;
+    float acc[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc[k] = 0.f;
+#pragma unroll
+    for (int u = 0; u < kCombBatch; ++u) {
+      if (u < R) {
+        float v[8];
+        unpack_chunk8<ELEM>(raw[p][u], v);
+        const float wj = ct.ws[u], sj = ct.sc[u];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float y = ELEM == 1 ? __fmul_rn(v[k], sj) : v[k];
+          acc[k] = __fadd_rn(acc[k], __fmul_rn(wj, y));
+        }
+      }
+    }
+    if (out_bf16) {
+      uint4 o;
+      uint32_t* ow = reinterpret_cast<uint32_t*>(&o);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) ow[q] = (uint32_t)bf16_rne(acc[2 * q]) | ((uint32_t)bf16_rne(acc[2 * q + 1]) << 16);
+      reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(dst) + t * H)[c] = o;
+    } else {
+      float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(dst) + t * H) + 2 * c;
+      o[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+      o[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+    }
+  }
+  return true;
 }
 
 template <int ELEM>
