@@ -125,3 +125,53 @@ def test_torchrun_ipc_bench_smoke(ranks, tmp_path):
     line = [x for x in p.stdout.splitlines() if x.startswith("{")][-1]
     d = json.loads(line)
     assert d["n_gpus"] == ranks and d["value"] > 0
+
+
+@pytest.mark.parametrize("ranks", [2, 4])
+def test_prefill_size_generic_path_multi_gpu(ranks):
+    """Large batch (generic fused kernel, grid barrier) across GPUs: grouped
+    payloads bit-exact vs the oracle, bf16 combine exact in bf16 bits."""
+    if NGPU < ranks:
+        pytest.skip(f"needs {ranks} GPUs")
+    import threading
+    T = 512
+    spec = moe.RoutingSpec(ranks=ranks, experts=64, max_tokens=T, topk=8, hidden=512,
+                           elem_size=2, scales=0, comb_elem_size=2, comb_scales=0)
+    os_ = ospec_of(spec)
+    rng = np.random.default_rng(7)
+    routes, values, weights = mo.random_step(os_, rng, tokens=T)
+    xb = [torch.from_numpy(v).to(torch.bfloat16) for v in values]
+    ref = mo.dispatch(os_, routes, [mo.encode_tokens(os_, x.float().numpy()) for x in xb])
+    mesh = moe.build_mesh(local_engines(list(range(ranks))), spec, timeout=20.0)
+    got, errs = [None] * ranks, []
+
+    def worker(r):
+        try:
+            torch.cuda.set_device(r)
+            rk = mesh[r]
+            rk.dispatch_send(xb[r].cuda(r), torch.from_numpy(routes[r]).cuda(r))
+            g = rk.dispatch_recv()
+            y = g.data.view(torch.bfloat16).reshape(g.data.shape[0], -1).clone()
+            rk.combine_send(y)
+            out = rk.combine_recv(torch.from_numpy(weights[r]).cuda(r), out_dtype=torch.bfloat16)
+            got[r] = (g.data.cpu().numpy(), out.view(torch.int16).cpu().numpy().view(np.uint16))
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(ranks)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(120)
+    try:
+        if errs:
+            raise errs[0]
+        outs = []
+        for r in range(ranks):
+            assert np.array_equal(got[r][0], ref.ranks[r].grouped.data)
+            outs.append(ref.ranks[r].grouped.data)
+        comb = mo.combine(os_, ref, outs, weights, comb_spec=os_)
+        for r in range(ranks):
+            assert np.array_equal(got[r][1], mo.bf16_encode(comb[r]))
+    finally:
+        close_mesh(mesh)
