@@ -98,6 +98,12 @@ int txb_ipc_export(int device, void* ptr, uint8_t* out_handle /*[64]*/);
 int txb_ipc_import(int device, const uint8_t* handle /*[64]*/, void** out_ptr);
 int txb_ipc_close(int device, void* ptr);
 int txb_enable_peer(int device, int peer_device);
+/* Device address of page-locked host memory (cudaHostAlloc / pinned torch
+ * tensors).  The kernels read inputs from and write results to such host
+ * buffers in place over PCIe (zero-copy), the way the reference's dispatch
+ * and combine take host arrays (moe.py:470-497, 814-866).  Fails with
+ * TXB_ERR_REGION for pageable memory. */
+int txb_host_device_ptr(void* host_ptr, void** out_device_ptr);
 
 /* ------------------------------------------------------- MoE hot path */
 

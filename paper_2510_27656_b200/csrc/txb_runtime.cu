@@ -109,4 +109,15 @@ int txb_enable_peer(int device, int peer_device) {
   return TXB_OK;
 }
 
+int txb_host_device_ptr(void* host_ptr, void** out_device_ptr) {
+  cudaPointerAttributes a;
+  TXB_CUDA(cudaPointerGetAttributes(&a, host_ptr));
+  if (a.type != cudaMemoryTypeHost) {
+    set_error("pointer %p is not page-locked host memory", host_ptr);
+    return TXB_ERR_REGION;
+  }
+  TXB_CUDA(cudaHostGetDevicePointer(out_device_ptr, host_ptr, 0));
+  return TXB_OK;
+}
+
 }  // extern "C"

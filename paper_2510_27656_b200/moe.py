@@ -253,6 +253,18 @@ def _sp(t: torch.Tensor | None) -> C.c_void_p:
     return C.c_void_p(t.data_ptr() if t is not None else 0)
 
 
+def _pinned(t) -> bool:
+    """A page-locked CPU tensor the kernels can address in place."""
+    return isinstance(t, torch.Tensor) and not t.is_cuda and t.is_pinned() and t.is_contiguous()
+
+
+def _mapped(t: torch.Tensor) -> C.c_void_p:
+    """Device address of a pinned host tensor (zero-copy over PCIe)."""
+    out = C.c_void_p()
+    _lib.call("txb_host_device_ptr", C.c_void_p(t.data_ptr()), C.byref(out))
+    return out
+
+
 def encode_tokens(spec: RoutingSpec, values):
     """[n, hidden] values -> [n, payload_bytes] wire rows (moe.py:231-246),
     on the GPU.  numpy in -> numpy out (current device); CUDA f32/bf16
@@ -406,6 +418,7 @@ class MoeRank:
         self._cta_bad = torch.zeros(_lib.TXB_MAX_CTAS, dtype=torch.int32, device=dev)
         self._send_list = torch.zeros(G, dtype=torch.int32, device=dev)
         self._info = torch.zeros(2 * L + 3, dtype=torch.int64, device=dev)
+        self._routes_in = torch.zeros((max(1, T), R), dtype=torch.int64, device=dev)
         self._info_host = torch.zeros(2 * L + 3, dtype=torch.int64).pin_memory()
         self._grouped = self.region.tensor(int(sh.off_grouped), (G, int(sh.payload_bytes)), torch.uint8)
         self._route_views = [self.region.tensor(int(sh.off_route) + k * spec.ranks * spec.experts * 8,
@@ -557,7 +570,16 @@ class MoeRank:
         spec = self.spec
         dev = torch.device("cuda", self.device)
         host = not isinstance(routes, torch.Tensor) or not isinstance(payload, torch.Tensor)
-        if isinstance(routes, torch.Tensor) and routes.is_cuda:
+        if _pinned(routes) and routes.dtype == torch.int64:
+            # page-locked host routes: one async copy into a resident device
+            # buffer; range / duplicate checks run on the device
+            if routes.ndim != 2 or routes.shape[1] != spec.topk:
+                raise ProtocolError(f"route array shape {tuple(routes.shape)} is not (tokens, {spec.topk})")
+            if routes.shape[0] > spec.max_tokens:
+                raise ProtocolError(f"{routes.shape[0]} tokens exceed the {spec.max_tokens}-token limit")
+            r_dev = self._routes_in[:routes.shape[0]]
+            r_dev.copy_(routes, non_blocking=True)
+        elif isinstance(routes, torch.Tensor) and routes.is_cuda:
             if routes.ndim != 2 or routes.shape[1] != spec.topk:
                 raise ProtocolError(f"route array shape {tuple(routes.shape)} is not (tokens, {spec.topk})")
             if routes.shape[0] > spec.max_tokens:
@@ -567,8 +589,13 @@ class MoeRank:
             r = _check_routes(spec, routes.cpu().numpy() if isinstance(routes, torch.Tensor) else routes)
             r_dev = torch.from_numpy(np.ascontiguousarray(r)).to(dev)
         n = int(r_dev.shape[0])
-        if isinstance(payload, torch.Tensor) and payload.is_cuda:
-            p = payload.contiguous()
+        p_ptr = None
+        if isinstance(payload, torch.Tensor) and (payload.is_cuda or _pinned(payload)):
+            # device tensors, or page-locked host tensors the dispatch kernel
+            # reads in place over PCIe (no separate host-to-device copy)
+            p = payload if not payload.is_cuda else payload.contiguous()
+            if not p.is_cuda:
+                p_ptr = _mapped(p)
             if p.dtype == torch.uint8:
                 if tuple(p.shape) != (n, spec.payload_bytes):
                     raise ProtocolError(f"payload shape {tuple(p.shape)} is not ({n}, {spec.payload_bytes})")
@@ -600,7 +627,7 @@ class MoeRank:
         st.fused = self.fused and not self.host_gated and _between is None
         if st.fused:
             # route + dispatch + receive metadata in one cooperative kernel
-            _lib.call("txb_moe_dispatch_fused", self._shape_p, self._bufs_p, _sp(p), kind, n,
+            _lib.call("txb_moe_dispatch_fused", self._shape_p, self._bufs_p, p_ptr or _sp(p), kind, n,
                       _sp(r_dev), self._tmo(None), sid)
             return
         _lib.call("txb_moe_route", self._shape_p, self._bufs_p, _sp(r_dev), n, sid)
@@ -610,7 +637,7 @@ class MoeRank:
             step = st.step
             self._gate(lambda c: all(v >= step for v in c["route_tag"][step & 1])
                        and all(v >= step - 1 for v in c["done"]), step, "route counts", None)
-        _lib.call("txb_moe_dispatch", self._shape_p, self._bufs_p, _sp(p), kind, n, _sp(r_dev),
+        _lib.call("txb_moe_dispatch", self._shape_p, self._bufs_p, p_ptr or _sp(p), kind, n, _sp(r_dev),
                   self._tmo(None), 0, sid)
         if self.host_gated:
             torch.cuda.current_stream(self.device).synchronize()
@@ -715,16 +742,27 @@ class MoeRank:
             torch.cuda.current_stream(self.device).synchronize()
 
     def combine_recv(self, weights, timeout: float | None = 30.0, *,
-                     out_dtype: torch.dtype = torch.float32, sync: bool | None = None):
+                     out_dtype: torch.dtype = torch.float32, sync: bool | None = None,
+                     out: torch.Tensor | None = None):
         """Weighted fp32 sum of the returned expert outputs per token
-        (moe.py:802-833); out_dtype bf16 rounds RNE at the end."""
+        (moe.py:802-833); out_dtype bf16 rounds RNE at the end.
+
+        `weights` and `out` may be page-locked host tensors: the combine
+        kernel then reads the weights and writes the result rows in place
+        over PCIe.  `out` (device or pinned host, (n, hidden), out_dtype,
+        contiguous) is returned when given."""
         st = self._cur
         if st is None or st.grouped is None:
             raise ProtocolError("combine before dispatch completed")
         self._raise_if_failed()
         spec = self.spec
         dev = torch.device("cuda", self.device)
-        if isinstance(weights, torch.Tensor) and weights.is_cuda:
+        w_ptr = None
+        if _pinned(weights) and weights.dtype == torch.float32:
+            w = weights
+            wshape = tuple(w.shape)
+            w_ptr = _mapped(w)
+        elif isinstance(weights, torch.Tensor) and weights.is_cuda:
             w = weights
             if w.dtype != torch.float32:
                 w = w.float()
@@ -739,19 +777,31 @@ class MoeRank:
             raise ProtocolError(f"weight shape {wshape} is not ({st.n}, {spec.topk})")
         if out_dtype not in (torch.float32, torch.bfloat16):
             raise ProtocolError(f"out_dtype {out_dtype} not in (float32, bfloat16)")
-        out = torch.empty((st.n, spec.hidden), dtype=out_dtype, device=dev)
+        o_ptr = None
+        if out is None:
+            out = torch.empty((st.n, spec.hidden), dtype=out_dtype, device=dev)
+        else:
+            if tuple(out.shape) != (st.n, spec.hidden) or out.dtype != out_dtype or not out.is_contiguous():
+                raise ProtocolError(f"out must be a contiguous ({st.n}, {spec.hidden}) {out_dtype} tensor")
+            if out.is_cuda:
+                if out.device.index != self.device:
+                    raise ProtocolError(f"out on {out.device}, rank runs on cuda:{self.device}")
+            elif _pinned(out):
+                o_ptr = _mapped(out)
+            else:
+                raise ProtocolError("out must be a CUDA tensor or a page-locked host tensor")
         sync = st.sync if sync is None else (sync or st.host)
         if st.out is None:
             raise ProtocolError("combine_recv before combine_send")
         bf = 1 if out_dtype == torch.bfloat16 else 0
         if st.fused:
-            _lib.call("txb_moe_combine_fused", self._shape_p, self._bufs_p, _sp(st.out), st.ld, _sp(w),
-                      st.n, _sp(out), bf, self._tmo(timeout), self._sid())
+            _lib.call("txb_moe_combine_fused", self._shape_p, self._bufs_p, _sp(st.out), st.ld, w_ptr or _sp(w),
+                      st.n, o_ptr or _sp(out), bf, self._tmo(timeout), self._sid())
         else:
             if self.host_gated:
                 self._gate(lambda c: c["comb_ctr"] >= c["comb_target"], st.step, "combine writes", timeout)
-            _lib.call("txb_moe_combine_recv", self._shape_p, self._bufs_p, _sp(st.out), st.ld, _sp(w),
-                      st.n, _sp(out), bf, self._tmo(timeout), self._sid())
+            _lib.call("txb_moe_combine_recv", self._shape_p, self._bufs_p, _sp(st.out), st.ld, w_ptr or _sp(w),
+                      st.n, o_ptr or _sp(out), bf, self._tmo(timeout), self._sid())
         st.keep.append(w)
         if sync:
             self._event(st)

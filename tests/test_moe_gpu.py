@@ -131,6 +131,45 @@ def test_dsv3_decode_ep1_full_size(fused):
         rk.close()
 
 
+@pytest.mark.parametrize("fused", [True, False])
+def test_pinned_host_zero_copy_matches_device_mode(fused):
+    """Page-locked host inputs (activations, routes, weights) and a pinned
+    host `out`: the kernels read / write them in place over PCIe; the
+    grouped payloads and the combined rows equal the device-mode step
+    bit for bit, and the oracle's."""
+    spec = moe.RoutingSpec(ranks=1, experts=256, max_tokens=128, topk=8, hidden=7168,
+                           elem_size=1, scales=56, comb_elem_size=2, comb_scales=0)
+    os_ = ospec_of(spec)
+    cs = mo.Spec(1, 256, 128, 8, hidden=7168, elem_size=2, scales=0)
+    mesh = moe.build_mesh(local_engines([0]), spec)
+    rk = mesh[0]
+    rk.fused = fused
+    try:
+        for step, T in enumerate([128, 77]):
+            rng = np.random.default_rng(300 + step)
+            routes, values, weights = mo.random_step(os_, rng, tokens=T)
+            xb = torch.from_numpy(values[0]).to(torch.bfloat16)
+            res, _ = _oracle_round(os_, routes, [xb.float().numpy()])
+            rk.dispatch_send(xb.pin_memory(), torch.from_numpy(routes[0]).pin_memory())
+            g = rk.dispatch_recv()
+            assert np.array_equal(_np(g.data), res.ranks[0].grouped.data)
+            y = (moe.decode_tokens(spec, g.data) * 0.75).to(torch.bfloat16)
+            rk.combine_send(y)
+            oh = torch.empty((T, spec.hidden), dtype=torch.bfloat16).pin_memory()
+            out = rk.combine_recv(torch.from_numpy(weights[0]).pin_memory(), out_dtype=torch.bfloat16, out=oh)
+            assert out is oh
+            outs = [mo.bf16_encode(y.float().cpu().numpy()).view(np.uint8).reshape(y.shape[0], -1)]
+            ref = mo.combine(os_, res, outs, weights, comb_spec=cs)[0]
+            assert np.array_equal(mo.bf16_encode(ref), oh.view(torch.int16).numpy().view(np.uint16))
+        with pytest.raises(ProtocolError, match="out must be"):
+            rk.dispatch_send(xb.cuda(), torch.from_numpy(routes[0]).cuda())
+            rk.dispatch_recv()
+            rk.combine_send(y)
+            rk.combine_recv(torch.from_numpy(weights[0]).cuda(), out=torch.empty(3, 3))
+    finally:
+        rk.close()
+
+
 def test_multi_step_and_empty_steps():
     """Ragged token counts including empty steps, several steps in a row."""
     spec = moe.RoutingSpec(ranks=2, experts=8, max_tokens=12, topk=3, hidden=64, elem_size=4, scales=0)
