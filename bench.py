@@ -287,6 +287,18 @@ def run_b200(a) -> None:
         graph.replay()
         ev[k][1].record(stream)
     torch.cuda.synchronize()
+    # L2-warm steps (no flush between; SURVEY.md §8d asks for both numbers)
+    b2b = []
+    for k in range(max(20, K // 2)):
+        if world > 1:
+            rk.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        graph.replay()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        b2b.append(e0.elapsed_time(e1) * 1e3)
+    b2b = _max_over_ranks(b2b, world)
     clk = clocks.stop()
     err, _ = rk.status()
     assert err == 0, f"device error word {err:#x}"
@@ -353,6 +365,7 @@ def run_b200(a) -> None:
                    "parallelism": f"ep{n_gpu}"},
         "p90_us": round(float(np.percentile(tot, 90)), 2),
         "p99_us": round(float(np.percentile(tot, 99)), 2),
+        "p50_l2_warm_us": round(float(np.median(b2b)), 2),
         "tokens_per_s": round(n_gpu * tokens / (p50 * 1e-6), 1),
         "kernel_us": {k: round(v, 2) for k, v in kt.items()},
         "roofline": roofline,

@@ -216,6 +216,9 @@ int txb_imm_add(uint64_t* const* ctrs, int n, uint64_t value, int single_device,
 /* Block `stream` until *ctr >= threshold (device-side ImmFlag wait); on
  * timeout sets TXB_EV_WAIT_IMM in *err (may be NULL). */
 int txb_imm_wait(const uint64_t* ctr, uint64_t threshold, uint64_t timeout_ns, uint32_t* err, void* stream);
+/* Diagnostics: one %globaltimer sample (ns) written to *out on `stream`,
+ * the clock the kernels' phase stamps (txb_moe_bufs.prof) use. */
+int txb_globaltimer(uint64_t* out, void* stream);
 /* Per-tensor fp8 narrowing of bf16 words (weights.prepare, weights.py:383-387):
  * out = e4m3(x / f32(amax/448)) bytes followed by the f32 scale (n + 4 bytes). */
 int txb_fp8_quantize_tensor(const uint16_t* x, int64_t n, uint32_t* amax_scratch, uint8_t* out, void* stream);

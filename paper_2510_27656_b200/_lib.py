@@ -109,6 +109,7 @@ SIGNATURES: dict[str, list] = {
     "txb_copy_pages": [C.POINTER(Pages), _INT, _VP],
     "txb_imm_add": [_VP, _INT, _U64, _INT, _VP],
     "txb_imm_wait": [_VP, _U64, _U64, _VP, _VP],
+    "txb_globaltimer": [_VP, _VP],
     "txb_fp8_quantize_tensor": [_VP, _I64, _VP, _VP, _VP],
     "txb_encode_rows": [_VP, _INT, _I64, _I32, _I32, _I32, _VP, _VP],
     "txb_decode_rows": [_VP, _I64, _I32, _I32, _I32, _VP, _VP],

@@ -191,6 +191,12 @@ __global__ void k_imm_wait(const uint64_t* ctr, uint64_t threshold, uint64_t tim
   }
 }
 
+// Device clock sample (%globaltimer, ns) into *out: brackets a stream's
+// work in the same clock domain as the kernels' phase stamps.
+__global__ void k_globaltimer(uint64_t* out) {
+  if (threadIdx.x == 0) *out = globaltimer();
+}
+
 // Per-tensor fp8 quantisation of bf16 words (weights.prepare narrowing,
 // weights.py:383-387 -> kernels.fp8_quantize over the whole tensor):
 // pass 1 reduces amax over finite values into *amax_bits (non-negative
@@ -276,6 +282,12 @@ int txb_imm_add(uint64_t* const* ctrs, int n, uint64_t value, int single_device,
 
 int txb_imm_wait(const uint64_t* ctr, uint64_t threshold, uint64_t timeout_ns, uint32_t* err, void* stream) {
   k_imm_wait<<<1, 32, 0, (cudaStream_t)stream>>>(ctr, threshold, timeout_ns, err);
+  TXB_CUDA(cudaGetLastError());
+  return TXB_OK;
+}
+
+int txb_globaltimer(uint64_t* out, void* stream) {
+  k_globaltimer<<<1, 32, 0, (cudaStream_t)stream>>>(out);
   TXB_CUDA(cudaGetLastError());
   return TXB_OK;
 }

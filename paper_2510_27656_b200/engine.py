@@ -26,6 +26,7 @@ import torch
 
 from . import _lib, memory
 from .errors import ProtocolError, RegionError, TransferError
+from .trace import TraceRecorder
 
 
 @dataclass(frozen=True)
@@ -234,6 +235,7 @@ class ImmFlag:
         if not self._fired and self.engine.imm_received_total(self.imm) >= self.threshold:
             self._fired = True
             self.engine._disarm(self.imm, self)
+            self.engine.trace.record("imm_fire", imm=self.imm)
             if self.cb is not None:
                 self.cb(self)
         return self._fired
@@ -277,7 +279,8 @@ class TransferEngine:
     _TICKETS = 64
 
     def __init__(self, fabric: NvlinkFabric | None = None, *, device: int = 0,
-                 name: str | None = None, rails: int = 1, engine_id: int | None = None) -> None:
+                 name: str | None = None, rails: int = 1, engine_id: int | None = None,
+                 trace: bool = False) -> None:
         if not 1 <= rails <= 4:
             raise TransferError(f"rail count {rails} outside 1..4")
         self.fabric = fabric or NvlinkFabric()
@@ -298,6 +301,8 @@ class TransferEngine:
         self._opened: dict[tuple, memory.Region] = {}
         self.use_tma = True        # TMA bulk copies for 16-byte aligned pages
         self.timing: list | None = None
+        self.trace = TraceRecorder(self.name, enabled=trace)
+        self._op_ids = itertools.count(1)
 
     def main_address(self) -> NetAddr:
         import socket
@@ -368,6 +373,7 @@ class TransferEngine:
                    self._imm.ipc_handle())
         with self._lock:
             self._mrs[rid] = (h, d, buf)
+        self.trace.record("reg_mr", region=rid, nbytes=length)
         return h, d
 
     def dereg_mr(self, handle: MrHandle) -> None:
@@ -419,10 +425,24 @@ class TransferEngine:
         t = torch.from_numpy(np.asarray(pages.indices, dtype=np.int64)).pin_memory()
         return t.to(torch.device("cuda", self.device), non_blocking=True)
 
+    def post_op(self, label: str, dst: str, nbytes: int, imm: int | None = None, posts: int = 1) -> int:
+        """Trace one submitted transfer: op_submit with its label and one
+        wr_post per logical write it performs on the fabric (the events
+        check_moe / check_kvcache audit, docs/trace.md)."""
+        op = next(self._op_ids)
+        if self.trace.enabled:
+            if label:
+                self.trace.label_transfer(op, label)
+            self.trace.record("op_submit", transfer=op, dst=dst, nbytes=int(nbytes), imm=imm)
+            for _ in range(posts):
+                self.trace.record("wr_post", transfer=op, dst=dst)
+        return op
+
     def _launch_pages(self, src_base: int, src_pages: Pages, desc: MrDesc, dst_pages: Pages,
                       page_len: int, npages: int, imm: int | None,
-                      idx: tuple | None = None) -> CompletionFlag:
+                      idx: tuple | None = None, label: str = "") -> CompletionFlag:
         self._ensure_imm()
+        self.post_op(label, desc.owner, page_len * npages, imm)
         dst_base, dst_imm = self._peer_base(desc)
         j = _lib.Pages()
         j.src_base, j.src_offset, j.src_stride = src_base, src_pages.offset, src_pages.stride
@@ -484,7 +504,7 @@ class TransferEngine:
             raise TransferError("zero-length write requires an immediate")
         self._check_imm(imm)
         flag = self._launch_pages(rec.base, Pages((0,), 0, src_off), desc, Pages((0,), 0, dst_off),
-                                  length, 1 if length else 0, imm)
+                                  length, 1 if length else 0, imm, label=label)
         return self._done(flag, on_done)
 
     def submit_paged_writes(self, page_len: int, src: tuple, dst: tuple, imm: int | None = None,
@@ -505,7 +525,7 @@ class TransferEngine:
         self._check_pages(dst_pages, page_len, desc.length, "destination")
         self._check_imm(imm)
         flag = self._launch_pages(rec.base, src_pages, desc, dst_pages, page_len,
-                                  len(src_pages.indices), imm, idx=device_indices or (True,))
+                                  len(src_pages.indices), imm, idx=device_indices or (True,), label=label)
         return self._done(flag, on_done)
 
     @staticmethod
@@ -556,7 +576,7 @@ class TransferEngine:
             if d.length == 0 and imm is None:
                 continue
             flag = self._launch_pages(rec.base, Pages((0,), 0, d.src), d.desc, Pages((0,), 0, d.offset),
-                                      d.length, 1 if d.length else 0, imm)
+                                      d.length, 1 if d.length else 0, imm, label=label)
         return self._done(flag, on_done)
 
     def submit_barrier(self, group: int, imm: int, dsts: Sequence[tuple], on_done: Callable | None = None,
@@ -571,6 +591,8 @@ class TransferEngine:
             if not 0 <= off <= desc.length:
                 raise TransferError(f"barrier offset {off} out of bounds")
             ptrs.append(self._imm_slot_ptr(imm, self._peer_base(desc)[1]))
+        for desc, _ in dsts:
+            self.post_op(label, desc.owner, 0, imm)
         dev = torch.device("cuda", self.device)
         tab = torch.tensor(ptrs, dtype=torch.int64).to(dev, non_blocking=True)
         sd = 1 if all(self._single_device(d) for d, _ in dsts) else 0
@@ -616,6 +638,7 @@ class TransferEngine:
             self._consumed[imm] = base + count
             flag = ImmFlag(self, imm, base + count, cb)
             self._armed[imm] = flag
+        self.trace.record("imm_arm", imm=imm, count=count)
         flag._check()
         return flag
 
@@ -657,8 +680,9 @@ class TransferEngine:
         self.close()
 
 
-def local_engines(devices: Sequence[int], fabric: NvlinkFabric | None = None) -> list[TransferEngine]:
+def local_engines(devices: Sequence[int], fabric: NvlinkFabric | None = None,
+                  trace: bool = False) -> list[TransferEngine]:
     """One engine per device in this process (the single-box analog of the
     reference test harness's `engines(cfg, n)`, tests/_fabric.py:35-44)."""
     fab = fabric or NvlinkFabric()
-    return [TransferEngine(fab, device=d, name=f"e{i}") for i, d in enumerate(devices)]
+    return [TransferEngine(fab, device=d, name=f"e{i}", trace=trace) for i, d in enumerate(devices)]

@@ -623,6 +623,7 @@ class MoeRank:
             self._cur = st
         st.keep = [r_dev, p]
         self._event(st)
+        self._trace_dispatch(st)
         sid = self._sid()
         st.fused = self.fused and not self.host_gated and _between is None
         if st.fused:
@@ -673,6 +674,9 @@ class MoeRank:
         data = self._grouped[:total]
         rows = self._rows[:total]
         srcs = self._sources[:total]
+        if self.engine.trace.enabled:
+            self.engine.trace.record("moe_dispatch_done", step=st.step, tokens=int(sizes.sum()),
+                                     used=int(info[2 * L + 1]), capacity=self.spec.capacity)
         if st.host:
             g = GroupedTokens(data.cpu().numpy(), sizes.numpy(), starts.numpy(),
                               rows.cpu().numpy(), srcs.cpu().numpy())
@@ -680,6 +684,31 @@ class MoeRank:
             g = GroupedTokens(data, sizes, starts, rows, srcs)
         st.grouped = g
         return g
+
+    # ------------------------------------------------------------- tracing
+
+    def _trace_dispatch(self, st: "_Step") -> None:
+        """Host view of the step's fabric writes (docs/trace.md, moe.*):
+        per peer one route-row write and one token write; the kernel does
+        both with device stores, so these are logical posts."""
+        eng = self.engine
+        if not eng.trace.enabled:
+            return
+        eng.trace.record("moe_host_signal", step=st.step, tokens=st.n)
+        E = self.spec.experts
+        for q in range(self.spec.ranks):
+            if q != self.rank:
+                eng.post_op("moe.route", f"r{q}", 8 * E)
+                eng.post_op("moe.tok.main", f"r{q}", 0)
+
+    def _trace_combine(self, st: "_Step") -> None:
+        eng = self.engine
+        if not eng.trace.enabled:
+            return
+        for q in range(self.spec.ranks):
+            if q != self.rank:
+                eng.post_op("moe.comb", f"r{q}", 0)
+                eng.post_op("moe.dbar", f"r{q}", 0)
 
     @property
     def last_layout(self) -> DispatchLayout | None:
@@ -735,6 +764,7 @@ class MoeRank:
             self._dirty.fill_(1)
         st.keep.append(out)
         st.out, st.ld = out, ld
+        self.engine.trace.record("moe_combine_store", step=st.step)
         if st.fused:
             return                    # sent by the fused combine kernel in combine_recv
         _lib.call("txb_moe_combine_send", self._shape_p, self._bufs_p, _sp(out), ld, 0, self._sid())
@@ -803,12 +833,14 @@ class MoeRank:
             _lib.call("txb_moe_combine_recv", self._shape_p, self._bufs_p, _sp(st.out), st.ld, w_ptr or _sp(w),
                       st.n, o_ptr or _sp(out), bf, self._tmo(timeout), self._sid())
         st.keep.append(w)
+        self._trace_combine(st)
         if sync:
             self._event(st)
             torch.cuda.current_stream(self.device).synchronize()
             err, _ = self.status()
             if err:
                 self._check_err(err, st.step)
+            self.engine.trace.record("moe_combine_done", step=st.step, tokens=st.n)
             if len(st.ev) == 3:
                 t1 = st.ev[0].elapsed_time(st.ev[1]) * 1e3
                 t2 = st.ev[0].elapsed_time(st.ev[2]) * 1e3

@@ -31,8 +31,8 @@ def devices_for(n: int) -> list[int]:
     return list(range(n)) if count >= n else [0] * n
 
 
-def make_mesh(spec: moe.RoutingSpec, private: int | None = None, timeout: float = 30.0):
-    engines = local_engines(devices_for(spec.ranks))
+def make_mesh(spec: moe.RoutingSpec, private: int | None = None, timeout: float = 30.0, trace: bool = False):
+    engines = local_engines(devices_for(spec.ranks), trace=trace)
     pv = None if private is None else moe.PrivateBufferConfig(private)
     return moe.build_mesh(engines, spec, private=pv, timeout=timeout)
 

@@ -81,3 +81,26 @@ def test_capacity_error():
     s = moe.RoutingSpec(2, 4, 2, 2, hidden=8, elem_size=4, scales=0)
     with pytest.raises(ProtocolError, match="routes 5 copies, limit 4"):
         moe.RouteMatrix(s, np.array([[5, 0, 0, 0], [0, 0, 0, 0]]))
+
+
+def test_trace_recorder_roundtrip(tmp_path):
+    """TraceRecorder (railtx trace.py:33-99 semantics): total order, kind +
+    field matching, transfer labels, JSON-lines dump/load; a disabled
+    recorder keeps nothing."""
+    from paper_2510_27656_b200.trace import TraceRecorder, load_path
+    tr = TraceRecorder("e0")
+    tr.label_transfer(7, "moe.comb")
+    a = tr.record("wr_post", transfer=7, dst="r1")
+    b = tr.record("moe_dispatch_done", step=1, used=3, capacity=8)
+    tr.record("wr_post", transfer=8, dst="r2")
+    assert a.seq < b.seq and len(tr) == 3
+    assert [e.fields["dst"] for e in tr.events("wr_post")] == ["r1", "r2"]
+    assert tr.events("wr_post", dst="r2")[0].fields["transfer"] == 8
+    assert tr.labels() == {7: "moe.comb"} and tr.label_of(8) is None
+    p = tmp_path / "t.jsonl"
+    tr.dump_path(str(p))
+    rows = load_path(str(p))
+    assert [r["kind"] for r in rows] == ["wr_post", "moe_dispatch_done", "wr_post", "label"]
+    assert rows[1]["used"] == 3 and rows[3]["label"] == "moe.comb" and rows[3]["transfer_id"] == 7
+    off = TraceRecorder("e1", enabled=False)
+    assert off.record("x") is None and len(off) == 0

@@ -170,6 +170,48 @@ def test_pinned_host_zero_copy_matches_device_mode(fused):
         rk.close()
 
 
+def test_check_moe_trace_audit():
+    """check_moe (_invariants.py:334-364): results equal the oracle, the
+    traced receive occupancy stays within capacity, and the per-peer write
+    budget holds (<= 2 token writes, exactly 1 combine write per peer per
+    step), audited from the engines' traces."""
+    spec = moe.RoutingSpec(ranks=2, experts=4, max_tokens=4, topk=2, hidden=8, elem_size=4, scales=0)
+    os_ = ospec_of(spec)
+    mesh = make_mesh(spec, private=2, trace=True)
+    try:
+        rng = np.random.default_rng(104)
+        steps = 3
+        for _ in range(steps):
+            routes, values, weights = mo.random_step(os_, rng)
+            res = run_moe_round(mesh, spec, routes, values, weights)
+            ref = mo.dispatch(os_, routes, [mo.encode_tokens(os_, v) for v in values])
+            for q in range(spec.ranks):
+                assert np.array_equal(_np(res[q][0].data), ref.ranks[q].grouped.data)
+        for rk in mesh:
+            tr = rk.engine.trace
+            done = tr.events("moe_dispatch_done")
+            assert len(done) == steps
+            for ev in done:
+                assert ev.fields["used"] <= ev.fields["capacity"]
+            assert len(tr.events("moe_host_signal")) == steps
+            assert len(tr.events("moe_combine_store")) == steps
+            assert len(tr.events("moe_combine_done")) == steps
+            labels = tr.labels()
+            tok = comb = 0
+            for ev in tr.events("wr_post"):
+                lb = labels.get(ev.fields.get("transfer"), "")
+                tok += lb.startswith("moe.tok.")
+                comb += lb == "moe.comb"
+            peers = spec.ranks - 1
+            assert tok <= 2 * steps * peers
+            assert comb == steps * peers
+            # ordering: each step's host signal precedes its dispatch_done
+            for a_, b_ in zip(tr.events("moe_host_signal"), done):
+                assert a_.seq < b_.seq and a_.fields["step"] == b_.fields["step"]
+    finally:
+        close_mesh(mesh)
+
+
 def test_multi_step_and_empty_steps():
     """Ragged token counts including empty steps, several steps in a row."""
     spec = moe.RoutingSpec(ranks=2, experts=8, max_tokens=12, topk=3, hidden=64, elem_size=4, scales=0)
