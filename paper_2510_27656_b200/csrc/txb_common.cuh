@@ -141,7 +141,7 @@ __host__ __device__ inline uint8_t* comb_of(void* region, const txb_moe_shape& s
 // thread of the block must call it.  Returns the total.  `tmp` needs 33
 // ints.  Out of line: one copy of the code serves every call site (the
 // fused kernels are instruction-fetch bound when the code balloons).
-static __device__ __noinline__ int block_scan_i32(int* a, int len, int* tmp) {
+static __device__ __forceinline__ int block_scan_i32_body(int* a, int len, int* tmp) {
   const int nt = blockDim.x, tid = threadIdx.x;
   const int per = (len + nt - 1) / nt;
   const int lo = min(len, tid * per), hi = min(len, lo + per);
@@ -175,6 +175,19 @@ static __device__ __noinline__ int block_scan_i32(int* a, int len, int* tmp) {
   const int total = tmp[32];
   __syncthreads();
   return total;
+}
+
+static __device__ __noinline__ int block_scan_i32(int* a, int len, int* tmp) {
+  return block_scan_i32_body(a, len, tmp);
+}
+
+// Call-site choice: INL = inline copy (a straight-line decode path, where a
+// call into cold out-of-line code costs an instruction-fetch miss per
+// call), else the shared out-of-line copy.
+template <bool INL>
+__device__ __forceinline__ int block_scan(int* a, int len, int* tmp) {
+  if constexpr (INL) return block_scan_i32_body(a, len, tmp);
+  else return block_scan_i32(a, len, tmp);
 }
 
 // ------------------------------------------------------------- row copy

@@ -92,11 +92,14 @@ struct Shared {  // static shared state of one CTA
 // Direct counts: shared atomics (order-free) for the histogram; the stable
 // rank of each of this CTA's copies (token order within an expert, the
 // (local_expert, t, j) slab order of moe.py:514-521) is the number of
-// earlier copies with its expert.  Validation (moe.py:142-155): range, and
+// earlier copies with its expert, counted afterwards by one warp per copy
+// with ballots over the batch's expert ids (staged as int32 in `rv`, m
+// entries of shared memory).  Validation (moe.py:142-155): range, and
 // duplicates within a token -- R-1 shuffles when R divides 32 (a token's
 // copies sit in consecutive lanes), loads otherwise.
 __device__ uint32_t route_counts_direct(const txb_moe_shape& s, const int64_t* routes, int64_t n, uint32_t* hist,
-                                        int32_t* rank_out, int cta, int ncta, Shared& sh) {
+                                        int32_t* rv, int32_t* rank_out, int cta, int ncta, Shared& sh,
+                                        const txb_moe_bufs& bufs) {
   const int E = s.experts, R = s.topk, tid = threadIdx.x;
   const int m = (int)(n * R);
   const int nmine = n > cta ? (int)((n - cta + ncta - 1) / ncta) : 0;
@@ -115,13 +118,13 @@ __device__ uint32_t route_counts_direct(const txb_moe_shape& s, const int64_t* r
     const int64_t v = routes[i];
     sh.own_e[k] = (v >= 0 && v < E) ? (int)v : -1;
     sh.own_i[k] = i;
-    sh.own_rank[k] = 0;
   }
   if (tid == 0) {
     sh.bad = 0;
     sh.direct = 1;
   }
   __syncthreads();
+  stamp(bufs, 19);
   const bool lanes = (32 % R) == 0;
   for (int base = 0, u = 0; base < m; base += blockDim.x, ++u) {
     const int i = base + tid;
@@ -134,28 +137,42 @@ __device__ uint32_t route_counts_direct(const txb_moe_shape& s, const int64_t* r
     } else if (valid) {
       v = routes[i];
     }
+    const bool in_range = v >= 0 && v < E;
+    // int32 ids; out-of-range entries get lane-unique negatives (no false dups)
+    const int v32 = in_range ? (int)v : -1 - (tid & 31);
     const int j = i % R;
     bool dup = false;
     if (lanes) {
       for (int jj = 1; jj < R; ++jj) {
-        const int64_t u = __shfl_up_sync(0xffffffffu, v, jj);
-        dup |= (jj <= j) && (u == v);
+        const int w = __shfl_up_sync(0xffffffffu, v32, jj);
+        dup |= (jj <= j) && (w == v32);
       }
     } else if (valid) {
       for (int jj = 1; jj <= j; ++jj) dup |= routes[i - jj] == v;
     }
     if (!valid) continue;
-    if (v < 0 || v >= E) {
+    rv[i] = in_range ? v32 : -1;
+    if (!in_range) {
       atomicOr(&sh.bad, TXB_EV_ROUTE_RANGE);
       continue;
     }
     if (dup) atomicOr(&sh.bad, TXB_EV_ROUTE_DUP);
-    atomicAdd(&hist[(int)v], 1u);
-    for (int k = 0; k < nw; ++k)
-      if (sh.own_e[k] == (int)v && i < sh.own_i[k]) atomicAdd(&sh.own_rank[k], 1u);
+    atomicAdd(&hist[v32], 1u);
   }
   __syncthreads();
-  for (int k = tid; k < nw; k += blockDim.x) rank_out[sh.own_i[k]] = (int32_t)sh.own_rank[k];
+  {
+    const int lane = tid & 31, warp = tid >> 5, nwarp = nt >> 5;
+    for (int k = warp; k < nw; k += nwarp) {
+      const int e = sh.own_e[k], lim = sh.own_i[k];
+      int cnt = 0;
+      for (int b0 = 0; b0 < lim; b0 += 32) {
+        const int q = b0 + lane;
+        cnt += __popc(__ballot_sync(0xffffffffu, q < lim && rv[q] == e));
+      }
+      if (lane == 0) rank_out[lim] = cnt;
+      if (lane == 0) sh.own_rank[k] = (uint32_t)cnt;
+    }
+  }
   const uint32_t b = sh.bad;
   if (b)
     for (int e = tid; e < E; e += blockDim.x) hist[e] = 0;  // publish an empty row
@@ -602,8 +619,9 @@ __device__ __forceinline__ RecvTables recv_carve(const txb_moe_shape& s, int* sm
   return t;
 }
 
-__device__ __noinline__ void recv_tables(const txb_moe_shape& s, const uint32_t* C, int* sm, int64_t* info,
-                                         int cta, Shared& sh) {
+template <bool INL>
+__device__ __forceinline__ void recv_tables_body(const txb_moe_shape& s, const uint32_t* C, int* sm, int64_t* info,
+                                                 int cta, Shared& sh, const txb_moe_bufs& b) {
   const int N = s.ranks, E = s.experts, L = s.local_experts, me = s.me;
   const int tid = threadIdx.x, nt = blockDim.x;
   RecvTables t = recv_carve(s, sm);
@@ -622,6 +640,7 @@ __device__ __noinline__ void recv_tables(const txb_moe_shape& s, const uint32_t*
     }
   }
   __syncthreads();
+  stamp(b, 16);
   for (int le = tid; le < L; le += nt) {
     int run = 0;
     for (int q = 0; q < N; ++q) {
@@ -633,10 +652,12 @@ __device__ __noinline__ void recv_tables(const txb_moe_shape& s, const uint32_t*
     t.gstart[le] = pad_up(run);
   }
   __syncthreads();
+  stamp(b, 17);
   // one scan over [padded group sizes (L) | counts flattened source-major
   // (N*L)]: the first part gives group_starts, the second (minus the padded
   // total) recv_start[me][q] + sum_{le'<le} a[q][le'] (moe.py:178-184, 204-213)
-  const int all = block_scan_i32(t.gstart, L + N * L, sh.tmp);
+  const int all = block_scan<INL>(t.gstart, L + N * L, sh.tmp);
+  stamp(b, 18);
   const int padded_total = N * L ? t.rowbase[0] : all;
   for (int i = tid; i < N * L; i += nt) t.rowbase[i] -= padded_total;
   if (tid == 0) {
@@ -658,9 +679,14 @@ __device__ __noinline__ void recv_tables(const txb_moe_shape& s, const uint32_t*
   }
 }
 
-__device__ __noinline__ void recv_rows(const txb_moe_shape& s, int* sm, int64_t* rows, int64_t* sources,
-                                       int32_t* ret, uint8_t* G, uint8_t* dirty, int32_t* send_list,
-                                       uint32_t* send_cnt, int cta, int ncta) {
+__device__ __noinline__ void recv_tables(const txb_moe_shape& s, const uint32_t* C, int* sm, int64_t* info,
+                                         int cta, Shared& sh, const txb_moe_bufs& b) {
+  recv_tables_body<false>(s, C, sm, info, cta, sh, b);
+}
+
+__device__ __forceinline__ void recv_rows_body(const txb_moe_shape& s, int* sm, int64_t* rows, int64_t* sources,
+                                               int32_t* ret, uint8_t* G, uint8_t* dirty, int32_t* send_list,
+                                               uint32_t* send_cnt, int cta, int ncta) {
   const int N = s.ranks, L = s.local_experts;
   const RecvTables t = recv_carve(s, sm);
   const int padded_total = t.tot[0];
@@ -698,6 +724,18 @@ __device__ __noinline__ void recv_rows(const txb_moe_shape& s, int* sm, int64_t*
       if (q != s.me) send_list[atomicAdd(send_cnt, 1u)] = g;
     }
   }
+}
+
+__device__ __noinline__ void recv_rows(const txb_moe_shape& s, int* sm, int64_t* rows, int64_t* sources,
+                                       int32_t* ret, uint8_t* G, uint8_t* dirty, int32_t* send_list,
+                                       uint32_t* send_cnt, int cta, int ncta) {
+  recv_rows_body(s, sm, rows, sources, ret, G, dirty, send_list, send_cnt, cta, ncta);
+}
+
+// The step's error word into info (what dispatch_recv reads); also on the
+// early-return paths, where CTA 0 has latched its own failure.
+__device__ void publish_err(Flags* f, int64_t* info, int L) {
+  if (threadIdx.x == 0) info[2 * L + 2] = (int64_t)*reinterpret_cast<volatile uint32_t*>(&f->err);
 }
 
 __device__ void wait_tokens(Flags* f, int64_t* info, int L, uint64_t timeout_ns) {
@@ -772,20 +810,26 @@ __device__ bool combine_reduce(const txb_moe_shape& s, Flags* f, const uint8_t* 
   const int64_t Pc = s.comb_bytes;
   const int H = s.hidden, R = s.topk;
   const bool vec = combine_vec<ELEM>(Pc, comb, out, ld, H, gidx);
-  if (cta < n) combine_prep(ct, comb, Pc, out, ld, pos, gidx, w, cta, R);
+  const bool split = vec && R <= kCombBatch && cta < n && H / 8 <= 2 * (int)blockDim.x && n <= ncta;
+  if (cta < n) combine_prep(ct, comb, Pc, out, ld, pos, gidx, split ? nullptr : w, cta, R);
+  // EP=1: every row is this rank's own and already written (stream order)
+  const bool solo = s.ranks == 1;
   auto wait = [&]() -> bool {
     if (threadIdx.x == 0) {
-      const uint64_t dl = globaltimer() + timeout_ns;
-      sh.fail = spin_ge(&f->comb_ctr, f->comb_target, dl) ? 0u : TXB_EV_WAIT_COMBINE;
-      if (sh.fail) atomicOr(&f->err, sh.fail);
+      if (solo) {
+        sh.fail = 0;
+      } else {
+        const uint64_t dl = globaltimer() + timeout_ns;
+        sh.fail = spin_ge(&f->comb_ctr, f->comb_target, dl) ? 0u : TXB_EV_WAIT_COMBINE;
+        if (sh.fail) atomicOr(&f->err, sh.fail);
+      }
     }
     __syncthreads();
     return sh.fail == 0;
   };
-  const bool split = vec && R <= kCombBatch && cta < n && H / 8 <= 2 * (int)blockDim.x && n <= ncta;
   if (split) {
     __syncthreads();  // ct staged
-    if (!combine_token_split<ELEM>(ct, H, R, cta, dst, out_bf16, wait)) return false;
+    if (!combine_token_split<ELEM>(ct, H, R, cta, w, dst, out_bf16, wait)) return false;
     __syncthreads();
     return true;
   }
@@ -807,7 +851,9 @@ __device__ bool combine_reduce(const txb_moe_shape& s, Flags* f, const uint8_t* 
 __device__ void end_of_step(const txb_moe_shape& s, void* const* peers, Flags* f, uint64_t step, int ncta) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
+    // EP>1: this CTA's reads of the step's buffers happen before the peers
+    // may reuse them; EP=1 has no peers and the kernel boundary orders the rest
+    if (s.ranks > 1) __threadfence();
     const uint32_t t = atomicAdd(&f->ticket, 1u);
     if (t == (uint32_t)ncta - 1) {
       f->ticket = 0;
@@ -863,7 +909,7 @@ k_recv(txb_moe_shape s, txb_moe_bufs b, uint64_t timeout_ns) {
   uint32_t* C = reinterpret_cast<uint32_t*>(dsm + cmat_offset(s));
   if (!wait_routes(s, f, route_of(b.region, s, (int)(step & 1)), C, step, timeout_ns, sh)) return;
   int* rt = reinterpret_cast<int*>(dsm + recv_offset(s));
-  recv_tables(s, C, rt, b.info, blockIdx.x, sh);
+  recv_tables(s, C, rt, b.info, blockIdx.x, sh, b);
   recv_rows(s, rt, b.rows, b.sources, b.ret_slot, grouped_of(b.region, s), b.dirty, b.send_list, &f->send_cnt,
             blockIdx.x, gridDim.x);
   if (blockIdx.x == 0) wait_tokens(f, b.info, s.local_experts, timeout_ns);
@@ -912,13 +958,15 @@ k_dispatch_fused(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
   uint32_t* wc = hist + ((s.experts + 3) & ~3);
   uint32_t* C = reinterpret_cast<uint32_t*>(dsm + cmat_offset(s));
   int* rt = reinterpret_cast<int*>(dsm + recv_offset(s));
+  const bool solo = s.ranks == 1;
   stamp(b, 0);
   if constexpr (DECODE) {
     RowRegs pre;
     RowRaw raw;
     // issue the token's loads first; route counting runs while they land
     load_row_raw<SRC, ELEM>(x, cta, s.hidden, s.payload_bytes, raw);
-    const uint32_t bad = route_counts_direct(s, routes, n, hist, b.rank_scratch, cta, ncta, sh);
+    const uint32_t bad = route_counts_direct(s, routes, n, hist, reinterpret_cast<int32_t*>(hist + s.experts),
+                                             b.rank_scratch, cta, ncta, sh, b);
     stamp(b, 14);
     finish_row_regs<SRC, ELEM>(raw, pre, sh.red);
     stamp(b, 1);
@@ -926,20 +974,32 @@ k_dispatch_fused(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
     own_positions(s, hist, b.pos, bad, sh);
     for (int q = threadIdx.x; q < s.ranks; q += blockDim.x) sh.cnt[q] = 0;
     stamp(b, 2);
-    if (!wait_routes(s, f, route_of(b.region, s, (int)(step & 1)), C, step, timeout_ns, sh)) return;
+    // EP=1: the route matrix is this CTA's own histogram and the kernel
+    // boundary orders the stores before any reader -- no exchange, fence,
+    // counter or wait (the published row still feeds last_layout)
+    const uint32_t* Cm = hist;
+    if (!solo) {
+      if (!wait_routes(s, f, route_of(b.region, s, (int)(step & 1)), C, step, timeout_ns, sh)) {
+        if (cta == 0) publish_err(f, b.info, s.local_experts);
+        return;
+      }
+      Cm = C;
+    }
     stamp(b, 3);
     if (!bad) {
-      own_dests(s, C, b.peers, b.gidx, sh);
+      own_dests(s, Cm, b.peers, b.gidx, sh);
       stamp(b, 15);
       if (pre.ok) store_row_regs<SRC, ELEM>(pre, s.hidden, s.scales, sh.dstp, s.topk);
       else dispatch_row_slow<SRC, ELEM>(s, x, cta, sh);
     }
     stamp(b, 5);
     // the receive tables overlap the stores in flight; the fence follows
-    recv_tables(s, C, rt, b.info, cta, sh);
+    recv_tables_body<true>(s, Cm, rt, b.info, cta, sh, b);
     stamp(b, 4);
-    if (cta == 0 && threadIdx.x == 0) f->tok_target += (uint64_t)recv_carve(s, rt).tot[1];
-    signal_counts(s, b.peers, offsetof(Flags, tok_ctr), sh);
+    if (!solo) {
+      if (cta == 0 && threadIdx.x == 0) f->tok_target += (uint64_t)recv_carve(s, rt).tot[1];
+      signal_counts(s, b.peers, offsetof(Flags, tok_ctr), sh);
+    }
   } else {
     // contiguous token range per CTA, segmented counting with a grid barrier
     const int64_t chunk = (n + ncta - 1) / ncta;
@@ -949,24 +1009,48 @@ k_dispatch_fused(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
     stamp(b, 1);
     route_publish(s, b.peers, f, hist, step, n, bad, cta, ncta);
     stamp(b, 2);
-    if (!wait_routes(s, f, route_of(b.region, s, (int)(step & 1)), C, step, timeout_ns, sh)) return;
+    // EP=1: the totals are the route matrix (copied out of `hist`, which
+    // the layout below overwrites)
+    const uint32_t* Cm = C;
+    if (solo) {
+      for (int e = threadIdx.x; e < s.experts; e += blockDim.x) C[e] = hist[e];
+      __syncthreads();
+    } else {
+      if (!wait_routes(s, f, route_of(b.region, s, (int)(step & 1)), C, step, timeout_ns, sh)) {
+        if (cta == 0) publish_err(f, b.info, s.local_experts);
+        return;
+      }
+      Cm = C;
+    }
     stamp(b, 3);
     int* baseg = reinterpret_cast<int*>(dsm);
-    if (!dispatch_layout(s, C, baseg, baseg + s.experts, f, cta == 0, sh)) return;
-    recv_tables(s, C, rt, b.info, cta, sh);
+    if (!dispatch_layout(s, Cm, baseg, baseg + s.experts, f, cta == 0 && !solo, sh)) {
+      if (cta == 0) publish_err(f, b.info, s.local_experts);
+      return;
+    }
+    recv_tables(s, Cm, rt, b.info, cta, sh, b);
     for (int q = threadIdx.x; q < s.ranks; q += blockDim.x) sh.cnt[q] = 0;
     __syncthreads();
     stamp(b, 4);
     if (!bad) dispatch_tokens<SRC, ELEM>(s, x, t0, t1, 1, routes, b.rank_scratch, b.gidx, b.peers, baseg, sh);
     stamp(b, 5);
-    signal_counts(s, b.peers, offsetof(Flags, tok_ctr), sh);
+    if (!solo) signal_counts(s, b.peers, offsetof(Flags, tok_ctr), sh);
   }
   // thread 0 fences and signals while the other warps fill the metadata
   stamp(b, 6);
-  recv_rows(s, rt, b.rows, b.sources, b.ret_slot, grouped_of(b.region, s), b.dirty, b.send_list, &f->send_cnt,
-            cta, ncta);
+  if constexpr (DECODE)
+    recv_rows_body(s, rt, b.rows, b.sources, b.ret_slot, grouped_of(b.region, s), b.dirty, b.send_list,
+                   &f->send_cnt, cta, ncta);
+  else
+    recv_rows(s, rt, b.rows, b.sources, b.ret_slot, grouped_of(b.region, s), b.dirty, b.send_list, &f->send_cnt,
+              cta, ncta);
   stamp(b, 7);
-  if (cta == 0) wait_tokens(f, b.info, s.local_experts, timeout_ns);
+  if (cta == 0) {
+    // EP=1: every CTA counted every route, so CTA 0 has latched any route
+    // error itself; the grid's end publishes the rows
+    if (!solo) wait_tokens(f, b.info, s.local_experts, timeout_ns);
+    else publish_err(f, b.info, s.local_experts);
+  }
   stamp(b, 8);
 }
 
@@ -1080,6 +1164,7 @@ static int set_smem(K kernel, size_t smem) {
 }
 
 // Launch helper; `coop` requests a cooperative launch (all CTAs resident).
+
 template <typename... KArgs, typename... Args>
 static int launch(void (*kernel)(KArgs...), int grid, int block, size_t smem, cudaStream_t st, bool coop,
                   Args... args) {
@@ -1089,11 +1174,14 @@ static int launch(void (*kernel)(KArgs...), int grid, int block, size_t smem, cu
   cfg.blockDim = dim3(block);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (coop) {
+    attr[na].id = cudaLaunchAttributeCooperative;
+    attr[na++].val.cooperative = 1;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = coop ? 1 : 0;
+  cfg.numAttrs = na;
   TXB_CUDA(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
   return TXB_OK;
 }
@@ -1286,13 +1374,16 @@ int txb_moe_dispatch_fused(const txb_moe_shape* s, const txb_moe_bufs* b, const 
   }
   const bool decode = n >= 1 && n <= sms && s->topk <= kMaxOwn && vec && nchunk <= 2 * kThreads;
   const int want = (int)(n < 1 ? 1 : (n < sms ? n : sms));
+  // decode: the route ids of the whole batch are staged after the histogram
+  const size_t rv_end = (size_t)(s->experts + n * s->topk) * 4 + 16;
+  const size_t smem_d = smem > rv_end ? smem : rv_end;
 #define TXB_F(SRC, ELEM)                                                                            \
   do {                                                                                              \
     if (decode) {                                                                                   \
       auto kd = k_dispatch_fused<SRC, ELEM, true>;                                                  \
-      if (int rc = set_smem(kd, smem)) return rc;                                                   \
-      if (coop_grid(kd, s->device, smem, want) == want)                                             \
-        return launch(kd, want, kThreads, smem, st, true, *s, *b, x, n, routes, timeout_ns);        \
+      if (int rc = set_smem(kd, smem_d)) return rc;                                                 \
+      if (coop_grid(kd, s->device, smem_d, want) == want)                                           \
+        return launch(kd, want, kThreads, smem_d, st, true, *s, *b, x, n, routes, timeout_ns);      \
     }                                                                                               \
     auto kg = k_dispatch_fused<SRC, ELEM, false>;                                                   \
     if (int rc = set_smem(kg, smem)) return rc;                                                     \

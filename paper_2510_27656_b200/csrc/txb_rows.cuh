@@ -390,7 +390,7 @@ __device__ __forceinline__ void combine_prep(CombTok& ct, const uint8_t* comb, i
   if (tid < R) {
     const int32_t gi = gidx ? gidx[t * R + tid] : -1;
     ct.rowp[tid] = gi >= 0 ? out_rows + (int64_t)gi * ld : comb + pos[t * R + tid] * Pc;
-    ct.ws[tid] = w[t * R + tid];
+    if (w) ct.ws[tid] = w[t * R + tid];
     ct.local[tid] = gi >= 0;
   }
 }
@@ -486,8 +486,11 @@ __device__ void combine_token(CombTok& ct, int64_t Pc, const uint8_t* comb, int 
 // rows this rank served itself are loaded BEFORE the completion wait, the
 // returned rows after it; the sum then runs in the reference order.  The
 // wait itself is done by `wait_fn` (thread 0 spins, then a barrier).
+// The weights (an input, usually cold) are fetched after the row loads are
+// in flight; the wait's barrier publishes them.
 template <int ELEM, typename Wait>
-__device__ bool combine_token_split(CombTok& ct, int H, int R, int64_t t, void* dst, int out_bf16, Wait wait_fn) {
+__device__ bool combine_token_split(CombTok& ct, int H, int R, int64_t t, const float* w, void* dst, int out_bf16,
+                                    Wait wait_fn) {
   const int tid = threadIdx.x, nt = blockDim.x;
   constexpr int CPT = ELEM == 4 ? 1 : 2;
   const int c0 = tid;
@@ -498,6 +501,7 @@ __device__ bool combine_token_split(CombTok& ct, int H, int R, int64_t t, void* 
     for (int u = 0; u < kCombBatch; ++u)
       if (u < R && ct.local[u] && c0 + p * nt < H / 8)
         raw[p][u] = load_chunk8<ELEM>(ct.rowp[u], (int64_t)(c0 + p * nt) * 8);
+  if (tid >= nt - 32 && tid - (nt - 32) < R) ct.ws[tid - (nt - 32)] = w[t * R + tid - (nt - 32)];
   if (!wait_fn()) return false;
 #pragma unroll
   for (int p = 0; p < CPT; ++p)

@@ -29,6 +29,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="decode")
 ap.add_argument("--reps", type=int, default=50)
 ap.add_argument("--mode", default="graph", choices=["graph", "eager", "empty"])
+ap.add_argument("--noflush", action="store_true")
 a = ap.parse_args()
 
 world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -89,8 +90,14 @@ else:
     rk._bufs.prof = 0
     run = g.replay
 rows = []
+detail = []
+ORDER = [0, 19, 14, 1, 2, 3, 15, 5, 16, 17, 18, 4, 6, 7, 8, 9, 10, 11, 12, 13]
+STAMP = {0: "start", 19: "own routes in", 14: "counted(+loads)", 1: "encoded", 2: "published+pos", 3: "routes-in", 15: "dests",
+         5: "stored", 16: "T:loaded", 17: "T:srcpre", 18: "T:scan", 4: "tables", 6: "signalled", 7: "metadata", 8: "tokens-in", 9: "c:start", 10: "c:sent",
+         11: "c:signalled", 12: "c:reduced", 13: "c:end"}
 for k in range(a.reps + 5):
-    flush.fill_(k & 0xFF)
+    if not a.noflush:
+        flush.fill_(k & 0xFF)
     if world > 1:
         rk.barrier()
     _lib.call("txb_globaltimer", C.c_void_p(gt.data_ptr() + 16), sid)   # barrier done
@@ -114,6 +121,11 @@ for k in range(a.reps + 5):
         v = p[:, i][p[:, i] > 0]
         return (v.max() - base) / 1e3 if v.size else np.nan
 
+    det = []
+    for k in ORDER:
+        v = p[:, k][p[:, k] > 0]
+        det.append(((np.median(v) - base) / 1e3, (v.max() - base) / 1e3) if v.size else (np.nan, np.nan))
+    detail.append(det)
     rows.append([e0.elapsed_time(e1) * 1e3, (t[2] - base) / 1e3, lo(0), hi(3), hi(8), lo(9), hi(11), hi(13),
                  (t[1] - base) / 1e3])
 med = np.median(np.asarray(rows), axis=0).tolist()
@@ -125,6 +137,17 @@ if world > 1:
     dist.all_gather_object(allr, mine)
 else:
     allr = [mine]
+dmed = np.nanmedian(np.asarray(detail), axis=0)
+lines = [f"  {STAMP[k]:16s} median CTA {m:7.2f}  last CTA {x:7.2f}" for k, (m, x) in zip(ORDER, dmed.tolist())]
+alld = [None] * world
+if world > 1:
+    dist.all_gather_object(alld, lines)
+else:
+    alld = [lines]
+if rank == 0:
+    for r, ls in enumerate(alld):
+        print(f"rank {r} phase stamps (us from graph start, median over reps)")
+        print("\n".join(ls))
 if rank == 0:
     print("us, device clock of each rank relative to its graph start (median over reps)")
     print("rank " + " ".join(f"{n:>18}" for n in names))
