@@ -14,66 +14,13 @@
 // destination's ImmCounter slot -- exactly once per operation and only
 // after the whole payload is visible, as engine.py:9-17 requires.
 #include "txb_common.cuh"
+#include "txb_tma.cuh"
 
 namespace txb {
 
 constexpr int kCopyThreads = 256;
 constexpr int kPiece = 16 * 1024;  // bytes per TMA piece (one smem stage)
 constexpr int kStages = 8;
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(phase)
-      : "memory");
-}
-
-// global -> shared bulk load, completion counted on the mbarrier
-__device__ __forceinline__ void tma_load(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(smem)),
-      "l"(gmem), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
-// shared -> global bulk store (bulk-group completion)
-__device__ __forceinline__ void tma_store(void* gmem, const void* smem, uint32_t bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem), "r"(smem_u32(smem)),
-               "r"(bytes)
-               : "memory");
-  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-}
-
-// at most kStages-1 stores may still be reading shared memory: the oldest
-// stage is free again
-__device__ __forceinline__ void tma_store_wait_read() {
-  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kStages - 1) : "memory");
-}
-
-__device__ __forceinline__ void tma_store_wait_all() {  // writes performed
-  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-}
-
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 struct PieceRef {
   const uint8_t* src;
@@ -125,7 +72,7 @@ __global__ void __launch_bounds__(kCopyThreads, 1) k_copy_pages(txb_pages j) {
         tma_store(p.dst, stage + s * kPiece, p.bytes);
         const int64_t kn = k + (int64_t)kStages * gridDim.x;
         if (kn < total) {
-          tma_store_wait_read();  // the stage stored kStages-1 pieces ago is free
+          tma_store_wait_read<kStages>();  // the stage stored kStages-1 pieces ago is free
           const PieceRef q = piece_of(j, kn, per_page);
           mbar_expect_tx(&bars[s], q.bytes);
           tma_load(stage + s * kPiece, q.src, q.bytes, &bars[s]);
