@@ -333,7 +333,10 @@ def run_b200(a) -> None:
     # algorithmic bytes per launch: EP=1 moves everything
     # through HBM; EP>1 is bounded by the larger of NVLink egress/ingress
     if n_gpu == 1:
-        bytes_k = {"dispatch": tokens * H * 2 + tokens * R * P + ex["pad_rows"] * P,
+        # dispatch reads n*H*in_elem and writes n*R*P;
+        # combine reads n*R*Pc and writes n*H*out_elem (padding rows are
+        # not algorithmic: they are re-zeroed only when dirty)
+        bytes_k = {"dispatch": tokens * H * 2 + tokens * R * P,
                    "combine": tokens * R * Pc + tokens * H * 2}
         bound = "hbm"
     else:
@@ -341,11 +344,19 @@ def run_b200(a) -> None:
                    "combine": max(ex["valid_rows"] - ex["self_rows"], ex["out_rows"]) * Pc}
         bound = "nvlink"
     dom = max(names, key=lambda k: kt[k])
+    # DRAM bytes per launch of that kernel from the committed ncu capture
+    # (EP=1 decode only; profiles/r01_ncu_traffic.json)
+    traffic = None
+    tf = ROOT / "profiles" / "r01_ncu_traffic.json"
+    if n_gpu == 1 and a.config == "decode" and tf.exists():
+        t = json.loads(tf.read_text()).get(f"k_{dom}_fused")
+        if t:
+            traffic = int(t["dram_read"] + t["dram_write"])
     peak = hbm_peak if bound == "hbm" else nvl_peak
     achieved = bytes_k[dom] / (kt[dom] * 1e-6) / 1e9
     roofline = {"bound": bound, "kernel": f"k_{dom}_fused",
                 "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": None,
+                "frac": round(achieved / peak, 4), "traffic": traffic,
                 "peak_source": ("MEASURED_PEAKS.json hbm_gbs (burst copy)" if bound == "hbm"
                                 else "B200_PROFILING.md measured peer copy 770 GB/s (fallback)"),
                 "algorithmic_bytes": int(bytes_k[dom]), "kernel_us": round(kt[dom], 2),
