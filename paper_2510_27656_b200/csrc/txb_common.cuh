@@ -141,8 +141,17 @@ __host__ __device__ inline uint8_t* comb_of(void* region, const txb_moe_shape& s
 // thread of the block must call it.  Returns the total.  `tmp` needs 33
 // ints.  Out of line: one copy of the code serves every call site (the
 // fused kernels are instruction-fetch bound when the code balloons).
-static __device__ __forceinline__ int block_scan_i32_body(int* a, int len, int* tmp) {
-  const int nt = blockDim.x, tid = threadIdx.x;
+// A thread group that synchronises on its own hardware barrier: the whole
+// CTA (barrier 0, what __syncthreads uses) or a warp-aligned role of it on a
+// named barrier, so two roles of one CTA can run different phases at once.
+struct Grp {
+  int tid, nt, bar;
+  __device__ static Grp cta() { return Grp{(int)threadIdx.x, (int)blockDim.x, 0}; }
+  __device__ void sync() const { asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(nt) : "memory"); }
+};
+
+static __device__ __forceinline__ int block_scan_i32_body(int* a, int len, int* tmp, const Grp& g) {
+  const int nt = g.nt, tid = g.tid;
   const int per = (len + nt - 1) / nt;
   const int lo = min(len, tid * per), hi = min(len, lo + per);
   int sum = 0;
@@ -154,7 +163,7 @@ static __device__ __forceinline__ int block_scan_i32_body(int* a, int len, int* 
     if (lane >= o) x += y;
   }
   if (lane == 31) tmp[warp] = x;
-  __syncthreads();
+  g.sync();
   if (warp == 0) {
     const int nw = (nt + 31) >> 5;
     int w = lane < nw ? tmp[lane] : 0;
@@ -165,7 +174,7 @@ static __device__ __forceinline__ int block_scan_i32_body(int* a, int len, int* 
     if (lane < nw) tmp[lane] = w;  // inclusive warp totals
     if (lane == nw - 1) tmp[32] = w;
   }
-  __syncthreads();
+  g.sync();
   int run = (x - sum) + (warp ? tmp[warp - 1] : 0);
   for (int i = lo; i < hi; ++i) {
     const int v = a[i];
@@ -173,21 +182,21 @@ static __device__ __forceinline__ int block_scan_i32_body(int* a, int len, int* 
     run += v;
   }
   const int total = tmp[32];
-  __syncthreads();
+  g.sync();
   return total;
 }
 
 static __device__ __noinline__ int block_scan_i32(int* a, int len, int* tmp) {
-  return block_scan_i32_body(a, len, tmp);
+  return block_scan_i32_body(a, len, tmp, Grp::cta());
 }
 
 // Call-site choice: INL = inline copy (a straight-line decode path, where a
 // call into cold out-of-line code costs an instruction-fetch miss per
 // call), else the shared out-of-line copy.
 template <bool INL>
-__device__ __forceinline__ int block_scan(int* a, int len, int* tmp) {
-  if constexpr (INL) return block_scan_i32_body(a, len, tmp);
-  else return block_scan_i32(a, len, tmp);
+__device__ __forceinline__ int block_scan(int* a, int len, int* tmp, const Grp& g) {
+  if constexpr (INL) return block_scan_i32_body(a, len, tmp, g);
+  else return block_scan_i32(a, len, tmp);  // whole CTA only
 }
 
 // ------------------------------------------------------------- row copy

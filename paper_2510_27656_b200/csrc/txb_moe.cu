@@ -99,21 +99,23 @@ struct Shared {  // static shared state of one CTA
 // copies sit in consecutive lanes), loads otherwise.
 __device__ uint32_t route_counts_direct(const txb_moe_shape& s, const int64_t* routes, int64_t n, uint32_t* hist,
                                         int32_t* rv, int32_t* rank_out, int cta, int ncta, Shared& sh,
-                                        const txb_moe_bufs& bufs) {
-  const int E = s.experts, R = s.topk, tid = threadIdx.x;
+                                        const txb_moe_bufs& bufs, const Grp& g) {
+  const int E = s.experts, R = s.topk, tid = g.tid;
   const int m = (int)(n * R);
   const int nmine = n > cta ? (int)((n - cta + ncta - 1) / ncta) : 0;
   const int nw = nmine * R;
   // issue every route load this thread needs (its own copies and up to
   // kPre entries of the batch) before the first barrier
   constexpr int kPre = 4;
-  const int nt = blockDim.x;
+  const int nt = g.nt;
   const bool pre_ok = m <= kPre * nt;
   int64_t pre[kPre];
 #pragma unroll
   for (int u = 0; u < kPre; ++u) pre[u] = (pre_ok && u * nt + tid < m) ? routes[u * nt + tid] : -1;
-  for (int e = tid; e < E; e += blockDim.x) hist[e] = 0;
-  for (int k = tid; k < nw; k += blockDim.x) {
+  #pragma unroll 1
+  for (int e = tid; e < E; e += nt) hist[e] = 0;
+  #pragma unroll 1
+  for (int k = tid; k < nw; k += nt) {
     const int i = (cta + (k / R) * ncta) * R + (k % R);
     const int64_t v = routes[i];
     sh.own_e[k] = (v >= 0 && v < E) ? (int)v : -1;
@@ -123,10 +125,11 @@ __device__ uint32_t route_counts_direct(const txb_moe_shape& s, const int64_t* r
     sh.bad = 0;
     sh.direct = 1;
   }
-  __syncthreads();
+  g.sync();
   stamp(bufs, 19);
   const bool lanes = (32 % R) == 0;
-  for (int base = 0, u = 0; base < m; base += blockDim.x, ++u) {
+  #pragma unroll 1
+  for (int base = 0, u = 0; base < m; base += nt, ++u) {
     const int i = base + tid;
     const bool valid = i < m;
     int64_t v = -1;
@@ -143,11 +146,13 @@ __device__ uint32_t route_counts_direct(const txb_moe_shape& s, const int64_t* r
     const int j = i % R;
     bool dup = false;
     if (lanes) {
+      #pragma unroll 1
       for (int jj = 1; jj < R; ++jj) {
         const int w = __shfl_up_sync(0xffffffffu, v32, jj);
         dup |= (jj <= j) && (w == v32);
       }
     } else if (valid) {
+      #pragma unroll 1
       for (int jj = 1; jj <= j; ++jj) dup |= routes[i - jj] == v;
     }
     if (!valid) continue;
@@ -159,9 +164,10 @@ __device__ uint32_t route_counts_direct(const txb_moe_shape& s, const int64_t* r
     if (dup) atomicOr(&sh.bad, TXB_EV_ROUTE_DUP);
     atomicAdd(&hist[v32], 1u);
   }
-  __syncthreads();
+  g.sync();
   {
     const int lane = tid & 31, warp = tid >> 5, nwarp = nt >> 5;
+    #pragma unroll 1
     for (int k = warp; k < nw; k += nwarp) {
       const int e = sh.own_e[k], lim = sh.own_i[k];
       int cnt = 0;
@@ -175,8 +181,9 @@ __device__ uint32_t route_counts_direct(const txb_moe_shape& s, const int64_t* r
   }
   const uint32_t b = sh.bad;
   if (b)
-    for (int e = tid; e < E; e += blockDim.x) hist[e] = 0;  // publish an empty row
-  __syncthreads();
+    #pragma unroll 1
+    for (int e = tid; e < E; e += nt) hist[e] = 0;  // publish an empty row
+  g.sync();
   return b;
 }
 
@@ -368,22 +375,30 @@ __device__ void route_positions(const txb_moe_shape& s, const int64_t* routes, i
 // CTA holds the full histogram; CTA `part` of `nparts` stores its slice.
 // Part 0 also books the copies that will come back from other ranks.
 __device__ void route_publish(const txb_moe_shape& s, void* const* peers, Flags* f, const uint32_t* hist,
-                              uint64_t step, int64_t n, uint32_t bad, int part, int nparts) {
+                              uint64_t step, int64_t n, uint32_t bad, int part, int nparts,
+                              const Grp& g = Grp::cta()) {
   const int E = s.experts, N = s.ranks, L = s.local_experts;
   const int slot = (int)(step & 1);
   const uint64_t tag = (uint64_t)(uint32_t)step << 32;
-  for (int idx = part * blockDim.x + threadIdx.x; idx < N * E; idx += nparts * blockDim.x) {
+  #pragma unroll 1
+  for (int idx = part * g.nt + g.tid; idx < N * E; idx += nparts * g.nt) {
     const int d = idx / E, e = idx - d * E;
-    st_relaxed_sys(route_of(peers[d], s, slot) + (size_t)s.me * E + e, tag | hist[e]);
+    if (N == 1) *(route_of(peers[d], s, slot) + (size_t)s.me * E + e) = tag | hist[e];
+    else st_relaxed_sys(route_of(peers[d], s, slot) + (size_t)s.me * E + e, tag | hist[e]);
   }
-  if (part == 0 && threadIdx.x < 32) {
+  if (part == 0 && g.tid < 32) {
     // copies this rank serves itself do not come back through the counter
-    const int lane = threadIdx.x;
+    const int lane = g.tid;
     uint32_t self = 0;
+    #pragma unroll 1
     for (int le = lane; le < L; le += 32) self += hist[s.me * L + le];
     for (int o = 16; o; o >>= 1) self += __shfl_xor_sync(0xffffffffu, self, o);
     // per-source step tags for host-side gating / diagnostics only
-    for (int d = lane; d < N; d += 32) st_relaxed_sys(&flags_of(peers[d], s)->route_tag[slot][s.me], step);
+    #pragma unroll 1
+    for (int d = lane; d < N; d += 32) {
+      if (N == 1) flags_of(peers[d], s)->route_tag[slot][s.me] = step;
+      else st_relaxed_sys(&flags_of(peers[d], s)->route_tag[slot][s.me], step);
+    }
     if (lane == 0) {
       f->comb_target += bad ? 0 : (uint64_t)(n * s.topk) - self;
       if (bad) atomicOr(&f->err, bad);
@@ -396,13 +411,14 @@ __device__ void route_publish(const txb_moe_shape& s, void* const* peers, Flags*
 // Acquire every route word of this step (tag == step) into Cs[N*E] (shared
 // memory) and wait for every peer's end-of-previous-step barrier.
 __device__ bool wait_routes(const txb_moe_shape& s, Flags* f, const uint64_t* C, uint32_t* Cs, uint64_t step,
-                            uint64_t timeout_ns, Shared& sh) {
-  if (threadIdx.x == 0) sh.fail = 0;
-  __syncthreads();
+                            uint64_t timeout_ns, Shared& sh, const Grp& g = Grp::cta()) {
+  if (g.tid == 0) sh.fail = 0;
+  g.sync();
   const uint64_t dl = globaltimer() + timeout_ns;
   const uint32_t want = (uint32_t)step;
   const int NE = s.ranks * s.experts;
-  for (int i = threadIdx.x; i < NE; i += blockDim.x) {
+  #pragma unroll 1
+  for (int i = g.tid; i < NE; i += g.nt) {
     uint64_t v = ld_relaxed_sys(C + i);
     uint32_t it = 0;
     while ((uint32_t)(v >> 32) != want) {
@@ -414,12 +430,13 @@ __device__ bool wait_routes(const txb_moe_shape& s, Flags* f, const uint64_t* C,
     }
     Cs[i] = (uint32_t)v;
   }
-  if (threadIdx.x < 32)
-    for (int q = threadIdx.x; q < s.ranks; q += 32)
+  if (g.tid < 32)
+    #pragma unroll 1
+    for (int q = g.tid; q < s.ranks; q += 32)
       if (!spin_ge(&f->done[q], step - 1, dl)) atomicOr(&sh.fail, TXB_EV_WAIT_BARRIER);
-  __syncthreads();
+  g.sync();
   const uint32_t fl = sh.fail;
-  if (fl && threadIdx.x == 0) atomicOr(&f->err, fl);
+  if (fl && g.tid == 0) atomicOr(&f->err, fl);
   return fl == 0;
 }
 
@@ -468,11 +485,13 @@ __device__ bool dispatch_layout(const txb_moe_shape& s, const uint32_t* C, int* 
 // instead of block-wide scans (one warp per copy, no block barrier).
 // pos = sum_{e' < e} hist[e'] + rank (moe.py:514-521).
 __device__ void own_positions(const txb_moe_shape& s, const uint32_t* hist, int64_t* pos, uint32_t bad,
-                              Shared& sh) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+                              Shared& sh, const Grp& g = Grp::cta()) {
+  const int lane = g.tid & 31, warp = g.tid >> 5, nwarp = g.nt >> 5;
+  #pragma unroll 1
   for (int k = warp; k < s.topk; k += nwarp) {
     const int e = sh.own_e[k];
     int acc = 0;
+    #pragma unroll 1
     for (int x = lane; x < e; x += 32) acc += (int)hist[x];
     for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) pos[sh.own_i[k]] = bad ? -1 : (int64_t)acc + sh.own_rank[k];
@@ -482,17 +501,21 @@ __device__ void own_positions(const txb_moe_shape& s, const uint32_t* hist, int6
 // grouped row on owner d of copy k: group_starts_d[le] + sum_{s' < me}
 // counts[s', e] + rank; books gidx and the counts.
 __device__ void own_dests(const txb_moe_shape& s, const uint32_t* C, void* const* peers, int32_t* gidx,
-                          Shared& sh) {
+                          Shared& sh, const Grp& g = Grp::cta()) {
   const int N = s.ranks, E = s.experts, L = s.local_experts;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const int lane = g.tid & 31, warp = g.tid >> 5, nwarp = g.nt >> 5;
+  #pragma unroll 1
   for (int k = warp; k < s.topk; k += nwarp) {
     const int e = sh.own_e[k], d = e / L, le = e - d * L;
     int acc = 0;
+    #pragma unroll 1
     for (int x = lane; x < le; x += 32) {
       int col = 0;
+      #pragma unroll 1
       for (int q = 0; q < N; ++q) col += (int)C[q * E + d * L + x];
       acc += pad_up(col);
     }
+    #pragma unroll 1
     for (int q = lane; q < s.me; q += 32) acc += (int)C[q * E + e];
     for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) {
@@ -502,7 +525,7 @@ __device__ void own_dests(const txb_moe_shape& s, const uint32_t* C, void* const
       atomicAdd(&sh.cnt[d], 1u);
     }
   }
-  __syncthreads();
+  g.sync();
 }
 
 // ------------------------------------------------------------------- P4
@@ -576,9 +599,11 @@ __device__ void signal_counts(const txb_moe_shape& s, void* const* peers, size_t
   __syncthreads();
   if (threadIdx.x == 0) {
     bool any = false;
+    #pragma unroll 1
     for (int d = 0; d < s.ranks; ++d) any |= sh.cnt[d] != 0;
     if (any) {
       fence_release(s.single_device);
+      #pragma unroll 1
       for (int d = 0; d < s.ranks; ++d)
         if (sh.cnt[d])
           red_relaxed_sys_add(reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(flags_of(peers[d], s)) + field),
@@ -621,10 +646,12 @@ __device__ __forceinline__ RecvTables recv_carve(const txb_moe_shape& s, int* sm
 
 template <bool INL>
 __device__ __forceinline__ void recv_tables_body(const txb_moe_shape& s, const uint32_t* C, int* sm, int64_t* info,
-                                                 int cta, Shared& sh, const txb_moe_bufs& b) {
+                                                 int cta, Shared& sh, const txb_moe_bufs& b,
+                                                 const Grp& g = Grp::cta()) {
   const int N = s.ranks, E = s.experts, L = s.local_experts, me = s.me;
-  const int tid = threadIdx.x, nt = blockDim.x;
+  const int tid = g.tid, nt = g.nt;
   RecvTables t = recv_carve(s, sm);
+  #pragma unroll 1
   for (int i = tid; i < N * L; i += nt) {
     const int q = i / L, le = i - q * L;
     t.a[i] = (int)C[q * E + me * L + le];
@@ -632,17 +659,21 @@ __device__ __forceinline__ void recv_tables_body(const txb_moe_shape& s, const u
   }
   {
     const int warp = tid >> 5, lane = tid & 31, nwarp = nt >> 5;
+    #pragma unroll 1
     for (int q = warp; q < N; q += nwarp) {
       int acc = 0;
+      #pragma unroll 1
       for (int e = lane; e < me * L; e += 32) acc += (int)C[q * E + e];
       for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
       if (lane == 0) t.pre_all[q] = acc;
     }
   }
-  __syncthreads();
+  g.sync();
   stamp(b, 16);
+  #pragma unroll 1
   for (int le = tid; le < L; le += nt) {
     int run = 0;
+    #pragma unroll 1
     for (int q = 0; q < N; ++q) {
       t.srcpre[le * (N + 1) + q] = run;
       run += t.a[q * L + le];
@@ -651,23 +682,26 @@ __device__ __forceinline__ void recv_tables_body(const txb_moe_shape& s, const u
     t.gsize[le] = run;
     t.gstart[le] = pad_up(run);
   }
-  __syncthreads();
+  g.sync();
   stamp(b, 17);
   // one scan over [padded group sizes (L) | counts flattened source-major
   // (N*L)]: the first part gives group_starts, the second (minus the padded
   // total) recv_start[me][q] + sum_{le'<le} a[q][le'] (moe.py:178-184, 204-213)
-  const int all = block_scan<INL>(t.gstart, L + N * L, sh.tmp);
+  const int all = block_scan<INL>(t.gstart, L + N * L, sh.tmp, g);
   stamp(b, 18);
   const int padded_total = N * L ? t.rowbase[0] : all;
+  #pragma unroll 1
   for (int i = tid; i < N * L; i += nt) t.rowbase[i] -= padded_total;
   if (tid == 0) {
     t.tot[0] = padded_total;
     t.tot[1] = all - padded_total;
   }
-  __syncthreads();
+  g.sync();
+  #pragma unroll 1
   for (int i = tid; i < N * L; i += nt) t.retbase[i] = t.pre_all[i / L] + (t.rowbase[i] - t.rowbase[(i / L) * L]);
-  __syncthreads();
+  g.sync();
   if (cta == 0) {
+    #pragma unroll 1
     for (int le = tid; le < L; le += nt) {
       info[le] = t.gsize[le];
       info[L + le] = t.gstart[le];
@@ -684,15 +718,36 @@ __device__ __noinline__ void recv_tables(const txb_moe_shape& s, const uint32_t*
   recv_tables_body<false>(s, C, sm, info, cta, sh, b);
 }
 
+// Dirty flags of the first kPreDirty rows a warp of group `g` will visit in
+// recv_rows_body, loaded at kernel start so the (cold) byte reads are off
+// the kernel's tail.  Byte i of the result = dirty[row i] (0 beyond G).
+constexpr int kPreDirty = 4;
+
+__device__ __forceinline__ uint32_t prefetch_dirty(const txb_moe_shape& s, const uint8_t* dirty, int cta, int ncta,
+                                                   const Grp& g) {
+  const int nwarp = g.nt >> 5, warp = g.tid >> 5;
+  uint32_t pd = 0;
+#pragma unroll
+  for (int i = 0; i < kPreDirty; ++i) {
+    const int64_t r = (int64_t)cta * nwarp + warp + (int64_t)i * ncta * nwarp;
+    if (r < s.grouped_rows) pd |= (uint32_t)dirty[r] << (8 * i);
+  }
+  return pd;
+}
+
+// pd: prefetch_dirty of the same group (or ~0u: read the flags here).
 __device__ __forceinline__ void recv_rows_body(const txb_moe_shape& s, int* sm, int64_t* rows, int64_t* sources,
                                                int32_t* ret, uint8_t* G, uint8_t* dirty, int32_t* send_list,
-                                               uint32_t* send_cnt, int cta, int ncta) {
+                                               uint32_t* send_cnt, int cta, int ncta, const Grp& grp = Grp::cta(),
+                                               uint32_t pd = ~0u) {
   const int N = s.ranks, L = s.local_experts;
   const RecvTables t = recv_carve(s, sm);
   const int padded_total = t.tot[0];
   const int64_t P = s.payload_bytes;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
-  for (int g = cta * nwarp + warp; g < padded_total; g += ncta * nwarp) {
+  const int warp = grp.tid >> 5, lane = grp.tid & 31, nwarp = grp.nt >> 5;
+  int it = 0;
+  #pragma unroll 1
+  for (int g = cta * nwarp + warp; g < padded_total; g += ncta * nwarp, ++it) {
     int lo = 0, hi = L - 1;  // last le with gstart[le] <= g
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
@@ -703,7 +758,7 @@ __device__ __forceinline__ void recv_rows_body(const txb_moe_shape& s, int* sm, 
     if (k >= t.gsize[le]) {
       // padding rows read as zero (moe.py:719); only rows that held data
       // since they were last zeroed need the store
-      const bool d = dirty[g] != 0;
+      const bool d = (pd != ~0u && it < kPreDirty) ? ((pd >> (8 * it)) & 0xFFu) != 0 : dirty[g] != 0;
       if (d) zero_row(G + (int64_t)g * P, P, lane, 32);
       if (lane == 0) {
         rows[g] = -1;
@@ -966,7 +1021,7 @@ k_dispatch_fused(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
     // issue the token's loads first; route counting runs while they land
     load_row_raw<SRC, ELEM>(x, cta, s.hidden, s.payload_bytes, raw);
     const uint32_t bad = route_counts_direct(s, routes, n, hist, reinterpret_cast<int32_t*>(hist + s.experts),
-                                             b.rank_scratch, cta, ncta, sh, b);
+                                             b.rank_scratch, cta, ncta, sh, b, Grp::cta());
     stamp(b, 14);
     finish_row_regs<SRC, ELEM>(raw, pre, sh.red);
     stamp(b, 1);
@@ -1048,6 +1103,98 @@ k_dispatch_fused(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
   if (cta == 0) {
     // EP=1: every CTA counted every route, so CTA 0 has latched any route
     // error itself; the grid's end publishes the rows
+    if (!solo) wait_tokens(f, b.info, s.local_experts, timeout_ns);
+    else publish_err(f, b.info, s.local_experts);
+  }
+  stamp(b, 8);
+}
+
+// Decode dispatch with two warp roles on named barriers, so phases that do
+// not depend on each other run at once instead of one after another:
+//   routing (warps 0-7, barrier 1): count, publish, positions, route
+//     acquire, destinations; hand-off (barrier 3); receive tables;
+//   token (warps 8-15, barrier 2): load + amax + encode the CTA's token
+//     while the routing role counts; hand-off; store the copies while the
+//     routing role builds the receive tables.
+// Then the whole CTA signals, fills the receive metadata and waits.
+// Eligible when the row fits the token role's registers (<= 2 chunks per
+// thread) and every route id fits the staging area (host checks).
+constexpr int kRouteRole = kThreads / 2;
+
+__device__ __forceinline__ void named_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+template <int SRC, int ELEM>
+__global__ void __launch_bounds__(kThreads, 1)
+k_dispatch_roles(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, int64_t n,
+                 const int64_t* __restrict__ routes, uint64_t timeout_ns) {
+  extern __shared__ __align__(16) uint8_t dsm[];
+  __shared__ Shared sh;
+  __shared__ uint32_t skip, fail;  // routing -> token: no stores / route acquire failed
+  Flags* f = flags_of(b.region, s);
+  const uint64_t step = cur_step(f);
+  const int cta = blockIdx.x, ncta = gridDim.x;
+  uint32_t* hist = reinterpret_cast<uint32_t*>(dsm);
+  uint32_t* C = reinterpret_cast<uint32_t*>(dsm + cmat_offset(s));
+  int* rt = reinterpret_cast<int*>(dsm + recv_offset(s));
+  const bool solo = s.ranks == 1;
+  stamp(b, 0);
+  if (threadIdx.x >= kRouteRole) {
+    const Grp tg{(int)threadIdx.x - kRouteRole, kThreads - kRouteRole, 2};
+    RowRaw raw;
+    RowRegs pre;
+    load_row_raw<SRC, ELEM>(x, cta, s.hidden, s.payload_bytes, raw, tg);
+    finish_row_regs<SRC, ELEM>(raw, pre, sh.red, tg);
+    if (b.prof && tg.tid == 0) b.prof[blockIdx.x * 32 + 1] = globaltimer();
+    named_sync(3, kThreads);  // destinations are in sh.dstp
+    if (!skip) store_row_regs<SRC, ELEM>(pre, s.hidden, s.scales, sh.dstp, s.topk, tg);
+    if (b.prof && tg.tid == 0) b.prof[blockIdx.x * 32 + 20] = globaltimer();
+  } else {
+    const Grp rg{(int)threadIdx.x, kRouteRole, 1};
+    const uint32_t pd = prefetch_dirty(s, b.dirty, cta, ncta, rg);
+    const uint32_t bad = route_counts_direct(s, routes, n, hist, reinterpret_cast<int32_t*>(hist + s.experts),
+                                             b.rank_scratch, cta, ncta, sh, b, rg);
+    stamp(b, 14);
+    route_publish(s, b.peers, f, hist, step, n, bad, cta, ncta, rg);
+    own_positions(s, hist, b.pos, bad, sh, rg);
+    for (int q = rg.tid; q < s.ranks; q += rg.nt) sh.cnt[q] = 0;
+    stamp(b, 2);
+    const uint32_t* Cm = hist;
+    bool ok = true;
+    if (!solo) {
+      ok = wait_routes(s, f, route_of(b.region, s, (int)(step & 1)), C, step, timeout_ns, sh, rg);
+      Cm = C;
+    } else {
+      rg.sync();  // counters zeroed before own_dests adds to them
+    }
+    stamp(b, 3);
+    if (ok && !bad) own_dests(s, Cm, b.peers, b.gidx, sh, rg);
+    if (rg.tid == 0) {
+      skip = (!ok || bad) ? 1u : 0u;
+      fail = ok ? 0u : 1u;
+    }
+    named_sync(3, kThreads);
+    stamp(b, 15);
+    if (ok) {
+      recv_tables_body<true>(s, Cm, rt, b.info, cta, sh, b, rg);
+      if (!solo && cta == 0 && rg.tid == 0) f->tok_target += (uint64_t)recv_carve(s, rt).tot[1];
+      stamp(b, 4);
+      // receive metadata while the token role's stores drain
+      recv_rows_body(s, rt, b.rows, b.sources, b.ret_slot, grouped_of(b.region, s), b.dirty, b.send_list,
+                     &f->send_cnt, cta, ncta, rg, pd);
+    }
+    stamp(b, 7);
+  }
+  __syncthreads();  // stores issued, receive tables and rows built
+  if (fail) {
+    if (cta == 0) publish_err(f, b.info, s.local_experts);
+    return;
+  }
+  stamp(b, 5);
+  if (!solo) signal_counts(s, b.peers, offsetof(Flags, tok_ctr), sh);
+  stamp(b, 6);
+  if (cta == 0) {
     if (!solo) wait_tokens(f, b.info, s.local_experts, timeout_ns);
     else publish_err(f, b.info, s.local_experts);
   }
@@ -1373,12 +1520,20 @@ int txb_moe_dispatch_fused(const txb_moe_shape* s, const txb_moe_bufs* b, const 
           ((uintptr_t)x % salign == 0) && ((int64_t)s->hidden * srcb % salign == 0);
   }
   const bool decode = n >= 1 && n <= sms && s->topk <= kMaxOwn && vec && nchunk <= 2 * kThreads;
+  // two warp roles when the token fits the token role's registers
+  const bool roles = decode && nchunk <= 2 * (kThreads - kRouteRole);
   const int want = (int)(n < 1 ? 1 : (n < sms ? n : sms));
   // decode: the route ids of the whole batch are staged after the histogram
   const size_t rv_end = (size_t)(s->experts + n * s->topk) * 4 + 16;
   const size_t smem_d = smem > rv_end ? smem : rv_end;
 #define TXB_F(SRC, ELEM)                                                                            \
   do {                                                                                              \
+    if (roles) {                                                                                    \
+      auto kr = k_dispatch_roles<SRC, ELEM>;                                                        \
+      if (int rc = set_smem(kr, smem_d)) return rc;                                                 \
+      if (coop_grid(kr, s->device, smem_d, want) == want)                                           \
+        return launch(kr, want, kThreads, smem_d, st, true, *s, *b, x, n, routes, timeout_ns);      \
+    }                                                                                               \
     if (decode) {                                                                                   \
       auto kd = k_dispatch_fused<SRC, ELEM, true>;                                                  \
       if (int rc = set_smem(kd, smem_d)) return rc;                                                 \

@@ -51,21 +51,21 @@ __device__ __forceinline__ float load_val(const void* x, int src, int64_t off) {
 }
 
 // Block-wide max of non-negative floats; every thread gets the result.
-__device__ __forceinline__ float block_max(float v, float* red) {
-  const int tid = threadIdx.x, nt = blockDim.x;
+__device__ __forceinline__ float block_max(float v, float* red, const Grp& g = Grp::cta()) {
+  const int tid = g.tid, nt = g.nt;
 #pragma unroll
   for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
   if ((tid & 31) == 0) red[tid >> 5] = v;
-  __syncthreads();
+  g.sync();
   if (tid < 32) {
     float a = tid < ((nt + 31) >> 5) ? red[tid] : 0.f;
 #pragma unroll
     for (int o = 16; o; o >>= 1) a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, o));
     if (tid == 0) red[32] = a;
   }
-  __syncthreads();
+  g.sync();
   const float r = red[32];
-  __syncthreads();
+  g.sync();
   return r;
 }
 
@@ -202,8 +202,9 @@ struct RowRaw {
 };
 
 template <int SRC, int ELEM>
-__device__ __forceinline__ void load_row_raw(const void* x, int64_t t, int H, int64_t P, RowRaw& rr) {
-  const int tid = threadIdx.x, nt = blockDim.x;
+__device__ __forceinline__ void load_row_raw(const void* x, int64_t t, int H, int64_t P, RowRaw& rr,
+                                             const Grp& g = Grp::cta()) {
+  const int tid = g.tid, nt = g.nt;
   rr.ok = false;
   if constexpr (SRC == TXB_SRC_ROWS) {
     const uint8_t* src = reinterpret_cast<const uint8_t*>(x) + t * P;
@@ -244,8 +245,8 @@ __device__ __forceinline__ void load_row_raw(const void* x, int64_t t, int H, in
 
 // Finish a raw row into encoded chunks (per-row amax reduce for fp8).
 template <int SRC, int ELEM>
-__device__ void finish_row_regs(const RowRaw& rr, RowRegs& r, float* red) {
-  const int tid = threadIdx.x, nt = blockDim.x;
+__device__ void finish_row_regs(const RowRaw& rr, RowRegs& r, float* red, const Grp& g = Grp::cta()) {
+  const int tid = g.tid, nt = g.nt;
   r.ok = rr.ok;
   r.nchunk = rr.nchunk;
   r.scale = 1.0f;
@@ -274,7 +275,7 @@ __device__ void finish_row_regs(const RowRaw& rr, RowRegs& r, float* red) {
       }
     }
     if constexpr (ELEM == 1) {
-      amax = block_max(amax, red);
+      amax = block_max(amax, red, g);
       r.scale = amax > 0.f ? __fdiv_rn(amax, 448.0f) : 1.0f;  // kernels.py:133-134
     }
 #pragma unroll
@@ -285,8 +286,9 @@ __device__ void finish_row_regs(const RowRaw& rr, RowRegs& r, float* red) {
 
 // Store a RowRegs row to nd destination rows (plus the scale slots).
 template <int SRC, int ELEM>
-__device__ void store_row_regs(const RowRegs& r, int H, int scales, uint8_t* const* dst, int nd) {
-  const int tid = threadIdx.x, nt = blockDim.x;
+__device__ void store_row_regs(const RowRegs& r, int H, int scales, uint8_t* const* dst, int nd,
+                               const Grp& g = Grp::cta()) {
+  const int tid = g.tid, nt = g.nt;
 #pragma unroll
   for (int u = 0; u < 2; ++u) {
     const int c = tid + u * nt;

@@ -30,6 +30,8 @@ ap.add_argument("--config", default="decode")
 ap.add_argument("--reps", type=int, default=50)
 ap.add_argument("--mode", default="graph", choices=["graph", "eager", "empty"])
 ap.add_argument("--noflush", action="store_true")
+ap.add_argument("--mid", action="store_true", help="a %globaltimer kernel between dispatch and combine")
+ap.add_argument("--sleep", type=int, default=0, help="GPU sleep cycles queued before the graph (host runs ahead)")
 a = ap.parse_args()
 
 world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -64,6 +66,8 @@ sid = C.c_void_p(stream.cuda_stream)
 def step():
     rk.dispatch_send(xd, rd, sync=False)
     rk.dispatch_recv(sync=False)
+    if a.mid:
+        _lib.call("txb_globaltimer", C.c_void_p(gt.data_ptr() + 24), sid)
     rk.combine_send(y)
     rk.combine_recv(wd, out_dtype=torch.bfloat16, sync=False)
 
@@ -91,9 +95,9 @@ else:
     run = g.replay
 rows = []
 detail = []
-ORDER = [0, 19, 14, 1, 2, 3, 15, 5, 16, 17, 18, 4, 6, 7, 8, 9, 10, 11, 12, 13]
+ORDER = [0, 19, 14, 1, 2, 3, 15, 20, 16, 17, 18, 4, 7, 5, 6, 8, 9, 10, 11, 12, 13]
 STAMP = {0: "start", 19: "own routes in", 14: "counted(+loads)", 1: "encoded", 2: "published+pos", 3: "routes-in", 15: "dests",
-         5: "stored", 16: "T:loaded", 17: "T:srcpre", 18: "T:scan", 4: "tables", 6: "signalled", 7: "metadata", 8: "tokens-in", 9: "c:start", 10: "c:sent",
+         5: "joined", 20: "tok stored", 16: "T:loaded", 17: "T:srcpre", 18: "T:scan", 4: "tables", 6: "signalled", 7: "metadata", 8: "tokens-in", 9: "c:start", 10: "c:sent",
          11: "c:signalled", 12: "c:reduced", 13: "c:end"}
 for k in range(a.reps + 5):
     if not a.noflush:
@@ -103,6 +107,8 @@ for k in range(a.reps + 5):
     _lib.call("txb_globaltimer", C.c_void_p(gt.data_ptr() + 16), sid)   # barrier done
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     prof.zero_()
+    if a.sleep:
+        torch.cuda._sleep(a.sleep)
     e0.record(stream)
     run()
     e1.record(stream)
@@ -122,15 +128,15 @@ for k in range(a.reps + 5):
         return (v.max() - base) / 1e3 if v.size else np.nan
 
     det = []
-    for k in ORDER:
-        v = p[:, k][p[:, k] > 0]
+    for kk in ORDER:
+        v = p[:, kk][p[:, kk] > 0]
         det.append(((np.median(v) - base) / 1e3, (v.max() - base) / 1e3) if v.size else (np.nan, np.nan))
     detail.append(det)
     rows.append([e0.elapsed_time(e1) * 1e3, (t[2] - base) / 1e3, lo(0), hi(3), hi(8), lo(9), hi(11), hi(13),
-                 (t[1] - base) / 1e3])
+                 (t[1] - base) / 1e3, (t[3] - base) / 1e3 if a.mid else np.nan])
 med = np.median(np.asarray(rows), axis=0).tolist()
 names = ["event_span", "barrier_done", "disp_start", "routes_in_last", "disp_end", "comb_start",
-         "comb_signalled_last", "comb_end", "graph_end"]
+         "comb_signalled_last", "comb_end", "graph_end", "mid_stamp"]
 mine = dict(zip(names, [round(v, 2) for v in med]))
 allr = [None] * world
 if world > 1:
