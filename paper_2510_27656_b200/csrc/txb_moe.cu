@@ -812,6 +812,7 @@ __device__ void combine_send_rows(const txb_moe_shape& s, Flags* f, const uint8_
                                   void* const* peers, const int64_t* sources, const int32_t* ret,
                                   const int32_t* send_list, int cta, int ncta, Shared& sh) {
   const int N = s.ranks, tid = threadIdx.x;
+  #pragma unroll 1
   for (int q = tid; q < N; q += blockDim.x) sh.cnt[q] = 0;
   __syncthreads();
   if (N == 1) return;  // every row is this rank's own: read in place by C2
@@ -823,6 +824,7 @@ __device__ void combine_send_rows(const txb_moe_shape& s, Flags* f, const uint8_
   if (vec) {
     const int cpr = (int)((Pc + kChunk - 1) / kChunk);
     const int items = total * cpr;
+    #pragma unroll 1
     for (int it = cta * nwarp + warp; it < items; it += ncta * nwarp) {
       const int r = it / cpr, c = it - r * cpr;
       const int g = send_list[r];
@@ -841,6 +843,7 @@ __device__ void combine_send_rows(const txb_moe_shape& s, Flags* f, const uint8_
     }
     return;
   }
+  #pragma unroll 1
   for (int r = cta * nwarp + warp; r < total; r += ncta * nwarp) {
     const int g = send_list[r];
     const int q = (int)sources[g];
@@ -889,6 +892,7 @@ __device__ bool combine_reduce(const txb_moe_shape& s, Flags* f, const uint8_t* 
     return true;
   }
   if (!wait()) return false;
+  #pragma unroll 1
   for (int64_t t = cta; t < n; t += ncta) {
     if (t != cta) {
       combine_prep(ct, comb, Pc, out, ld, pos, gidx, w, t, R);
@@ -915,6 +919,7 @@ __device__ void end_of_step(const txb_moe_shape& s, void* const* peers, Flags* f
       f->send_cnt = 0;
       *reinterpret_cast<volatile uint64_t*>(&f->step) = step;
       fence_release(s.single_device);
+      #pragma unroll 1
       for (int q = 0; q < s.ranks; ++q) st_relaxed_sys(&flags_of(peers[q], s)->done[s.me], step);
     }
   }
