@@ -92,23 +92,45 @@ def _inputs(wl: dict, rank: int, tokens: int, seed: int = 0):
 # ------------------------------------------------------------ CPU baseline
 
 
-def cpu_port_step(ospec, cspec, x_bf16_f32, routes, w, mo):
-    """One step of the reference algorithm on the host (oracle port):
-    encode -> dispatch regroup -> expert stand-in in bf16 -> combine return
-    -> fp32 weighted sum -> bf16 out."""
-    pay = mo.encode_tokens(ospec, x_bf16_f32)
+def cpu_port_step(ospec, cspec, xb, routes, w, outs, mo, pool=None, nthr: int = 1):
+    """One step of the reference algorithm on the host (oracle port), the
+    same work the GPU step times: encode the bf16 values to fp8 rows ->
+    dispatch regroup -> return the (given) expert output rows -> fp32
+    weighted sum -> bf16 out.  The per-token parts (encode, decode + sum,
+    bf16 rounding) run in `nthr` row chunks on a thread pool (numpy drops the
+    GIL inside its array kernels); the regroup is one vectorised gather."""
+    n = xb.shape[0]
+    chunks = [c for c in np.array_split(np.arange(n), nthr) if c.size]
+    run = (lambda f, xs: list(pool.map(f, xs))) if pool is not None else (lambda f, xs: [f(c) for c in xs])
+    pay = np.concatenate(run(lambda c: mo.encode_tokens(ospec, xb[c]), chunks))
     res = mo.dispatch(ospec, [routes], [pay])
-    g = res.ranks[0].grouped
-    y = mo.decode_tokens(ospec, g.data)
-    outs = [mo.bf16_encode(y).view(np.uint8).reshape(y.shape[0], -1)]
-    comb = mo.combine(ospec, res, outs, [w], comb_spec=cspec)[0]
-    return mo.bf16_encode(comb)
+    rr = res.ranks[0]
+    valid = np.nonzero(rr.grouped.rows >= 0)[0]
+    send = np.zeros((max(1, rr.pos.size), cspec.payload_bytes), np.uint8)
+    send[rr.src_slot[valid]] = outs[valid]
+    R = rr.pos.shape[1]
+
+    def reduce(c):
+        y = mo.decode_tokens(cspec, send[rr.pos[c].ravel()])
+        return mo.bf16_encode(mo.weighted_combine(y, np.arange(c.size * R).reshape(c.size, R), w[c]))
+
+    return np.concatenate(run(reduce, chunks))
+
+
+def _host_threads() -> int:
+    try:
+        return max(1, len(os.sched_getaffinity(0)))
+    except AttributeError:
+        return max(1, os.cpu_count() or 1)
 
 
 def cpu_baseline(wl: dict, tokens: int, seconds: float) -> dict:
-    """The oracle port timed on the host (one thread), EP=1, on a bounded
-    sample: the full step when it is short, else a 512-token slice scaled
-    linearly to the step's token count (stated in `sample`)."""
+    """The oracle port timed on the host with every host thread (row chunks
+    on a thread pool), EP=1, on a bounded sample: the full step when it is
+    short, else a 512-token slice scaled linearly to the step's token count
+    (stated in `sample`).  The result is checked against the serial oracle
+    once before timing."""
+    from concurrent.futures import ThreadPoolExecutor
     from oracle import moe_oracle as mo
     sample = min(tokens, 512)
     E, R, H = wl["experts"], wl["topk"], wl["hidden"]
@@ -116,19 +138,29 @@ def cpu_baseline(wl: dict, tokens: int, seconds: float) -> dict:
     cspec = mo.Spec(1, E, sample, R, hidden=H, elem_size=2, scales=0)
     x, routes, w = _inputs(wl, 0, sample)
     xb = mo.bf16_decode(mo.bf16_encode(x))
-    cpu_port_step(ospec, cspec, xb, routes, w, mo)  # warm
-    times = []
-    t_end = time.perf_counter() + seconds
-    while time.perf_counter() < t_end or len(times) < 3:
-        t0 = time.perf_counter()
-        cpu_port_step(ospec, cspec, xb, routes, w, mo)
-        times.append((time.perf_counter() - t0) * 1e6)
+    # synthetic expert outputs (bf16 rows), like the GPU step's
+    rows = mo.dispatch(ospec, [routes], [mo.encode_tokens(ospec, xb)]).ranks[0].grouped.rows.size
+    outs = mo.bf16_encode(np.random.default_rng(5).standard_normal((rows, H)).astype(np.float32))
+    outs = outs.view(np.uint8).reshape(rows, -1)
+    nthr = _host_threads()
+    with ThreadPoolExecutor(nthr) as pool:
+        got = cpu_port_step(ospec, cspec, xb, routes, w, outs, mo, pool, nthr)  # warm
+        res = mo.dispatch(ospec, [routes], [mo.encode_tokens(ospec, xb)])
+        want = mo.bf16_encode(mo.combine(ospec, res, [outs], [w], comb_spec=cspec)[0])
+        assert np.array_equal(got, want), "threaded port differs from the serial oracle"
+        times = []
+        t_end = time.perf_counter() + seconds
+        while time.perf_counter() < t_end or len(times) < 3:
+            t0 = time.perf_counter()
+            cpu_port_step(ospec, cspec, xb, routes, w, outs, mo, pool, nthr)
+            times.append((time.perf_counter() - t0) * 1e6)
     v = statistics.median(times) * tokens / sample
     what = (f"{len(times)} full EP=1 steps" if sample == tokens else
             f"{len(times)} EP=1 steps on a {sample}-token slice, scaled x{tokens / sample:g} to {tokens} tokens")
-    return {"value": round(v, 1), "unit": "us", "cores": 1, "kind": "port",
+    return {"value": round(v, 1), "unit": "us", "cores": nthr, "kind": "port",
             "sample": f"{what} ({wl['name']}, H={H}, E={E}, top-{R}); numpy oracle port "
-                      f"(oracle/moe_oracle.py), single thread, p50"}
+                      f"(oracle/moe_oracle.py): fp8 encode, regroup, return of given bf16 expert rows, "
+                      f"fp32 weighted sum, bf16 out; row chunks on {nthr} threads, p50"}
 
 
 # ------------------------------------------------------------ clocks

@@ -104,3 +104,12 @@ def test_trace_recorder_roundtrip(tmp_path):
     assert rows[1]["used"] == 3 and rows[3]["label"] == "moe.comb" and rows[3]["transfer_id"] == 7
     off = TraceRecorder("e1", enabled=False)
     assert off.record("x") is None and len(off) == 0
+
+
+def test_cpu_baseline_threaded_port_matches_oracle():
+    """The reference arm's threaded oracle port (bench.cpu_baseline) checks
+    itself against the serial oracle before timing; run it on a small shape."""
+    import bench
+    wl = dict(bench.WORKLOADS["decode"], tokens=16, experts=16, hidden=256, scales=4)
+    r = bench.cpu_baseline(wl, 16, 0.05)
+    assert r["kind"] == "port" and r["cores"] >= 1 and r["value"] > 0
