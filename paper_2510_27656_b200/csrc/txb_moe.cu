@@ -128,6 +128,8 @@ __device__ uint32_t route_counts_direct(const txb_moe_shape& s, const int64_t* r
   g.sync();
   stamp(bufs, 19);
   const bool lanes = (32 % R) == 0;
+  const bool rstep = (nt % R) == 0;
+  const int j0 = tid % R;
   #pragma unroll 1
   for (int base = 0, u = 0; base < m; base += nt, ++u) {
     const int i = base + tid;
@@ -143,11 +145,19 @@ __device__ uint32_t route_counts_direct(const txb_moe_shape& s, const int64_t* r
     const bool in_range = v >= 0 && v < E;
     // int32 ids; out-of-range entries get lane-unique negatives (no false dups)
     const int v32 = in_range ? (int)v : -1 - (tid & 31);
-    const int j = i % R;
+    // copy index within the token; constant per thread when R | nt
+    const int j = rstep ? j0 : i % R;
     bool dup = false;
     if (lanes) {
+#pragma unroll
+      for (int jj = 1; jj < 8; ++jj) {
+        if (jj < R) {
+          const int w = __shfl_up_sync(0xffffffffu, v32, jj);
+          dup |= (jj <= j) && (w == v32);
+        }
+      }
       #pragma unroll 1
-      for (int jj = 1; jj < R; ++jj) {
+      for (int jj = 8; jj < R; ++jj) {
         const int w = __shfl_up_sync(0xffffffffu, v32, jj);
         dup |= (jj <= j) && (w == v32);
       }
@@ -165,12 +175,14 @@ __device__ uint32_t route_counts_direct(const txb_moe_shape& s, const int64_t* r
     atomicAdd(&hist[v32], 1u);
   }
   g.sync();
+  stamp(bufs, 22);
   {
     const int lane = tid & 31, warp = tid >> 5, nwarp = nt >> 5;
     #pragma unroll 1
     for (int k = warp; k < nw; k += nwarp) {
       const int e = sh.own_e[k], lim = sh.own_i[k];
       int cnt = 0;
+#pragma unroll 8
       for (int b0 = 0; b0 < lim; b0 += 32) {
         const int q = b0 + lane;
         cnt += __popc(__ballot_sync(0xffffffffu, q < lim && rv[q] == e));
@@ -748,10 +760,18 @@ __device__ __forceinline__ void recv_rows_body(const txb_moe_shape& s, int* sm, 
   int it = 0;
   #pragma unroll 1
   for (int g = cta * nwarp + warp; g < padded_total; g += ncta * nwarp, ++it) {
-    int lo = 0, hi = L - 1;  // last le with gstart[le] <= g
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (t.gstart[mid] <= g) lo = mid; else hi = mid - 1;
+    // last le with gstart[le] <= g: the warp tests 32 candidates per round
+    // (two rounds for L <= 1024) instead of a serial binary search
+    int lo = 0, span = L;
+    #pragma unroll 1
+    while (span > 1) {
+      const int stp = (span + 31) >> 5;
+      const int cand = lo + lane * stp;
+      const unsigned m = __ballot_sync(0xffffffffu, cand < lo + span && t.gstart[cand] <= g);
+      const int last = 31 - __clz(m);  // lane 0 (cand = lo) always qualifies
+      const int nlo = lo + last * stp;
+      span = min(stp, lo + span - nlo);
+      lo = nlo;
     }
     const int le = lo;
     const int k = g - t.gstart[le];

@@ -89,6 +89,63 @@ def test_fused_encode_dispatch_matches_oracle(elem, src, fused):
         close_mesh(mesh)
 
 
+@pytest.mark.parametrize("topk,tokens,experts,elem,hidden", [
+    (3, 37, 48, 1, 1024),     # R does not divide 32: loaded duplicate check, i % R ranks
+    (12, 20, 64, 1, 512),     # R > 8: shuffle duplicate check past the unrolled part
+    (8, 1, 256, 1, 7168),     # a single token
+    (8, 148, 384, 1, 2048),   # as many tokens as SMs (last decode-shaped batch)
+    (5, 64, 40, 2, 2048),     # bf16 rows that fit the token role (<= 2 chunks per thread)
+    (2, 16, 8, 4, 256),       # f32 rows
+])
+def test_decode_roles_kernel_shapes(topk, tokens, experts, elem, hidden):
+    """Odd decode shapes through the fused (warp-role) dispatch: payloads,
+    rows, sources, pos and the combine bit-exact vs the oracle, two steps."""
+    spec = moe.RoutingSpec(ranks=1, experts=experts, max_tokens=tokens, topk=topk, hidden=hidden,
+                           elem_size=elem, scales=4 if elem == 1 else 0)
+    os_ = ospec_of(spec)
+    mesh = moe.build_mesh(local_engines([0]), spec)
+    rk = mesh[0]
+    try:
+        for step in range(2):
+            rng = np.random.default_rng(1000 * topk + tokens + step)
+            routes, values, weights = mo.random_step(os_, rng, tokens=tokens)
+            xb = torch.from_numpy(values[0]).to(torch.bfloat16)
+            res, _ = _oracle_round(os_, routes, [xb.float().numpy()])
+            rk.dispatch_send(xb.cuda(), torch.from_numpy(routes[0]).cuda())
+            g = rk.dispatch_recv()
+            want = res.ranks[0].grouped
+            assert np.array_equal(_np(g.data), want.data)
+            assert np.array_equal(_np(g.rows), want.rows)
+            assert np.array_equal(_np(g.sources), want.sources)
+            assert np.array_equal(rk.pos.cpu().numpy(), res.ranks[0].pos)
+            rk.combine_send(g.data)
+            out = rk.combine_recv(torch.from_numpy(weights[0]).cuda())
+            assert np.array_equal(_np(out), mo.combine(os_, res, [want.data], weights)[0])
+    finally:
+        rk.close()
+
+
+@pytest.mark.parametrize("bad", ["dup", "range"])
+def test_device_route_errors_decode_path(bad):
+    """Device-validated routes on the decode (warp-role) path: a duplicate
+    or out-of-range expert is latched and raised at dispatch_recv."""
+    spec = moe.RoutingSpec(ranks=1, experts=64, max_tokens=32, topk=8, hidden=1024, elem_size=1, scales=4)
+    mesh = moe.build_mesh(local_engines([0]), spec)
+    rk = mesh[0]
+    try:
+        routes = np.stack([np.random.default_rng(t).permutation(64)[:8] for t in range(32)]).astype(np.int64)
+        if bad == "dup":
+            routes[7, 5] = routes[7, 2]
+        else:
+            routes[30, 0] = 64
+        x = torch.randn(32, 1024, device="cuda").to(torch.bfloat16)
+        rk.dispatch_send(x, torch.from_numpy(routes).cuda())
+        with pytest.raises(ProtocolError, match="duplicate" if bad == "dup" else "out of range"):
+            rk.dispatch_recv()
+    finally:
+        rk.close()
+
+
 @pytest.mark.parametrize("fused", [True, False])
 def test_dsv3_decode_ep1_full_size(fused):
     """DeepSeek-V3 decode shape at EP=1 (128 tok, H=7168, E=256, top-8),
