@@ -267,6 +267,24 @@ __device__ __forceinline__ float2 fp8x2_to_f2(uint16_t v) {
   return __half22float2(*reinterpret_cast<__half2*>(&raw));
 }
 
+// x / s rounded to nearest even, given r = RN(1/s): a multiply and two
+// Markstein corrections (the residual x - q*s is exact in an FMA; once q is
+// within an ulp of x/s, RN(q + residual * r) is the correctly rounded
+// quotient when nothing over- or underflows).  One correction is not
+// enough: RN(x * r) can be two ulps off.  Quotients outside the safe
+// normal range, zeros, infinities and NaNs take the IEEE division.
+// Bit-identical to __fdiv_rn; checked exhaustively on the GPU through the
+// fp8 encode (tests/test_moe_gpu.py).
+static __device__ __noinline__ float div_rn_slow(float x, float s) { return __fdiv_rn(x, s); }
+
+__device__ __forceinline__ float div_rn_by(float x, float s, float r) {
+  const float q0 = __fmul_rn(x, r);
+  const float q1 = __fmaf_rn(__fmaf_rn(-q0, s, x), r, q0);
+  const float q = __fmaf_rn(__fmaf_rn(-q1, s, x), r, q1);
+  const float a = fabsf(q);
+  return (a >= 0x1p-120f && a <= 0x1p120f) ? q : div_rn_slow(x, s);
+}
+
 // bf16 RNE with the reference NaN rule 0x7FC0|hi (kernels.py:144-150).
 __device__ __forceinline__ uint16_t bf16_rne(float x) {
   uint32_t b = __float_as_uint(x);

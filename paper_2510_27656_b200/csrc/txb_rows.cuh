@@ -75,11 +75,12 @@ __device__ __forceinline__ uint4 encode_chunk(const float* v, float scale) {
   uint4 o;
   uint32_t* ow = reinterpret_cast<uint32_t*>(&o);
   if constexpr (ELEM == 1) {
-    // x / f32(scale) with an IEEE division, then e4m3 RNE satfinite
+    // x / f32(scale) correctly rounded, then e4m3 RNE satfinite
+    const float rs = __frcp_rn(scale);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const uint32_t lo = fp8x2(__fdiv_rn(v[4 * q], scale), __fdiv_rn(v[4 * q + 1], scale));
-      const uint32_t hi = fp8x2(__fdiv_rn(v[4 * q + 2], scale), __fdiv_rn(v[4 * q + 3], scale));
+      const uint32_t lo = fp8x2(div_rn_by(v[4 * q], scale, rs), div_rn_by(v[4 * q + 1], scale, rs));
+      const uint32_t hi = fp8x2(div_rn_by(v[4 * q + 2], scale, rs), div_rn_by(v[4 * q + 3], scale, rs));
       ow[q] = lo | (hi << 16);
     }
   } else if constexpr (ELEM == 2) {

@@ -416,3 +416,41 @@ def test_large_batch_generic_fused_path(tokens, experts, elem):
             assert np.array_equal(_np(out), ref)
     finally:
         rk.close()
+
+
+@pytest.mark.parametrize("amax", [1.0, 3.14159265, 0.70710677, 1e-3, 12345.678, 65504.0, 2.0 ** -60,
+                                  1.1, 1.9999999, 0.33333334, 7.77e-5, 2.5e10, 1.5, 5.0])
+def test_fp8_encode_division_exhaustive(amax):
+    """The fp8 encode divides by the per-token scale with a multiply and two
+    FMAs (div_rn_by) instead of an IEEE division.  Every f32 value x with
+    |x| <= amax (both signs; amax itself sits in each row so it sets the
+    scale) must give the same e4m3 byte as RN(x / f32(amax/448)) through
+    torch's e4m3fn cast, saturated (== the reference codec, SURVEY probe P3)."""
+    H = 4096
+    spec = moe.RoutingSpec(ranks=1, experts=8, max_tokens=1, topk=1, hidden=H, elem_size=1, scales=4)
+    a32 = np.float32(amax)
+    hi = int(a32.view(np.uint32))
+    # IEEE f32 amax/448 (numpy; torch's tensor / python-scalar multiplies by
+    # a rounded reciprocal instead) -- the scale the kernel computes
+    s = torch.tensor(np.float32(a32) / np.float32(448.0), device="cuda")
+    per = H - 1
+    chunk_rows = 1 << 14
+    step = chunk_rows * per
+    bad = 0
+    for sign in (0, 1 << 31):
+        for lo in range(0, hi + 1, step):
+            bits = torch.arange(lo, min(hi + 1, lo + step), dtype=torch.int64, device="cuda")
+            n = bits.numel()
+            rows = (n + per - 1) // per
+            pad = rows * per - n
+            bits = torch.cat([bits, torch.zeros(pad, dtype=torch.int64, device="cuda")]) | sign
+            vals = (bits.to(torch.int32)).view(torch.float32).view(rows, per)
+            x = torch.cat([torch.full((rows, 1), float(a32), device="cuda"), vals], dim=1)
+            enc = moe.encode_tokens(spec, x)
+            got = enc[:, :H]
+            assert torch.equal(enc[:, H:H + 4].contiguous().view(torch.float32).flatten(), s.expand(rows))
+            # satfinite like the reference codec: torch's e4m3fn cast does not
+            # saturate, so clamp first (RNE maps (448, 464) to 448 anyway)
+            want = (x / s).clamp(-448.0, 448.0).to(torch.float8_e4m3fn).view(torch.uint8)
+            bad += int((got != want).sum())
+    assert bad == 0, f"{bad} e4m3 bytes differ for amax={amax}"
