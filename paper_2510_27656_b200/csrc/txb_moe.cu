@@ -128,51 +128,44 @@ __device__ uint32_t route_counts_direct(const txb_moe_shape& s, const int64_t* r
   g.sync();
   stamp(bufs, 19);
   const bool lanes = (32 % R) == 0;
-  const bool rstep = (nt % R) == 0;
-  const int j0 = tid % R;
-  #pragma unroll 1
-  for (int base = 0, u = 0; base < m; base += nt, ++u) {
-    const int i = base + tid;
+  const int lane = tid & 31;
+  // lanes of this thread's token within its warp (R | 32 and R | nt: a
+  // token's copies sit in consecutive lanes of one warp in every pass)
+  const bool tok_lanes = lanes && (nt % R) == 0;
+  const unsigned tokmask = tok_lanes ? (R == 32 ? 0xffffffffu : ((1u << R) - 1u) << (lane - lane % R)) : 0u;
+  // one entry: stage its id, count it, flag range / duplicate errors
+  auto entry = [&](int i, int64_t v) {
     const bool valid = i < m;
-    int64_t v = -1;
-    if (pre_ok) {
-#pragma unroll
-      for (int q = 0; q < kPre; ++q)
-        if (q == u) v = pre[q];
-    } else if (valid) {
-      v = routes[i];
-    }
     const bool in_range = v >= 0 && v < E;
     // int32 ids; out-of-range entries get lane-unique negatives (no false dups)
-    const int v32 = in_range ? (int)v : -1 - (tid & 31);
-    // copy index within the token; constant per thread when R | nt
-    const int j = rstep ? j0 : i % R;
+    const int v32 = in_range ? (int)v : -1 - lane;
     bool dup = false;
-    if (lanes) {
-#pragma unroll
-      for (int jj = 1; jj < 8; ++jj) {
-        if (jj < R) {
-          const int w = __shfl_up_sync(0xffffffffu, v32, jj);
-          dup |= (jj <= j) && (w == v32);
-        }
-      }
-      #pragma unroll 1
-      for (int jj = 8; jj < R; ++jj) {
-        const int w = __shfl_up_sync(0xffffffffu, v32, jj);
-        dup |= (jj <= j) && (w == v32);
-      }
+    if (tok_lanes) {
+      dup = __popc(__match_any_sync(0xffffffffu, v32) & tokmask) > 1;
     } else if (valid) {
+      const int j = i % R;
       #pragma unroll 1
       for (int jj = 1; jj <= j; ++jj) dup |= routes[i - jj] == v;
     }
-    if (!valid) continue;
+    if (!valid) return;
     rv[i] = in_range ? v32 : -1;
     if (!in_range) {
       atomicOr(&sh.bad, TXB_EV_ROUTE_RANGE);
-      continue;
+      return;
     }
     if (dup) atomicOr(&sh.bad, TXB_EV_ROUTE_DUP);
     atomicAdd(&hist[v32], 1u);
+  };
+  if (pre_ok) {
+#pragma unroll
+    for (int u = 0; u < kPre; ++u)
+      if (u * nt < m) entry(u * nt + tid, pre[u]);
+  } else {
+    #pragma unroll 1
+    for (int base = 0; base < m; base += nt) {
+      const int i = base + tid;
+      entry(i, i < m ? routes[i] : -1);
+    }
   }
   g.sync();
   stamp(bufs, 22);
