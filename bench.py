@@ -521,10 +521,56 @@ def e2e_times(rk, x, routes, w, stream, flush, dev, K: int, world: int) -> dict:
 # ------------------------------------------------------------ reference arm
 
 
+def reference_live(wl: dict, tokens: int, steps: int = 3) -> dict:
+    """The unmodified reference (railtx, installed into baseline/_ref with
+    pip --no-deps; pure Python + numpy + numba) run through its own public
+    API on the host: encode_tokens -> MoeRank.dispatch_send ->
+    dispatch_recv -> combine_send (identity expert) -> combine_recv over a
+    SimFabric, one rank (moe.py:470-833).  Its payloads are fp8 or f32
+    (elem_size 2 does not exist there), so a bf16 workload runs as f32.
+    Bounded sample: at most 512 tokens, scaled linearly to the step."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "railtx").is_dir():
+        return {"unavailable": "baseline/_ref/railtx not installed (see DESIGN.md section 9)"}
+    sys.path.insert(0, str(ref))
+    try:
+        from railtx import FaultConfig, SimFabric, TransferEngine
+        from railtx import moe as rmoe
+    except Exception as exc:  # numba or numpy missing on this host
+        return {"unavailable": f"railtx import failed: {exc!r}"[:200]}
+    sample = min(tokens, 512)
+    elem, scales = (1, wl["scales"]) if wl["elem"] == 1 else (4, 0)
+    spec = rmoe.RoutingSpec(ranks=1, experts=wl["experts"], max_tokens=sample, topk=wl["topk"],
+                            hidden=wl["hidden"], elem_size=elem, scales=scales)
+    eng = TransferEngine(SimFabric(FaultConfig(mtu=1 << 20)), rails=1, name="ref0")
+    rk = rmoe.build_mesh([eng], spec, ranks_per_node=1)[0]
+    x, routes, w = _inputs(wl, 0, sample)
+    times = []
+    try:
+        for i in range(steps + 2):  # two warm-up steps (numba JIT)
+            t0 = time.perf_counter()
+            rk.dispatch_send(rmoe.encode_tokens(spec, x), routes)
+            g = rk.dispatch_recv(120.0)
+            rk.combine_send(g.data)
+            rk.combine_recv(w, 120.0)
+            if i >= 2:
+                times.append((time.perf_counter() - t0) * 1e6)
+    finally:
+        rk.close()
+        eng.close()
+    v = statistics.median(times) * tokens / sample
+    return {"value": round(v, 1), "unit": "us", "cores": 1, "kind": "reference",
+            "sample": f"{len(times)} steps of the unmodified railtx MoeRank API (baseline/_ref), EP=1 over "
+                      f"SimFabric, {sample} tokens" + (f" scaled x{tokens / sample:g}" if sample < tokens else "")
+                      + f", {'fp8' if elem == 1 else 'f32'} payloads, identity expert, p50 after 2 warm-up steps"}
+
+
 def run_reference(a) -> None:
-    """The reference's algorithm on the host cores: railtx is pure Python and
-    cannot travel to the GPU box, so the oracle port of it is timed
-    (DESIGN.md §9).  Rank 0 only; other ranks exit without work."""
+    """The reference's algorithm on the host cores, on this arm's config.
+    `value` is the oracle port of it with every host thread (the faster,
+    conservative CPU baseline); the unmodified reference from
+    baseline/_ref, run through its own API, is timed beside it
+    (`reference_live`).  Rank 0 only; other ranks exit without work."""
     world, rank, _ = _dist()
     if rank != 0:
         return
@@ -540,8 +586,9 @@ def run_reference(a) -> None:
                       "experts": wl["experts"], "topk": wl["topk"], "ep": 1},
            "cpu_baseline": cb,
            "e2e": {"value": cb["value"], "unit": "us", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-           "note": "reference railtx is pure Python and cannot travel to the GPU box; this arm times "
-                   "the oracle port of its algorithm (oracle/moe_oracle.py) on the host cores"}
+           "reference_live": reference_live(wl, tokens),
+           "note": "value: the threaded oracle port of railtx's algorithm (oracle/moe_oracle.py) on the host "
+                   "cores; reference_live: the unmodified railtx API from baseline/_ref, single thread"}
     print(json.dumps(res), flush=True)
 
 
