@@ -99,7 +99,7 @@ __device__ __forceinline__ bool spin_ge(const uint64_t* p, uint64_t target, uint
 // tok_ctr/comb_ctr receive release-adds from every peer; the rest is local.
 struct Flags {
   uint64_t route_tag[2][TXB_MAX_RANKS];  // [step parity][source] = step
-  uint64_t done[TXB_MAX_RANKS];          // [peer] = last step whose combine_send finished
+  uint64_t done[TXB_MAX_RANKS];          // [peer] = last step whose reads of this region finished (published by the peer's next route phase)
   uint64_t tok_ctr;                      // rows received (dispatch)
   uint64_t comb_ctr;                     // rows received (combine)
   uint64_t pad0[6];

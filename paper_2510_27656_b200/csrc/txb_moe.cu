@@ -398,11 +398,23 @@ __device__ void route_publish(const txb_moe_shape& s, void* const* peers, Flags*
     #pragma unroll 1
     for (int le = lane; le < L; le += 32) self += hist[s.me * L + le];
     for (int o = 16; o; o >>= 1) self += __shfl_xor_sync(0xffffffffu, self, o);
-    // per-source step tags for host-side gating / diagnostics only
+    // per-source step tags (host-side gating / diagnostics), and the
+    // buffer-reuse barrier of the previous step (moe.dbar): every read this
+    // rank made of its buffers in step-1 finished before this kernel began
+    // (stream order), so peers may now overwrite them.  Publishing it here
+    // rather than at the end of the combine keeps a system-scope fence and
+    // N remote stores off the step's tail; peers wait for it together with
+    // this step's route words, which they need anyway.
     #pragma unroll 1
     for (int d = lane; d < N; d += 32) {
-      if (N == 1) flags_of(peers[d], s)->route_tag[slot][s.me] = step;
-      else st_relaxed_sys(&flags_of(peers[d], s)->route_tag[slot][s.me], step);
+      Flags* pf = flags_of(peers[d], s);
+      if (N == 1) {
+        pf->route_tag[slot][s.me] = step;
+        pf->done[s.me] = step - 1;
+      } else {
+        st_relaxed_sys(&pf->route_tag[slot][s.me], step);
+        st_relaxed_sys(&pf->done[s.me], step - 1);
+      }
     }
     if (lane == 0) {
       f->comb_target += bad ? 0 : (uint64_t)(n * s.topk) - self;
@@ -876,7 +888,8 @@ __device__ void combine_send_rows(const txb_moe_shape& s, Flags* f, const uint8_
 template <int ELEM>
 __device__ bool combine_reduce(const txb_moe_shape& s, Flags* f, const uint8_t* comb, const uint8_t* out,
                                int64_t ld, const int64_t* pos, const int32_t* gidx, const float* w, int64_t n,
-                               void* dst, int out_bf16, uint64_t timeout_ns, int cta, int ncta, Shared& sh) {
+                               void* dst, int out_bf16, uint64_t timeout_ns, int cta, int ncta, Shared& sh,
+                               uint64_t* prof = nullptr) {
   __shared__ CombTok ct;
   const int64_t Pc = s.comb_bytes;
   const int H = s.hidden, R = s.topk;
@@ -894,6 +907,7 @@ __device__ bool combine_reduce(const txb_moe_shape& s, Flags* f, const uint8_t* 
         sh.fail = spin_ge(&f->comb_ctr, f->comb_target, dl) ? 0u : TXB_EV_WAIT_COMBINE;
         if (sh.fail) atomicOr(&f->err, sh.fail);
       }
+      if (prof) prof[blockIdx.x * 32 + 23] = globaltimer();
     }
     __syncthreads();
     return sh.fail == 0;
@@ -917,23 +931,18 @@ __device__ bool combine_reduce(const txb_moe_shape& s, Flags* f, const uint8_t* 
   return true;
 }
 
-// End of step: the last CTA (ticket) publishes the barrier tag to every peer
-// ("all my reads of this step's buffers are done", moe.dbar) and advances
-// the local step counter.
-__device__ void end_of_step(const txb_moe_shape& s, void* const* peers, Flags* f, uint64_t step, int ncta) {
+// End of step: the last CTA (ticket) resets the step's scratch counters and
+// advances the local step counter.  The buffer-reuse barrier tag (done) is
+// published by the next step's route phase (route_publish), so the tail of
+// the combine carries no fence and no remote store.
+__device__ void end_of_step(Flags* f, uint64_t step, int ncta) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    // EP>1: this CTA's reads of the step's buffers happen before the peers
-    // may reuse them; EP=1 has no peers and the kernel boundary orders the rest
-    if (s.ranks > 1) __threadfence();
     const uint32_t t = atomicAdd(&f->ticket, 1u);
     if (t == (uint32_t)ncta - 1) {
       f->ticket = 0;
       f->send_cnt = 0;
       *reinterpret_cast<volatile uint64_t*>(&f->step) = step;
-      fence_release(s.single_device);
-      #pragma unroll 1
-      for (int q = 0; q < s.ranks; ++q) st_relaxed_sys(&flags_of(peers[q], s)->done[s.me], step);
     }
   }
 }
@@ -1005,7 +1014,7 @@ k_comb_recv(txb_moe_shape s, txb_moe_bufs b, const uint8_t* __restrict__ out, in
   const uint64_t step = cur_step(f);
   combine_reduce<ELEM>(s, f, comb_of(b.region, s), out, ld, b.pos, b.gidx, w, n, dst, out_bf16, timeout_ns,
                        blockIdx.x, gridDim.x, sh);
-  end_of_step(s, b.peers, f, step, gridDim.x);
+  end_of_step(f, step, gridDim.x);
 }
 
 // ------------------------------------------------------------ fused kernels
@@ -1235,9 +1244,9 @@ k_combine_fused(txb_moe_shape s, txb_moe_bufs b, const uint8_t* __restrict__ out
   __syncthreads();
   stamp(b, 11);
   combine_reduce<ELEM>(s, f, comb_of(b.region, s), out, ld, b.pos, b.gidx, w, n, dst, out_bf16, timeout_ns,
-                       blockIdx.x, gridDim.x, sh);
+                       blockIdx.x, gridDim.x, sh, b.prof);
   stamp(b, 12);
-  end_of_step(s, b.peers, f, step, gridDim.x);
+  end_of_step(f, step, gridDim.x);
   stamp(b, 13);
 }
 
