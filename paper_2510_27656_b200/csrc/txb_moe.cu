@@ -50,6 +50,12 @@ constexpr int kMaxOwn = 64;        // copies per CTA of the direct-count path
 
 __device__ __forceinline__ int pad_up(int x) { return (x + kGroupPad - 1) / kGroupPad * kGroupPad; }
 
+// Programmatic dependent launch (sm_90+): let the next kernel on the stream
+// be scheduled now / wait for the previous one to complete.  Both are no-ops
+// when the launch carries no programmatic dependency.
+__device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // Optional phase stamps for profiling (txb_moe_bufs.prof, [grid][32]).
 __device__ __forceinline__ void stamp(const txb_moe_bufs& b, int k) {
   if (b.prof && threadIdx.x == 0) b.prof[blockIdx.x * 32 + k] = globaltimer();
@@ -76,6 +82,11 @@ __host__ __device__ inline size_t cmat_offset(const txb_moe_shape& s) {
   return recv_offset(s) + (smem_recv(s.ranks, s.local_experts) + 15) / 16 * 16;
 }
 
+// decode, one rank: [histogram E | staged ids n*R] then the receive tables
+__host__ __device__ inline size_t solo_recv_offset(const txb_moe_shape& s, int64_t n) {
+  return ((size_t)(s.experts + n * s.topk) * 4 + 16 + 15) / 16 * 16;
+}
+
 struct Shared {  // static shared state of one CTA
   uint32_t bad, fail, recv_me, direct;
   int tmp[33];
@@ -97,9 +108,29 @@ struct Shared {  // static shared state of one CTA
 // entries of shared memory).  Validation (moe.py:142-155): range, and
 // duplicates within a token -- R-1 shuffles when R divides 32 (a token's
 // copies sit in consecutive lanes), loads otherwise.
+// Stable rank of each of this CTA's nw copies: one warp per copy counts the
+// earlier entries of the batch with the same expert (ballots over rv).
+__device__ __forceinline__ void own_ranks(const int32_t* rv, int32_t* rank_out, int nw, Shared& sh, const Grp& g) {
+  const int lane = g.tid & 31, warp = g.tid >> 5, nwarp = g.nt >> 5;
+  #pragma unroll 1
+  for (int k = warp; k < nw; k += nwarp) {
+    const int e = sh.own_e[k], lim = sh.own_i[k];
+    int cnt = 0;
+#pragma unroll 8
+    for (int b0 = 0; b0 < lim; b0 += 32) {
+      const int q = b0 + lane;
+      cnt += __popc(__ballot_sync(0xffffffffu, q < lim && rv[q] == e));
+    }
+    if (lane == 0) rank_out[lim] = cnt;
+    if (lane == 0) sh.own_rank[k] = (uint32_t)cnt;
+  }
+}
+
+// with_ranks = false: histogram, staging and validation only (the caller
+// runs own_ranks on another warp group).
 __device__ uint32_t route_counts_direct(const txb_moe_shape& s, const int64_t* routes, int64_t n, uint32_t* hist,
                                         int32_t* rv, int32_t* rank_out, int cta, int ncta, Shared& sh,
-                                        const txb_moe_bufs& bufs, const Grp& g) {
+                                        const txb_moe_bufs& bufs, const Grp& g, bool with_ranks = true) {
   const int E = s.experts, R = s.topk, tid = g.tid;
   const int m = (int)(n * R);
   const int nmine = n > cta ? (int)((n - cta + ncta - 1) / ncta) : 0;
@@ -169,21 +200,7 @@ __device__ uint32_t route_counts_direct(const txb_moe_shape& s, const int64_t* r
   }
   g.sync();
   stamp(bufs, 22);
-  {
-    const int lane = tid & 31, warp = tid >> 5, nwarp = nt >> 5;
-    #pragma unroll 1
-    for (int k = warp; k < nw; k += nwarp) {
-      const int e = sh.own_e[k], lim = sh.own_i[k];
-      int cnt = 0;
-#pragma unroll 8
-      for (int b0 = 0; b0 < lim; b0 += 32) {
-        const int q = b0 + lane;
-        cnt += __popc(__ballot_sync(0xffffffffu, q < lim && rv[q] == e));
-      }
-      if (lane == 0) rank_out[lim] = cnt;
-      if (lane == 0) sh.own_rank[k] = (uint32_t)cnt;
-    }
-  }
+  if (with_ranks) own_ranks(rv, rank_out, nw, sh, g);
   const uint32_t b = sh.bad;
   if (b)
     #pragma unroll 1
@@ -509,7 +526,7 @@ __device__ void own_positions(const txb_moe_shape& s, const uint32_t* hist, int6
     const int e = sh.own_e[k];
     int acc = 0;
     #pragma unroll 1
-    for (int x = lane; x < e; x += 32) acc += (int)hist[x];
+    for (int x = lane; x < (bad ? 0 : e); x += 32) acc += (int)hist[x];
     for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) pos[sh.own_i[k]] = bad ? -1 : (int64_t)acc + sh.own_rank[k];
   }
@@ -1042,6 +1059,7 @@ k_dispatch_fused(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
   int* rt = reinterpret_cast<int*>(dsm + recv_offset(s));
   const bool solo = s.ranks == 1;
   stamp(b, 0);
+  grid_dep_launch();
   if constexpr (DECODE) {
     RowRegs pre;
     RowRaw raw;
@@ -1152,7 +1170,67 @@ __device__ __forceinline__ void named_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
+//
+// SOLO (one rank): the route matrix is this CTA's histogram, so the roles
+// split differently right after it: the token role ranks its copies and
+// derives positions and destinations, then stores; the routing role
+// publishes the row and builds the receive tables and rows meanwhile.  Both
+// halves start from the histogram instead of the receive metadata waiting
+// for the destinations.
 template <int SRC, int ELEM>
+__device__ __forceinline__ void dispatch_roles_solo(const txb_moe_shape& s, const txb_moe_bufs& b, const void* x,
+                                                    int64_t n, const int64_t* routes, Flags* f, uint64_t step,
+                                                    uint8_t* dsm, Shared& sh) {
+  __shared__ uint32_t bad_s;
+  const int cta = blockIdx.x, ncta = gridDim.x;
+  uint32_t* hist = reinterpret_cast<uint32_t*>(dsm);
+  int32_t* rv = reinterpret_cast<int32_t*>(hist + s.experts);
+  // the receive tables are built while the token role still reads the
+  // staged ids: they live after them (solo_recv_offset), not over them
+  int* rt = reinterpret_cast<int*>(dsm + solo_recv_offset(s, n));
+  if (threadIdx.x >= kRouteRole) {
+    const Grp tg{(int)threadIdx.x - kRouteRole, kThreads - kRouteRole, 2};
+    RowRaw raw;
+    RowRegs pre;
+    load_row_raw<SRC, ELEM>(x, cta, s.hidden, s.payload_bytes, raw, tg);
+    finish_row_regs<SRC, ELEM>(raw, pre, sh.red, tg);
+    if (b.prof && tg.tid == 0) b.prof[blockIdx.x * 32 + 1] = globaltimer();
+    for (int q = tg.tid; q < s.ranks; q += tg.nt) sh.cnt[q] = 0;
+    named_sync(3, kThreads);  // histogram, staged ids and own copies ready
+    const uint32_t bad = bad_s;
+    const int nw = (n > cta ? (int)((n - cta + ncta - 1) / ncta) : 0) * s.topk;
+    if (!bad) {
+      own_ranks(rv, b.rank_scratch, nw, sh, tg);
+      tg.sync();
+    }
+    own_positions(s, hist, b.pos, bad, sh, tg);
+    if (!bad) {
+      own_dests(s, hist, b.peers, b.gidx, sh, tg);
+      if (b.prof && tg.tid == 0) b.prof[blockIdx.x * 32 + 15] = globaltimer();
+      store_row_regs<SRC, ELEM>(pre, s.hidden, s.scales, sh.dstp, s.topk, tg);
+    }
+    if (b.prof && tg.tid == 0) b.prof[blockIdx.x * 32 + 20] = globaltimer();
+  } else {
+    const Grp rg{(int)threadIdx.x, kRouteRole, 1};
+    const uint32_t pd = prefetch_dirty(s, b.dirty, cta, ncta, rg);
+    const uint32_t bad = route_counts_direct(s, routes, n, hist, rv, b.rank_scratch, cta, ncta, sh, b, rg, false);
+    if (rg.tid == 0) bad_s = bad;
+    named_sync(3, kThreads);
+    stamp(b, 14);
+    route_publish(s, b.peers, f, hist, step, n, bad, cta, ncta, rg);
+    recv_tables_body<true>(s, hist, rt, b.info, cta, sh, b, rg);
+    stamp(b, 4);
+    recv_rows_body(s, rt, b.rows, b.sources, b.ret_slot, grouped_of(b.region, s), b.dirty, b.send_list,
+                   &f->send_cnt, cta, ncta, rg, pd);
+    stamp(b, 7);
+  }
+  __syncthreads();
+  stamp(b, 5);
+  if (cta == 0) publish_err(f, b.info, s.local_experts);
+  stamp(b, 8);
+}
+
+template <int SRC, int ELEM, bool SOLO>
 __global__ void __launch_bounds__(kThreads, 1)
 k_dispatch_roles(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, int64_t n,
                  const int64_t* __restrict__ routes, uint64_t timeout_ns) {
@@ -1167,6 +1245,11 @@ k_dispatch_roles(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
   int* rt = reinterpret_cast<int*>(dsm + recv_offset(s));
   const bool solo = s.ranks == 1;
   stamp(b, 0);
+  grid_dep_launch();
+  if constexpr (SOLO) {
+    dispatch_roles_solo<SRC, ELEM>(s, b, x, n, routes, f, step, dsm, sh);
+    return;
+  }
   if (threadIdx.x >= kRouteRole) {
     const Grp tg{(int)threadIdx.x - kRouteRole, kThreads - kRouteRole, 2};
     RowRaw raw;
@@ -1234,6 +1317,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 k_combine_fused(txb_moe_shape s, txb_moe_bufs b, const uint8_t* __restrict__ out, int64_t ld,
                 const float* __restrict__ w, int64_t n, void* dst, int out_bf16, uint64_t timeout_ns) {
   __shared__ Shared sh;
+  grid_dep_wait();  // the producing dispatch (or expert) kernel has completed
   Flags* f = flags_of(b.region, s);
   const uint64_t step = cur_step(f);
   stamp(b, 9);
@@ -1339,9 +1423,12 @@ static int set_smem(K kernel, size_t smem) {
 
 // Launch helper; `coop` requests a cooperative launch (all CTAs resident).
 
+// `pdl` marks the launch as a programmatic dependent of the previous kernel
+// on the stream: its CTAs may be scheduled while that kernel drains, and
+// block in griddepcontrol.wait until it has completed.
 template <typename... KArgs, typename... Args>
-static int launch(void (*kernel)(KArgs...), int grid, int block, size_t smem, cudaStream_t st, bool coop,
-                  Args... args) {
+static int launch_ex(void (*kernel)(KArgs...), int grid, int block, size_t smem, cudaStream_t st, bool coop,
+                     bool pdl, Args... args) {
   if (int rc = set_smem(kernel, smem)) return rc;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -1354,10 +1441,20 @@ static int launch(void (*kernel)(KArgs...), int grid, int block, size_t smem, cu
     attr[na].id = cudaLaunchAttributeCooperative;
     attr[na++].val.cooperative = 1;
   }
+  if (pdl) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na++].val.programmaticStreamSerializationAllowed = 1;
+  }
   cfg.attrs = attr;
   cfg.numAttrs = na;
   TXB_CUDA(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
   return TXB_OK;
+}
+
+template <typename... KArgs, typename... Args>
+static int launch(void (*kernel)(KArgs...), int grid, int block, size_t smem, cudaStream_t st, bool coop,
+                  Args... args) {
+  return launch_ex(kernel, grid, block, smem, st, coop, false, args...);
 }
 
 // Largest cooperative grid for a kernel (one wave).
@@ -1553,13 +1650,15 @@ int txb_moe_dispatch_fused(const txb_moe_shape* s, const txb_moe_bufs* b, const 
   // decode: the route ids of the whole batch are staged after the histogram
   const size_t rv_end = (size_t)(s->experts + n * s->topk) * 4 + 16;
   const size_t smem_d = smem > rv_end ? smem : rv_end;
+  const size_t solo_end = solo_recv_offset(*s, n) + smem_recv(s->ranks, s->local_experts);
+  const size_t smem_r = s->ranks == 1 && solo_end > smem_d ? solo_end : smem_d;
 #define TXB_F(SRC, ELEM)                                                                            \
   do {                                                                                              \
     if (roles) {                                                                                    \
-      auto kr = k_dispatch_roles<SRC, ELEM>;                                                        \
-      if (int rc = set_smem(kr, smem_d)) return rc;                                                 \
-      if (coop_grid(kr, s->device, smem_d, want) == want)                                           \
-        return launch(kr, want, kThreads, smem_d, st, true, *s, *b, x, n, routes, timeout_ns);      \
+      auto kr = s->ranks == 1 ? k_dispatch_roles<SRC, ELEM, true> : k_dispatch_roles<SRC, ELEM, false>; \
+      if (int rc = set_smem(kr, smem_r)) return rc;                                                 \
+      if (coop_grid(kr, s->device, smem_r, want) == want)                                           \
+        return launch(kr, want, kThreads, smem_r, st, true, *s, *b, x, n, routes, timeout_ns);      \
     }                                                                                               \
     if (decode) {                                                                                   \
       auto kd = k_dispatch_fused<SRC, ELEM, true>;                                                  \
@@ -1588,8 +1687,11 @@ int txb_moe_combine_fused(const txb_moe_shape* s, const txb_moe_bufs* b, const v
 #define TXB_C(ELEM)                                                                                   \
   do {                                                                                                \
     const int grid = coop_grid(k_combine_fused<ELEM>, s->device, 0, sms);                             \
-    return launch(k_combine_fused<ELEM>, grid, kThreads, 0, st, true, *s, *b, o, ld, weights, n, out, \
-                  out_bf16, timeout_ns);                                                              \
+    /* one rank: no cross-CTA waits, so no co-residency requirement; launched */                      \
+    /* as a programmatic dependent so its CTAs land while the dispatch drains */                      \
+    const bool solo = s->ranks == 1;                                                                  \
+    return launch_ex(k_combine_fused<ELEM>, grid, kThreads, 0, st, !solo, solo, *s, *b, o, ld, weights, \
+                     n, out, out_bf16, timeout_ns);                                                   \
   } while (0)
   switch (s->comb_elem_size) {
     case 1: TXB_C(1);
