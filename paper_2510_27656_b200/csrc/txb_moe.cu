@@ -87,6 +87,10 @@ __host__ __device__ inline size_t solo_recv_offset(const txb_moe_shape& s, int64
   return ((size_t)(s.experts + n * s.topk) * 4 + 16 + 15) / 16 * 16;
 }
 
+__host__ __device__ inline size_t roles_cmat_offset(const txb_moe_shape& s, int64_t n) {
+  return solo_recv_offset(s, n) + (smem_recv(s.ranks, s.local_experts) + 15) / 16 * 16;
+}
+
 struct Shared {  // static shared state of one CTA
   uint32_t bad, fail, recv_me, direct;
   int tmp[33];
@@ -451,18 +455,33 @@ __device__ bool wait_routes(const txb_moe_shape& s, Flags* f, const uint64_t* C,
   const uint64_t dl = globaltimer() + timeout_ns;
   const uint32_t want = (uint32_t)step;
   const int NE = s.ranks * s.experts;
+  // kW words per thread per pass; every poll re-issues the loads of all the
+  // words still pending at once, so the pass ends one memory round trip
+  // after its last word lands (not one round trip per word)
+  constexpr int kW = 8;
   #pragma unroll 1
-  for (int i = g.tid; i < NE; i += g.nt) {
-    uint64_t v = ld_relaxed_sys(C + i);
+  for (int base = g.tid; base < NE; base += kW * g.nt) {
+    uint32_t pending = 0;
+#pragma unroll
+    for (int u = 0; u < kW; ++u)
+      if (base + u * g.nt < NE) pending |= 1u << u;
     uint32_t it = 0;
-    while ((uint32_t)(v >> 32) != want) {
-      if (((++it) & 255u) == 0 && globaltimer() > dl) {
+    while (pending) {
+      uint64_t v[kW];
+#pragma unroll
+      for (int u = 0; u < kW; ++u)
+        if (pending & (1u << u)) v[u] = ld_relaxed_sys(C + base + u * g.nt);
+#pragma unroll
+      for (int u = 0; u < kW; ++u)
+        if ((pending & (1u << u)) && (uint32_t)(v[u] >> 32) == want) {
+          Cs[base + u * g.nt] = (uint32_t)v[u];
+          pending &= ~(1u << u);
+        }
+      if (pending && ((++it) & 255u) == 0 && globaltimer() > dl) {
         atomicOr(&sh.fail, TXB_EV_WAIT_ROUTE);
         break;
       }
-      v = ld_relaxed_sys(C + i);
     }
-    Cs[i] = (uint32_t)v;
   }
   if (g.tid < 32)
     #pragma unroll 1
@@ -1236,20 +1255,24 @@ k_dispatch_roles(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
                  const int64_t* __restrict__ routes, uint64_t timeout_ns) {
   extern __shared__ __align__(16) uint8_t dsm[];
   __shared__ Shared sh;
-  __shared__ uint32_t skip, fail;  // routing -> token: no stores / route acquire failed
+  __shared__ uint32_t bad_s, fail;  // routing -> token: route error / route acquire failed
   Flags* f = flags_of(b.region, s);
   const uint64_t step = cur_step(f);
   const int cta = blockIdx.x, ncta = gridDim.x;
   uint32_t* hist = reinterpret_cast<uint32_t*>(dsm);
   uint32_t* C = reinterpret_cast<uint32_t*>(dsm + cmat_offset(s));
   int* rt = reinterpret_cast<int*>(dsm + recv_offset(s));
-  const bool solo = s.ranks == 1;
   stamp(b, 0);
   grid_dep_launch();
   if constexpr (SOLO) {
     dispatch_roles_solo<SRC, ELEM>(s, b, x, n, routes, f, step, dsm, sh);
     return;
   }
+  // [hist | staged ids] [receive tables] [route matrix]: the token role
+  // reads the staged ids while the routing role fills the matrix and tables
+  int32_t* rv = reinterpret_cast<int32_t*>(hist + s.experts);
+  rt = reinterpret_cast<int*>(dsm + solo_recv_offset(s, n));
+  C = reinterpret_cast<uint32_t*>(dsm + roles_cmat_offset(s, n));
   if (threadIdx.x >= kRouteRole) {
     const Grp tg{(int)threadIdx.x - kRouteRole, kThreads - kRouteRole, 2};
     RowRaw raw;
@@ -1257,38 +1280,40 @@ k_dispatch_roles(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
     load_row_raw<SRC, ELEM>(x, cta, s.hidden, s.payload_bytes, raw, tg);
     finish_row_regs<SRC, ELEM>(raw, pre, sh.red, tg);
     if (b.prof && tg.tid == 0) b.prof[blockIdx.x * 32 + 1] = globaltimer();
-    named_sync(3, kThreads);  // destinations are in sh.dstp
-    if (!skip) store_row_regs<SRC, ELEM>(pre, s.hidden, s.scales, sh.dstp, s.topk, tg);
+    for (int q = tg.tid; q < s.ranks; q += tg.nt) sh.cnt[q] = 0;
+    named_sync(3, kThreads);  // A: histogram, staged ids and own copies ready
+    const uint32_t bad = bad_s;
+    const int nw = (n > cta ? (int)((n - cta + ncta - 1) / ncta) : 0) * s.topk;
+    // ranks and send slots while the count row travels to the peers
+    if (!bad) {
+      own_ranks(rv, b.rank_scratch, nw, sh, tg);
+      tg.sync();
+    }
+    own_positions(s, hist, b.pos, bad, sh, tg);
+    named_sync(3, kThreads);  // B: route matrix acquired (or failed)
+    if (!fail && !bad) {
+      own_dests(s, C, b.peers, b.gidx, sh, tg);
+      if (b.prof && tg.tid == 0) b.prof[blockIdx.x * 32 + 15] = globaltimer();
+      store_row_regs<SRC, ELEM>(pre, s.hidden, s.scales, sh.dstp, s.topk, tg);
+    }
     if (b.prof && tg.tid == 0) b.prof[blockIdx.x * 32 + 20] = globaltimer();
   } else {
     const Grp rg{(int)threadIdx.x, kRouteRole, 1};
     const uint32_t pd = prefetch_dirty(s, b.dirty, cta, ncta, rg);
-    const uint32_t bad = route_counts_direct(s, routes, n, hist, reinterpret_cast<int32_t*>(hist + s.experts),
-                                             b.rank_scratch, cta, ncta, sh, b, rg);
+    const uint32_t bad = route_counts_direct(s, routes, n, hist, rv, b.rank_scratch, cta, ncta, sh, b, rg, false);
+    if (rg.tid == 0) bad_s = bad;
+    named_sync(3, kThreads);  // A
     stamp(b, 14);
+    // the count row goes out before this CTA ranks its copies (token role)
     route_publish(s, b.peers, f, hist, step, n, bad, cta, ncta, rg);
-    own_positions(s, hist, b.pos, bad, sh, rg);
-    for (int q = rg.tid; q < s.ranks; q += rg.nt) sh.cnt[q] = 0;
     stamp(b, 2);
-    const uint32_t* Cm = hist;
-    bool ok = true;
-    if (!solo) {
-      ok = wait_routes(s, f, route_of(b.region, s, (int)(step & 1)), C, step, timeout_ns, sh, rg);
-      Cm = C;
-    } else {
-      rg.sync();  // counters zeroed before own_dests adds to them
-    }
+    const bool ok = wait_routes(s, f, route_of(b.region, s, (int)(step & 1)), C, step, timeout_ns, sh, rg);
+    if (rg.tid == 0) fail = ok ? 0u : 1u;
+    named_sync(3, kThreads);  // B
     stamp(b, 3);
-    if (ok && !bad) own_dests(s, Cm, b.peers, b.gidx, sh, rg);
-    if (rg.tid == 0) {
-      skip = (!ok || bad) ? 1u : 0u;
-      fail = ok ? 0u : 1u;
-    }
-    named_sync(3, kThreads);
-    stamp(b, 15);
     if (ok) {
-      recv_tables_body<true>(s, Cm, rt, b.info, cta, sh, b, rg);
-      if (!solo && cta == 0 && rg.tid == 0) f->tok_target += (uint64_t)recv_carve(s, rt).tot[1];
+      recv_tables_body<true>(s, C, rt, b.info, cta, sh, b, rg);
+      if (cta == 0 && rg.tid == 0) f->tok_target += (uint64_t)recv_carve(s, rt).tot[1];
       stamp(b, 4);
       // receive metadata while the token role's stores drain
       recv_rows_body(s, rt, b.rows, b.sources, b.ret_slot, grouped_of(b.region, s), b.dirty, b.send_list,
@@ -1302,12 +1327,9 @@ k_dispatch_roles(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
     return;
   }
   stamp(b, 5);
-  if (!solo) signal_counts(s, b.peers, offsetof(Flags, tok_ctr), sh);
+  signal_counts(s, b.peers, offsetof(Flags, tok_ctr), sh);
   stamp(b, 6);
-  if (cta == 0) {
-    if (!solo) wait_tokens(f, b.info, s.local_experts, timeout_ns);
-    else publish_err(f, b.info, s.local_experts);
-  }
+  if (cta == 0) wait_tokens(f, b.info, s.local_experts, timeout_ns);
   stamp(b, 8);
 }
 
@@ -1650,8 +1672,9 @@ int txb_moe_dispatch_fused(const txb_moe_shape* s, const txb_moe_bufs* b, const 
   // decode: the route ids of the whole batch are staged after the histogram
   const size_t rv_end = (size_t)(s->experts + n * s->topk) * 4 + 16;
   const size_t smem_d = smem > rv_end ? smem : rv_end;
-  const size_t solo_end = solo_recv_offset(*s, n) + smem_recv(s->ranks, s->local_experts);
-  const size_t smem_r = s->ranks == 1 && solo_end > smem_d ? solo_end : smem_d;
+  const size_t roles_end = s->ranks == 1 ? solo_recv_offset(*s, n) + smem_recv(s->ranks, s->local_experts)
+                                         : roles_cmat_offset(*s, n) + smem_cmat(s->ranks, s->experts);
+  const size_t smem_r = roles_end > smem_d ? roles_end : smem_d;
 #define TXB_F(SRC, ELEM)                                                                            \
   do {                                                                                              \
     if (roles) {                                                                                    \
