@@ -883,10 +883,14 @@ __device__ void combine_send_rows(const txb_moe_shape& s, Flags* f, const uint8_
   const int lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
   const bool vec = (Pc % 16 == 0) && (ld % 16 == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
   if (vec) {
+    // each CTA takes one contiguous run of chunks (whole rows, in order), its
+    // warps interleaved over it: per-CTA shares equal to within one chunk,
+    // and each CTA's peer writes stay sequential
     const int cpr = (int)((Pc + kChunk - 1) / kChunk);
     const int items = total * cpr;
+    const int it1 = (int)((int64_t)items * (cta + 1) / ncta);
     #pragma unroll 1
-    for (int it = cta * nwarp + warp; it < items; it += ncta * nwarp) {
+    for (int it = (int)((int64_t)items * cta / ncta) + warp; it < it1; it += nwarp) {
       const int r = it / cpr, c = it - r * cpr;
       const int g = send_list[r];
       const int q = (int)sources[g];
@@ -1713,7 +1717,7 @@ int txb_moe_combine_fused(const txb_moe_shape* s, const txb_moe_bufs* b, const v
     /* one rank: no cross-CTA waits, so no co-residency requirement; launched */                      \
     /* as a programmatic dependent so its CTAs land while the dispatch drains */                      \
     const bool solo = s->ranks == 1;                                                                  \
-    return launch_ex(k_combine_fused<ELEM>, grid, kThreads, 0, st, !solo, solo, *s, *b, o, ld, weights, \
+    return launch_ex(k_combine_fused<ELEM>, grid, kThreads, 0, st, !solo, true, *s, *b, o, ld, weights, \
                      n, out, out_bf16, timeout_ns);                                                   \
   } while (0)
   switch (s->comb_elem_size) {
