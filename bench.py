@@ -401,11 +401,22 @@ def run_b200(a) -> None:
         t = json.loads(tf.read_text()).get(kname[dom])
         if t:
             traffic = int(t["dram_read"] + t["dram_write"])
+    traffic_src = "ncu dram__bytes_read.sum + dram__bytes_write.sum (profiles/r01_ncu_traffic.json)"
+    nf = ROOT / "profiles" / "r01_nvlink" / "summary.json"
+    if n_gpu == 2 and nf.exists():
+        # NVLink bytes on the wire per launch at EP=2, from the ncu capture of
+        # the host-gated split kernels that move the same rows
+        t = json.loads(nf.read_text()).get(a.config, {}).get(dom)
+        if t:
+            traffic = int(t["nvltx_wire"])
+            traffic_src = (f"ncu nvltx__bytes.sum (wire) of {t['kernel']} at EP=2 (profiles/r01_nvlink); "
+                           f"user data {t['nvltx_user']} B")
     peak = hbm_peak if bound == "hbm" else nvl_peak
     achieved = bytes_k[dom] / (kt[dom] * 1e-6) / 1e9
     roofline = {"bound": bound, "kernel": kname[dom],
                 "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
+                "traffic_source": traffic_src if traffic is not None else None,
                 "peak_source": ("MEASURED_PEAKS.json hbm_gbs (burst copy)" if bound == "hbm"
                                 else "B200_PROFILING.md measured peer copy 770 GB/s (fallback)"),
                 "algorithmic_bytes": int(bytes_k[dom]), "kernel_us": round(kt[dom], 2),
