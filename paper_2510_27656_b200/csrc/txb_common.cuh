@@ -114,7 +114,7 @@ struct Flags {
   uint32_t gbar_gen;
   uint32_t send_cnt;     // grouped rows to return to other ranks (this step)
   uint32_t pad2;
-  uint64_t pad1[1];
+  uint64_t gbar_arrive;  // monotone grid-barrier counter (+TXB_MAX_CTAS per barrier)
   uint64_t bar[TXB_MAX_RANKS];  // [peer] = last barrier epoch peer reached
 };
 

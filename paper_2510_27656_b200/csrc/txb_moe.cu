@@ -268,23 +268,24 @@ __device__ __noinline__ uint32_t route_counts_chunked(const txb_moe_shape& s, co
   return b;
 }
 
-// Grid barrier for cooperative launches (every CTA resident): arrival
-// counter + generation word in the rank's local flags.
+// Grid barrier for cooperative launches (every CTA resident): one release
+// atomic per CTA on a monotone 64-bit counter and an acquire poll.  CTA 0
+// adds K - (ncta - 1) and every other CTA 1, so each barrier raises the
+// counter by exactly K = TXB_MAX_CTAS whatever the grid size: every CTA of
+// barrier j sees old in [jK, (j+1)K) and waits for (j+1)K.  One atomic hop,
+// no reset (the last arriver does not have to bump a generation word).
 __device__ void grid_sync(Flags* f, int ncta) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    volatile uint32_t* gen = &f->gbar_gen;
-    const uint32_t my = *gen;
-    __threadfence();
-    if (atomicAdd(&f->gbar_count, 1u) == (uint32_t)ncta - 1) {
-      f->gbar_count = 0;
-      __threadfence();
-      atomicAdd(&f->gbar_gen, 1u);
-    } else {
-      while (*gen == my) {
-      }
-    }
-    __threadfence();
+    constexpr uint64_t K = TXB_MAX_CTAS;
+    const uint64_t add = blockIdx.x == 0 ? K - (uint64_t)(ncta - 1) : 1;
+    uint64_t old;
+    asm volatile("atom.add.release.gpu.global.u64 %0, [%1], %2;" : "=l"(old) : "l"(&f->gbar_arrive), "l"(add) : "memory");
+    const uint64_t target = (old / K + 1) * K;
+    uint64_t v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(&f->gbar_arrive) : "memory");
+    } while (v < target);
   }
   __syncthreads();
 }
@@ -298,7 +299,7 @@ __device__ __noinline__ uint32_t route_counts_segmented(const txb_moe_shape& s, 
                                                        uint32_t* hist, uint32_t* wc, int32_t* rank_out,
                                                        int64_t* pos, int64_t t0, int64_t t1,
                                                        uint32_t* cta_hist, uint32_t* cta_bad, Flags* f, int cta,
-                                                       int ncta, Shared& sh) {
+                                                       int ncta, Shared& sh, const txb_moe_bufs& bufs) {
   const int E = s.experts, R = s.topk;
   const int tid = threadIdx.x, warp = tid >> 5, nwarps = blockDim.x >> 5;
   if (tid == 0) {
@@ -340,20 +341,55 @@ __device__ __noinline__ uint32_t route_counts_segmented(const txb_moe_shape& s, 
     if (e >= 0) rank_out[i] = (int32_t)(wc[warp * E + e] + lr);
     __syncthreads();
   }
+  stamp(bufs, 19);
   for (int e = tid; e < E; e += blockDim.x) cta_hist[(size_t)cta * E + e] = hist[e];
   if (tid == 0) cta_bad[cta] = sh.bad;
   grid_sync(f, ncta);
+  stamp(bufs, 22);
+  // Column prefixes, distributed: CTA `cta` owns experts [e0, e1); one warp
+  // per expert loads the column of per-CTA counts (all loads in flight), scans
+  // it and writes the exclusive prefix back in place, the total in row ncta.
+  // After a second grid barrier every CTA reads its own row: O(E) loads per
+  // CTA instead of O(ncta * E) (TXB_MAX_CTAS rows leave room for row ncta).
+  {
+    const int lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+    const int e0 = (int)((int64_t)E * cta / ncta), e1 = (int)((int64_t)E * (cta + 1) / ncta);
+    constexpr int kQ = 8;  // 32 * kQ CTAs per pass
+    #pragma unroll 1
+    for (int e = e0 + warp; e < e1; e += nwarps) {
+      int run = 0;
+      #pragma unroll 1
+      for (int qb = 0; qb < ncta; qb += 32 * kQ) {
+        int c[kQ];
+#pragma unroll
+        for (int u = 0; u < kQ; ++u) {
+          const int q = qb + u * 32 + lane;
+          c[u] = q < ncta ? (int)cta_hist[(size_t)q * E + e] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < kQ; ++u) {
+          int x = c[u];
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+          }
+          const int q = qb + u * 32 + lane;
+          if (q < ncta) cta_hist[(size_t)q * E + e] = (uint32_t)(run + x - c[u]);
+          run += __shfl_sync(0xffffffffu, x, 31);
+        }
+      }
+      if (lane == 0) cta_hist[(size_t)ncta * E + e] = (uint32_t)run;
+    }
+  }
+  stamp(bufs, 24);
+  grid_sync(f, ncta);
+  stamp(bufs, 25);
   int* basev = reinterpret_cast<int*>(wc);   // [E] counts of earlier CTAs
   int* ex = basev + E;                       // [E] exclusive prefix of the totals
   for (int e = tid; e < E; e += blockDim.x) {
-    int before = 0, total = 0;
-    for (int q = 0; q < ncta; ++q) {
-      const int c = (int)cta_hist[(size_t)q * E + e];
-      total += c;
-      if (q < cta) before += c;
-    }
-    basev[e] = before;
-    hist[e] = (uint32_t)total;
+    basev[e] = (int)cta_hist[(size_t)cta * E + e];
+    hist[e] = cta_hist[(size_t)ncta * E + e];
   }
   for (int q = tid; q < ncta; q += blockDim.x)
     if (cta_bad[q]) atomicOr(&sh.bad, cta_bad[q]);
@@ -842,10 +878,55 @@ __device__ __forceinline__ void recv_rows_body(const txb_moe_shape& s, int* sm, 
   }
 }
 
-__device__ __noinline__ void recv_rows(const txb_moe_shape& s, int* sm, int64_t* rows, int64_t* sources,
-                                       int32_t* ret, uint8_t* G, uint8_t* dirty, int32_t* send_list,
-                                       uint32_t* send_cnt, int cta, int ncta) {
-  recv_rows_body(s, sm, rows, sources, ret, G, dirty, send_list, send_cnt, cta, ncta);
+// Large batches: the same metadata with one THREAD per grouped row (group by
+// binary search, source by a short scan), then one warp per local expert
+// zero-fills that group's padding rows that hold stale data.  A warp per
+// row would walk tens of thousands of rows one round trip at a time.
+__device__ __noinline__ void recv_rows_flat(const txb_moe_shape& s, int* sm, int64_t* rows, int64_t* sources,
+                                            int32_t* ret, uint8_t* G, uint8_t* dirty, int32_t* send_list,
+                                            uint32_t* send_cnt, int cta, int ncta) {
+  const int N = s.ranks, L = s.local_experts;
+  const RecvTables t = recv_carve(s, sm);
+  const int padded_total = t.tot[0];
+  const int64_t P = s.payload_bytes;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  #pragma unroll 1
+  for (int g = cta * nt + tid; g < padded_total; g += ncta * nt) {
+    int lo = 0, hi = L - 1;  // last le with gstart[le] <= g
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (t.gstart[mid] <= g) lo = mid;
+      else hi = mid - 1;
+    }
+    const int le = lo, k = g - t.gstart[le];
+    if (k >= t.gsize[le]) {
+      rows[g] = -1;
+      sources[g] = -1;
+      ret[g] = -1;
+      continue;
+    }
+    dirty[g] = 1;
+    const int* sp = t.srcpre + le * (N + 1);
+    int q = 0;
+    while (sp[q + 1] <= k) ++q;
+    const int kk = k - sp[q];
+    rows[g] = t.rowbase[q * L + le] + kk;
+    sources[g] = q;
+    ret[g] = t.retbase[q * L + le] + kk;
+    if (q != s.me) send_list[atomicAdd(send_cnt, 1u)] = g;
+  }
+  const int lane = tid & 31, warp = tid >> 5, nwarp = nt >> 5;
+  #pragma unroll 1
+  for (int le = cta * nwarp + warp; le < L; le += ncta * nwarp) {
+    const int g1 = le + 1 < L ? t.gstart[le + 1] : padded_total;
+    #pragma unroll 1
+    for (int g = t.gstart[le] + t.gsize[le]; g < g1; ++g) {
+      if (!dirty[g]) continue;
+      zero_row(G + (int64_t)g * P, P, lane, 32);
+      __syncwarp();
+      if (lane == 0) dirty[g] = 0;
+    }
+  }
 }
 
 // The step's error word into info (what dispatch_recv reads); also on the
@@ -1032,8 +1113,8 @@ k_recv(txb_moe_shape s, txb_moe_bufs b, uint64_t timeout_ns) {
   if (!wait_routes(s, f, route_of(b.region, s, (int)(step & 1)), C, step, timeout_ns, sh)) return;
   int* rt = reinterpret_cast<int*>(dsm + recv_offset(s));
   recv_tables(s, C, rt, b.info, blockIdx.x, sh, b);
-  recv_rows(s, rt, b.rows, b.sources, b.ret_slot, grouped_of(b.region, s), b.dirty, b.send_list, &f->send_cnt,
-            blockIdx.x, gridDim.x);
+  recv_rows_flat(s, rt, b.rows, b.sources, b.ret_slot, grouped_of(b.region, s), b.dirty, b.send_list,
+                 &f->send_cnt, blockIdx.x, gridDim.x);
   if (blockIdx.x == 0) wait_tokens(f, b.info, s.local_experts, timeout_ns);
 }
 
@@ -1128,7 +1209,7 @@ k_dispatch_fused(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
     const int64_t chunk = (n + ncta - 1) / ncta;
     const int64_t t0 = n < cta * chunk ? n : cta * chunk, t1 = n < t0 + chunk ? n : t0 + chunk;
     const uint32_t bad = route_counts_segmented(s, routes, hist, wc, b.rank_scratch, b.pos, t0, t1, b.cta_hist,
-                                                b.cta_bad, f, cta, ncta, sh);
+                                                b.cta_bad, f, cta, ncta, sh, b);
     stamp(b, 1);
     route_publish(s, b.peers, f, hist, step, n, bad, cta, ncta);
     stamp(b, 2);
@@ -1165,8 +1246,8 @@ k_dispatch_fused(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
     recv_rows_body(s, rt, b.rows, b.sources, b.ret_slot, grouped_of(b.region, s), b.dirty, b.send_list,
                    &f->send_cnt, cta, ncta);
   else
-    recv_rows(s, rt, b.rows, b.sources, b.ret_slot, grouped_of(b.region, s), b.dirty, b.send_list, &f->send_cnt,
-              cta, ncta);
+    recv_rows_flat(s, rt, b.rows, b.sources, b.ret_slot, grouped_of(b.region, s), b.dirty, b.send_list,
+                   &f->send_cnt, cta, ncta);
   stamp(b, 7);
   if (cta == 0) {
     // EP=1: every CTA counted every route, so CTA 0 has latched any route
