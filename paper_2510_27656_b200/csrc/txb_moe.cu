@@ -1566,9 +1566,9 @@ static int launch(void (*kernel)(KArgs...), int grid, int block, size_t smem, cu
 
 // Largest cooperative grid for a kernel (one wave).
 template <typename K>
-static int coop_grid(K kernel, int dev, size_t smem, int want) {
+static int coop_grid(K kernel, int dev, size_t smem, int want, int block = kThreads) {
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem);
   const int cap = (per_sm > 0 ? per_sm : 1) * sm_count(dev);
   if (want > cap) want = cap;
   return want < 1 ? 1 : want;
@@ -1794,11 +1794,15 @@ int txb_moe_combine_fused(const txb_moe_shape* s, const txb_moe_bufs* b, const v
   const int sms = sm_count(s->device);
 #define TXB_C(ELEM)                                                                                   \
   do {                                                                                                \
-    const int grid = coop_grid(k_combine_fused<ELEM>, s->device, 0, sms);                             \
+    /* large batches: half-size CTAs, two per SM, so one CTA's row loads */                           \
+    /* overlap the other's arithmetic and stores (tokens are reduced one per */                       \
+    /* CTA pass); decode keeps one 512-thread CTA per token */                                        \
+    const int blk = n > sms ? kThreads / 2 : kThreads;                                                \
+    const int grid = coop_grid(k_combine_fused<ELEM>, s->device, 0, blk == kThreads ? sms : 2 * sms, blk); \
     /* one rank: no cross-CTA waits, so no co-residency requirement; launched */                      \
     /* as a programmatic dependent so its CTAs land while the dispatch drains */                      \
     const bool solo = s->ranks == 1;                                                                  \
-    return launch_ex(k_combine_fused<ELEM>, grid, kThreads, 0, st, !solo, true, *s, *b, o, ld, weights, \
+    return launch_ex(k_combine_fused<ELEM>, grid, blk, 0, st, !solo, true, *s, *b, o, ld, weights,    \
                      n, out, out_bf16, timeout_ns);                                                   \
   } while (0)
   switch (s->comb_elem_size) {
