@@ -82,6 +82,11 @@ __host__ __device__ inline size_t cmat_offset(const txb_moe_shape& s) {
   return recv_offset(s) + (smem_recv(s.ranks, s.local_experts) + 15) / 16 * 16;
 }
 
+// large batches: the per-copy destination pointers after the route matrix
+__host__ __device__ inline size_t flat_offset(const txb_moe_shape& s) {
+  return (cmat_offset(s) + smem_cmat(s.ranks, s.experts) + 15) / 16 * 16;
+}
+
 // decode, one rank: [histogram E | staged ids n*R] then the receive tables
 __host__ __device__ inline size_t solo_recv_offset(const txb_moe_shape& s, int64_t n) {
   return ((size_t)(s.experts + n * s.topk) * 4 + 16 + 15) / 16 * 16;
@@ -682,6 +687,53 @@ __device__ __noinline__ void dispatch_tokens(const txb_moe_shape& s, const void*
   }
 }
 
+// Large batches, rows that need no per-token reduction (bf16 / f32 rows,
+// raw payload rows): the destinations of all the CTA's copies are resolved
+// up front into shared memory (one pass, one memory round trip), so the
+// token loop has no barrier and no metadata load, and every thread keeps
+// the next token's chunks in flight while it stores the current token's
+// R copies.  Returns false (nothing done) when the shape is not eligible or
+// the pointer table does not fit `dp`'s capacity; the caller then runs
+// dispatch_tokens.
+template <int SRC, int ELEM>
+__device__ __noinline__ bool dispatch_tokens_flat(const txb_moe_shape& s, const void* x, int64_t t0, int64_t t1,
+                                                  const int64_t* routes, const int32_t* rank_in, int32_t* gidx,
+                                                  void* const* peers, const int* baseg, uint8_t** dp, int cap,
+                                                  Shared& sh) {
+  if constexpr (ELEM == 1 && SRC != TXB_SRC_ROWS) {
+    return false;  // fp8 rows need a per-token amax across the CTA
+  } else {
+    const int R = s.topk, L = s.local_experts, tid = threadIdx.x, nt = blockDim.x;
+    const int64_t P = s.payload_bytes;
+    const int m = (int)((t1 - t0) * R);
+    if (t1 <= t0 || m > cap) return false;
+    RowRaw cur;
+    load_row_raw<SRC, ELEM>(x, t0, s.hidden, P, cur);
+    if (!cur.ok) return false;  // uniform across the CTA (shape / alignment)
+    #pragma unroll 1
+    for (int k = tid; k < m; k += nt) {
+      const int64_t i = t0 * R + k;
+      const int e = (int)routes[i];
+      const int d = e / L;
+      const int64_t g = (int64_t)baseg[e] + rank_in[i];
+      dp[k] = grouped_of(peers[d], s) + g * P;
+      gidx[i] = d == s.me ? (int32_t)g : -1;
+      atomicAdd(&sh.cnt[d], 1u);
+    }
+    __syncthreads();
+    #pragma unroll 1
+    for (int64_t t = t0; t < t1; ++t) {
+      RowRaw nxt;
+      if (t + 1 < t1) load_row_raw<SRC, ELEM>(x, t + 1, s.hidden, P, nxt);
+      RowRegs r;
+      finish_row_regs<SRC, ELEM>(cur, r, sh.red);
+      store_row_regs<SRC, ELEM>(r, s.hidden, s.scales, dp + (t - t0) * R, R);
+      cur = nxt;
+    }
+    return true;
+  }
+}
+
 // Completion of this CTA's stores: one release fence, then a relaxed add of
 // the row count on every destination's counter at byte offset `field`.
 __device__ void signal_counts(const txb_moe_shape& s, void* const* peers, size_t field, Shared& sh) {
@@ -1236,7 +1288,17 @@ k_dispatch_fused(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
     for (int q = threadIdx.x; q < s.ranks; q += blockDim.x) sh.cnt[q] = 0;
     __syncthreads();
     stamp(b, 4);
-    if (!bad) dispatch_tokens<SRC, ELEM>(s, x, t0, t1, 1, routes, b.rank_scratch, b.gidx, b.peers, baseg, sh);
+    if (!bad) {
+      // destination pointer table after the route matrix copy, sized by the
+      // host through the dynamic shared-memory size
+      uint32_t dyn;
+      asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+      const size_t fo = flat_offset(s);
+      const int cap = dyn > fo ? (int)((dyn - fo) / sizeof(uint8_t*)) : 0;
+      if (!dispatch_tokens_flat<SRC, ELEM>(s, x, t0, t1, routes, b.rank_scratch, b.gidx, b.peers, baseg,
+                                           reinterpret_cast<uint8_t**>(dsm + fo), cap, sh))
+        dispatch_tokens<SRC, ELEM>(s, x, t0, t1, 1, routes, b.rank_scratch, b.gidx, b.peers, baseg, sh);
+    }
     stamp(b, 5);
     if (!solo) signal_counts(s, b.peers, offsetof(Flags, tok_ctr), sh);
   }
@@ -1774,10 +1836,15 @@ int txb_moe_dispatch_fused(const txb_moe_shape* s, const txb_moe_bufs* b, const 
       if (coop_grid(kd, s->device, smem_d, want) == want)                                           \
         return launch(kd, want, kThreads, smem_d, st, true, *s, *b, x, n, routes, timeout_ns);      \
     }                                                                                               \
+    /* + the destination pointer table of dispatch_tokens_flat (<= 64 KiB) */                      \
     auto kg = k_dispatch_fused<SRC, ELEM, false>;                                                   \
-    if (int rc = set_smem(kg, smem)) return rc;                                                     \
-    const int grid = coop_grid(kg, s->device, smem, want);                                          \
-    return launch(kg, grid, kThreads, smem, st, true, *s, *b, x, n, routes, timeout_ns);            \
+    const int64_t per = (n + want - 1) / want * s->topk;                                            \
+    size_t smem_g = flat_offset(*s) + (size_t)per * sizeof(uint8_t*);                               \
+    if (per * (int64_t)sizeof(uint8_t*) > 64 * 1024) smem_g = smem;                                 \
+    if (smem_g < smem) smem_g = smem;                                                               \
+    if (int rc = set_smem(kg, smem_g)) return rc;                                                   \
+    const int grid = coop_grid(kg, s->device, smem_g, want);                                        \
+    return launch(kg, grid, kThreads, smem_g, st, true, *s, *b, x, n, routes, timeout_ns);          \
   } while (0)
   TXB_SWITCH_SRC_ELEM(src_kind, s->elem_size, TXB_F);
 #undef TXB_F
