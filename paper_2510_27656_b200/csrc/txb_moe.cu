@@ -36,6 +36,7 @@
 // counter with a cumulative threshold, so delivery order across NVLink is
 // irrelevant (engine.py:9-17, ImmCounterTable engine.py:138-205).
 #include <cstddef>
+#include <cstdlib>
 #include <cstdio>
 
 #include "txb_rows.cuh"
@@ -90,10 +91,6 @@ __host__ __device__ inline size_t flat_offset(const txb_moe_shape& s) {
 // decode, one rank: [histogram E | staged ids n*R] then the receive tables
 __host__ __device__ inline size_t solo_recv_offset(const txb_moe_shape& s, int64_t n) {
   return ((size_t)(s.experts + n * s.topk) * 4 + 16 + 15) / 16 * 16;
-}
-
-__host__ __device__ inline size_t roles_cmat_offset(const txb_moe_shape& s, int64_t n) {
-  return solo_recv_offset(s, n) + (smem_recv(s.ranks, s.local_experts) + 15) / 16 * 16;
 }
 
 struct Shared {  // static shared state of one CTA
@@ -1402,24 +1399,20 @@ k_dispatch_roles(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
                  const int64_t* __restrict__ routes, uint64_t timeout_ns) {
   extern __shared__ __align__(16) uint8_t dsm[];
   __shared__ Shared sh;
-  __shared__ uint32_t bad_s, fail;  // routing -> token: route error / route acquire failed
+  __shared__ uint32_t skip, fail;  // routing -> token: no stores / route acquire failed
   Flags* f = flags_of(b.region, s);
   const uint64_t step = cur_step(f);
   const int cta = blockIdx.x, ncta = gridDim.x;
   uint32_t* hist = reinterpret_cast<uint32_t*>(dsm);
   uint32_t* C = reinterpret_cast<uint32_t*>(dsm + cmat_offset(s));
   int* rt = reinterpret_cast<int*>(dsm + recv_offset(s));
+  const bool solo = s.ranks == 1;
   stamp(b, 0);
   grid_dep_launch();
   if constexpr (SOLO) {
     dispatch_roles_solo<SRC, ELEM>(s, b, x, n, routes, f, step, dsm, sh);
     return;
   }
-  // [hist | staged ids] [receive tables] [route matrix]: the token role
-  // reads the staged ids while the routing role fills the matrix and tables
-  int32_t* rv = reinterpret_cast<int32_t*>(hist + s.experts);
-  rt = reinterpret_cast<int*>(dsm + solo_recv_offset(s, n));
-  C = reinterpret_cast<uint32_t*>(dsm + roles_cmat_offset(s, n));
   if (threadIdx.x >= kRouteRole) {
     const Grp tg{(int)threadIdx.x - kRouteRole, kThreads - kRouteRole, 2};
     RowRaw raw;
@@ -1427,40 +1420,38 @@ k_dispatch_roles(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
     load_row_raw<SRC, ELEM>(x, cta, s.hidden, s.payload_bytes, raw, tg);
     finish_row_regs<SRC, ELEM>(raw, pre, sh.red, tg);
     if (b.prof && tg.tid == 0) b.prof[blockIdx.x * 32 + 1] = globaltimer();
-    for (int q = tg.tid; q < s.ranks; q += tg.nt) sh.cnt[q] = 0;
-    named_sync(3, kThreads);  // A: histogram, staged ids and own copies ready
-    const uint32_t bad = bad_s;
-    const int nw = (n > cta ? (int)((n - cta + ncta - 1) / ncta) : 0) * s.topk;
-    // ranks and send slots while the count row travels to the peers
-    if (!bad) {
-      own_ranks(rv, b.rank_scratch, nw, sh, tg);
-      tg.sync();
-    }
-    own_positions(s, hist, b.pos, bad, sh, tg);
-    named_sync(3, kThreads);  // B: route matrix acquired (or failed)
-    if (!fail && !bad) {
-      own_dests(s, C, b.peers, b.gidx, sh, tg);
-      if (b.prof && tg.tid == 0) b.prof[blockIdx.x * 32 + 15] = globaltimer();
-      store_row_regs<SRC, ELEM>(pre, s.hidden, s.scales, sh.dstp, s.topk, tg);
-    }
+    named_sync(3, kThreads);  // destinations are in sh.dstp
+    if (!skip) store_row_regs<SRC, ELEM>(pre, s.hidden, s.scales, sh.dstp, s.topk, tg);
     if (b.prof && tg.tid == 0) b.prof[blockIdx.x * 32 + 20] = globaltimer();
   } else {
     const Grp rg{(int)threadIdx.x, kRouteRole, 1};
     const uint32_t pd = prefetch_dirty(s, b.dirty, cta, ncta, rg);
-    const uint32_t bad = route_counts_direct(s, routes, n, hist, rv, b.rank_scratch, cta, ncta, sh, b, rg, false);
-    if (rg.tid == 0) bad_s = bad;
-    named_sync(3, kThreads);  // A
+    const uint32_t bad = route_counts_direct(s, routes, n, hist, reinterpret_cast<int32_t*>(hist + s.experts),
+                                             b.rank_scratch, cta, ncta, sh, b, rg);
     stamp(b, 14);
-    // the count row goes out before this CTA ranks its copies (token role)
     route_publish(s, b.peers, f, hist, step, n, bad, cta, ncta, rg);
+    own_positions(s, hist, b.pos, bad, sh, rg);
+    for (int q = rg.tid; q < s.ranks; q += rg.nt) sh.cnt[q] = 0;
     stamp(b, 2);
-    const bool ok = wait_routes(s, f, route_of(b.region, s, (int)(step & 1)), C, step, timeout_ns, sh, rg);
-    if (rg.tid == 0) fail = ok ? 0u : 1u;
-    named_sync(3, kThreads);  // B
+    const uint32_t* Cm = hist;
+    bool ok = true;
+    if (!solo) {
+      ok = wait_routes(s, f, route_of(b.region, s, (int)(step & 1)), C, step, timeout_ns, sh, rg);
+      Cm = C;
+    } else {
+      rg.sync();  // counters zeroed before own_dests adds to them
+    }
     stamp(b, 3);
+    if (ok && !bad) own_dests(s, Cm, b.peers, b.gidx, sh, rg);
+    if (rg.tid == 0) {
+      skip = (!ok || bad) ? 1u : 0u;
+      fail = ok ? 0u : 1u;
+    }
+    named_sync(3, kThreads);
+    stamp(b, 15);
     if (ok) {
-      recv_tables_body<true>(s, C, rt, b.info, cta, sh, b, rg);
-      if (cta == 0 && rg.tid == 0) f->tok_target += (uint64_t)recv_carve(s, rt).tot[1];
+      recv_tables_body<true>(s, Cm, rt, b.info, cta, sh, b, rg);
+      if (!solo && cta == 0 && rg.tid == 0) f->tok_target += (uint64_t)recv_carve(s, rt).tot[1];
       stamp(b, 4);
       // receive metadata while the token role's stores drain
       recv_rows_body(s, rt, b.rows, b.sources, b.ret_slot, grouped_of(b.region, s), b.dirty, b.send_list,
@@ -1474,9 +1465,12 @@ k_dispatch_roles(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
     return;
   }
   stamp(b, 5);
-  signal_counts(s, b.peers, offsetof(Flags, tok_ctr), sh);
+  if (!solo) signal_counts(s, b.peers, offsetof(Flags, tok_ctr), sh);
   stamp(b, 6);
-  if (cta == 0) wait_tokens(f, b.info, s.local_experts, timeout_ns);
+  if (cta == 0) {
+    if (!solo) wait_tokens(f, b.info, s.local_experts, timeout_ns);
+    else publish_err(f, b.info, s.local_experts);
+  }
   stamp(b, 8);
 }
 
@@ -1819,9 +1813,8 @@ int txb_moe_dispatch_fused(const txb_moe_shape* s, const txb_moe_bufs* b, const 
   // decode: the route ids of the whole batch are staged after the histogram
   const size_t rv_end = (size_t)(s->experts + n * s->topk) * 4 + 16;
   const size_t smem_d = smem > rv_end ? smem : rv_end;
-  const size_t roles_end = s->ranks == 1 ? solo_recv_offset(*s, n) + smem_recv(s->ranks, s->local_experts)
-                                         : roles_cmat_offset(*s, n) + smem_cmat(s->ranks, s->experts);
-  const size_t smem_r = roles_end > smem_d ? roles_end : smem_d;
+  const size_t solo_end = solo_recv_offset(*s, n) + smem_recv(s->ranks, s->local_experts);
+  const size_t smem_r = s->ranks == 1 && solo_end > smem_d ? solo_end : smem_d;
 #define TXB_F(SRC, ELEM)                                                                            \
   do {                                                                                              \
     if (roles) {                                                                                    \
@@ -1869,7 +1862,8 @@ int txb_moe_combine_fused(const txb_moe_shape* s, const txb_moe_bufs* b, const v
     /* one rank: no cross-CTA waits, so no co-residency requirement; launched */                      \
     /* as a programmatic dependent so its CTAs land while the dispatch drains */                      \
     const bool solo = s->ranks == 1;                                                                  \
-    return launch_ex(k_combine_fused<ELEM>, grid, blk, 0, st, !solo, true, *s, *b, o, ld, weights,    \
+    static const bool no_pdl = getenv("TXB_NO_PDL") != nullptr;                                       \
+    return launch_ex(k_combine_fused<ELEM>, grid, blk, 0, st, !solo, !no_pdl, *s, *b, o, ld, weights, \
                      n, out, out_bf16, timeout_ns);                                                   \
   } while (0)
   switch (s->comb_elem_size) {

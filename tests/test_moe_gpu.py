@@ -388,11 +388,14 @@ def test_kernel_registry_matches_oracle():
     assert np.array_equal(kernels.weighted_combine(y, pos, w), mo.weighted_combine(y, pos, w))
 
 
+@pytest.mark.parametrize("src", ["values", "rows"])
 @pytest.mark.parametrize("tokens,experts,elem", [(600, 256, 2), (300, 384, 1), (1024, 64, 4)])
-def test_large_batch_generic_fused_path(tokens, experts, elem):
+def test_large_batch_generic_fused_path(tokens, experts, elem, src):
     """Batches larger than the SM count take the generic fused kernel:
-    contiguous token ranges per CTA, segmented route counting with a grid
-    barrier.  Bit-exact grouped data / metadata / combine vs the oracle."""
+    contiguous token ranges per CTA, segmented route counting with two grid
+    barriers, the barrier-free token loop for rows without a per-token amax
+    (f32/bf16 values, or pre-encoded payload rows of any element size).
+    Bit-exact grouped data / metadata / combine vs the oracle."""
     spec = moe.RoutingSpec(ranks=1, experts=experts, max_tokens=tokens, topk=8, hidden=256,
                            elem_size=elem, scales=4 if elem == 1 else 0)
     os_ = ospec_of(spec)
@@ -402,8 +405,10 @@ def test_large_batch_generic_fused_path(tokens, experts, elem):
     mesh = moe.build_mesh(local_engines([0]), spec)
     rk = mesh[0]
     try:
+        payload = (torch.from_numpy(values[0]).cuda() if src == "values"
+                   else torch.from_numpy(mo.encode_tokens(os_, values[0])).cuda())
         for rep in range(2):
-            rk.dispatch_send(torch.from_numpy(values[0]).cuda(), torch.from_numpy(routes[0]).cuda())
+            rk.dispatch_send(payload, torch.from_numpy(routes[0]).cuda())
             g = rk.dispatch_recv()
             want = res.ranks[0].grouped
             assert np.array_equal(_np(g.data), want.data)

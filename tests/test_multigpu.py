@@ -53,22 +53,29 @@ def test_golden_one_rank_per_gpu(name):
         close_mesh(mesh)
 
 
+@pytest.mark.parametrize("shape", ["dsv3", "kimi"])
 @pytest.mark.parametrize("ranks", [2, 4, 8])
-def test_dsv3_decode_device_mode(ranks):
-    """DeepSeek-V3 decode shape, EP=ranks over NVLink, fused fp8 encode in the
-    dispatch kernel, bf16 combine rows; several steps back to back."""
+def test_dsv3_decode_device_mode(ranks, shape):
+    """DeepSeek-V3 decode shape (256 experts, uniform routes) or Kimi-K2 shape
+    (384 experts, bench.py's skewed routes), EP=ranks over NVLink, fused fp8
+    encode in the dispatch kernel, bf16 combine rows; several steps back to
+    back."""
     if NGPU < ranks:
         pytest.skip(f"needs {ranks} GPUs")
     import threading
-    spec = moe.RoutingSpec(ranks=ranks, experts=256, max_tokens=128, topk=8, hidden=7168,
+    import bench
+    E = 256 if shape == "dsv3" else 384
+    spec = moe.RoutingSpec(ranks=ranks, experts=E, max_tokens=128, topk=8, hidden=7168,
                            elem_size=1, scales=56, comb_elem_size=2, comb_scales=0)
     os_ = ospec_of(spec)
-    cs = mo.Spec(ranks, 256, 128, 8, hidden=7168, elem_size=2, scales=0)
+    cs = mo.Spec(ranks, E, 128, 8, hidden=7168, elem_size=2, scales=0)
     mesh = moe.build_mesh(local_engines(list(range(ranks))), spec, timeout=20.0)
     try:
         for step in range(3):
             rng = np.random.default_rng(200 + step)
             routes, values, weights = mo.random_step(os_, rng, tokens=128)
+            if shape == "kimi":
+                routes = [bench.routes_for(bench.WORKLOADS["kimi"], rng, 128) for _ in range(ranks)]
             xb = [torch.from_numpy(v).to(torch.bfloat16) for v in values]
             ref = mo.dispatch(os_, routes, [mo.encode_tokens(os_, x.float().numpy()) for x in xb])
             got = [None] * ranks
