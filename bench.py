@@ -397,8 +397,9 @@ def run_b200(a) -> None:
     # (EP=1 decode only; profiles/r01_ncu_traffic.json)
     traffic = None
     tf = ROOT / "profiles" / "r01_ncu_traffic.json"
-    if n_gpu == 1 and a.config == "decode" and tf.exists():
-        t = json.loads(tf.read_text()).get(kname[dom])
+    if n_gpu == 1 and a.config in ("decode", "prefill") and tf.exists():
+        tj = json.loads(tf.read_text())
+        t = (tj if a.config == "decode" else tj.get(a.config, {})).get(kname[dom])
         if t:
             traffic = int(t["dram_read"] + t["dram_write"])
     traffic_src = "ncu dram__bytes_read.sum + dram__bytes_write.sum (profiles/r01_ncu_traffic.json)"
