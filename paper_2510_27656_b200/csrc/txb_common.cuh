@@ -116,6 +116,7 @@ struct Flags {
   uint32_t pad2;
   uint64_t gbar_arrive;  // monotone grid-barrier counter (+TXB_MAX_CTAS per barrier)
   uint64_t bar[TXB_MAX_RANKS];  // [peer] = last barrier epoch peer reached
+  uint32_t phase_cnt[16];       // send-list fill per phase (large batches, this step)
 };
 
 __host__ __device__ inline Flags* flags_of(void* region, const txb_moe_shape& s) {
@@ -133,6 +134,24 @@ __host__ __device__ inline uint8_t* grouped_of(void* region, const txb_moe_shape
 }
 __host__ __device__ inline uint8_t* comb_of(void* region, const txb_moe_shape& s) {
   return reinterpret_cast<uint8_t*>(region) + s.off_comb;
+}
+
+// Per-token completion (large batches, see txb_moe.cu: kTokWaitMin), placed
+// after the combine rows: tokc[T] u64 -- rows of token t returned to this
+// rank (release-adds from the expert ranks), tokt[T] u64 -- cumulative
+// expected tokc (local), srctok[G] i32 -- origin token index of each grouped
+// row (written by the origin with the row during the dispatch).
+__host__ __device__ inline uint64_t tok_offset(const txb_moe_shape& s) {
+  return (s.off_comb + (uint64_t)s.comb_rows * (uint64_t)s.comb_bytes + 255) / 256 * 256;
+}
+__host__ __device__ inline uint64_t* tokc_of(void* region, const txb_moe_shape& s) {
+  return reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(region) + tok_offset(s));
+}
+__host__ __device__ inline uint64_t* tokt_of(void* region, const txb_moe_shape& s) {
+  return tokc_of(region, s) + s.max_tokens;
+}
+__host__ __device__ inline int32_t* srctok_of(void* region, const txb_moe_shape& s) {
+  return reinterpret_cast<int32_t*>(tokc_of(region, s) + 2 * (uint64_t)s.max_tokens);
 }
 
 // ------------------------------------------------------------- block scan

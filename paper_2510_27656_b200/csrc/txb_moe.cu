@@ -48,6 +48,16 @@ constexpr int kMaxExperts = 1536;  // shared-memory bound of the route phase
 constexpr int kThreads = 512;      // block size of the main kernels
 constexpr int kRouteThreads = 1024;
 constexpr int kMaxOwn = 64;        // copies per CTA of the direct-count path
+// Per-token combine completion for large batches (max_tokens above this, on
+// every rank alike): each expert rank's warps return whole rows, fence and
+// release-add a per-origin-token counter, so the origin reduces a token as
+// soon as its rows are in instead of after the last row of the step.  Every
+// dispatch kernel books the expected count (tokt) so the counters stay in
+// step whichever path a step takes.
+constexpr int kTokWaitMin = 256;
+__host__ __device__ inline bool tok_mode(const txb_moe_shape& s) {
+  return s.max_tokens > kTokWaitMin && s.ranks > 1;
+}
 
 __device__ __forceinline__ int pad_up(int x) { return (x + kGroupPad - 1) / kGroupPad * kGroupPad; }
 
@@ -613,10 +623,13 @@ __device__ void own_dests(const txb_moe_shape& s, const uint32_t* C, void* const
       const int g = acc + (int)sh.own_rank[k];
       sh.dstp[k] = grouped_of(peers[d], s) + (int64_t)g * s.payload_bytes;
       gidx[sh.own_i[k]] = d == s.me ? g : -1;
+      if (tok_mode(s)) srctok_of(peers[d], s)[g] = sh.own_i[k] / s.topk;
       atomicAdd(&sh.cnt[d], 1u);
     }
   }
   g.sync();
+  // one token per CTA on these paths: book its rows that will come back
+  if (tok_mode(s) && g.tid == 0) tokt_of(peers[s.me], s)[sh.own_i[0] / s.topk] += s.topk - sh.cnt[s.me];
 }
 
 // ------------------------------------------------------------------- P4
@@ -640,6 +653,7 @@ __device__ __forceinline__ void token_dests(const txb_moe_shape& s, const int64_
     const int64_t g = (int64_t)baseg[e] + rank;
     sh.dstp[tid] = grouped_of(peers[d], s) + g * s.payload_bytes;
     gidx[t * R + tid] = d == s.me ? (int32_t)g : -1;
+    if (tok_mode(s)) srctok_of(peers[d], s)[g] = (int32_t)t;
     atomicAdd(&sh.cnt[d], 1u);
   }
   __syncthreads();
@@ -715,6 +729,7 @@ __device__ __noinline__ bool dispatch_tokens_flat(const txb_moe_shape& s, const 
       const int64_t g = (int64_t)baseg[e] + rank_in[i];
       dp[k] = grouped_of(peers[d], s) + g * P;
       gidx[i] = d == s.me ? (int32_t)g : -1;
+      if (tok_mode(s)) srctok_of(peers[d], s)[g] = (int32_t)(i / R);
       atomicAdd(&sh.cnt[d], 1u);
     }
     __syncthreads();
@@ -931,14 +946,55 @@ __device__ __forceinline__ void recv_rows_body(const txb_moe_shape& s, int* sm, 
 // binary search, source by a short scan), then one warp per local expert
 // zero-fills that group's padding rows that hold stale data.  A warp per
 // row would walk tens of thousands of rows one round trip at a time.
+//
+// With per-token completion (tok_mode) the rows to return are listed in
+// kPhases phases by their relative position k/m inside their (source, local
+// expert) segment.  A segment holds its source's tokens in ascending order,
+// so phase ~ origin token / n: the combine walks the list grid-stride and
+// returns early tokens' rows first, which is the order the origins reduce.
+constexpr int kPhases = 16;
+
 __device__ __noinline__ void recv_rows_flat(const txb_moe_shape& s, int* sm, int64_t* rows, int64_t* sources,
                                             int32_t* ret, uint8_t* G, uint8_t* dirty, int32_t* send_list,
-                                            uint32_t* send_cnt, int cta, int ncta) {
+                                            uint32_t* send_cnt, int cta, int ncta, uint32_t* phase_cnt) {
   const int N = s.ranks, L = s.local_experts;
   const RecvTables t = recv_carve(s, sm);
   const int padded_total = t.tot[0];
   const int64_t P = s.payload_bytes;
   const int tid = threadIdx.x, nt = blockDim.x;
+  __shared__ int phase_base[kPhases];
+  const bool phased = tok_mode(s) && phase_cnt;
+  if (phased) {
+    // rows per phase over every remote segment, then exclusive prefix
+    if (tid < kPhases) phase_base[tid] = 0;
+    __syncthreads();
+    int c[kPhases];
+#pragma unroll
+    for (int ph = 0; ph < kPhases; ++ph) c[ph] = 0;
+    #pragma unroll 1
+    for (int i = tid; i < N * L; i += nt) {
+      if (i / L == s.me) continue;
+      const int m = t.a[i];
+#pragma unroll
+      for (int ph = 0; ph < kPhases; ++ph) c[ph] += (ph + 1) * m / kPhases - ph * m / kPhases;
+    }
+#pragma unroll
+    for (int ph = 0; ph < kPhases; ++ph) {
+      int v = c[ph];
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if ((tid & 31) == 0 && v) atomicAdd(&phase_base[ph], v);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int run = 0;
+      for (int ph = 0; ph < kPhases; ++ph) {
+        const int v = phase_base[ph];
+        phase_base[ph] = run;
+        run += v;
+      }
+    }
+    __syncthreads();
+  }
   #pragma unroll 1
   for (int g = cta * nt + tid; g < padded_total; g += ncta * nt) {
     int lo = 0, hi = L - 1;  // last le with gstart[le] <= g
@@ -962,7 +1018,19 @@ __device__ __noinline__ void recv_rows_flat(const txb_moe_shape& s, int* sm, int
     rows[g] = t.rowbase[q * L + le] + kk;
     sources[g] = q;
     ret[g] = t.retbase[q * L + le] + kk;
-    if (q != s.me) send_list[atomicAdd(send_cnt, 1u)] = g;
+    if (q != s.me) {
+      if (phased) {
+        const int m = t.a[q * L + le];
+        int ph = (int)((int64_t)kk * kPhases / m);
+        // the phase whose [ph*m/P, (ph+1)*m/P) range holds kk
+        while (ph > 0 && kk < ph * m / kPhases) --ph;
+        while (ph + 1 < kPhases && kk >= (ph + 1) * m / kPhases) ++ph;
+        send_list[phase_base[ph] + atomicAdd(&phase_cnt[ph], 1u)] = g;
+        atomicAdd(send_cnt, 1u);
+      } else {
+        send_list[atomicAdd(send_cnt, 1u)] = g;
+      }
+    }
   }
   const int lane = tid & 31, warp = tid >> 5, nwarp = nt >> 5;
   #pragma unroll 1
@@ -1012,6 +1080,51 @@ __device__ void combine_send_rows(const txb_moe_shape& s, Flags* f, const uint8_
   const int64_t Pc = s.comb_bytes;
   const int lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
   const bool vec = (Pc % 16 == 0) && (ld % 16 == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+  if (vec && tok_mode(s)) {
+    // per-token completion: each warp returns whole rows, walking the
+    // (phase-ordered) list grid-stride, and after every kBatch rows fences
+    // once and release-adds the origin token's counter of each of them
+    constexpr int kBatch = 4;
+    const int32_t* srct = srctok_of(peers[s.me], s);
+    const int n16 = (int)(Pc >> 4);
+    const int gw = cta * nwarp + warp, ngw = ncta * nwarp;
+    int pend_q = 0, pend_t = 0, npend = 0;
+    auto flush = [&]() {
+      __syncwarp();
+      if (lane == 0 && npend) fence_acqrel_sys();
+      #pragma unroll 1
+      for (int k = 0; k < npend; ++k) {
+        const int qk = __shfl_sync(0xffffffffu, pend_q, k), tk = __shfl_sync(0xffffffffu, pend_t, k);
+        if (lane == 0) red_relaxed_sys_add(tokc_of(peers[qk], s) + tk, 1);
+      }
+      npend = 0;
+    };
+    #pragma unroll 1
+    for (int r = gw; r < total; r += ngw) {  // the list is in phase order: grid-stride keeps it
+      const int g = send_list[r];
+      const int q = (int)sources[g];
+      const int4* src = reinterpret_cast<const int4*>(out + (int64_t)g * ld);
+      int4* dst = reinterpret_cast<int4*>(comb_of(peers[q], s) + (int64_t)ret[g] * Pc);
+      #pragma unroll 1
+      for (int c0 = 0; c0 < n16; c0 += 128) {
+        int4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (c0 + lane + 32 * u < n16) v[u] = src[c0 + lane + 32 * u];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (c0 + lane + 32 * u < n16) dst[c0 + lane + 32 * u] = v[u];
+      }
+      if (lane == npend) {
+        pend_q = q;
+        pend_t = srct[g];
+      }
+      if (lane == 0) atomicAdd(&sh.cnt[q], 1u);
+      if (++npend == kBatch) flush();
+    }
+    flush();
+    return;
+  }
   if (vec) {
     // each CTA takes one contiguous run of chunks (whole rows, in order), its
     // warps interleaved over it: per-CTA shares equal to within one chunk,
@@ -1059,7 +1172,7 @@ template <int ELEM>
 __device__ bool combine_reduce(const txb_moe_shape& s, Flags* f, const uint8_t* comb, const uint8_t* out,
                                int64_t ld, const int64_t* pos, const int32_t* gidx, const float* w, int64_t n,
                                void* dst, int out_bf16, uint64_t timeout_ns, int cta, int ncta, Shared& sh,
-                               uint64_t* prof = nullptr) {
+                               uint64_t* prof = nullptr, void* region = nullptr) {
   __shared__ CombTok ct;
   const int64_t Pc = s.comb_bytes;
   const int H = s.hidden, R = s.topk;
@@ -1088,13 +1201,22 @@ __device__ bool combine_reduce(const txb_moe_shape& s, Flags* f, const uint8_t* 
     __syncthreads();
     return true;
   }
-  if (!wait()) return false;
+  // large batches with per-token completion (fused path only: `region`):
+  // each token waits for its own rows, so the reduce overlaps the returns
+  const bool per_tok = region && tok_mode(s);
+  if (!per_tok && !wait()) return false;
+  const uint64_t* tokc = per_tok ? tokc_of(region, s) : nullptr;
+  const uint64_t* tokt = per_tok ? tokt_of(region, s) : nullptr;
+  const uint64_t dl = globaltimer() + timeout_ns;
   #pragma unroll 1
   for (int64_t t = cta; t < n; t += ncta) {
-    if (t != cta) {
-      combine_prep(ct, comb, Pc, out, ld, pos, gidx, w, t, R);
-      __syncthreads();
+    if (t != cta) combine_prep(ct, comb, Pc, out, ld, pos, gidx, w, t, R);
+    if (per_tok && threadIdx.x == 0) {
+      sh.fail = spin_ge(tokc + t, tokt[t], dl) ? 0u : TXB_EV_WAIT_COMBINE;
+      if (sh.fail) atomicOr(&f->err, sh.fail);
     }
+    __syncthreads();
+    if (per_tok && sh.fail) return false;
     combine_token<ELEM>(ct, Pc, comb, H, R, t, dst, out_bf16, vec);
     __syncthreads();
   }
@@ -1112,6 +1234,7 @@ __device__ void end_of_step(Flags* f, uint64_t step, int ncta) {
     if (t == (uint32_t)ncta - 1) {
       f->ticket = 0;
       f->send_cnt = 0;
+      for (int ph = 0; ph < kPhases; ++ph) f->phase_cnt[ph] = 0;
       *reinterpret_cast<volatile uint64_t*>(&f->step) = step;
     }
   }
@@ -1163,7 +1286,7 @@ k_recv(txb_moe_shape s, txb_moe_bufs b, uint64_t timeout_ns) {
   int* rt = reinterpret_cast<int*>(dsm + recv_offset(s));
   recv_tables(s, C, rt, b.info, blockIdx.x, sh, b);
   recv_rows_flat(s, rt, b.rows, b.sources, b.ret_slot, grouped_of(b.region, s), b.dirty, b.send_list,
-                 &f->send_cnt, blockIdx.x, gridDim.x);
+                 &f->send_cnt, blockIdx.x, gridDim.x, nullptr);
   if (blockIdx.x == 0) wait_tokens(f, b.info, s.local_experts, timeout_ns);
 }
 
@@ -1295,6 +1418,15 @@ k_dispatch_fused(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
       if (!dispatch_tokens_flat<SRC, ELEM>(s, x, t0, t1, routes, b.rank_scratch, b.gidx, b.peers, baseg,
                                            reinterpret_cast<uint8_t**>(dsm + fo), cap, sh))
         dispatch_tokens<SRC, ELEM>(s, x, t0, t1, 1, routes, b.rank_scratch, b.gidx, b.peers, baseg, sh);
+      if (tok_mode(s)) {
+        uint64_t* tokt = tokt_of(b.region, s);
+        #pragma unroll 1
+        for (int64_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
+          int remote = 0;
+          for (int j = 0; j < s.topk; ++j) remote += (int)routes[t * s.topk + j] / s.local_experts != s.me;
+          tokt[t] += remote;
+        }
+      }
     }
     stamp(b, 5);
     if (!solo) signal_counts(s, b.peers, offsetof(Flags, tok_ctr), sh);
@@ -1306,7 +1438,7 @@ k_dispatch_fused(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
                    &f->send_cnt, cta, ncta);
   else
     recv_rows_flat(s, rt, b.rows, b.sources, b.ret_slot, grouped_of(b.region, s), b.dirty, b.send_list,
-                   &f->send_cnt, cta, ncta);
+                   &f->send_cnt, cta, ncta, f->phase_cnt);
   stamp(b, 7);
   if (cta == 0) {
     // EP=1: every CTA counted every route, so CTA 0 has latched any route
@@ -1484,16 +1616,29 @@ k_combine_fused(txb_moe_shape s, txb_moe_bufs b, const uint8_t* __restrict__ out
   Flags* f = flags_of(b.region, s);
   const uint64_t step = cur_step(f);
   stamp(b, 9);
-  combine_send_rows(s, flags_of(b.region, s), out, ld, b.peers, b.sources, b.ret_slot, b.send_list, blockIdx.x,
-                    gridDim.x, sh);
+  // Large batches with per-token completion (two half-size CTAs per SM):
+  // even CTAs return rows, odd CTAs reduce tokens as their rows land, so
+  // the reduce runs during the returns instead of after them.
+  const int ncta = gridDim.x;
+  const bool roles = tok_mode(s) && blockDim.x < kThreads && ncta >= 2;
+  const bool sender = !roles || (blockIdx.x & 1) == 0;
+  const int sidx = roles ? (int)blockIdx.x >> 1 : (int)blockIdx.x, nsend = roles ? (ncta + 1) >> 1 : ncta;
+  const int ridx = roles ? (int)blockIdx.x >> 1 : (int)blockIdx.x, nred = roles ? ncta >> 1 : ncta;
+  if (sender) {
+    combine_send_rows(s, f, out, ld, b.peers, b.sources, b.ret_slot, b.send_list, sidx, nsend, sh);
+  } else {
+    for (int q = threadIdx.x; q < s.ranks; q += blockDim.x) sh.cnt[q] = 0;
+    __syncthreads();
+  }
   stamp(b, 10);
   signal_counts(s, b.peers, offsetof(Flags, comb_ctr), sh);
   __syncthreads();
   stamp(b, 11);
-  combine_reduce<ELEM>(s, f, comb_of(b.region, s), out, ld, b.pos, b.gidx, w, n, dst, out_bf16, timeout_ns,
-                       blockIdx.x, gridDim.x, sh, b.prof);
+  if (!roles || !sender)
+    combine_reduce<ELEM>(s, f, comb_of(b.region, s), out, ld, b.pos, b.gidx, w, n, dst, out_bf16, timeout_ns,
+                         ridx, nred, sh, b.prof, b.region);
   stamp(b, 12);
-  end_of_step(f, step, gridDim.x);
+  end_of_step(f, step, ncta);
   stamp(b, 13);
 }
 
@@ -1690,7 +1835,9 @@ int txb_moe_plan(txb_moe_shape* s) {
   s->off_grouped = off;
   off = align_up(off + (uint64_t)s->grouped_rows * s->payload_bytes, 4096);
   s->off_comb = off;
-  off = align_up(off + (uint64_t)s->comb_rows * s->comb_bytes, 4096);
+  off = align_up(off + (uint64_t)s->comb_rows * s->comb_bytes, 256);
+  // per-token completion words + origin token index per grouped row
+  off = align_up(off + 2ull * (uint64_t)T * 8 + (uint64_t)s->grouped_rows * 4, 4096);
   s->region_bytes = off;
   return TXB_OK;
 }
