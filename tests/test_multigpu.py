@@ -182,3 +182,57 @@ def test_prefill_size_generic_path_multi_gpu(ranks):
             assert np.array_equal(got[r][1], mo.bf16_encode(comb[r]))
     finally:
         close_mesh(mesh)
+
+
+@pytest.mark.parametrize("ranks", [2, 4])
+def test_per_token_completion_mixed_batches(ranks):
+    """max_tokens above the per-token threshold: large steps use per-token
+    combine completion (whole-row returns, per-origin-token counters), small
+    steps the decode kernels and the global counter, empty steps neither.
+    The counters must stay consistent across any sequence of them; every
+    step is checked bit-exactly (grouped data, bf16 combine bits)."""
+    if NGPU < ranks:
+        pytest.skip(f"needs {ranks} GPUs")
+    import threading
+    T = 600
+    spec = moe.RoutingSpec(ranks=ranks, experts=32, max_tokens=T, topk=4, hidden=256,
+                           elem_size=2, scales=0, comb_elem_size=2, comb_scales=0)
+    os_ = ospec_of(spec)
+    mesh = moe.build_mesh(local_engines(list(range(ranks))), spec, timeout=20.0)
+    try:
+        for step, n in enumerate([600, 90, 0, 333, 17, 600]):
+            rng = np.random.default_rng(900 + step)
+            routes, values, weights = mo.random_step(os_, rng, tokens=n)
+            xb = [torch.from_numpy(v).to(torch.bfloat16) for v in values]
+            ref = mo.dispatch(os_, routes, [mo.encode_tokens(os_, x.float().numpy()) for x in xb])
+            got, errs = [None] * ranks, []
+
+            def worker(r):
+                try:
+                    torch.cuda.set_device(r)
+                    rk = mesh[r]
+                    rk.dispatch_send(xb[r].cuda(r), torch.from_numpy(routes[r]).cuda(r))
+                    g = rk.dispatch_recv()
+                    y = g.data.view(torch.bfloat16).reshape(g.data.shape[0], spec.hidden).clone()
+                    rk.combine_send(y)
+                    out = rk.combine_recv(torch.from_numpy(weights[r]).cuda(r), out_dtype=torch.bfloat16)
+                    got[r] = (g.data.cpu().numpy(), out.view(torch.int16).cpu().numpy().view(np.uint16))
+                except Exception as e:  # noqa: BLE001
+                    errs.append(e)
+
+            th = [threading.Thread(target=worker, args=(r,)) for r in range(ranks)]
+            for t in th:
+                t.start()
+            for t in th:
+                t.join(120)
+            if errs:
+                raise errs[0]
+            outs = []
+            for r in range(ranks):
+                assert np.array_equal(got[r][0], ref.ranks[r].grouped.data), (step, r)
+                outs.append(ref.ranks[r].grouped.data)
+            comb = mo.combine(os_, ref, outs, weights, comb_spec=os_)
+            for r in range(ranks):
+                assert np.array_equal(got[r][1], mo.bf16_encode(comb[r])), (step, r)
+    finally:
+        close_mesh(mesh)
