@@ -92,29 +92,39 @@ def _inputs(wl: dict, rank: int, tokens: int, seed: int = 0):
 # ------------------------------------------------------------ CPU baseline
 
 
-def cpu_port_step(ospec, cspec, xb, routes, w, outs, mo, pool=None, nthr: int = 1):
-    """One step of the reference algorithm on the host (oracle port), the
-    same work the GPU step times: encode the bf16 values to fp8 rows ->
-    dispatch regroup -> return the (given) expert output rows -> fp32
-    weighted sum -> bf16 out.  The per-token parts (encode, decode + sum,
-    bf16 rounding) run in `nthr` row chunks on a thread pool (numpy drops the
-    GIL inside its array kernels); the regroup is one vectorised gather."""
-    n = xb.shape[0]
-    chunks = [c for c in np.array_split(np.arange(n), nthr) if c.size]
+def cpu_port_step(ospec, cspec, xbs, routes, ws, outs, mo, pool=None, nthr: int = 1):
+    """One step of the reference algorithm on the host (oracle port) for all
+    ospec.ranks ranks, the same work the GPU step times: encode the bf16
+    values to fp8 rows -> dispatch regroup -> return the (given) expert output
+    rows to their origins -> fp32 weighted sum -> bf16 out.  The per-token
+    parts (encode, decode + sum, bf16 rounding) run in `nthr` row chunks on a
+    thread pool (numpy drops the GIL inside its array kernels); the regroup
+    and the returns are vectorised gathers / scatters."""
+    N = len(xbs)
     run = (lambda f, xs: list(pool.map(f, xs))) if pool is not None else (lambda f, xs: [f(c) for c in xs])
-    pay = np.concatenate(run(lambda c: mo.encode_tokens(ospec, xb[c]), chunks))
-    res = mo.dispatch(ospec, [routes], [pay])
-    rr = res.ranks[0]
-    valid = np.nonzero(rr.grouped.rows >= 0)[0]
-    send = np.zeros((max(1, rr.pos.size), cspec.payload_bytes), np.uint8)
-    send[rr.src_slot[valid]] = outs[valid]
-    R = rr.pos.shape[1]
+    jobs = [(r, c) for r in range(N) for c in np.array_split(np.arange(xbs[r].shape[0]), nthr) if c.size]
+    enc = run(lambda rc: mo.encode_tokens(ospec, xbs[rc[0]][rc[1]]), jobs)
+    pays = [np.concatenate([e for (r, _), e in zip(jobs, enc) if r == q] or
+                           [np.zeros((0, ospec.payload_bytes), np.uint8)]) for q in range(N)]
+    res = mo.dispatch(ospec, routes, pays)
+    send = [np.zeros((max(1, res.ranks[q].pos.size), cspec.payload_bytes), np.uint8) for q in range(N)]
+    for d in range(N):
+        rr = res.ranks[d]
+        valid = np.nonzero(rr.grouped.rows >= 0)[0]
+        srcs = rr.grouped.sources[valid]
+        for q in range(N):
+            m = valid[srcs == q]
+            send[q][rr.src_slot[m]] = outs[d][m]
+    R = ospec.topk
 
-    def reduce(c):
-        y = mo.decode_tokens(cspec, send[rr.pos[c].ravel()])
-        return mo.bf16_encode(mo.weighted_combine(y, np.arange(c.size * R).reshape(c.size, R), w[c]))
+    def reduce(rc):
+        r, c = rc
+        y = mo.decode_tokens(cspec, send[r][res.ranks[r].pos[c].ravel()])
+        return mo.bf16_encode(mo.weighted_combine(y, np.arange(c.size * R).reshape(c.size, R), ws[r][c]))
 
-    return np.concatenate(run(reduce, chunks))
+    red = run(reduce, jobs)
+    return [np.concatenate([o for (r, _), o in zip(jobs, red) if r == q] or
+                           [np.zeros((0, ospec.hidden), np.uint16)]) for q in range(N)]
 
 
 def _host_threads() -> int:
@@ -124,40 +134,47 @@ def _host_threads() -> int:
         return max(1, os.cpu_count() or 1)
 
 
-def cpu_baseline(wl: dict, tokens: int, seconds: float) -> dict:
+def cpu_baseline(wl: dict, tokens: int, seconds: float, ranks: int = 1) -> dict:
     """The oracle port timed on the host with every host thread (row chunks
-    on a thread pool), EP=1, on a bounded sample: the full step when it is
-    short, else a 512-token slice scaled linearly to the step's token count
-    (stated in `sample`).  The result is checked against the serial oracle
-    once before timing."""
+    on a thread pool), for `ranks` ranks (the reference runs every rank of an
+    EP=N step in one host process over its SimFabric), on a bounded sample:
+    the full step when it is short, else a 512-token slice per rank scaled
+    linearly to the step's token count (stated in `sample`).  The result is
+    checked against the serial oracle once before timing."""
     from concurrent.futures import ThreadPoolExecutor
     from oracle import moe_oracle as mo
     sample = min(tokens, 512)
     E, R, H = wl["experts"], wl["topk"], wl["hidden"]
-    ospec = mo.Spec(1, E, sample, R, hidden=H, elem_size=wl["elem"], scales=wl["scales"])
-    cspec = mo.Spec(1, E, sample, R, hidden=H, elem_size=2, scales=0)
-    x, routes, w = _inputs(wl, 0, sample)
-    xb = mo.bf16_decode(mo.bf16_encode(x))
+    N = ranks
+    ospec = mo.Spec(N, E, sample, R, hidden=H, elem_size=wl["elem"], scales=wl["scales"])
+    cspec = mo.Spec(N, E, sample, R, hidden=H, elem_size=2, scales=0)
+    ins = [_inputs(wl, r, sample) for r in range(N)]
+    xbs = [mo.bf16_decode(mo.bf16_encode(x)) for x, _, _ in ins]
+    routes = [rt for _, rt, _ in ins]
+    ws = [w for _, _, w in ins]
+    res = mo.dispatch(ospec, routes, [mo.encode_tokens(ospec, xb) for xb in xbs])
     # synthetic expert outputs (bf16 rows), like the GPU step's
-    rows = mo.dispatch(ospec, [routes], [mo.encode_tokens(ospec, xb)]).ranks[0].grouped.rows.size
-    outs = mo.bf16_encode(np.random.default_rng(5).standard_normal((rows, H)).astype(np.float32))
-    outs = outs.view(np.uint8).reshape(rows, -1)
+    outs = []
+    for d in range(N):
+        rows = res.ranks[d].grouped.rows.size
+        o = mo.bf16_encode(np.random.default_rng(5 + d).standard_normal((rows, H)).astype(np.float32))
+        outs.append(o.view(np.uint8).reshape(rows, -1))
     host = _host_threads()
-    res = mo.dispatch(ospec, [routes], [mo.encode_tokens(ospec, xb)])
-    want = mo.bf16_encode(mo.combine(ospec, res, [outs], [w], comb_spec=cspec)[0])
+    want = [mo.bf16_encode(c) for c in mo.combine(ospec, res, outs, ws, comb_spec=cspec)]
     # thread count: the fastest of 1, 2, 4, ... host threads on a short trial
     # (tiny per-thread chunks lose to Python overhead on many-core hosts)
     cands = sorted({min(host, 1 << k) for k in range(0, 8)})
     best = None
     for nthr in cands:
         with ThreadPoolExecutor(nthr) as pool:
-            got = cpu_port_step(ospec, cspec, xb, routes, w, outs, mo, pool, nthr)
-            assert np.array_equal(got, want), "threaded port differs from the serial oracle"
+            got = cpu_port_step(ospec, cspec, xbs, routes, ws, outs, mo, pool, nthr)
+            assert all(np.array_equal(g, wv) for g, wv in zip(got, want)), \
+                "threaded port differs from the serial oracle"
             trial = []
             t_end = time.perf_counter() + min(0.5, seconds / (2 * len(cands)))
             while time.perf_counter() < t_end or len(trial) < 2:
                 t0 = time.perf_counter()
-                cpu_port_step(ospec, cspec, xb, routes, w, outs, mo, pool, nthr)
+                cpu_port_step(ospec, cspec, xbs, routes, ws, outs, mo, pool, nthr)
                 trial.append(time.perf_counter() - t0)
         if best is None or statistics.median(trial) < best[1]:
             best = (nthr, statistics.median(trial))
@@ -167,11 +184,12 @@ def cpu_baseline(wl: dict, tokens: int, seconds: float) -> dict:
         t_end = time.perf_counter() + seconds
         while time.perf_counter() < t_end or len(times) < 3:
             t0 = time.perf_counter()
-            cpu_port_step(ospec, cspec, xb, routes, w, outs, mo, pool, nthr)
+            cpu_port_step(ospec, cspec, xbs, routes, ws, outs, mo, pool, nthr)
             times.append((time.perf_counter() - t0) * 1e6)
     v = statistics.median(times) * tokens / sample
-    what = (f"{len(times)} full EP=1 steps" if sample == tokens else
-            f"{len(times)} EP=1 steps on a {sample}-token slice, scaled x{tokens / sample:g} to {tokens} tokens")
+    what = (f"{len(times)} full EP={N} steps ({N} ranks on the host)" if sample == tokens else
+            f"{len(times)} EP={N} steps on a {sample}-token slice per rank, scaled x{tokens / sample:g} "
+            f"to {tokens} tokens")
     return {"value": round(v, 1), "unit": "us", "cores": nthr, "kind": "port",
             "sample": f"{what} ({wl['name']}, H={H}, E={E}, top-{R}); numpy oracle port "
                       f"(oracle/moe_oracle.py): fp8 encode, regroup, return of given bf16 expert rows, "
@@ -533,14 +551,17 @@ def e2e_times(rk, x, routes, w, stream, flush, dev, K: int, world: int) -> dict:
 # ------------------------------------------------------------ reference arm
 
 
-def reference_live(wl: dict, tokens: int, steps: int = 3) -> dict:
+def reference_live(wl: dict, tokens: int, steps: int = 3, ranks: int = 1) -> dict:
     """The unmodified reference (railtx, installed into baseline/_ref with
     pip --no-deps; pure Python + numpy + numba) run through its own public
-    API on the host: encode_tokens -> MoeRank.dispatch_send ->
-    dispatch_recv -> combine_send (identity expert) -> combine_recv over a
-    SimFabric, one rank (moe.py:470-833).  Its payloads are fp8 or f32
-    (elem_size 2 does not exist there), so a bf16 workload runs as f32.
-    Bounded sample: at most 512 tokens, scaled linearly to the step."""
+    API on the host: per rank encode_tokens -> MoeRank.dispatch_send ->
+    dispatch_recv -> combine_send (identity expert) -> combine_recv, all
+    `ranks` ranks in one process over a SimFabric with one thread per rank
+    (its test harness's model, moe.py:470-833, _invariants.py:254-292).
+    Its payloads are fp8 or f32 (elem_size 2 does not exist there), so a
+    bf16 workload runs as f32.  Bounded sample: at most 512 tokens per rank,
+    scaled linearly to the step."""
+    import threading
     ref = ROOT / "baseline" / "_ref"
     if not (ref / "railtx").is_dir():
         return {"unavailable": "baseline/_ref/railtx not installed (see DESIGN.md section 9)"}
@@ -552,28 +573,49 @@ def reference_live(wl: dict, tokens: int, steps: int = 3) -> dict:
         return {"unavailable": f"railtx import failed: {exc!r}"[:200]}
     sample = min(tokens, 512)
     elem, scales = (1, wl["scales"]) if wl["elem"] == 1 else (4, 0)
-    spec = rmoe.RoutingSpec(ranks=1, experts=wl["experts"], max_tokens=sample, topk=wl["topk"],
+    N = ranks
+    spec = rmoe.RoutingSpec(ranks=N, experts=wl["experts"], max_tokens=sample, topk=wl["topk"],
                             hidden=wl["hidden"], elem_size=elem, scales=scales)
-    eng = TransferEngine(SimFabric(FaultConfig(mtu=1 << 20)), rails=1, name="ref0")
-    rk = rmoe.build_mesh([eng], spec, ranks_per_node=1)[0]
-    x, routes, w = _inputs(wl, 0, sample)
+    fab = SimFabric(FaultConfig(mtu=1 << 20))
+    engs = [TransferEngine(fab, rails=1, name=f"ref{r}") for r in range(N)]
+    mesh = rmoe.build_mesh(engs, spec, ranks_per_node=N)
+    ins = [_inputs(wl, r, sample) for r in range(N)]
+    errs: list = []
+
+    def rank_step(r: int) -> None:
+        try:
+            x, routes, w = ins[r]
+            rk = mesh[r]
+            rk.dispatch_send(rmoe.encode_tokens(spec, x), routes)
+            g = rk.dispatch_recv(300.0)
+            rk.combine_send(g.data)
+            rk.combine_recv(w, 300.0)
+        except Exception as exc:  # surfaced below
+            errs.append(exc)
+
     times = []
     try:
         for i in range(steps + 2):  # two warm-up steps (numba JIT)
             t0 = time.perf_counter()
-            rk.dispatch_send(rmoe.encode_tokens(spec, x), routes)
-            g = rk.dispatch_recv(120.0)
-            rk.combine_send(g.data)
-            rk.combine_recv(w, 120.0)
+            th = [threading.Thread(target=rank_step, args=(r,)) for r in range(N)]
+            for t in th:
+                t.start()
+            for t in th:
+                t.join()
+            if errs:
+                return {"unavailable": f"railtx step failed: {errs[0]!r}"[:200]}
             if i >= 2:
                 times.append((time.perf_counter() - t0) * 1e6)
     finally:
-        rk.close()
-        eng.close()
+        for rk in mesh:
+            rk.close()
+        for e in engs:
+            e.close()
     v = statistics.median(times) * tokens / sample
-    return {"value": round(v, 1), "unit": "us", "cores": 1, "kind": "reference",
-            "sample": f"{len(times)} steps of the unmodified railtx MoeRank API (baseline/_ref), EP=1 over "
-                      f"SimFabric, {sample} tokens" + (f" scaled x{tokens / sample:g}" if sample < tokens else "")
+    return {"value": round(v, 1), "unit": "us", "cores": N, "kind": "reference",
+            "sample": f"{len(times)} steps of the unmodified railtx MoeRank API (baseline/_ref), EP={N} "
+                      f"({N} rank threads over SimFabric), {sample} tokens per rank"
+                      + (f" scaled x{tokens / sample:g}" if sample < tokens else "")
                       + f", {'fp8' if elem == 1 else 'f32'} payloads, identity expert, p50 after 2 warm-up steps"}
 
 
@@ -588,19 +630,20 @@ def run_reference(a) -> None:
         return
     wl = WORKLOADS[a.config]
     tokens = a.tokens or wl["tokens"]
-    cb = cpu_baseline(wl, tokens, max(2.0, min(a.cpu_seconds, 30.0)))
+    N = max(world, a.gpus)  # the reference runs all N ranks of an EP=N step on the host
+    cb = cpu_baseline(wl, tokens, max(2.0, min(a.cpu_seconds, 30.0)), ranks=N)
     res = {"impl": "reference", "metric": wl["metric"], "value": cb["value"], "unit": "us",
            "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "higher_is_better": False,
            "scaling": "weak", "vs_baseline": None,
            "dtype": ("fp8-e4m3" if wl["elem"] == 1 else "bf16") + " dispatch / bf16 combine (fp32 accumulate)",
            "data": "synthetic",
            "config": {"workload": wl["name"], "tokens_per_rank": tokens, "hidden": wl["hidden"],
-                      "experts": wl["experts"], "topk": wl["topk"], "ep": 1},
+                      "experts": wl["experts"], "topk": wl["topk"], "ep": N},
            "cpu_baseline": cb,
            "e2e": {"value": cb["value"], "unit": "us", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-           "reference_live": reference_live(wl, tokens),
+           "reference_live": reference_live(wl, tokens, ranks=N),
            "note": "value: the threaded oracle port of railtx's algorithm (oracle/moe_oracle.py) on the host "
-                   "cores; reference_live: the unmodified railtx API from baseline/_ref, single thread"}
+                   "cores; reference_live: the unmodified railtx API from baseline/_ref, one thread per rank"}
     print(json.dumps(res), flush=True)
 
 

@@ -106,10 +106,14 @@ def test_trace_recorder_roundtrip(tmp_path):
     assert off.record("x") is None and len(off) == 0
 
 
-def test_cpu_baseline_threaded_port_matches_oracle():
+@pytest.mark.parametrize("ranks", [1, 3])
+def test_cpu_baseline_threaded_port_matches_oracle(ranks):
     """The reference arm's threaded oracle port (bench.cpu_baseline) checks
-    itself against the serial oracle before timing; run it on a small shape."""
+    itself against the serial oracle before timing; run it on a small shape,
+    one rank and an EP=3 step (every rank on the host, as the reference's
+    SimFabric runs it)."""
     import bench
-    wl = dict(bench.WORKLOADS["decode"], tokens=16, experts=16, hidden=256, scales=4)
-    r = bench.cpu_baseline(wl, 16, 0.05)
+    wl = dict(bench.WORKLOADS["decode"], tokens=16, experts=24, hidden=256, scales=4)
+    r = bench.cpu_baseline(wl, 16, 0.05, ranks=ranks)
     assert r["kind"] == "port" and r["cores"] >= 1 and r["value"] > 0
+    assert f"EP={ranks}" in r["sample"]
