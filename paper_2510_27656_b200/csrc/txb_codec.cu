@@ -91,6 +91,7 @@ extern "C" {
 
 int txb_encode_rows(const void* values, int src_kind, int64_t n, int32_t hidden, int32_t elem_size,
                     int32_t scales, void* out, void* stream) {
+  DeviceFor on_dev(stream, out);
   if (n <= 0) return TXB_OK;
   if (elem_size == 1 && scales < 1) {
     set_error("quantized payloads need at least one scale slot");
@@ -119,6 +120,7 @@ int txb_encode_rows(const void* values, int src_kind, int64_t n, int32_t hidden,
 
 int txb_decode_rows(const void* rows, int64_t n, int32_t hidden, int32_t elem_size, int32_t scales, float* out,
                     void* stream) {
+  DeviceFor on_dev(stream, out);
   if (n <= 0) return TXB_OK;
   const int64_t P = (int64_t)hidden * elem_size + 4LL * scales;
   const int grid = grid_for(n, 1);
@@ -135,6 +137,7 @@ int txb_decode_rows(const void* rows, int64_t n, int32_t hidden, int32_t elem_si
 }
 
 int txb_pack_rows(const void* src, int64_t width, const int64_t* rows, int64_t k, void* out, void* stream) {
+  DeviceFor on_dev(stream, out);
   if (k <= 0) return TXB_OK;
   k_pack_rows<<<grid_for(k, 8), 256, 0, (cudaStream_t)stream>>>((const uint8_t*)src, width, rows, k, (uint8_t*)out);
   TXB_CUDA(cudaGetLastError());
@@ -143,6 +146,7 @@ int txb_pack_rows(const void* src, int64_t width, const int64_t* rows, int64_t k
 
 int txb_weighted_combine(const float* y, int64_t hidden, const int64_t* pos, const float* w, int64_t n, int32_t topk,
                          float* out, void* stream) {
+  DeviceFor on_dev(stream, out);
   if (n <= 0) return TXB_OK;
   if (topk > kMaxTopk) {
     set_error("topk %d above the supported %d", topk, kMaxTopk);
@@ -154,6 +158,7 @@ int txb_weighted_combine(const float* y, int64_t hidden, const int64_t* pos, con
 }
 
 int txb_fp8_encode(const float* x, int64_t n, uint8_t* out, void* stream) {
+  DeviceFor on_dev(stream, out);
   if (n <= 0) return TXB_OK;
   k_fp8_encode<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(x, n, out);
   TXB_CUDA(cudaGetLastError());
@@ -161,6 +166,7 @@ int txb_fp8_encode(const float* x, int64_t n, uint8_t* out, void* stream) {
 }
 
 int txb_fp8_decode(const uint8_t* b, int64_t n, float* out, void* stream) {
+  DeviceFor on_dev(stream, out);
   if (n <= 0) return TXB_OK;
   k_fp8_decode<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(b, n, out);
   TXB_CUDA(cudaGetLastError());
@@ -168,6 +174,7 @@ int txb_fp8_decode(const uint8_t* b, int64_t n, float* out, void* stream) {
 }
 
 int txb_bf16_encode(const float* x, int64_t n, uint16_t* out, void* stream) {
+  DeviceFor on_dev(stream, out);
   if (n <= 0) return TXB_OK;
   k_bf16_encode<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(x, n, out);
   TXB_CUDA(cudaGetLastError());

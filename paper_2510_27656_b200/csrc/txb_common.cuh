@@ -26,6 +26,33 @@ int cuda_fail(cudaError_t e, const char* what);
     if (_e != cudaSuccess) return ::txb::cuda_fail(_e, #call); \
   } while (0)
 
+// Entry points that take a caller's stream launch on the device that stream
+// belongs to; for the legacy default stream (handle 0, shared by every
+// device) on the device that owns `p`.  Without this a call made while
+// another device is current would run on that device and reach the
+// buffers over NVLink.  The caller's current device is restored on return.
+struct DeviceFor {
+  int prev = -1;
+  DeviceFor(void* stream, const void* p) {
+    cudaGetDevice(&prev);
+    int dev = -1;
+    if (stream && cudaStreamGetDevice(static_cast<cudaStream_t>(stream), &dev) == cudaSuccess) {
+      if (dev != prev) cudaSetDevice(dev);
+      return;
+    }
+    cudaGetLastError();
+    cudaPointerAttributes at;
+    if (p && cudaPointerGetAttributes(&at, p) == cudaSuccess && at.type == cudaMemoryTypeDevice &&
+        at.device != prev)
+      cudaSetDevice(at.device);
+    cudaGetLastError();
+  }
+  ~DeviceFor() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
 // ------------------------------------------------------------ PTX wrappers
 
 __device__ __forceinline__ uint64_t globaltimer() {

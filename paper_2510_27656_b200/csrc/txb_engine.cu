@@ -151,7 +151,27 @@ __global__ void k_globaltimer(uint64_t* out) {
 // scale = amax/448 (1.0 when 0) and writes the f32 scale footer.
 __global__ void k_amax_bf16(const uint16_t* __restrict__ x, int64_t n, uint32_t* amax_bits) {
   float m = 0.f;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nthr = (int64_t)gridDim.x * blockDim.x;
+  const bool vec = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+  const int64_t n8 = vec ? n / 8 : 0;
+  // 16-byte loads, two in flight per thread per pass
+  for (int64_t c = tid; c < n8; c += 2 * nthr) {
+    uint4 v[2];
+    v[0] = reinterpret_cast<const uint4*>(x)[c];
+    if (c + nthr < n8) v[1] = reinterpret_cast<const uint4*>(x)[c + nthr];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      if (u == 1 && c + nthr >= n8) break;
+      const uint32_t* w = reinterpret_cast<const uint32_t*>(&v[u]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float a = __uint_as_float(w[k] << 16), b = __uint_as_float(w[k] & 0xFFFF0000u);
+        if (isfinite(a)) m = fmaxf(m, fabsf(a));
+        if (isfinite(b)) m = fmaxf(m, fabsf(b));
+      }
+    }
+  }
+  for (int64_t i = 8 * n8 + tid; i < n; i += nthr) {
     const float v = bf16_to_f(x[i]);
     if (isfinite(v)) m = fmaxf(m, fabsf(v));
   }
@@ -159,12 +179,32 @@ __global__ void k_amax_bf16(const uint16_t* __restrict__ x, int64_t n, uint32_t*
   if ((threadIdx.x & 31) == 0) atomicMax(amax_bits, __float_as_uint(m));
 }
 
+// x / scale correctly rounded (div_rn_by: reciprocal multiply + two FMA
+// corrections, bit-identical to the IEEE division), e4m3 RNE satfinite;
+// 16-byte loads of 8 bf16, 8-byte stores of 8 fp8.
 __global__ void k_quant_bf16_fp8(const uint16_t* __restrict__ x, int64_t n, const uint32_t* amax_bits,
                                  uint8_t* __restrict__ out) {
   const float amax = __uint_as_float(*amax_bits);
   const float scale = amax > 0.f ? __fdiv_rn(amax, 448.0f) : 1.0f;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = (uint8_t)(fp8x2(__fdiv_rn(bf16_to_f(x[i]), scale), 0.f) & 0xFF);
+  const float rs = __frcp_rn(scale);
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nthr = (int64_t)gridDim.x * blockDim.x;
+  const bool vec = ((reinterpret_cast<uintptr_t>(x) & 15) == 0) && ((reinterpret_cast<uintptr_t>(out) & 7) == 0);
+  const int64_t n8 = vec ? n / 8 : 0;
+  for (int64_t c = tid; c < n8; c += nthr) {
+    const uint4 v = reinterpret_cast<const uint4*>(x)[c];
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(&v);
+    uint32_t o[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const float f0 = __uint_as_float(w[2 * q] << 16), f1 = __uint_as_float(w[2 * q] & 0xFFFF0000u);
+      const float f2 = __uint_as_float(w[2 * q + 1] << 16), f3 = __uint_as_float(w[2 * q + 1] & 0xFFFF0000u);
+      o[q] = fp8x2(div_rn_by(f0, scale, rs), div_rn_by(f1, scale, rs)) |
+             (fp8x2(div_rn_by(f2, scale, rs), div_rn_by(f3, scale, rs)) << 16);
+    }
+    reinterpret_cast<uint2*>(out)[c] = make_uint2(o[0], o[1]);
+  }
+  for (int64_t i = 8 * n8 + tid; i < n; i += nthr)
+    out[i] = (uint8_t)(fp8x2(div_rn_by(bf16_to_f(x[i]), scale, rs), 0.f) & 0xFF);
   if (blockIdx.x == 0 && threadIdx.x < 4) out[n + threadIdx.x] = (uint8_t)(__float_as_uint(scale) >> (8 * threadIdx.x));
 }
 
@@ -198,6 +238,7 @@ int txb_copy_pages(const txb_pages* j, int grid, void* stream) {
     set_error("negative page count or length");
     return TXB_ERR_TRANSFER;
   }
+  DeviceFor on_dev(stream, j->src_base);
   txb_pages job = *j;
   const int64_t per_page = job.page_len > 0 ? (job.page_len + kPiece - 1) / kPiece : 0;
   const int64_t total = job.npages * per_page;
@@ -221,6 +262,7 @@ int txb_copy_pages(const txb_pages* j, int grid, void* stream) {
 }
 
 int txb_imm_add(uint64_t* const* ctrs, int n, uint64_t value, int single_device, void* stream) {
+  DeviceFor on_dev(stream, ctrs);
   if (n <= 0) return TXB_OK;
   k_imm_add<<<1, 128, 0, (cudaStream_t)stream>>>(ctrs, n, value, single_device);
   TXB_CUDA(cudaGetLastError());
@@ -228,18 +270,21 @@ int txb_imm_add(uint64_t* const* ctrs, int n, uint64_t value, int single_device,
 }
 
 int txb_imm_wait(const uint64_t* ctr, uint64_t threshold, uint64_t timeout_ns, uint32_t* err, void* stream) {
+  DeviceFor on_dev(stream, ctr);
   k_imm_wait<<<1, 32, 0, (cudaStream_t)stream>>>(ctr, threshold, timeout_ns, err);
   TXB_CUDA(cudaGetLastError());
   return TXB_OK;
 }
 
 int txb_globaltimer(uint64_t* out, void* stream) {
+  DeviceFor on_dev(stream, out);
   k_globaltimer<<<1, 32, 0, (cudaStream_t)stream>>>(out);
   TXB_CUDA(cudaGetLastError());
   return TXB_OK;
 }
 
 int txb_fp8_quantize_tensor(const uint16_t* x, int64_t n, uint32_t* amax_scratch, uint8_t* out, void* stream) {
+  DeviceFor on_dev(stream, x);
   cudaStream_t st = (cudaStream_t)stream;
   TXB_CUDA(cudaMemsetAsync(amax_scratch, 0, sizeof(uint32_t), st));
   int64_t g = (n + 255) / 256;
