@@ -105,3 +105,26 @@ def test_layout_agrees_across_ranks():
 def test_max_over_ranks():
     out = _run("max")
     assert out[0][1] == out[1][1] == [2.0, 5.0, 3.0]
+
+
+def test_reference_arm_under_torchrun_world2():
+    """The driver launches `bench.py --impl reference` the same way as the
+    B200 arm (torchrun, one process per GPU).  Rank 0 alone times the
+    reference's EP=2 step on the host and prints one JSON line; rank 1 exits
+    cleanly.  Runs on CPU (no GPU is touched on this path)."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--impl", "reference",
+           "--gpus", "2", "--steps", "3", "--warmup", "3", "--cpu-seconds", "1", "--tokens", "16"]
+    p = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-2000:]
+    lines = [x for x in p.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, p.stdout
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["config"]["ep"] == 2 and d["value"] > 0
+    assert d["cpu_baseline"]["kind"] == "port" and "EP=2" in d["cpu_baseline"]["sample"]
+    assert d["e2e"]["h2d_bytes_per_step"] == 0
