@@ -116,15 +116,20 @@ def test_dsv3_decode_device_mode(ranks, shape):
         close_mesh(mesh)
 
 
-@pytest.mark.parametrize("ranks", [2])
-def test_torchrun_ipc_bench_smoke(ranks, tmp_path):
-    """One rank per process over CUDA IPC (connect_process_group): a short
-    bench run under torchrun must finish and print one JSON line."""
+@pytest.mark.parametrize("config", ["decode", "kimi"])
+@pytest.mark.parametrize("ranks", [2, 4])
+def test_torchrun_ipc_bench_smoke(ranks, config, tmp_path):
+    """One rank per process over CUDA IPC (connect_process_group): a bench
+    run under torchrun (graph replays, L2 flush, device barrier, e2e from
+    pinned host memory; ~200 steps in all) must finish and print one JSON
+    line.  The Kimi-shape case is the one that exposed an intermittent fault
+    no thread-mesh test showed."""
     if NGPU < ranks:
         pytest.skip(f"needs {ranks} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={ranks}",
-           "--master-addr", "127.0.0.1", "--master-port", "29531", str(ROOT / "bench.py"),
-           "--gpus", str(ranks), "--steps", "5", "--warmup", "3", "--no-cpu-baseline"]
+           "--master-addr", "127.0.0.1", "--master-port", str(29531 + ranks + (10 if config == "kimi" else 0)),
+           str(ROOT / "bench.py"), "--config", config,
+           "--gpus", str(ranks), "--steps", "60", "--warmup", "3", "--no-cpu-baseline"]
     env = dict(os.environ)
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
     assert p.returncode == 0, p.stderr[-4000:]
