@@ -125,7 +125,8 @@ typedef struct txb_moe_bufs {
   uint32_t* cta_hist;    /* [TXB_MAX_CTAS][experts] per-CTA counts of the segmented route phase */
   uint32_t* cta_bad;     /* [TXB_MAX_CTAS] per-CTA route validation bits */
   int32_t* send_list;    /* [grouped_rows] grouped rows whose source is another rank */
-  uint64_t* prof;        /* optional [grid][16] %globaltimer phase stamps (NULL = off) */
+  uint64_t* prof;        /* optional [grid][32] %globaltimer phase stamps, grid = the launch's CTA
+                            count (<= TXB_MAX_CTAS; NULL = off) */
 } txb_moe_bufs;
 
 /* Validate a RoutingSpec (moe.py:52-70) and fill the derived fields. */
@@ -149,7 +150,9 @@ int txb_moe_dispatch_fused(const txb_moe_shape* s, const txb_moe_bufs* b, const 
  * after the expected rows arrived out[t] = sum_j w[t,j] * row(t,j) in fp32,
  * j ascending, no FMA (kernels.weighted_combine, kernels.py:206-242);
  * out_bf16 selects bf16 RNE output (kernels.bf16_encode, kernels.py:144-150).
- * The last CTA publishes the end-of-step barrier (moe.dbar) to every peer. */
+ * The last CTA (ticket) advances the local step counter; the end-of-step
+ * barrier (moe.dbar) is published by the NEXT dispatch's route phase, next to
+ * its count row, so the combine's tail carries no remote store. */
 int txb_moe_combine_fused(const txb_moe_shape* s, const txb_moe_bufs* b, const void* outputs, int64_t ld,
                           const float* weights, int64_t n, void* out, int out_bf16, uint64_t timeout_ns,
                           void* stream);

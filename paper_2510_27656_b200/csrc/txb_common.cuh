@@ -53,6 +53,26 @@ struct DeviceFor {
   }
 };
 
+// Entry points that name their device explicitly (a rank's shape, a region)
+// make it current for the call and restore the caller's device on return,
+// so a call never leaves torch's current device pointing at another rank.
+struct OnDevice {
+  int prev = -1;
+  cudaError_t err = cudaSuccess;
+  explicit OnDevice(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (dev != prev) err = cudaSetDevice(dev);
+  }
+  ~OnDevice() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+#define TXB_ON_DEVICE(dev)                                      \
+  ::txb::OnDevice _on_dev(dev);                                 \
+  if (_on_dev.err != cudaSuccess) return ::txb::cuda_fail(_on_dev.err, "cudaSetDevice")
+
 // ------------------------------------------------------------ PTX wrappers
 
 __device__ __forceinline__ uint64_t globaltimer() {

@@ -1848,7 +1848,7 @@ int txb_moe_route(const txb_moe_shape* s, const txb_moe_bufs* b, const int64_t* 
     set_error("%lld tokens exceed the %d-token limit", (long long)n, s->max_tokens);
     return TXB_ERR_PROTOCOL;
   }
-  TXB_CUDA(cudaSetDevice(s->device));
+  TXB_ON_DEVICE(s->device);
   const size_t smem = smem_route(s->experts, kRouteThreads / 32);
   return launch(k_route, 1, kRouteThreads, smem, (cudaStream_t)stream, false, *s, *b, routes, n);
 }
@@ -1874,7 +1874,7 @@ int txb_moe_route(const txb_moe_shape* s, const txb_moe_bufs* b, const int64_t* 
 int txb_moe_dispatch(const txb_moe_shape* s, const txb_moe_bufs* b, const void* x, int src_kind, int64_t n,
                      const int64_t* routes, uint64_t timeout_ns, int grid, void* stream) {
   if (int rc = check(s, b)) return rc;
-  TXB_CUDA(cudaSetDevice(s->device));
+  TXB_ON_DEVICE(s->device);
   if (grid <= 0) {
     const int64_t g = n < 1 ? 1 : n;
     grid = (int)(g < 4 * sm_count(s->device) ? g : 4 * sm_count(s->device));
@@ -1890,7 +1890,7 @@ int txb_moe_dispatch(const txb_moe_shape* s, const txb_moe_bufs* b, const void* 
 
 int txb_moe_dispatch_recv(const txb_moe_shape* s, const txb_moe_bufs* b, uint64_t timeout_ns, void* stream) {
   if (int rc = check(s, b)) return rc;
-  TXB_CUDA(cudaSetDevice(s->device));
+  TXB_ON_DEVICE(s->device);
   const size_t smem = smem_main(s, false);
   const int64_t wpb = kThreads / 32;
   int grid = (int)((s->grouped_rows + wpb - 1) / wpb);
@@ -1902,7 +1902,7 @@ int txb_moe_dispatch_recv(const txb_moe_shape* s, const txb_moe_bufs* b, uint64_
 int txb_moe_combine_send(const txb_moe_shape* s, const txb_moe_bufs* b, const void* outputs, int64_t ld, int grid,
                          void* stream) {
   if (int rc = check(s, b)) return rc;
-  TXB_CUDA(cudaSetDevice(s->device));
+  TXB_ON_DEVICE(s->device);
   if (grid <= 0) {
     const int64_t want = (s->grouped_rows + (kThreads / 32) - 1) / (kThreads / 32);
     const int cap = 2 * sm_count(s->device);
@@ -1915,7 +1915,7 @@ int txb_moe_combine_recv(const txb_moe_shape* s, const txb_moe_bufs* b, const vo
                          const float* weights, int64_t n, void* out, int out_bf16, uint64_t timeout_ns,
                          void* stream) {
   if (int rc = check(s, b)) return rc;
-  TXB_CUDA(cudaSetDevice(s->device));
+  TXB_ON_DEVICE(s->device);
   const int grid = (int)(n < 1 ? 1 : (n < 2 * sm_count(s->device) ? n : 2 * sm_count(s->device)));
   cudaStream_t st = (cudaStream_t)stream;
   const uint8_t* o = (const uint8_t*)outputs;
@@ -1937,7 +1937,7 @@ int txb_moe_dispatch_fused(const txb_moe_shape* s, const txb_moe_bufs* b, const 
     set_error("fused dispatch needs the per-CTA scratch (cta_hist / cta_bad)");
     return TXB_ERR_REGION;
   }
-  TXB_CUDA(cudaSetDevice(s->device));
+  TXB_ON_DEVICE(s->device);
   const size_t smem = smem_main(s, true);
   cudaStream_t st = (cudaStream_t)stream;
   const int sms = sm_count(s->device);
@@ -1995,7 +1995,7 @@ int txb_moe_combine_fused(const txb_moe_shape* s, const txb_moe_bufs* b, const v
                           const float* weights, int64_t n, void* out, int out_bf16, uint64_t timeout_ns,
                           void* stream) {
   if (int rc = check(s, b)) return rc;
-  TXB_CUDA(cudaSetDevice(s->device));
+  TXB_ON_DEVICE(s->device);
   cudaStream_t st = (cudaStream_t)stream;
   const uint8_t* o = (const uint8_t*)outputs;
   const int sms = sm_count(s->device);
@@ -2023,7 +2023,7 @@ int txb_moe_combine_fused(const txb_moe_shape* s, const txb_moe_bufs* b, const v
 
 int txb_moe_barrier(const txb_moe_shape* s, const txb_moe_bufs* b, uint64_t timeout_ns, void* stream) {
   if (int rc = check(s, b)) return rc;
-  TXB_CUDA(cudaSetDevice(s->device));
+  TXB_ON_DEVICE(s->device);
   return launch(k_barrier, 1, 128, 0, (cudaStream_t)stream, false, *s, *b, timeout_ns);
 }
 
@@ -2032,7 +2032,7 @@ int txb_moe_status(const txb_moe_shape* s, void* region, uint32_t* err, uint64_t
     set_error("null shape or region");
     return TXB_ERR_PROTOCOL;
   }
-  TXB_CUDA(cudaSetDevice(s->device));
+  TXB_ON_DEVICE(s->device);
   // read on a private non-blocking stream so the snapshot never waits for
   // (or serialises with) kernels that are spinning on other streams
   static thread_local cudaStream_t side[64] = {nullptr};

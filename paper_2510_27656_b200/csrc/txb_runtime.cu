@@ -47,7 +47,7 @@ int txb_alloc(int device, uint64_t bytes, void** out_ptr) {
     set_error("txb_alloc: null out pointer");
     return TXB_ERR_REGION;
   }
-  TXB_CUDA(cudaSetDevice(device));
+  TXB_ON_DEVICE(device);
   void* p = nullptr;
   TXB_CUDA(cudaMalloc(&p, bytes ? bytes : 256));
   TXB_CUDA(cudaMemset(p, 0, bytes ? bytes : 256));
@@ -57,20 +57,20 @@ int txb_alloc(int device, uint64_t bytes, void** out_ptr) {
 }
 
 int txb_free(int device, void* ptr) {
-  TXB_CUDA(cudaSetDevice(device));
+  TXB_ON_DEVICE(device);
   TXB_CUDA(cudaFree(ptr));
   return TXB_OK;
 }
 
 int txb_memset(int device, void* ptr, int value, uint64_t bytes, void* stream) {
-  TXB_CUDA(cudaSetDevice(device));
+  TXB_ON_DEVICE(device);
   TXB_CUDA(cudaMemsetAsync(ptr, value, bytes, (cudaStream_t)stream));
   return TXB_OK;
 }
 
 int txb_ipc_export(int device, void* ptr, uint8_t* out_handle) {
   static_assert(sizeof(cudaIpcMemHandle_t) == TXB_IPC_HANDLE_BYTES, "ipc handle size");
-  TXB_CUDA(cudaSetDevice(device));
+  TXB_ON_DEVICE(device);
   cudaIpcMemHandle_t h;
   TXB_CUDA(cudaIpcGetMemHandle(&h, ptr));
   memcpy(out_handle, &h, sizeof(h));
@@ -78,7 +78,7 @@ int txb_ipc_export(int device, void* ptr, uint8_t* out_handle) {
 }
 
 int txb_ipc_import(int device, const uint8_t* handle, void** out_ptr) {
-  TXB_CUDA(cudaSetDevice(device));
+  TXB_ON_DEVICE(device);
   cudaIpcMemHandle_t h;
   memcpy(&h, handle, sizeof(h));
   TXB_CUDA(cudaIpcOpenMemHandle(out_ptr, h, cudaIpcMemLazyEnablePeerAccess));
@@ -86,14 +86,14 @@ int txb_ipc_import(int device, const uint8_t* handle, void** out_ptr) {
 }
 
 int txb_ipc_close(int device, void* ptr) {
-  TXB_CUDA(cudaSetDevice(device));
+  TXB_ON_DEVICE(device);
   TXB_CUDA(cudaIpcCloseMemHandle(ptr));
   return TXB_OK;
 }
 
 int txb_enable_peer(int device, int peer_device) {
   if (device == peer_device) return TXB_OK;
-  TXB_CUDA(cudaSetDevice(device));
+  TXB_ON_DEVICE(device);
   int ok = 0;
   TXB_CUDA(cudaDeviceCanAccessPeer(&ok, device, peer_device));
   if (!ok) {

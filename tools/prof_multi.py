@@ -13,7 +13,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import numpy as np
 import torch
 
-from paper_2510_27656_b200 import moe
+from paper_2510_27656_b200 import _lib, moe
 from paper_2510_27656_b200.engine import local_engines
 
 ap = argparse.ArgumentParser()
@@ -46,7 +46,7 @@ def worker(r):
     side = torch.cuda.Stream()
     torch.cuda.set_stream(side)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
-    prof = torch.zeros(148 * 32, dtype=torch.int64, device="cuda")
+    prof = torch.zeros(_lib.TXB_MAX_CTAS * 32, dtype=torch.int64, device="cuda")  # [grid][32], grid <= TXB_MAX_CTAS
 
     def one():
         rk.dispatch_send(x, rt, sync=False)
@@ -76,7 +76,7 @@ def worker(r):
         g.replay()
         e1.record()
         torch.cuda.synchronize()
-        res.append(prof.view(148, 32).cpu().numpy().astype(np.float64))
+        res.append(prof.view(_lib.TXB_MAX_CTAS, 32).cpu().numpy().astype(np.float64))
         ts.append(e0.elapsed_time(e1) * 1e3)
     rk._bufs.prof = 0
     stamps[r] = res[-1]

@@ -9,7 +9,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import numpy as np
 import torch
 
-from paper_2510_27656_b200 import moe
+from paper_2510_27656_b200 import _lib, moe
 from paper_2510_27656_b200.engine import local_engines
 
 ap = argparse.ArgumentParser()
@@ -37,7 +37,7 @@ assert err == 0, hex(err)
 print("ok")
 
 # phase stamps of the fused kernels (%globaltimer, per CTA)
-prof = torch.zeros(148 * 16, dtype=torch.int64, device="cuda")
+prof = torch.zeros(_lib.TXB_MAX_CTAS * 32, dtype=torch.int64, device="cuda")  # [grid][32], grid <= TXB_MAX_CTAS
 rk._bufs.prof = prof.data_ptr()
 names = ["start", "counted", "positions", "routes-in", "layout", "stored", "signalled", "metadata",
          "tokens-in", "c:start", "c:sent", "c:signalled", "c:reduced", "c:end"]
@@ -67,7 +67,7 @@ else:
         prof.zero_()
         one()
         torch.cuda.synchronize()
-p = prof.view(148, 16).cpu().numpy().astype(np.float64)
+p = prof.view(_lib.TXB_MAX_CTAS, 32).cpu().numpy().astype(np.float64)
 rk._bufs.prof = 0
 act = p[:, 0] > 0
 t0 = p[act, 0].min()

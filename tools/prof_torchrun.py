@@ -57,7 +57,7 @@ y = torch.randn(int(rk._shape.grouped_rows), H, device=dev).to(torch.bfloat16)
 flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
 stream = torch.cuda.Stream(dev)
 torch.cuda.set_stream(stream)
-NS = 148
+NS = _lib.TXB_MAX_CTAS  # stamp rows: one per CTA of the largest launch (<= TXB_MAX_CTAS)
 prof = torch.zeros(NS * 32, dtype=torch.int64, device=dev)
 gt = torch.zeros(4, dtype=torch.int64, device=dev)
 sid = C.c_void_p(stream.cuda_stream)
