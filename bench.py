@@ -59,6 +59,8 @@ def _args():
     ap.add_argument("--tokens", type=int, default=None)
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--private", type=int, default=None,
+                    help="PrivateBufferConfig.tokens (default: build_mesh's min(32, tokens))")
     return ap.parse_args()
 
 
@@ -285,16 +287,17 @@ def run_b200(a) -> None:
     E, R, H = wl["experts"], wl["topk"], wl["hidden"]
     spec = moe.RoutingSpec(ranks=n_gpu, experts=E, max_tokens=tokens, topk=R, hidden=H,
                            elem_size=wl["elem"], scales=wl["scales"], comb_elem_size=2, comb_scales=0)
+    priv = moe.PrivateBufferConfig(a.private) if a.private is not None else None
     if world > 1:
         import torch.distributed as dist
         # setup-only plumbing (IPC-handle exchange, barriers, max-over-ranks
         # of the timings); the data path is the txb kernels over NVLink
         dist.init_process_group("gloo")
         eng = TransferEngine(NvlinkFabric(group=dist.group.WORLD), device=local)
-        rk = moe.connect_process_group(eng, spec)
+        rk = moe.connect_process_group(eng, spec, private=priv)
     else:
         eng = TransferEngine(NvlinkFabric(), device=local)
-        rk = moe.build_mesh([eng], spec)[0]
+        rk = moe.build_mesh([eng], spec, private=priv)[0]
     rk.record_stats = False
     x, routes, w = _inputs(wl, rank, tokens)
     xd = torch.from_numpy(x).to(dev).to(torch.bfloat16)
@@ -457,7 +460,7 @@ def run_b200(a) -> None:
                    "routing": f"{wl['routing']} top-{R}", "l2": "flushed before every step (512 MiB write)",
                    "timing": "public-API step captured as a CUDA graph; CUDA event nodes inside the graph around "
                              "the step (device time, graph launch excluded), p50 over steps of the max over ranks",
-                   "parallelism": f"ep{n_gpu}"},
+                   "parallelism": f"ep{n_gpu}", "private_tokens": rk.private_tokens},
         "p90_us": round(float(np.percentile(tot, 90)), 2),
         "p99_us": round(float(np.percentile(tot, 99)), 2),
         "p50_l2_warm_us": round(float(np.median(b2b)), 2),

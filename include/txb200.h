@@ -48,6 +48,7 @@ extern "C" {
 #define TXB_EV_WAIT_COMBINE 0x20u   /* timed out waiting for combine writes        */
 #define TXB_EV_CAPACITY 0x40u       /* destination needs more slots than capacity  */
 #define TXB_EV_WAIT_IMM 0x80u       /* txb_imm_wait timeout (engine primitive)     */
+#define TXB_EV_WAIT_PRIV 0x100u     /* timed out waiting for speculative private rows */
 
 /* Row encodings (RoutingSpec.elem_size, moe.py:40-50; 2 = bf16 extension). */
 #define TXB_ELEM_FP8 1
@@ -73,6 +74,10 @@ typedef struct txb_moe_shape {
   int32_t device; /* CUDA device of this rank's region and stream */
   int32_t single_device; /* 1 when every rank of the mesh lives on this device:
                             completion fences drop from .sys to .gpu scope */
+  int32_t priv_tokens;   /* speculative private rows per source (PrivateBufferConfig.tokens,
+                            moe.py:92-102; 0..max_tokens): a source stores the first
+                            priv_tokens rows of its slab for a peer into that peer's private
+                            slab before the route exchange completes (moe.py:556-582) */
   /* derived by txb_moe_plan */
   int32_t local_experts;
   int64_t payload_bytes;  /* dispatch row bytes  = hidden*elem + 4*scales */
@@ -80,7 +85,7 @@ typedef struct txb_moe_shape {
   int64_t capacity;       /* N*T*max(R, L) (moe.py:80-83)                 */
   int64_t grouped_rows;   /* allocated grouped rows (tight bound + padding) */
   int64_t comb_rows;      /* T*R */
-  uint64_t off_flags, off_route, off_grouped, off_comb, region_bytes;
+  uint64_t off_flags, off_route, off_grouped, off_comb, off_priv, region_bytes;
 } txb_moe_shape;
 
 /* ------------------------------------------------------------ runtime */
@@ -177,8 +182,12 @@ int txb_moe_barrier(const txb_moe_shape* s, const txb_moe_bufs* b, uint64_t time
 
 /* Read the rank's latched error word and counters (synchronous, on a
  * private non-blocking stream; for the host's ProtocolError diagnostics,
- * moe.py:869-899).  counters receives [step, tok_ctr, tok_target,
- * comb_ctr, comb_target] then route_tag[2][N] and done[N]; NULL skips. */
+ * moe.py:869-899).  counters receives [step, tok_ctr, tok_target, comb_ctr,
+ * comb_target, priv_ctr[0], priv_ctr[1], priv_target[0], priv_target[1],
+ * priv_step] (10 words), then route_tag[2][N], then seven [N] lanes: done,
+ * tok_src, tok_src_target, comb_src, comb_src_target, priv_src,
+ * priv_src_target (rows received from / expected of each source rank);
+ * 10 + 9N words in all.  NULL skips. */
 int txb_moe_status(const txb_moe_shape* s, void* region, uint32_t* err, uint64_t* counters,
                    int64_t ncounters);
 

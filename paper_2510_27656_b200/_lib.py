@@ -33,6 +33,7 @@ EV_WAIT_BARRIER = 0x10
 EV_WAIT_COMBINE = 0x20
 EV_CAPACITY = 0x40
 EV_WAIT_IMM = 0x80
+EV_WAIT_PRIV = 0x100
 
 SRC_ROWS, SRC_F32, SRC_BF16 = 0, 1, 2
 
@@ -45,11 +46,11 @@ class Shape(C.Structure):
         ("topk", C.c_int32), ("hidden", C.c_int32), ("elem_size", C.c_int32),
         ("scales", C.c_int32), ("comb_elem_size", C.c_int32), ("comb_scales", C.c_int32),
         ("me", C.c_int32), ("device", C.c_int32), ("single_device", C.c_int32),
-        ("local_experts", C.c_int32),
+        ("priv_tokens", C.c_int32), ("local_experts", C.c_int32),
         ("payload_bytes", C.c_int64), ("comb_bytes", C.c_int64), ("capacity", C.c_int64),
         ("grouped_rows", C.c_int64), ("comb_rows", C.c_int64),
         ("off_flags", C.c_uint64), ("off_route", C.c_uint64), ("off_grouped", C.c_uint64),
-        ("off_comb", C.c_uint64), ("region_bytes", C.c_uint64),
+        ("off_comb", C.c_uint64), ("off_priv", C.c_uint64), ("region_bytes", C.c_uint64),
     ]
 
 

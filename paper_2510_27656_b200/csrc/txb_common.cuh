@@ -149,7 +149,8 @@ struct Flags {
   uint64_t done[TXB_MAX_RANKS];          // [peer] = last step whose reads of this region finished (published by the peer's next route phase)
   uint64_t tok_ctr;                      // rows received (dispatch)
   uint64_t comb_ctr;                     // rows received (combine)
-  uint64_t pad0[6];
+  uint64_t priv_ctr[2];                  // [step parity] speculative private rows received
+  uint64_t pad0[4];
   // local-only state (written by this rank's kernels, in stream order)
   uint64_t step;         // last completed step (every kernel of step k reads k-1)
   uint64_t tok_target;   // cumulative expected tok_ctr
@@ -164,6 +165,24 @@ struct Flags {
   uint64_t gbar_arrive;  // monotone grid-barrier counter (+TXB_MAX_CTAS per barrier)
   uint64_t bar[TXB_MAX_RANKS];  // [peer] = last barrier epoch peer reached
   uint32_t phase_cnt[16];       // send-list fill per phase (large batches, this step)
+  // speculative private rows (moe.py:556-582): cumulative expected
+  // priv_ctr per step parity (advanced at the end of each step by that
+  // step's count, priv_step, which the dispatch books once the route
+  // matrix is known)
+  uint64_t priv_target[2];
+  uint64_t priv_step;
+  uint64_t pad3;
+  // Per-source lanes, for the timeout diagnostics only (moe.py:874-899):
+  // every signal also adds its count to the slot of its source rank, and
+  // the receiver books the cumulative count it expects from each source,
+  // so a timeout names the ranks that have not delivered.  The waits use
+  // the aggregate counters above.
+  uint64_t tok_src[TXB_MAX_RANKS];     // [source] token rows received (peer-written)
+  uint64_t comb_src[TXB_MAX_RANKS];    // [source] combine rows received (peer-written)
+  uint64_t priv_src[TXB_MAX_RANKS];    // [source] private rows received (peer-written)
+  uint64_t tok_src_t[TXB_MAX_RANKS];   // [source] cumulative expected (local)
+  uint64_t comb_src_t[TXB_MAX_RANKS];
+  uint64_t priv_src_t[TXB_MAX_RANKS];
 };
 
 __host__ __device__ inline Flags* flags_of(void* region, const txb_moe_shape& s) {
@@ -199,6 +218,24 @@ __host__ __device__ inline uint64_t* tokt_of(void* region, const txb_moe_shape& 
 }
 __host__ __device__ inline int32_t* srctok_of(void* region, const txb_moe_shape& s) {
   return reinterpret_cast<int32_t*>(tokc_of(region, s) + 2 * (uint64_t)s.max_tokens);
+}
+
+// Speculative private slabs (PrivateBufferConfig, moe.py:92-102, 556-582):
+// rows [2 parity][N source][priv_tokens][P] at off_priv, then the origin
+// token index of each row, i32 [2][N][priv_tokens] (for per-token combine
+// completion).  A source stores the first priv_tokens rows of its slab for
+// this rank here before the route exchange has finished; the receiver moves
+// them to their grouped rows once the layout is known.  Step parity double
+// buffering makes the early stores safe without a wait: a source writes
+// parity p at step k only after it saw this rank's end-of-step k-2 barrier.
+__host__ __device__ inline uint8_t* priv_rows_of(void* region, const txb_moe_shape& s, int parity, int src) {
+  return reinterpret_cast<uint8_t*>(region) + s.off_priv +
+         ((uint64_t)(parity * s.ranks + src) * (uint64_t)s.priv_tokens) * (uint64_t)s.payload_bytes;
+}
+__host__ __device__ inline int32_t* privsrc_of(void* region, const txb_moe_shape& s, int parity, int src) {
+  return reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(region) + s.off_priv +
+                                    2ull * s.ranks * s.priv_tokens * (uint64_t)s.payload_bytes) +
+         (uint64_t)(parity * s.ranks + src) * s.priv_tokens;
 }
 
 // ------------------------------------------------------------- block scan

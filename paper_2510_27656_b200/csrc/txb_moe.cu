@@ -81,7 +81,7 @@ __device__ __forceinline__ uint64_t cur_step(Flags* f) {
 __host__ __device__ inline size_t smem_route(int E, int nwarps) { return (size_t)(1 + nwarps) * E * 4 + 16; }
 __host__ __device__ inline size_t smem_layout(int E) { return (size_t)(2 * E + 1) * 4; }
 __host__ __device__ inline size_t smem_recv(int N, int L) {
-  return (size_t)(3 * N * L + 2 + 2 * L + L * (N + 1) + N) * 4;
+  return (size_t)(3 * N * L + 2 + 2 * L + L * (N + 1) + N + N + (N + 1)) * 4;
 }
 __host__ __device__ inline size_t smem_cmat(int N, int E) { return ((size_t)N * E * 4 + 15) / 16 * 16; }
 // layout scratch [0, recv_offset), receive tables [recv_offset, cmat_offset),
@@ -107,8 +107,11 @@ struct Shared {  // static shared state of one CTA
   uint32_t bad, fail, recv_me, direct;
   int tmp[33];
   float red[33];
-  uint32_t cnt[TXB_MAX_RANKS];
-  uint8_t* dstp[kMaxTopk];
+  uint32_t cnt[TXB_MAX_RANKS];   // rows stored per destination (token / combine counter)
+  uint32_t pcnt[TXB_MAX_RANKS];  // speculative private rows stored per destination
+  int32_t sst[TXB_MAX_RANKS];    // send_start[me][d]: first slab slot of destination d
+  uint8_t* dstp[kMaxTopk];       // grouped-row destination of each own copy (null: private)
+  uint8_t* pdst[kMaxTopk];       // private-slab destination of each own copy (null: none)
   uint32_t own_rank[kMaxOwn];
   int32_t own_e[kMaxOwn];
   int32_t own_i[kMaxOwn];
@@ -485,6 +488,15 @@ __device__ void route_publish(const txb_moe_shape& s, void* const* peers, Flags*
         st_relaxed_sys(&pf->done[s.me], step - 1);
       }
     }
+    if (!bad)
+      #pragma unroll 1
+      for (int d = lane; d < N; d += 32) {
+        if (d == s.me) continue;
+        uint32_t c = 0;
+        #pragma unroll 1
+        for (int le = 0; le < L; ++le) c += hist[d * L + le];
+        f->comb_src_t[d] += c;
+      }
     if (lane == 0) {
       f->comb_target += bad ? 0 : (uint64_t)(n * s.topk) - self;
       if (bad) atomicOr(&f->err, bad);
@@ -544,13 +556,17 @@ __device__ bool wait_routes(const txb_moe_shape& s, Flags* f, const uint64_t* C,
 // ------------------------------------------------------------------- P3
 
 // baseg[e] = grouped row on owner(e) where this rank's first copy for e
-// lands: group_starts[le] + sum_{s' < me} counts[s', e].
+// lands: group_starts[le] + sum_{s' < me} counts[s', e];
+// sh.sst[d] = send_start[me][d] (moe.py:221-222), the slab base the
+// private-copy test of copy_dest measures from.
 __device__ bool dispatch_layout(const txb_moe_shape& s, const uint32_t* C, int* baseg, int* padded, Flags* f,
-                                bool book, Shared& sh) {
+                                Shared& sh) {
   const int N = s.ranks, E = s.experts, L = s.local_experts, tid = threadIdx.x;
-  if (tid == 0) {
-    sh.recv_me = 0;
-    sh.fail = 0;
+  if (tid == 0) sh.fail = 0;
+  for (int d = tid; d < N; d += blockDim.x) {
+    int a = 0;
+    for (int le = 0; le < L; ++le) a += (int)C[s.me * E + d * L + le];
+    sh.sst[d] = a;
   }
   __syncthreads();
   for (int e = tid; e < E; e += blockDim.x) {
@@ -562,7 +578,14 @@ __device__ bool dispatch_layout(const txb_moe_shape& s, const uint32_t* C, int* 
     }
     padded[e] = pad_up(col);
     baseg[e] = pre;
-    if (book && e / L == s.me) atomicAdd(&sh.recv_me, (uint32_t)col);
+  }
+  if (tid == 0) {
+    int run = 0;
+    for (int d = 0; d < N; ++d) {
+      const int v = sh.sst[d];
+      sh.sst[d] = run;
+      run += v;
+    }
   }
   __syncthreads();
   const int tot = block_scan_i32(padded, E, sh.tmp);
@@ -577,25 +600,87 @@ __device__ bool dispatch_layout(const txb_moe_shape& s, const uint32_t* C, int* 
     if (tid == 0) atomicOr(&f->err, fl);
     return false;
   }
-  if (book && tid == 0) f->tok_target += sh.recv_me;
   return true;
+}
+
+// Receive-side bookkeeping of one step, once the route matrix C is known
+// (one warp, CTA 0): the rows this rank expects on its token counter --
+// every copy routed to its experts except the speculative private rows,
+// min(priv_tokens, assigned[q][me]) from each other source q (moe.py:
+// 556-582, DispatchLayout.private_take) -- and this step's private rows
+// (priv_step, added to priv_target at the end of the step).  The per-source
+// expectations feed the timeout diagnostics.
+__device__ void book_recv(const txb_moe_shape& s, Flags* f, const uint32_t* C, int lane) {
+  const int N = s.ranks, E = s.experts, L = s.local_experts, me = s.me;
+  uint32_t tok = 0, pv = 0;
+  #pragma unroll 1
+  for (int q = lane; q < N; q += 32) {
+    uint32_t a = 0;
+    #pragma unroll 1
+    for (int le = 0; le < L; ++le) a += C[q * E + me * L + le];
+    const uint32_t take = (q != me && s.priv_tokens > 0) ? min(a, (uint32_t)s.priv_tokens) : 0u;
+    f->tok_src_t[q] += a - take;
+    f->priv_src_t[q] += take;
+    tok += a - take;
+    pv += take;
+  }
+  for (int o = 16; o; o >>= 1) {
+    tok += __shfl_xor_sync(0xffffffffu, tok, o);
+    pv += __shfl_xor_sync(0xffffffffu, pv, o);
+  }
+  if (lane == 0) {
+    f->tok_target += tok;
+    f->priv_step = pv;
+  }
 }
 
 // DECODE layout: this CTA's single token needs only its own R copies'
 // send slots and destination rows, so each comes from one warp reduction
 // instead of block-wide scans (one warp per copy, no block barrier).
 // pos = sum_{e' < e} hist[e'] + rank (moe.py:514-521).
+//
+// With `peers` (EP > 1, priv_tokens > 0) it also places the speculative
+// private copies (moe.py:556-582): a copy whose slot in its destination's
+// slab, pos - send_start[me][d], is below priv_tokens goes to d's private
+// slab for this rank, sh.pdst[k] (counted in sh.pcnt); every other copy
+// gets sh.pdst[k] = null.  That needs only this rank's own counts, so the
+// copy can be stored before the route exchange has finished.
 __device__ void own_positions(const txb_moe_shape& s, const uint32_t* hist, int64_t* pos, uint32_t bad,
-                              Shared& sh, const Grp& g = Grp::cta()) {
+                              Shared& sh, const Grp& g = Grp::cta(), void* const* peers = nullptr,
+                              uint64_t step = 0) {
   const int lane = g.tid & 31, warp = g.tid >> 5, nwarp = g.nt >> 5;
+  const int L = s.local_experts;
+  const bool priv = peers && s.priv_tokens > 0 && s.ranks > 1 && !bad;
   #pragma unroll 1
   for (int k = warp; k < s.topk; k += nwarp) {
     const int e = sh.own_e[k];
-    int acc = 0;
+    const int d0 = e >= 0 ? (e / L) * L : 0;
+    int acc = 0, acc0 = 0;
     #pragma unroll 1
-    for (int x = lane; x < (bad ? 0 : e); x += 32) acc += (int)hist[x];
-    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) pos[sh.own_i[k]] = bad ? -1 : (int64_t)acc + sh.own_rank[k];
+    for (int x = lane; x < (bad ? 0 : e); x += 32) {
+      const int h = (int)hist[x];
+      acc += h;
+      if (x < d0) acc0 += h;
+    }
+    for (int o = 16; o; o >>= 1) {
+      acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      acc0 += __shfl_xor_sync(0xffffffffu, acc0, o);
+    }
+    if (lane == 0) {
+      pos[sh.own_i[k]] = bad ? -1 : (int64_t)acc + sh.own_rank[k];
+      uint8_t* pd = nullptr;
+      const int d = d0 / L;
+      if (priv && d != s.me) {
+        const int sidx = acc - acc0 + (int)sh.own_rank[k];
+        if (sidx < s.priv_tokens) {
+          const int par = (int)(step & 1);
+          pd = priv_rows_of(peers[d], s, par, s.me) + (int64_t)sidx * s.payload_bytes;
+          if (tok_mode(s)) privsrc_of(peers[d], s, par, s.me)[sidx] = sh.own_i[k] / s.topk;
+          atomicAdd(&sh.pcnt[d], 1u);
+        }
+      }
+      sh.pdst[k] = pd;
+    }
   }
 }
 
@@ -607,6 +692,13 @@ __device__ void own_dests(const txb_moe_shape& s, const uint32_t* C, void* const
   const int lane = g.tid & 31, warp = g.tid >> 5, nwarp = g.nt >> 5;
   #pragma unroll 1
   for (int k = warp; k < s.topk; k += nwarp) {
+    if (sh.pdst[k]) {  // stored to the owner's private slab (own_positions)
+      if (lane == 0) {
+        sh.dstp[k] = nullptr;
+        gidx[sh.own_i[k]] = -1;
+      }
+      continue;
+    }
     const int e = sh.own_e[k], d = e / L, le = e - d * L;
     int acc = 0;
     #pragma unroll 1
@@ -636,10 +728,35 @@ __device__ void own_dests(const txb_moe_shape& s, const uint32_t* C, void* const
 
 // Destination rows of token t's copies (kt-th token of this CTA) into
 // sh.dstp; books gidx and per-destination counts.
+// Copy i (token t = i / R) to destination d: its private-slab row when its
+// slab slot pos[i] - send_start[me][d] is below priv_tokens (d != me), else
+// its grouped row baseg[e] + rank.  Books gidx, srctok and the counts.
+__device__ __forceinline__ uint8_t* copy_dest(const txb_moe_shape& s, void* const* peers, const int* baseg,
+                                              const int64_t* pos, int32_t* gidx, uint64_t step, int64_t i, int e,
+                                              int rank, Shared& sh) {
+  const int d = e / s.local_experts;
+  const int64_t t = i / s.topk;
+  if (d != s.me && s.priv_tokens > 0) {
+    const int64_t sidx = pos[i] - sh.sst[d];
+    if (sidx < s.priv_tokens) {
+      const int par = (int)(step & 1);
+      gidx[i] = -1;
+      if (tok_mode(s)) privsrc_of(peers[d], s, par, s.me)[sidx] = (int32_t)t;
+      atomicAdd(&sh.pcnt[d], 1u);
+      return priv_rows_of(peers[d], s, par, s.me) + sidx * s.payload_bytes;
+    }
+  }
+  const int64_t g = (int64_t)baseg[e] + rank;
+  gidx[i] = d == s.me ? (int32_t)g : -1;
+  if (tok_mode(s)) srctok_of(peers[d], s)[g] = (int32_t)t;
+  atomicAdd(&sh.cnt[d], 1u);
+  return grouped_of(peers[d], s) + g * s.payload_bytes;
+}
+
 __device__ __forceinline__ void token_dests(const txb_moe_shape& s, const int64_t* routes, const int32_t* rank_in,
-                                            int32_t* gidx, void* const* peers, const int* baseg, int64_t t, int kt,
-                                            Shared& sh) {
-  const int R = s.topk, L = s.local_experts, tid = threadIdx.x;
+                                            const int64_t* pos, int32_t* gidx, void* const* peers, const int* baseg,
+                                            int64_t t, int kt, uint64_t step, Shared& sh) {
+  const int R = s.topk, tid = threadIdx.x;
   if (tid < R) {
     int e, rank;
     if (sh.direct) {  // experts and ranks of this CTA's copies are in smem
@@ -649,12 +766,7 @@ __device__ __forceinline__ void token_dests(const txb_moe_shape& s, const int64_
       e = (int)routes[t * R + tid];
       rank = rank_in[t * R + tid];
     }
-    const int d = e / L;
-    const int64_t g = (int64_t)baseg[e] + rank;
-    sh.dstp[tid] = grouped_of(peers[d], s) + g * s.payload_bytes;
-    gidx[t * R + tid] = d == s.me ? (int32_t)g : -1;
-    if (tok_mode(s)) srctok_of(peers[d], s)[g] = (int32_t)t;
-    atomicAdd(&sh.cnt[d], 1u);
+    sh.dstp[tid] = copy_dest(s, peers, baseg, pos, gidx, step, t * R + tid, e, rank, sh);
   }
   __syncthreads();
 }
@@ -675,12 +787,13 @@ __device__ __noinline__ void dispatch_row_slow(const txb_moe_shape& s, const voi
 template <int SRC, int ELEM>
 __device__ __noinline__ void dispatch_tokens(const txb_moe_shape& s, const void* x, int64_t t0, int64_t t1,
                                              int64_t dt, const int64_t* routes, const int32_t* rank_in,
-                                             int32_t* gidx, void* const* peers, const int* baseg, Shared& sh) {
+                                             const int64_t* pos, int32_t* gidx, void* const* peers,
+                                             const int* baseg, uint64_t step, Shared& sh) {
   const int R = s.topk, tid = threadIdx.x;
   const int64_t P = s.payload_bytes;
   int kt = 0;
   for (int64_t t = t0; t < t1; t += dt, ++kt) {
-    token_dests(s, routes, rank_in, gidx, peers, baseg, t, kt, sh);
+    token_dests(s, routes, rank_in, pos, gidx, peers, baseg, t, kt, step, sh);
     if constexpr (SRC == TXB_SRC_ROWS) {
       const uint8_t* src = reinterpret_cast<const uint8_t*>(x) + t * P;
       if (vec_width(src, sh.dstp[0], P) == 16) {
@@ -708,8 +821,9 @@ __device__ __noinline__ void dispatch_tokens(const txb_moe_shape& s, const void*
 // dispatch_tokens.
 template <int SRC, int ELEM>
 __device__ __noinline__ bool dispatch_tokens_flat(const txb_moe_shape& s, const void* x, int64_t t0, int64_t t1,
-                                                  const int64_t* routes, const int32_t* rank_in, int32_t* gidx,
-                                                  void* const* peers, const int* baseg, uint8_t** dp, int cap,
+                                                  const int64_t* routes, const int32_t* rank_in,
+                                                  const int64_t* pos, int32_t* gidx, void* const* peers,
+                                                  const int* baseg, uint8_t** dp, int cap, uint64_t step,
                                                   Shared& sh) {
   if constexpr (ELEM == 1 && SRC != TXB_SRC_ROWS) {
     return false;  // fp8 rows need a per-token amax across the CTA
@@ -724,13 +838,7 @@ __device__ __noinline__ bool dispatch_tokens_flat(const txb_moe_shape& s, const 
     #pragma unroll 1
     for (int k = tid; k < m; k += nt) {
       const int64_t i = t0 * R + k;
-      const int e = (int)routes[i];
-      const int d = e / L;
-      const int64_t g = (int64_t)baseg[e] + rank_in[i];
-      dp[k] = grouped_of(peers[d], s) + g * P;
-      gidx[i] = d == s.me ? (int32_t)g : -1;
-      if (tok_mode(s)) srctok_of(peers[d], s)[g] = (int32_t)(i / R);
-      atomicAdd(&sh.cnt[d], 1u);
+      dp[k] = copy_dest(s, peers, baseg, pos, gidx, step, i, (int)routes[i], rank_in[i], sh);
     }
     __syncthreads();
     #pragma unroll 1
@@ -746,23 +854,54 @@ __device__ __noinline__ bool dispatch_tokens_flat(const txb_moe_shape& s, const 
   }
 }
 
+// Per-token completion (tok_mode): book the copies of tokens t0, t0 + dt,
+// ... < t1 that another rank serves -- the rows that will come back through
+// tokc[t].  Every dispatch path books them, so tokc and tokt stay in step
+// whichever path (fused, split) a step takes.
+__device__ __forceinline__ void book_tok_targets(const txb_moe_shape& s, const int64_t* routes, void* region,
+                                                 int64_t t0, int64_t t1, int64_t dt) {
+  if (!tok_mode(s)) return;
+  uint64_t* tokt = tokt_of(region, s);
+  #pragma unroll 1
+  for (int64_t t = t0 + (int64_t)threadIdx.x * dt; t < t1; t += (int64_t)blockDim.x * dt) {
+    int remote = 0;
+    for (int j = 0; j < s.topk; ++j) remote += (int)routes[t * s.topk + j] / s.local_experts != s.me;
+    tokt[t] += remote;
+  }
+}
+
 // Completion of this CTA's stores: one release fence, then a relaxed add of
-// the row count on every destination's counter at byte offset `field`.
-__device__ void signal_counts(const txb_moe_shape& s, void* const* peers, size_t field, Shared& sh) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    bool any = false;
-    #pragma unroll 1
-    for (int d = 0; d < s.ranks; ++d) any |= sh.cnt[d] != 0;
-    if (any) {
-      fence_release(s.single_device);
-      #pragma unroll 1
-      for (int d = 0; d < s.ranks; ++d)
-        if (sh.cnt[d])
-          red_relaxed_sys_add(reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(flags_of(peers[d], s)) + field),
-                              sh.cnt[d]);
+// the row counts on every destination's counters -- sh.cnt on the token
+// (kind 0) or combine (kind 1) counter, and for kind 0 sh.pcnt on the
+// private-row counter of this step's parity -- each also on the
+// destination's per-source slot of this rank (diagnostics).  Called by one
+// thread after the stores it covers are ordered before it (a barrier).
+__device__ void signal_rows_thread(const txb_moe_shape& s, void* const* peers, int kind, uint64_t step, Shared& sh,
+                                   bool with_main, bool with_priv) {
+  const int N = s.ranks, me = s.me, par = (int)(step & 1);
+  bool any = false;
+  #pragma unroll 1
+  for (int d = 0; d < N; ++d) any |= (with_main && sh.cnt[d]) || (with_priv && sh.pcnt[d]);
+  if (!any) return;
+  fence_release(s.single_device);
+  #pragma unroll 1
+  for (int d = 0; d < N; ++d) {
+    Flags* pf = flags_of(peers[d], s);
+    if (with_main && sh.cnt[d]) {
+      red_relaxed_sys_add(kind == 0 ? &pf->tok_ctr : &pf->comb_ctr, sh.cnt[d]);
+      red_relaxed_sys_add(kind == 0 ? &pf->tok_src[me] : &pf->comb_src[me], sh.cnt[d]);
+    }
+    if (with_priv && sh.pcnt[d]) {
+      red_relaxed_sys_add(&pf->priv_ctr[par], sh.pcnt[d]);
+      red_relaxed_sys_add(&pf->priv_src[me], sh.pcnt[d]);
+      sh.pcnt[d] = 0;
     }
   }
+}
+
+__device__ void signal_counts(const txb_moe_shape& s, void* const* peers, int kind, uint64_t step, Shared& sh) {
+  __syncthreads();
+  if (threadIdx.x == 0) signal_rows_thread(s, peers, kind, step, sh, true, kind == 0);
 }
 
 // ------------------------------------------------------------------- P5
@@ -781,9 +920,12 @@ struct RecvTables {
   int* gsize;    // [L]
   int* srcpre;   // [L][N+1]
   int* pre_all;  // [N] sum_{e' < me*L} C[q][e']
+  int* asg;      // [N] assigned[q][me]: copies source q routes to this rank
+  int* take;     // [N+1] private rows from q, min(priv_tokens, asg[q]) (0 for me); [N] = sum
 };
 
-__device__ __forceinline__ RecvTables recv_carve(const txb_moe_shape& s, int* sm) {
+__device__ __forceinline__ RecvTables recv_carve(const txb_moe_shape& s, const int* sm_c) {
+  int* sm = const_cast<int*>(sm_c);
   const int N = s.ranks, L = s.local_experts;
   RecvTables t;
   t.a = sm;
@@ -794,6 +936,8 @@ __device__ __forceinline__ RecvTables recv_carve(const txb_moe_shape& s, int* sm
   t.gsize = t.retbase + N * L;
   t.srcpre = t.gsize + L;
   t.pre_all = t.srcpre + L * (N + 1);
+  t.asg = t.pre_all + N;
+  t.take = t.asg + N;
   return t;
 }
 
@@ -814,14 +958,30 @@ __device__ __forceinline__ void recv_tables_body(const txb_moe_shape& s, const u
     const int warp = tid >> 5, lane = tid & 31, nwarp = nt >> 5;
     #pragma unroll 1
     for (int q = warp; q < N; q += nwarp) {
-      int acc = 0;
+      int acc = 0, a = 0;
       #pragma unroll 1
       for (int e = lane; e < me * L; e += 32) acc += (int)C[q * E + e];
-      for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (lane == 0) t.pre_all[q] = acc;
+      #pragma unroll 1
+      for (int e = lane; e < L; e += 32) a += (int)C[q * E + me * L + e];
+      for (int o = 16; o; o >>= 1) {
+        acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+      }
+      if (lane == 0) {
+        t.pre_all[q] = acc;
+        t.asg[q] = a;
+        t.take[q] = (q != me && s.priv_tokens > 0) ? min(a, s.priv_tokens) : 0;
+      }
     }
   }
   g.sync();
+  if (tid < 32) {
+    int v = 0;
+    #pragma unroll 1
+    for (int q = tid; q < N; q += 32) v += t.take[q];
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (tid == 0) t.take[N] = v;
+  }
   stamp(b, 16);
   #pragma unroll 1
   for (int le = tid; le < L; le += nt) {
@@ -1046,6 +1206,76 @@ __device__ __noinline__ void recv_rows_flat(const txb_moe_shape& s, int* sm, int
   }
 }
 
+// Speculative private rows (moe.py:693-698, private rows to the slab heads):
+// source q's first take[q] slab rows sit in this rank's private slab of the
+// step's parity; each goes to its grouped row.  Slab slot k of source q is
+// copy kk = k - off(le) of local expert le, where off(le) = sum_{le' < le}
+// a[q][le'] = rowbase[q*L+le] - rowbase[q*L] (the last le with off(le) <=
+// k), so its grouped row is gstart[le] + srcpre[le][q] + kk (SURVEY.md App.
+// A).  Work items are spread over warps (gw of ngw); a warp waits once,
+// before its first row, for the step's private counter.
+__device__ void recv_private_rows(const txb_moe_shape& s, const int* sm, void* region, uint64_t step,
+                                  uint64_t timeout_ns, int gw, int ngw, int lane) {
+  const int N = s.ranks, L = s.local_experts, Pt = s.priv_tokens;
+  if (Pt <= 0 || N == 1) return;
+  const RecvTables t = recv_carve(s, sm);
+  if (t.take[N] == 0) return;
+  Flags* f = flags_of(region, s);
+  const int par = (int)(step & 1);
+  const int64_t P = s.payload_bytes;
+  uint8_t* G = grouped_of(region, s);
+  bool waited = false;
+  #pragma unroll 1
+  for (int i = gw; i < N * Pt; i += ngw) {
+    const int q = i / Pt, k = i - q * Pt;
+    if (k >= t.take[q]) continue;
+    if (!waited) {
+      uint32_t ok = 1;
+      if (lane == 0) {
+        const uint64_t target = *reinterpret_cast<volatile uint64_t*>(&f->priv_target[par]) + (uint64_t)t.take[N];
+        ok = spin_ge(&f->priv_ctr[par], target, globaltimer() + timeout_ns) ? 1u : 0u;
+        if (!ok) atomicOr(&f->err, TXB_EV_WAIT_PRIV);
+      }
+      if (!__shfl_sync(0xffffffffu, ok, 0)) return;
+      waited = true;
+    }
+    const int* rb = t.rowbase + q * L;
+    int lo = 0, span = L;  // last le with off(le) <= k, 32 candidates per round
+    #pragma unroll 1
+    while (span > 1) {
+      const int stp = (span + 31) >> 5;
+      const int cand = lo + lane * stp;
+      const unsigned m = __ballot_sync(0xffffffffu, cand < lo + span && rb[cand] - rb[0] <= k);
+      const int last = 31 - __clz(m);
+      const int nlo = lo + last * stp;
+      span = min(stp, lo + span - nlo);
+      lo = nlo;
+    }
+    const int le = lo, kk = k - (rb[le] - rb[0]);
+    const int g = t.gstart[le] + t.srcpre[le * (N + 1) + q] + kk;
+    const uint8_t* src = priv_rows_of(region, s, par, q) + (int64_t)k * P;
+    uint8_t* dst = G + (int64_t)g * P;
+    if ((P & 15) == 0) {
+      const int4* sv = reinterpret_cast<const int4*>(src);
+      int4* dv = reinterpret_cast<int4*>(dst);
+      const int n16 = (int)(P >> 4);
+      #pragma unroll 1
+      for (int c0 = 0; c0 < n16; c0 += 128) {
+        int4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (c0 + lane + 32 * u < n16) v[u] = sv[c0 + lane + 32 * u];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (c0 + lane + 32 * u < n16) dv[c0 + lane + 32 * u] = v[u];
+      }
+    } else {
+      copy_row(dst, src, P, lane, 32);
+    }
+    if (lane == 0 && tok_mode(s)) srctok_of(region, s)[g] = privsrc_of(region, s, par, q)[k];
+  }
+}
+
 // The step's error word into info (what dispatch_recv reads); also on the
 // early-return paths, where CTA 0 has latched its own failure.
 __device__ void publish_err(Flags* f, int64_t* info, int L) {
@@ -1080,10 +1310,13 @@ __device__ void combine_send_rows(const txb_moe_shape& s, Flags* f, const uint8_
   const int64_t Pc = s.comb_bytes;
   const int lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
   const bool vec = (Pc % 16 == 0) && (ld % 16 == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
-  if (vec && tok_mode(s)) {
+  if (tok_mode(s)) {
     // per-token completion: each warp returns whole rows, walking the
     // (phase-ordered) list grid-stride, and after every kBatch rows fences
-    // once and release-adds the origin token's counter of each of them
+    // once and release-adds the origin token's counter of each of them.
+    // Every row shape takes this branch (rows that are not 16-byte
+    // vectorisable are copied with copy_row), because the origin's reduce
+    // waits on tokc whenever tok_mode holds.
     constexpr int kBatch = 4;
     const int32_t* srct = srctok_of(peers[s.me], s);
     const int n16 = (int)(Pc >> 4);
@@ -1103,17 +1336,21 @@ __device__ void combine_send_rows(const txb_moe_shape& s, Flags* f, const uint8_
     for (int r = gw; r < total; r += ngw) {  // the list is in phase order: grid-stride keeps it
       const int g = send_list[r];
       const int q = (int)sources[g];
-      const int4* src = reinterpret_cast<const int4*>(out + (int64_t)g * ld);
-      int4* dst = reinterpret_cast<int4*>(comb_of(peers[q], s) + (int64_t)ret[g] * Pc);
-      #pragma unroll 1
-      for (int c0 = 0; c0 < n16; c0 += 128) {
-        int4 v[4];
+      if (vec) {
+        const int4* src = reinterpret_cast<const int4*>(out + (int64_t)g * ld);
+        int4* dst = reinterpret_cast<int4*>(comb_of(peers[q], s) + (int64_t)ret[g] * Pc);
+        #pragma unroll 1
+        for (int c0 = 0; c0 < n16; c0 += 128) {
+          int4 v[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (c0 + lane + 32 * u < n16) v[u] = src[c0 + lane + 32 * u];
+          for (int u = 0; u < 4; ++u)
+            if (c0 + lane + 32 * u < n16) v[u] = src[c0 + lane + 32 * u];
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (c0 + lane + 32 * u < n16) dst[c0 + lane + 32 * u] = v[u];
+          for (int u = 0; u < 4; ++u)
+            if (c0 + lane + 32 * u < n16) dst[c0 + lane + 32 * u] = v[u];
+        }
+      } else {
+        copy_row(comb_of(peers[q], s) + (int64_t)ret[g] * Pc, out + (int64_t)g * ld, Pc, lane, 32);
       }
       if (lane == npend) {
         pend_q = q;
@@ -1234,6 +1471,8 @@ __device__ void end_of_step(Flags* f, uint64_t step, int ncta) {
     if (t == (uint32_t)ncta - 1) {
       f->ticket = 0;
       f->send_cnt = 0;
+      f->priv_target[step & 1] += f->priv_step;
+      f->priv_step = 0;
       for (int ph = 0; ph < kPhases; ++ph) f->phase_cnt[ph] = 0;
       *reinterpret_cast<volatile uint64_t*>(&f->step) = step;
     }
@@ -1266,13 +1505,16 @@ k_dispatch(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, int64_t 
   uint32_t* C = reinterpret_cast<uint32_t*>(dsm + cmat_offset(s));
   if (!wait_routes(s, f, route_of(b.region, s, (int)(step & 1)), C, step, timeout_ns, sh)) return;
   int* baseg = reinterpret_cast<int*>(dsm);
-  if (!dispatch_layout(s, C, baseg, baseg + s.experts, f, blockIdx.x == 0, sh)) return;
+  if (!dispatch_layout(s, C, baseg, baseg + s.experts, f, sh)) return;
+  if (blockIdx.x == 0 && threadIdx.x < 32) book_recv(s, f, C, threadIdx.x);
   if (*reinterpret_cast<volatile uint32_t*>(&f->err) & (TXB_EV_ROUTE_RANGE | TXB_EV_ROUTE_DUP)) return;
-  for (int q = threadIdx.x; q < s.ranks; q += blockDim.x) sh.cnt[q] = 0;
+  for (int q = threadIdx.x; q < s.ranks; q += blockDim.x) sh.cnt[q] = sh.pcnt[q] = 0;
   if (threadIdx.x == 0) sh.direct = 0;
   __syncthreads();
-  dispatch_tokens<SRC, ELEM>(s, x, blockIdx.x, n, gridDim.x, routes, b.rank_scratch, b.gidx, b.peers, baseg, sh);
-  signal_counts(s, b.peers, offsetof(Flags, tok_ctr), sh);
+  dispatch_tokens<SRC, ELEM>(s, x, blockIdx.x, n, gridDim.x, routes, b.rank_scratch, b.pos, b.gidx, b.peers, baseg,
+                             step, sh);
+  book_tok_targets(s, routes, b.region, blockIdx.x, n, gridDim.x);
+  signal_counts(s, b.peers, 0, step, sh);
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -1287,15 +1529,21 @@ k_recv(txb_moe_shape s, txb_moe_bufs b, uint64_t timeout_ns) {
   recv_tables(s, C, rt, b.info, blockIdx.x, sh, b);
   recv_rows_flat(s, rt, b.rows, b.sources, b.ret_slot, grouped_of(b.region, s), b.dirty, b.send_list,
                  &f->send_cnt, blockIdx.x, gridDim.x, nullptr);
+  {
+    const int nw = blockDim.x >> 5;
+    recv_private_rows(s, rt, b.region, step, timeout_ns, blockIdx.x * nw + (threadIdx.x >> 5), gridDim.x * nw,
+                      threadIdx.x & 31);
+  }
+  __syncthreads();
   if (blockIdx.x == 0) wait_tokens(f, b.info, s.local_experts, timeout_ns);
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
 k_comb_send(txb_moe_shape s, txb_moe_bufs b, const uint8_t* __restrict__ out, int64_t ld) {
   __shared__ Shared sh;
-  combine_send_rows(s, flags_of(b.region, s), out, ld, b.peers, b.sources, b.ret_slot, b.send_list, blockIdx.x,
-                    gridDim.x, sh);
-  signal_counts(s, b.peers, offsetof(Flags, comb_ctr), sh);
+  Flags* f = flags_of(b.region, s);
+  combine_send_rows(s, f, out, ld, b.peers, b.sources, b.ret_slot, b.send_list, blockIdx.x, gridDim.x, sh);
+  signal_counts(s, b.peers, 1, cur_step(f), sh);
 }
 
 template <int ELEM>
@@ -1346,9 +1594,10 @@ k_dispatch_fused(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
     stamp(b, 14);
     finish_row_regs<SRC, ELEM>(raw, pre, sh.red);
     stamp(b, 1);
+    for (int q = threadIdx.x; q < s.ranks; q += blockDim.x) sh.cnt[q] = sh.pcnt[q] = 0;
+    __syncthreads();
     route_publish(s, b.peers, f, hist, step, n, bad, cta, ncta);
-    own_positions(s, hist, b.pos, bad, sh);
-    for (int q = threadIdx.x; q < s.ranks; q += blockDim.x) sh.cnt[q] = 0;
+    own_positions(s, hist, b.pos, bad, sh, Grp::cta(), b.peers, step);
     stamp(b, 2);
     // EP=1: the route matrix is this CTA's own histogram and the kernel
     // boundary orders the stores before any reader -- no exchange, fence,
@@ -1364,6 +1613,9 @@ k_dispatch_fused(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
     stamp(b, 3);
     if (!bad) {
       own_dests(s, Cm, b.peers, b.gidx, sh);
+      // private copies (late on this path) and grouped rows in one pass
+      if (threadIdx.x < s.topk && sh.pdst[threadIdx.x]) sh.dstp[threadIdx.x] = sh.pdst[threadIdx.x];
+      __syncthreads();
       stamp(b, 15);
       if (pre.ok) store_row_regs<SRC, ELEM>(pre, s.hidden, s.scales, sh.dstp, s.topk);
       else dispatch_row_slow<SRC, ELEM>(s, x, cta, sh);
@@ -1373,8 +1625,8 @@ k_dispatch_fused(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
     recv_tables_body<true>(s, Cm, rt, b.info, cta, sh, b);
     stamp(b, 4);
     if (!solo) {
-      if (cta == 0 && threadIdx.x == 0) f->tok_target += (uint64_t)recv_carve(s, rt).tot[1];
-      signal_counts(s, b.peers, offsetof(Flags, tok_ctr), sh);
+      if (cta == 0 && threadIdx.x < 32) book_recv(s, f, Cm, threadIdx.x);
+      signal_counts(s, b.peers, 0, step, sh);
     }
   } else {
     // contiguous token range per CTA, segmented counting with a grid barrier
@@ -1400,12 +1652,13 @@ k_dispatch_fused(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
     }
     stamp(b, 3);
     int* baseg = reinterpret_cast<int*>(dsm);
-    if (!dispatch_layout(s, Cm, baseg, baseg + s.experts, f, cta == 0 && !solo, sh)) {
+    if (!dispatch_layout(s, Cm, baseg, baseg + s.experts, f, sh)) {
       if (cta == 0) publish_err(f, b.info, s.local_experts);
       return;
     }
+    if (!solo && cta == 0 && threadIdx.x < 32) book_recv(s, f, Cm, threadIdx.x);
     recv_tables(s, Cm, rt, b.info, cta, sh, b);
-    for (int q = threadIdx.x; q < s.ranks; q += blockDim.x) sh.cnt[q] = 0;
+    for (int q = threadIdx.x; q < s.ranks; q += blockDim.x) sh.cnt[q] = sh.pcnt[q] = 0;
     __syncthreads();
     stamp(b, 4);
     if (!bad) {
@@ -1415,21 +1668,14 @@ k_dispatch_fused(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
       asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
       const size_t fo = flat_offset(s);
       const int cap = dyn > fo ? (int)((dyn - fo) / sizeof(uint8_t*)) : 0;
-      if (!dispatch_tokens_flat<SRC, ELEM>(s, x, t0, t1, routes, b.rank_scratch, b.gidx, b.peers, baseg,
-                                           reinterpret_cast<uint8_t**>(dsm + fo), cap, sh))
-        dispatch_tokens<SRC, ELEM>(s, x, t0, t1, 1, routes, b.rank_scratch, b.gidx, b.peers, baseg, sh);
-      if (tok_mode(s)) {
-        uint64_t* tokt = tokt_of(b.region, s);
-        #pragma unroll 1
-        for (int64_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
-          int remote = 0;
-          for (int j = 0; j < s.topk; ++j) remote += (int)routes[t * s.topk + j] / s.local_experts != s.me;
-          tokt[t] += remote;
-        }
-      }
+      if (!dispatch_tokens_flat<SRC, ELEM>(s, x, t0, t1, routes, b.rank_scratch, b.pos, b.gidx, b.peers, baseg,
+                                           reinterpret_cast<uint8_t**>(dsm + fo), cap, step, sh))
+        dispatch_tokens<SRC, ELEM>(s, x, t0, t1, 1, routes, b.rank_scratch, b.pos, b.gidx, b.peers, baseg, step,
+                                   sh);
+      book_tok_targets(s, routes, b.region, t0, t1, 1);
     }
     stamp(b, 5);
-    if (!solo) signal_counts(s, b.peers, offsetof(Flags, tok_ctr), sh);
+    if (!solo) signal_counts(s, b.peers, 0, step, sh);
   }
   // thread 0 fences and signals while the other warps fill the metadata
   stamp(b, 6);
@@ -1439,7 +1685,12 @@ k_dispatch_fused(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
   else
     recv_rows_flat(s, rt, b.rows, b.sources, b.ret_slot, grouped_of(b.region, s), b.dirty, b.send_list,
                    &f->send_cnt, cta, ncta, f->phase_cnt);
+  {
+    const int nw = blockDim.x >> 5;
+    recv_private_rows(s, rt, b.region, step, timeout_ns, cta * nw + (threadIdx.x >> 5), ncta * nw, threadIdx.x & 31);
+  }
   stamp(b, 7);
+  __syncthreads();
   if (cta == 0) {
     // EP=1: every CTA counted every route, so CTA 0 has latched any route
     // error itself; the grid's end publishes the rows
@@ -1552,18 +1803,31 @@ k_dispatch_roles(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
     load_row_raw<SRC, ELEM>(x, cta, s.hidden, s.payload_bytes, raw, tg);
     finish_row_regs<SRC, ELEM>(raw, pre, sh.red, tg);
     if (b.prof && tg.tid == 0) b.prof[blockIdx.x * 32 + 1] = globaltimer();
+    // speculative private copies (moe.py:556-582): their destinations need
+    // only this rank's own counts, so they are stored while the route
+    // exchange is still in flight, and counted on the owners' private
+    // counters under their own release fence
+    named_sync(4, kThreads);  // private destinations are in sh.pdst
+    if (s.priv_tokens > 0) {
+      store_row_regs<SRC, ELEM>(pre, s.hidden, s.scales, sh.pdst, s.topk, tg);
+      if (b.prof && tg.tid == 0) b.prof[blockIdx.x * 32 + 26] = globaltimer();
+      tg.sync();
+      if (tg.tid == 0) signal_rows_thread(s, b.peers, 0, step, sh, false, true);
+    }
     named_sync(3, kThreads);  // destinations are in sh.dstp
     if (!skip) store_row_regs<SRC, ELEM>(pre, s.hidden, s.scales, sh.dstp, s.topk, tg);
     if (b.prof && tg.tid == 0) b.prof[blockIdx.x * 32 + 20] = globaltimer();
   } else {
     const Grp rg{(int)threadIdx.x, kRouteRole, 1};
     const uint32_t pd = prefetch_dirty(s, b.dirty, cta, ncta, rg);
+    for (int q = rg.tid; q < s.ranks; q += rg.nt) sh.cnt[q] = sh.pcnt[q] = 0;
     const uint32_t bad = route_counts_direct(s, routes, n, hist, reinterpret_cast<int32_t*>(hist + s.experts),
                                              b.rank_scratch, cta, ncta, sh, b, rg);
     stamp(b, 14);
     route_publish(s, b.peers, f, hist, step, n, bad, cta, ncta, rg);
-    own_positions(s, hist, b.pos, bad, sh, rg);
-    for (int q = rg.tid; q < s.ranks; q += rg.nt) sh.cnt[q] = 0;
+    own_positions(s, hist, b.pos, bad, sh, rg, b.peers, step);
+    rg.sync();
+    named_sync(4, kThreads);
     stamp(b, 2);
     const uint32_t* Cm = hist;
     bool ok = true;
@@ -1583,11 +1847,14 @@ k_dispatch_roles(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
     stamp(b, 15);
     if (ok) {
       recv_tables_body<true>(s, Cm, rt, b.info, cta, sh, b, rg);
-      if (!solo && cta == 0 && rg.tid == 0) f->tok_target += (uint64_t)recv_carve(s, rt).tot[1];
+      if (!solo && cta == 0 && rg.tid < 32) book_recv(s, f, Cm, rg.tid);
       stamp(b, 4);
-      // receive metadata while the token role's stores drain
+      // receive metadata while the token role's stores drain, then the
+      // private rows that arrived before the layout was known
       recv_rows_body(s, rt, b.rows, b.sources, b.ret_slot, grouped_of(b.region, s), b.dirty, b.send_list,
                      &f->send_cnt, cta, ncta, rg, pd);
+      const int nw = rg.nt >> 5;
+      recv_private_rows(s, rt, b.region, step, timeout_ns, cta * nw + (rg.tid >> 5), ncta * nw, rg.tid & 31);
     }
     stamp(b, 7);
   }
@@ -1597,7 +1864,7 @@ k_dispatch_roles(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
     return;
   }
   stamp(b, 5);
-  if (!solo) signal_counts(s, b.peers, offsetof(Flags, tok_ctr), sh);
+  if (!solo) signal_counts(s, b.peers, 0, step, sh);
   stamp(b, 6);
   if (cta == 0) {
     if (!solo) wait_tokens(f, b.info, s.local_experts, timeout_ns);
@@ -1631,7 +1898,7 @@ k_combine_fused(txb_moe_shape s, txb_moe_bufs b, const uint8_t* __restrict__ out
     __syncthreads();
   }
   stamp(b, 10);
-  signal_counts(s, b.peers, offsetof(Flags, comb_ctr), sh);
+  signal_counts(s, b.peers, 1, step, sh);
   __syncthreads();
   stamp(b, 11);
   if (!roles || !sender)
@@ -1818,6 +2085,11 @@ int txb_moe_plan(txb_moe_shape* s) {
     return TXB_ERR_PROTOCOL;
   }
   if (s->me < 0 || s->me >= s->ranks) { set_error("rank %d outside 0..%d", s->me, s->ranks - 1); return TXB_ERR_PROTOCOL; }
+  // PrivateBufferConfig.validate (moe.py:98-102)
+  if (s->priv_tokens < 0 || s->priv_tokens > s->max_tokens) {
+    set_error("private buffer of %d tokens outside 0..%d", s->priv_tokens, s->max_tokens);
+    return TXB_ERR_PROTOCOL;
+  }
   const int64_t N = s->ranks, T = s->max_tokens, R = s->topk;
   s->local_experts = s->experts / s->ranks;
   const int64_t L = s->local_experts;
@@ -1838,6 +2110,10 @@ int txb_moe_plan(txb_moe_shape* s) {
   off = align_up(off + (uint64_t)s->comb_rows * s->comb_bytes, 256);
   // per-token completion words + origin token index per grouped row
   off = align_up(off + 2ull * (uint64_t)T * 8 + (uint64_t)s->grouped_rows * 4, 4096);
+  // speculative private slabs [2][N][priv_tokens] rows + origin token index
+  s->off_priv = off;
+  const uint64_t npriv = 2ull * (uint64_t)N * (uint64_t)s->priv_tokens;
+  off = align_up(off + npriv * (uint64_t)s->payload_bytes + npriv * 4, 4096);
   s->region_bytes = off;
   return TXB_OK;
 }
@@ -2044,16 +2320,23 @@ int txb_moe_status(const txb_moe_shape* s, void* region, uint32_t* err, uint64_t
   if (err) *err = h.err;
   if (counters) {
     const int N = s->ranks;
-    uint64_t buf[5 + 3 * TXB_MAX_RANKS];
+    uint64_t buf[10 + 9 * TXB_MAX_RANKS];
     int k = 0;
     buf[k++] = h.step;
     buf[k++] = h.tok_ctr;
     buf[k++] = h.tok_target;
     buf[k++] = h.comb_ctr;
     buf[k++] = h.comb_target;
+    buf[k++] = h.priv_ctr[0];
+    buf[k++] = h.priv_ctr[1];
+    buf[k++] = h.priv_target[0];
+    buf[k++] = h.priv_target[1];
+    buf[k++] = h.priv_step;
     for (int p = 0; p < 2; ++p)
       for (int q = 0; q < N; ++q) buf[k++] = h.route_tag[p][q];
-    for (int q = 0; q < N; ++q) buf[k++] = h.done[q];
+    const uint64_t* lanes[7] = {h.done, h.tok_src, h.tok_src_t, h.comb_src, h.comb_src_t, h.priv_src, h.priv_src_t};
+    for (int l = 0; l < 7; ++l)
+      for (int q = 0; q < N; ++q) buf[k++] = lanes[l][q];
     for (int i = 0; i < k && i < ncounters; ++i) counters[i] = buf[i];
   }
   return TXB_OK;

@@ -285,7 +285,8 @@ __device__ void finish_row_regs(const RowRaw& rr, RowRegs& r, float* red, const 
   }
 }
 
-// Store a RowRegs row to nd destination rows (plus the scale slots).
+// Store a RowRegs row to nd destination rows (plus the scale slots); null
+// destinations are skipped (copies stored in another pass).
 template <int SRC, int ELEM>
 __device__ void store_row_regs(const RowRegs& r, int H, int scales, uint8_t* const* dst, int nd,
                                const Grp& g = Grp::cta()) {
@@ -294,13 +295,15 @@ __device__ void store_row_regs(const RowRegs& r, int H, int scales, uint8_t* con
   for (int u = 0; u < 2; ++u) {
     const int c = tid + u * nt;
     if (c < r.nchunk)
-      for (int j = 0; j < nd; ++j) reinterpret_cast<uint4*>(dst[j])[c] = r.c[u];
+      for (int j = 0; j < nd; ++j)
+        if (dst[j]) reinterpret_cast<uint4*>(dst[j])[c] = r.c[u];
   }
   if constexpr (SRC != TXB_SRC_ROWS) {
     const int64_t d0 = (int64_t)H * ELEM;  // 16-byte aligned on this path
     const uint32_t sbits = ELEM == 1 ? __float_as_uint(r.scale) : 0u;
     for (int b = tid; b < scales; b += nt)
-      for (int j = 0; j < nd; ++j) reinterpret_cast<uint32_t*>(dst[j] + d0)[b] = b == 0 ? sbits : 0u;
+      for (int j = 0; j < nd; ++j)
+        if (dst[j]) reinterpret_cast<uint32_t*>(dst[j] + d0)[b] = b == 0 ? sbits : 0u;
   }
 }
 

@@ -15,9 +15,10 @@ What changes underneath:
     row on the receiving GPU (the reference's recv slab + pack_rows
     regroup, moe.py:699-722, collapses into one peer store), and completion
     is a release-add on the receiver's counter (the ImmCounter);
-  * the speculative private-buffer round (moe.py:556-582) is accepted and
-    validated but folded away: the count exchange over NVLink takes
-    microseconds, and the outputs do not depend on it (SURVEY.md probe P5).
+  * the speculative private-buffer round (moe.py:556-582) runs on the
+    device: the first PrivateBufferConfig.tokens rows of each source's slab
+    for a peer are stored into that peer's private slab before the route
+    exchange completes, and moved to their grouped rows by the receiver.
 
 Inputs may be numpy arrays (host mode: results come back as numpy, exactly
 like the reference) or CUDA tensors (device mode: results stay on the GPU;
@@ -131,8 +132,10 @@ class RoutingSpec:
 
 @dataclass(frozen=True)
 class PrivateBufferConfig:
-    """Per-source speculative receive slots (moe.py:92-102).  Validated for
-    API compatibility; the device path writes final positions directly."""
+    """Per-source speculative receive slots (moe.py:92-102).  A source
+    stores the first `tokens` rows of its slab for a peer into that peer's
+    private slab before the route exchange completes (moe.py:556-582); the
+    receiver moves them to their grouped rows once the layout is known."""
 
     tokens: int = DEFAULT_PRIVATE
 
@@ -372,6 +375,7 @@ _WAIT_WHAT = (
     (_lib.EV_CAPACITY, "a destination needs more slots than its capacity"),
     (_lib.EV_WAIT_ROUTE, "route counts"),
     (_lib.EV_WAIT_BARRIER, "dispatch barrier"),
+    (_lib.EV_WAIT_PRIV, "speculative private rows"),
     (_lib.EV_WAIT_TOKEN, "token writes"),
     (_lib.EV_WAIT_COMBINE, "combine writes"),
 )
@@ -398,7 +402,7 @@ class MoeRank:
         sh = _lib.Shape(ranks=spec.ranks, experts=spec.experts, max_tokens=spec.max_tokens,
                         topk=spec.topk, hidden=spec.hidden, elem_size=spec.elem_size,
                         scales=spec.scales, comb_elem_size=ce, comb_scales=cs, me=rank,
-                        device=self.device)
+                        device=self.device, priv_tokens=private.tokens)
         _lib.call("txb_moe_plan", C.byref(sh))
         self._shape = sh
         self._shape_p = C.byref(sh)
@@ -495,21 +499,35 @@ class MoeRank:
         return ProtocolError(msg)
 
     def status(self) -> tuple[int, dict]:
-        """(error word, counters) read from the device (synchronous)."""
+        """(error word, counters) read from the device (synchronous); layout
+        as documented at txb_moe_status in include/txb200.h."""
         N = self.spec.ranks
-        cnt = (C.c_uint64 * (5 + 3 * N))()
+        cnt = (C.c_uint64 * (10 + 9 * N))()
         err = C.c_uint32(0)
         _lib.call("txb_moe_status", self._shape_p, C.c_void_p(self.region.ptr), C.byref(err),
                   cnt, len(cnt))
         v = list(cnt)
-        return int(err.value), {
-            "step": v[0], "tok_ctr": v[1], "tok_target": v[2], "comb_ctr": v[3],
-            "comb_target": v[4], "route_tag": [v[5:5 + N], v[5 + N:5 + 2 * N]],
-            "done": v[5 + 2 * N:5 + 3 * N]}
+        out = {"step": v[0], "tok_ctr": v[1], "tok_target": v[2], "comb_ctr": v[3],
+               "comb_target": v[4], "priv_ctr": v[5:7], "priv_target": v[7:9], "priv_step": v[9],
+               "route_tag": [v[10:10 + N], v[10 + N:10 + 2 * N]]}
+        k = 10 + 2 * N
+        for name in ("done", "tok_src", "tok_src_target", "comb_src", "comb_src_target",
+                     "priv_src", "priv_src_target"):
+            out[name] = v[k:k + N]
+            k += N
+        return int(err.value), out
 
-    def _diagnose(self, step: int, c: dict) -> dict:
-        """Which sources have not been heard from, per signal lane
-        (moe.py:874-899, rebuilt from the device counters)."""
+    # signal lanes in the order a step passes them; a timeout reports the
+    # lanes up to the one it waited on (later lanes are not due yet)
+    _LANES = {"route counts": 1, "dispatch barrier": 1, "speculative private rows": 3,
+              "token writes": 3, "combine writes": 4}
+
+    def _diagnose(self, step: int, c: dict, what: str = "combine writes") -> dict:
+        """Which source ranks have not delivered, per signal lane
+        (moe.py:874-899): route rows and the buffer-reuse barrier from the
+        step tags, token / private / combine rows from the per-source
+        counters against the per-source expectations the kernels booked."""
+        upto = self._LANES.get(what, 4)
         slot = step & 1
         diag: dict = {}
         miss = [q for q, v in enumerate(c["route_tag"][slot]) if v < step]
@@ -518,10 +536,14 @@ class MoeRank:
         miss = [q for q, v in enumerate(c["done"]) if v < step - 1]
         if miss:
             diag["barrier"] = miss
-        if c["tok_ctr"] < c["tok_target"]:
-            diag["token_rows_missing"] = c["tok_target"] - c["tok_ctr"]
-        if c["comb_ctr"] < c["comb_target"]:
-            diag["combine_rows_missing"] = c["comb_target"] - c["comb_ctr"]
+        for lane, got, want, lv in (("token", "tok_src", "tok_src_target", 3),
+                                    ("private", "priv_src", "priv_src_target", 3),
+                                    ("combine", "comb_src", "comb_src_target", 4)):
+            if lv > upto:
+                continue
+            miss = [q for q, (g, w) in enumerate(zip(c[got], c[want])) if g < w]
+            if miss:
+                diag[lane] = miss
         return diag
 
     def _check_err(self, err: int, step: int) -> None:
@@ -533,7 +555,7 @@ class MoeRank:
                 if bit in (_lib.EV_ROUTE_RANGE, _lib.EV_ROUTE_DUP, _lib.EV_CAPACITY):
                     raise self._fail(f"rank {self.rank} step {step - 1}: {what}")
                 raise self._fail(f"rank {self.rank} step {step - 1} timed out waiting for {what}; "
-                                 f"missing: {self._diagnose(step, c)}")
+                                 f"missing: {self._diagnose(step, c, what)}")
         raise self._fail(f"rank {self.rank}: device error word {err:#x}")
 
     def _gate(self, cond, step: int, what: str, timeout: float | None) -> None:
@@ -552,7 +574,7 @@ class MoeRank:
                 return
             if deadline is not None and time.monotonic() > deadline:
                 raise self._fail(f"rank {self.rank} step {step - 1} timed out waiting for {what}; "
-                                 f"missing: {self._diagnose(step, c)}")
+                                 f"missing: {self._diagnose(step, c, what)}")
             time.sleep(sleep)
             sleep = min(sleep * 2, 1e-3)
 
@@ -654,7 +676,10 @@ class MoeRank:
         sync = st.sync if sync is None else (sync or st.host)
         if not st.fused:
             if self.host_gated:
-                self._gate(lambda c: c["tok_ctr"] >= c["tok_target"], st.step, "token writes", timeout)
+                par = st.step & 1
+                self._gate(lambda c: c["tok_ctr"] >= c["tok_target"]
+                           and c["priv_ctr"][par] >= c["priv_target"][par] + c["priv_step"],
+                           st.step, "token writes", timeout)
             _lib.call("txb_moe_dispatch_recv", self._shape_p, self._bufs_p, self._tmo(timeout), self._sid())
         L = self.spec.local_experts
         if not sync:

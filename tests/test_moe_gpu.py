@@ -15,7 +15,7 @@ from oracle import moe_oracle as mo
 pytestmark = pytest.mark.gpu
 
 if torch.cuda.is_available():
-    from moe_driver import close_mesh, make_mesh, ospec_of, run_moe_round
+    from moe_driver import check_device_round, close_mesh, device_round, make_mesh, ospec_of, run_moe_round
     from paper_2510_27656_b200 import moe
     from paper_2510_27656_b200.engine import local_engines
     from paper_2510_27656_b200.errors import ProtocolError
@@ -459,3 +459,98 @@ def test_fp8_encode_division_exhaustive(amax):
             want = (x / s).clamp(-448.0, 448.0).to(torch.float8_e4m3fn).view(torch.uint8)
             bad += int((got != want).sum())
     assert bad == 0, f"{bad} e4m3 bytes differ for amax={amax}"
+
+
+PRIV_CASES = ["cfg1_full", "n3_e12_t11_r4", "n4_e16_t9_r4", "n8_e16_t7_r3", "fp8_dsv3ish", "fp8_n2_h33_odd"]
+
+
+@pytest.mark.parametrize("name", PRIV_CASES)
+@pytest.mark.parametrize("ptok", [0, 4, 32, "T"])
+def test_private_rounds_match_goldens(name, ptok):
+    """Speculative private-buffer round (moe.py:556-582, 693-698) at
+    PrivateBufferConfig.tokens in {0, 4, 32, T}: the first min(P, assigned)
+    rows of every (source, destination) slab travel through the receiver's
+    private slab and are moved to their grouped rows there.  Outputs must
+    not depend on P (the reference's own property, SURVEY.md probe P5):
+    every step bit-exact against the railtx goldens.  Several ranks share
+    this GPU (host-gated split kernels, which place the same rows)."""
+    case = load_moe(name)
+    spec = moe.RoutingSpec(**case.spec_args)
+    p = spec.max_tokens if ptok == "T" else min(int(ptok), spec.max_tokens)
+    mesh = make_mesh(spec, private=p)
+    try:
+        for st in case.steps:
+            res = run_moe_round(mesh, spec, st.routes, st.values, st.weights)
+            for q in range(spec.ranks):
+                g, comb, pos = res[q]
+                assert np.array_equal(pos, st.pos[q]), f"pos rank {q}"
+                assert np.array_equal(_np(g.rows), st.rows[q]), f"rows rank {q}"
+                assert np.array_equal(_np(g.data), st.data[q]), f"data rank {q} (P={p})"
+                assert np.array_equal(comb, st.combined[q]), f"combine rank {q}"
+    finally:
+        close_mesh(mesh)
+
+
+def test_route_timeout_names_the_silent_rank():
+    """A rank that never sends: the waiting rank raises ProtocolError with
+    the reference's message shape and the silent source in its diagnostics
+    (moe.py:869-899: 'rank r step s timed out waiting for route counts;
+    missing: {...}')."""
+    spec = moe.RoutingSpec(ranks=2, experts=8, max_tokens=16, topk=2, hidden=256, elem_size=4, scales=0)
+    mesh = moe.build_mesh(local_engines([0, 0]), spec, timeout=1.0)
+    try:
+        os_ = ospec_of(spec)
+        routes, values, _ = mo.random_step(os_, np.random.default_rng(3), tokens=16)
+        with pytest.raises(ProtocolError,
+                           match=r"rank 0 step 0 timed out waiting for route counts; missing: \{'route': \[1\]\}"):
+            mesh[0].dispatch_send(mo.encode_tokens(os_, values[0]), routes[0])
+    finally:
+        close_mesh(mesh)
+
+
+def test_token_timeout_names_the_silent_rank():
+    """Routes arrive but one rank's token rows never do: the receiver's
+    token lane names that source (per-source counters vs the per-source
+    expectations booked from the route matrix)."""
+    spec = moe.RoutingSpec(ranks=2, experts=8, max_tokens=16, topk=2, hidden=256, elem_size=4, scales=0)
+    mesh = moe.build_mesh(local_engines([0, 0]), spec, private=moe.PrivateBufferConfig(0), timeout=1.0)
+    try:
+        os_ = ospec_of(spec)
+        # every token of rank 1 routes to rank 0's experts, so rank 0 waits on rank 1
+        routes = [np.tile(np.array([[0, 1]], np.int64), (16, 1)), np.tile(np.array([[2, 3]], np.int64), (16, 1))]
+        values = [np.ones((16, 256), np.float32), np.ones((16, 256), np.float32)]
+        # rank 1 publishes its count row (route phase only) and stops there
+        import ctypes as C
+        from paper_2510_27656_b200 import _lib
+        r1 = mesh[1]
+        with r1._lock:
+            r1._step_no += 1
+        r_dev = torch.from_numpy(routes[1]).cuda()
+        _lib.call("txb_moe_route", r1._shape_p, r1._bufs_p, C.c_void_p(r_dev.data_ptr()), 16, r1._sid())
+        torch.cuda.synchronize()
+        mesh[0].dispatch_send(mo.encode_tokens(os_, values[0]), routes[0])
+        with pytest.raises(ProtocolError, match=r"rank 0 step 0 timed out waiting for token writes; "
+                                                r"missing: \{'token': \[1\]\}"):
+            mesh[0].dispatch_recv(1.0)
+    finally:
+        close_mesh(mesh)
+
+
+def test_per_token_mode_odd_rows_host_gated():
+    """max_tokens above the per-token threshold with combine rows that are
+    not 16-byte vectorisable (fp8, hidden 100: 132-byte rows, the ADVICE
+    case): every returned row also books its origin token's counter, and the
+    payloads and combine stay bit-exact."""
+    spec = moe.RoutingSpec(ranks=2, experts=8, max_tokens=300, topk=2, hidden=100, elem_size=1, scales=8)
+    mesh = make_mesh(spec, private=32)
+    try:
+        for step, n in enumerate([300, 41, 300]):
+            rng = np.random.default_rng(70 + step)
+            routes, values, weights = mo.random_step(ospec_of(spec), rng, tokens=n)
+            xb, got = device_round(mesh, spec, routes, values, weights, out_dtype=torch.float32)
+            check_device_round(spec, routes, xb, weights, got, f"step {step}")
+            for q in range(2):
+                _, c = mesh[q].status()
+                assert c["tok_ctr"] == c["tok_target"] and c["comb_ctr"] == c["comb_target"]
+    finally:
+        close_mesh(mesh)

@@ -21,7 +21,8 @@ ROOT = Path(__file__).resolve().parents[1]
 NGPU = torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 if NGPU:
-    from moe_driver import close_mesh, ospec_of, run_moe_round
+    from moe_driver import check_device_round, close_mesh, device_round, ospec_of, run_moe_round
+    from paper_2510_27656_b200.errors import ProtocolError
     from paper_2510_27656_b200 import moe
     from paper_2510_27656_b200.engine import local_engines
 
@@ -239,5 +240,114 @@ def test_per_token_completion_mixed_batches(ranks):
             comb = mo.combine(os_, ref, outs, weights, comb_spec=os_)
             for r in range(ranks):
                 assert np.array_equal(got[r][1], mo.bf16_encode(comb[r])), (step, r)
+    finally:
+        close_mesh(mesh)
+
+
+@pytest.mark.parametrize("ptok", [0, 4, 32, 128])
+@pytest.mark.parametrize("ranks", [2, 4, 8])
+def test_private_round_one_rank_per_gpu(ranks, ptok):
+    """DeepSeek-V3 decode shape over NVLink with the speculative private
+    round at P in {0, 4, 32, T}: the decode kernel stores each copy whose
+    slab slot is below P into the owner's private slab before the route
+    exchange completes; the owner moves it to its grouped row.  Payloads,
+    indices and the bf16 combine bit-exact vs the oracle, three steps."""
+    if NGPU < ranks:
+        pytest.skip(f"needs {ranks} GPUs")
+    spec = moe.RoutingSpec(ranks=ranks, experts=256, max_tokens=128, topk=8, hidden=7168,
+                           elem_size=1, scales=56, comb_elem_size=2, comb_scales=0)
+    mesh = moe.build_mesh(local_engines(list(range(ranks))), spec, private=moe.PrivateBufferConfig(ptok),
+                          timeout=20.0)
+    assert not mesh[0].host_gated
+    try:
+        for step in range(3):
+            rng = np.random.default_rng(500 + 10 * ptok + step)
+            routes, values, weights = mo.random_step(ospec_of(spec), rng, tokens=128 - 37 * (step == 1))
+            xb, got = device_round(mesh, spec, routes, values, weights, timeout=20.0)
+            check_device_round(spec, routes, xb, weights, got, f"P={ptok} step {step}")
+        _, c = mesh[0].status()
+        assert c["priv_ctr"][0] == c["priv_target"][0] and c["priv_ctr"][1] == c["priv_target"][1]
+    finally:
+        close_mesh(mesh)
+
+
+def test_route_timeout_fused_names_the_silent_rank():
+    """Fused path across two GPUs: rank 1 never sends, rank 0's dispatch
+    kernel gives up at its device deadline and dispatch_recv raises the
+    reference-shaped ProtocolError naming rank 1 (moe.py:869-899)."""
+    if NGPU < 2:
+        pytest.skip("needs 2 GPUs")
+    spec = moe.RoutingSpec(ranks=2, experts=16, max_tokens=32, topk=4, hidden=512, elem_size=1, scales=4)
+    mesh = moe.build_mesh(local_engines([0, 1]), spec, timeout=1.5)
+    try:
+        rng = np.random.default_rng(4)
+        routes, values, _ = mo.random_step(ospec_of(spec), rng, tokens=32)
+        torch.cuda.set_device(0)
+        mesh[0].dispatch_send(torch.from_numpy(values[0]).cuda(0), torch.from_numpy(routes[0]).cuda(0))
+        with pytest.raises(ProtocolError, match=r"rank 0 step 0 timed out waiting for route counts; "
+                                                r"missing: \{'route': \[1\]\}"):
+            mesh[0].dispatch_recv(1.5)
+    finally:
+        close_mesh(mesh)
+
+
+def test_combine_timeout_fused_names_the_silent_rank():
+    """Both ranks dispatch, rank 1 never returns its expert outputs: rank
+    0's combine gives up and names rank 1 in the combine lane."""
+    if NGPU < 2:
+        pytest.skip("needs 2 GPUs")
+    import threading
+    spec = moe.RoutingSpec(ranks=2, experts=16, max_tokens=32, topk=4, hidden=512, elem_size=1, scales=4)
+    mesh = moe.build_mesh(local_engines([0, 1]), spec, timeout=1.5)
+    try:
+        rng = np.random.default_rng(5)
+        routes, values, weights = mo.random_step(ospec_of(spec), rng, tokens=32)
+        gs = [None, None]
+
+        def disp(r):
+            torch.cuda.set_device(r)
+            mesh[r].dispatch_send(torch.from_numpy(values[r]).cuda(r), torch.from_numpy(routes[r]).cuda(r))
+            gs[r] = mesh[r].dispatch_recv(10.0)
+
+        th = [threading.Thread(target=disp, args=(r,)) for r in range(2)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join(60)
+        assert gs[0] is not None and gs[1] is not None
+        torch.cuda.set_device(0)
+        mesh[0].combine_send(gs[0].data)
+        with pytest.raises(ProtocolError, match=r"rank 0 step 0 timed out waiting for combine writes; "
+                                                r"missing: \{'combine': \[1\]\}"):
+            mesh[0].combine_recv(torch.from_numpy(weights[0]).cuda(0), 1.5)
+    finally:
+        close_mesh(mesh)
+
+
+@pytest.mark.parametrize("ranks", [2, 4])
+def test_per_token_mode_odd_rows_alternating_paths(ranks):
+    """max_tokens above the per-token threshold, fp8 rows of 132 bytes (not
+    16-byte vectorisable), and steps that alternate between
+    the fused kernels and the split kernels on every rank: per-token
+    counters (tokc / tokt) must stay in step across paths -- every step
+    bit-exact, and the counters balanced at the end."""
+    if NGPU < ranks:
+        pytest.skip(f"needs {ranks} GPUs")
+    spec = moe.RoutingSpec(ranks=ranks, experts=16, max_tokens=300, topk=4, hidden=100, elem_size=1, scales=8)
+    mesh = moe.build_mesh(local_engines(list(range(ranks))), spec, private=moe.PrivateBufferConfig(16),
+                          timeout=20.0)
+    try:
+        for step, (n, fused) in enumerate([(300, True), (300, False), (57, True), (300, True), (0, False),
+                                           (211, False), (300, True)]):
+            for rk in mesh:
+                rk.fused = fused
+            rng = np.random.default_rng(300 + step)
+            routes, values, weights = mo.random_step(ospec_of(spec), rng, tokens=n)
+            xb, got = device_round(mesh, spec, routes, values, weights, timeout=20.0, out_dtype=torch.float32)
+            check_device_round(spec, routes, xb, weights, got, f"step {step} fused={fused}")
+        for q, rk in enumerate(mesh):
+            _, c = rk.status()
+            assert c["tok_ctr"] == c["tok_target"], q
+            assert c["comb_ctr"] == c["comb_target"], q
     finally:
         close_mesh(mesh)
