@@ -64,6 +64,17 @@ def _args():
     return ap.parse_args()
 
 
+def workload_config(wl: dict, tokens: int, ep: int, private: int | None) -> dict:
+    """The `config` object both arms print (identical keys and values, so
+    the driver can match the GPU arm's line with the reference arm's)."""
+    P = wl["hidden"] * wl["elem"] + 4 * wl["scales"]
+    return {"workload": wl["name"], "tokens_per_rank": tokens, "hidden": wl["hidden"],
+            "experts": wl["experts"], "topk": wl["topk"], "ep": ep, "dispatch_row_bytes": P,
+            "combine_row_bytes": 2 * wl["hidden"], "routing": f"{wl['routing']} top-{wl['topk']}",
+            "parallelism": f"ep{ep}",
+            "private_tokens": private if private is not None else min(32, tokens)}
+
+
 def _dist():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -455,12 +466,10 @@ def run_b200(a) -> None:
         "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
         "dtype": ("fp8-e4m3" if wl["elem"] == 1 else "bf16") + " dispatch / bf16 combine (fp32 accumulate)",
         "data": "synthetic",
-        "config": {"workload": wl["name"], "tokens_per_rank": tokens, "hidden": H, "experts": E,
-                   "topk": R, "ep": n_gpu, "dispatch_row_bytes": P, "combine_row_bytes": Pc,
-                   "routing": f"{wl['routing']} top-{R}", "l2": "flushed before every step (512 MiB write)",
-                   "timing": "public-API step captured as a CUDA graph; CUDA event nodes inside the graph around "
-                             "the step (device time, graph launch excluded), p50 over steps of the max over ranks",
-                   "parallelism": f"ep{n_gpu}", "private_tokens": rk.private_tokens},
+        "config": workload_config(wl, tokens, n_gpu, rk.private_tokens),
+        "l2": "flushed before every step (512 MiB write)",
+        "timing": "public-API step captured as a CUDA graph; CUDA event nodes inside the graph around "
+                  "the step (device time, graph launch excluded), p50 over steps of the max over ranks",
         "p90_us": round(float(np.percentile(tot, 90)), 2),
         "p99_us": round(float(np.percentile(tot, 99)), 2),
         "p50_l2_warm_us": round(float(np.median(b2b)), 2),
@@ -644,8 +653,7 @@ def run_reference(a) -> None:
            "scaling": "weak", "vs_baseline": None,
            "dtype": ("fp8-e4m3" if wl["elem"] == 1 else "bf16") + " dispatch / bf16 combine (fp32 accumulate)",
            "data": "synthetic",
-           "config": {"workload": wl["name"], "tokens_per_rank": tokens, "hidden": wl["hidden"],
-                      "experts": wl["experts"], "topk": wl["topk"], "ep": N},
+           "config": workload_config(wl, tokens, N, a.private),
            "cpu_baseline": cb,
            "e2e": {"value": cb["value"], "unit": "us", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
            "reference_live": reference_live(wl, tokens, ranks=N),

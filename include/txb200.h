@@ -193,10 +193,14 @@ int txb_moe_status(const txb_moe_shape* s, void* region, uint32_t* err, uint64_t
 
 /* ------------------------------------------- engine primitives (phase 2) */
 
-/* ImmCounter table: one u64 receipt counter per slot, slot = imm % TXB_IMM_SLOTS
- * (ImmCounterTable, engine.py:138-205; receipts are counted on the device,
- * the host keeps `consumed` per imm so a value can be re-armed). */
-#define TXB_IMM_SLOTS 65536
+/* ImmCounter table (ImmCounterTable, engine.py:138-205), keyed by the full
+ * u32 imm: keys u64[TXB_IMM_SLOTS] (0 = empty, else imm + 1) followed by
+ * counts u64[TXB_IMM_SLOTS], open addressing.  The owner and every sender
+ * claim an imm's slot with a system-scope CAS on the owner's table
+ * (txb_imm_slot), so they agree on its counter whoever arrives first; the
+ * host keeps `consumed` per imm so a value can be re-armed. */
+#define TXB_IMM_SLOTS 131072
+#define TXB_MAX_JOBS 64 /* writes per txb_copy_jobs launch (a scatter's peer slices) */
 
 /* One paged write (submit_paged_writes, engine.py:438-466; a single write is
  * one page).  Page i: src_base + src_offset + src_idx[i]*src_stride ->
@@ -220,8 +224,52 @@ typedef struct txb_pages {
 } txb_pages;
 
 int txb_imm_table_slots(void);
+/* Slot of `imm` in an ImmCounter table (own or peer-mapped): insert = 1
+ * claims it if absent (TXB_ERR_TRANSFER when the table is full), 0 looks it
+ * up (*out_slot = -1 when absent).  Synchronous, on a private stream; the
+ * caller caches the slot. */
+int txb_imm_slot(uint64_t* table, uint32_t imm, int insert, int64_t* out_slot);
 /* Move the pages and release one increment on *imm_ctr (engine.py:480-508, 759-782). */
 int txb_copy_pages(const txb_pages* job, int grid, void* stream);
+/* 1..TXB_MAX_JOBS writes in ONE launch (submit_scatter's per-peer slices,
+ * engine.py:563-597): each job completes on its own, one increment on its
+ * imm_ctr after its whole payload is visible.  Jobs are passed by value
+ * (host array). */
+int txb_copy_jobs(const txb_pages* jobs, int njobs, int grid, void* stream);
+
+/* Persistent paged stream: the KV-cache layer-by-layer transfer
+ * (PrefillerNode._on_progress, kvcache.py:477-507) with the LayerClock
+ * (kvcache.py:317-334) on the device.  Step k (0-based) moves pages
+ * [k*pages_per_step, (k+1)*pages_per_step) of src_idx/dst_idx (page numbers,
+ * page_len bytes each) once *clock >= clock_base + k + 1, and releases one
+ * increment on *imm_ctr when the step is complete.  tickets: zeroed u32
+ * [nsteps] (device). */
+typedef struct txb_stream_job {
+  const void* src;
+  void* dst;
+  int64_t page_len;
+  const int64_t* src_idx;
+  const int64_t* dst_idx;
+  int64_t pages_per_step;
+  int32_t nsteps;
+  int32_t use_tma;
+  const uint64_t* clock;
+  uint64_t clock_base;
+  uint64_t* imm_ctr;
+  uint32_t* tickets;
+  uint64_t timeout_ns;
+  uint32_t* err;
+  int32_t single_device;
+  int32_t pad;
+} txb_stream_job;
+int txb_kv_stream(const txb_stream_job* job, int grid, void* stream);
+/* Device layer clock: write / wait on a u64 word in stream order through
+ * the GPU front end (cuStreamWriteValue64 / cuStreamWaitValue64 GEQ), no SM
+ * and no host thread; a one-thread kernel stands in where 64-bit stream
+ * memory operations are unavailable (wait: TXB_EV_WAIT_IMM in *err on
+ * timeout, err may be NULL). */
+int txb_stream_write_value64(uint64_t* addr, uint64_t value, void* stream);
+int txb_stream_wait_value64(const uint64_t* addr, uint64_t value, uint64_t timeout_ns, uint32_t* err, void* stream);
 /* Zero-length writes carrying an immediate: +value on each of n counters
  * (ctrs: device array of peer-mapped counter pointers) (submit_barrier). */
 int txb_imm_add(uint64_t* const* ctrs, int n, uint64_t value, int single_device, void* stream);

@@ -74,7 +74,19 @@ class Pages(C.Structure):
                 ("use_tma", C.c_int32), ("single_device", C.c_int32)]
 
 
-TXB_IMM_SLOTS = 65536
+class StreamJob(C.Structure):
+    """txb_stream_job (include/txb200.h): the persistent KV layer stream."""
+
+    _fields_ = [("src", C.c_void_p), ("dst", C.c_void_p), ("page_len", C.c_int64),
+                ("src_idx", C.c_void_p), ("dst_idx", C.c_void_p), ("pages_per_step", C.c_int64),
+                ("nsteps", C.c_int32), ("use_tma", C.c_int32), ("clock", C.c_void_p),
+                ("clock_base", C.c_uint64), ("imm_ctr", C.c_void_p), ("tickets", C.c_void_p),
+                ("timeout_ns", C.c_uint64), ("err", C.c_void_p), ("single_device", C.c_int32),
+                ("pad", C.c_int32)]
+
+
+TXB_IMM_SLOTS = 131072
+TXB_MAX_JOBS = 64
 
 _VP = C.c_void_p
 _I64 = C.c_int64
@@ -108,6 +120,11 @@ SIGNATURES: dict[str, list] = {
     "txb_moe_status": [C.POINTER(Shape), _VP, C.POINTER(C.c_uint32), C.POINTER(_U64), _I64],
     "txb_imm_table_slots": [],
     "txb_copy_pages": [C.POINTER(Pages), _INT, _VP],
+    "txb_copy_jobs": [C.POINTER(Pages), _INT, _INT, _VP],
+    "txb_kv_stream": [C.POINTER(StreamJob), _INT, _VP],
+    "txb_imm_slot": [_VP, C.c_uint32, _INT, C.POINTER(_I64)],
+    "txb_stream_write_value64": [_VP, _U64, _VP],
+    "txb_stream_wait_value64": [_VP, _U64, _U64, _VP, _VP],
     "txb_imm_add": [_VP, _INT, _U64, _INT, _VP],
     "txb_imm_wait": [_VP, _U64, _U64, _VP, _VP],
     "txb_globaltimer": [_VP, _VP],

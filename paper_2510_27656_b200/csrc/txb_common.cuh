@@ -36,6 +36,15 @@ struct DeviceFor {
   DeviceFor(void* stream, const void* p) {
     cudaGetDevice(&prev);
     int dev = -1;
+    // inside a stream capture only capture-safe calls are allowed: the
+    // capturing stream fixes the device, so leave it alone
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (stream && cudaStreamIsCapturing(static_cast<cudaStream_t>(stream), &cs) == cudaSuccess &&
+        cs != cudaStreamCaptureStatusNone) {
+      prev = -1;
+      return;
+    }
+    cudaGetLastError();
     if (stream && cudaStreamGetDevice(static_cast<cudaStream_t>(stream), &dev) == cudaSuccess) {
       if (dev != prev) cudaSetDevice(dev);
       return;

@@ -19,8 +19,10 @@
 namespace txb {
 
 constexpr int kCopyThreads = 256;
-constexpr int kPiece = 16 * 1024;  // bytes per TMA piece (one smem stage)
-constexpr int kStages = 8;
+constexpr int kPiece = 8 * 1024;   // bytes per piece (a KV page; one TMA stage)
+constexpr int kWarpStages = 2;     // TMA stages per issuing warp
+constexpr int kCopyWarps = kCopyThreads / 32;
+constexpr int kMaxJobs = TXB_MAX_JOBS;
 
 struct PieceRef {
   const uint8_t* src;
@@ -41,85 +43,242 @@ __device__ __forceinline__ PieceRef piece_of(const txb_pages& j, int64_t k, int6
   return p;
 }
 
-__global__ void __launch_bounds__(kCopyThreads, 1) k_copy_pages(txb_pages j) {
-  extern __shared__ __align__(128) uint8_t stage[];
-  __shared__ __align__(8) uint64_t bars[kStages];
-  __shared__ uint32_t last;
-  const int64_t per_page = (j.page_len + kPiece - 1) / kPiece;
-  const int64_t total = j.npages * per_page;
-  const bool tma = j.use_tma != 0;
-  if (tma) {
-    if (threadIdx.x == 0) {
-      for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    // thread 0 drives a kStages-deep TMA pipeline over this CTA's pieces
-    if (threadIdx.x == 0) {
-      uint32_t phase[kStages] = {};
-      const int64_t k0 = blockIdx.x;
-      // prologue: fill the stages
-      for (int s = 0; s < kStages && k0 + (int64_t)s * gridDim.x < total; ++s) {
-        const PieceRef p = piece_of(j, k0 + (int64_t)s * gridDim.x, per_page);
-        mbar_expect_tx(&bars[s], p.bytes);
-        tma_load(stage + s * kPiece, p.src, p.bytes, &bars[s]);
-      }
-      for (int64_t it = 0, k = k0; k < total; ++it, k += gridDim.x) {
-        const int s = (int)(it % kStages);
-        const PieceRef p = piece_of(j, k, per_page);
-        mbar_wait(&bars[s], phase[s]);
-        phase[s] ^= 1u;
-        tma_store(p.dst, stage + s * kPiece, p.bytes);
-        const int64_t kn = k + (int64_t)kStages * gridDim.x;
-        if (kn < total) {
-          tma_store_wait_read<kStages>();  // the stage stored kStages-1 pieces ago is free
-          const PieceRef q = piece_of(j, kn, per_page);
-          mbar_expect_tx(&bars[s], q.bytes);
-          tma_load(stage + s * kPiece, q.src, q.bytes, &bars[s]);
-        }
-      }
-      tma_store_wait_all();
-      // order the async-proxy global writes before the generic release below
-      asm volatile("fence.proxy.async.global;" ::: "memory");
-    }
+// One piece by one warp with 16-byte vectors: all loads in flight before
+// the first store.
+__device__ __forceinline__ void warp_copy_piece(const PieceRef& p, int lane) {
+  if (vec_width(p.src, p.dst, p.bytes) == 16) {
+    const int4* s = reinterpret_cast<const int4*>(p.src);
+    int4* d = reinterpret_cast<int4*>(p.dst);
+    const int nv = (int)(p.bytes >> 4);
+    constexpr int U = kPiece / 512;
+    int4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (lane + 32 * u < nv) v[u] = s[lane + 32 * u];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (lane + 32 * u < nv) d[lane + 32 * u] = v[u];
   } else {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int64_t k = (int64_t)blockIdx.x * nw + warp; k < total; k += (int64_t)gridDim.x * nw) {
-      const PieceRef p = piece_of(j, k, per_page);
-      const int w = vec_width(p.src, p.dst, p.bytes);
-      if (w == 16) {
-        // a whole 16-KiB piece is 32 int4 per lane: all loads in flight
-        // before the first store
-        const int4* s = reinterpret_cast<const int4*>(p.src);
-        int4* d = reinterpret_cast<int4*>(p.dst);
-        const int nv = (int)(p.bytes >> 4);
-        constexpr int U = kPiece / 512;
-        int4 v[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (lane + 32 * u < nv) v[u] = s[lane + 32 * u];
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (lane + 32 * u < nv) d[lane + 32 * u] = v[u];
-      } else {
-        copy_row(p.dst, p.src, p.bytes, lane, 32);
-      }
+    copy_row(p.dst, p.src, p.bytes, lane, 32);
+  }
+}
+
+// The pieces k = first, first + stride, ... < total of one warp.  TMA: lane
+// 0 of every warp drives its own kWarpStages-deep bulk-copy pipeline
+// (global -> shared -> global, mbarrier-tracked loads, bulk-group stores),
+// so eight issuers per CTA keep pieces in flight; vector: the warp copies
+// each piece with 16-byte loads and stores.
+template <typename PieceFn>
+__device__ __forceinline__ void warp_copy_range(int64_t first, int64_t stride, int64_t total, bool tma,
+                                                uint8_t* stage, uint64_t* bars, uint32_t* phase, PieceFn piece) {
+  const int lane = threadIdx.x & 31;
+  if (!tma) {
+    #pragma unroll 1
+    for (int64_t k = first; k < total; k += stride) warp_copy_piece(piece(k), lane);
+    return;
+  }
+  if (lane != 0) return;
+  #pragma unroll 1
+  for (int s = 0; s < kWarpStages && first + (int64_t)s * stride < total; ++s) {
+    const PieceRef p = piece(first + (int64_t)s * stride);
+    mbar_expect_tx(&bars[s], p.bytes);
+    tma_load(stage + s * kPiece, p.src, p.bytes, &bars[s]);
+  }
+  int64_t it = 0;
+  #pragma unroll 1
+  for (int64_t k = first; k < total; k += stride, ++it) {
+    const int s = (int)(it % kWarpStages);
+    const PieceRef p = piece(k);
+    mbar_wait(&bars[s], phase[s]);
+    phase[s] ^= 1u;
+    tma_store(p.dst, stage + s * kPiece, p.bytes);
+    const int64_t kn = k + (int64_t)kWarpStages * stride;
+    if (kn < total) {
+      tma_store_wait_read<kWarpStages>();  // the stage stored kWarpStages-1 pieces ago is free
+      const PieceRef q = piece(kn);
+      mbar_expect_tx(&bars[s], q.bytes);
+      tma_load(stage + s * kPiece, q.src, q.bytes, &bars[s]);
     }
   }
-  // completion: the last CTA releases one increment on the ImmCounter slot
+  tma_store_wait_all();
+  // order the async-proxy global writes before the generic release that follows
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+__device__ __forceinline__ void init_warp_bars(uint64_t* bars, bool tma) {
+  if (tma && (threadIdx.x & 31) == 0) {
+    for (int s = 0; s < kWarpStages; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+}
+
+// Every submitted write of one launch (a single write, a paged write, or
+// all the per-peer slices of a scatter): pieces of all jobs are numbered
+// through the prefix `start`, CTAs take them round-robin, and each job
+// completes on its own -- a CTA adds the pieces it moved of job i to job
+// i's ticket after a release fence; the CTA that brings the ticket to the
+// job's piece count resets it and releases one increment on that job's
+// ImmCounter slot, exactly once per write and only after its whole payload
+// is visible (engine.py:9-17).
+struct JobSet {
+  txb_pages job[kMaxJobs];
+  int64_t start[kMaxJobs + 1];
+  int32_t njobs;
+  int32_t use_tma;
+};
+
+__device__ __forceinline__ int job_of(const JobSet& js, int64_t k) {
+  int lo = 0, hi = js.njobs - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (js.start[mid] <= k) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(kCopyThreads, 1) k_copy_jobs(const __grid_constant__ JobSet js) {
+  extern __shared__ __align__(128) uint8_t stage[];
+  __shared__ __align__(8) uint64_t bars[kCopyWarps * kWarpStages];
+  __shared__ uint32_t done[kMaxJobs];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool tma = js.use_tma != 0;
+  for (int i = threadIdx.x; i < js.njobs; i += blockDim.x) done[i] = 0;
+  init_warp_bars(bars + warp * kWarpStages, tma);
+  __syncthreads();
+  const int64_t total = js.start[js.njobs];
+  uint32_t phase[kWarpStages] = {};
+  auto piece = [&](int64_t k) {
+    const int i = job_of(js, k);
+    const txb_pages& j = js.job[i];
+    return piece_of(j, k - js.start[i], (j.page_len + kPiece - 1) / kPiece);
+  };
+  const int64_t first = (int64_t)blockIdx.x * kCopyWarps + warp, stride = (int64_t)gridDim.x * kCopyWarps;
+  warp_copy_range(first, stride, total, tma, stage + (size_t)warp * kWarpStages * kPiece,
+                  bars + warp * kWarpStages, phase, piece);
+  if (lane == 0)
+    for (int64_t k = first; k < total; k += stride) atomicAdd(&done[job_of(js, k)], 1u);
   __syncthreads();
   if (threadIdx.x == 0) {
-    fence_release(j.single_device != 0);
-    last = (atomicAdd(j.ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
-  }
-  __syncthreads();
-  if (last && threadIdx.x == 0) {
-    *j.ticket = 0;
-    if (j.imm_ctr) {
-      fence_release(j.single_device != 0);
-      red_relaxed_sys_add(j.imm_ctr, 1);
+    bool any = false;
+    for (int i = 0; i < js.njobs; ++i) any |= done[i] != 0;
+    bool gpu_only = true;
+    for (int i = 0; i < js.njobs; ++i) gpu_only &= js.job[i].single_device != 0;
+    if (any) fence_release(gpu_only);
+    for (int i = 0; i < js.njobs; ++i) {
+      const txb_pages& j = js.job[i];
+      const uint32_t need = (uint32_t)(js.start[i + 1] - js.start[i]);
+      // zero-piece jobs (a zero-length write carrying an immediate) are
+      // completed by CTA 0
+      const uint32_t mine = need == 0 ? (blockIdx.x == 0 ? 1u : 0u) : done[i];
+      if (!mine) continue;
+      const uint32_t old = need == 0 ? 0u : atomicAdd(j.ticket, mine);
+      if (old + mine == (need == 0 ? 1u : need)) {
+        if (need) *j.ticket = 0;
+        if (j.imm_ctr) {
+          fence_release(j.single_device != 0);
+          red_relaxed_sys_add(j.imm_ctr, 1);
+        }
+      }
     }
   }
+}
+
+// Persistent paged stream (the KV-cache layer-by-layer transfer,
+// kvcache.py:477-507, with the LayerClock of kvcache.py:317-334 on the
+// device): step k (0-based) of the request moves pages_per_step pages
+// (indices [k*pages_per_step, (k+1)*pages_per_step) of the index arrays)
+// as soon as *clock >= clock_base + k + 1 -- the compute stream advances the
+// clock after each layer, no host in the loop -- and the CTA that finishes
+// a step last releases one increment on the request's ImmCounter slot.
+// CTAs run ahead independently; a step never waits for the previous step's
+// stragglers, only for the clock.
+__global__ void __launch_bounds__(kCopyThreads, 1) k_kv_stream(const __grid_constant__ txb_stream_job ks) {
+  extern __shared__ __align__(128) uint8_t stage[];
+  __shared__ __align__(8) uint64_t bars[kCopyWarps * kWarpStages];
+  __shared__ uint32_t fail;
+  const int warp = threadIdx.x >> 5;
+  const bool tma = ks.use_tma != 0;
+  init_warp_bars(bars + warp * kWarpStages, tma);
+  if (threadIdx.x == 0) fail = 0;
+  __syncthreads();
+  uint32_t phase[kWarpStages] = {};
+  const int64_t per_page = (ks.page_len + kPiece - 1) / kPiece;
+  const int64_t total = ks.pages_per_step * per_page;
+  const uint64_t dl = globaltimer() + ks.timeout_ns;
+  #pragma unroll 1
+  for (int k = 0; k < ks.nsteps; ++k) {
+    if (threadIdx.x == 0 && !spin_ge(ks.clock, ks.clock_base + (uint64_t)k + 1, dl)) {
+      fail = 1;
+      if (ks.err) atomicOr(ks.err, TXB_EV_WAIT_IMM);
+    }
+    __syncthreads();
+    if (fail) return;
+    const int64_t* si = ks.src_idx + (int64_t)k * ks.pages_per_step;
+    const int64_t* di = ks.dst_idx + (int64_t)k * ks.pages_per_step;
+    auto piece = [&](int64_t q) {
+      const int64_t page = q / per_page, pc = q - page * per_page;
+      const int64_t off = pc * kPiece, rem = ks.page_len - off;
+      PieceRef p;
+      p.src = reinterpret_cast<const uint8_t*>(ks.src) + si[page] * ks.page_len + off;
+      p.dst = reinterpret_cast<uint8_t*>(ks.dst) + di[page] * ks.page_len + off;
+      p.bytes = (uint32_t)(rem < kPiece ? rem : kPiece);
+      return p;
+    };
+    warp_copy_range((int64_t)blockIdx.x * kCopyWarps + warp, (int64_t)gridDim.x * kCopyWarps, total, tma,
+                    stage + (size_t)warp * kWarpStages * kPiece, bars + warp * kWarpStages, phase, piece);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      fence_release(ks.single_device != 0);
+      if (atomicAdd(&ks.tickets[k], 1u) == gridDim.x - 1) {
+        ks.tickets[k] = 0;
+        if (ks.imm_ctr) {
+          fence_release(ks.single_device != 0);
+          red_relaxed_sys_add(ks.imm_ctr, 1);
+        }
+      }
+    }
+  }
+}
+
+// Full-u32 ImmCounter table (ImmCounterTable, engine.py:138-205): keys
+// u64[TXB_IMM_SLOTS] (0 = empty, else imm + 1) then counts u64[SLOTS].
+// Open addressing with linear probing; a slot is claimed with a system-scope
+// CAS, so the owner and every sender (over NVLink) converge on the same slot
+// for an imm whoever arrives first.  Keys are never removed.
+__device__ __forceinline__ uint32_t imm_hash(uint32_t x) {
+  x ^= x >> 16;
+  x *= 0x7feb352du;
+  x ^= x >> 15;
+  x *= 0x846ca68bu;
+  x ^= x >> 16;
+  return x;
+}
+
+__global__ void k_imm_probe(uint64_t* keys, uint32_t imm, int insert, int64_t* out) {
+  if (threadIdx.x != 0) return;
+  const uint64_t key = (uint64_t)imm + 1;
+  uint32_t h = imm_hash(imm) & (TXB_IMM_SLOTS - 1);
+  for (int i = 0; i < TXB_IMM_SLOTS; ++i, h = (h + 1) & (TXB_IMM_SLOTS - 1)) {
+    unsigned long long cur;
+    if (insert) {
+      asm volatile("atom.cas.sys.global.b64 %0, [%1], %2, %3;"
+                   : "=l"(cur) : "l"(keys + h), "l"(0ull), "l"(key) : "memory");
+    } else {
+      asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(cur) : "l"(keys + h) : "memory");
+    }
+    if (cur == key || (insert && cur == 0)) {
+      *out = h;
+      return;
+    }
+    if (cur == 0) break;  // lookup: an empty slot ends the probe sequence
+  }
+  *out = -1;
+}
+
+__global__ void k_write_value(uint64_t* p, uint64_t v) {
+  if (threadIdx.x == 0) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 // Zero-length write carrying an immediate (barrier leg, engine.py:599-619).
@@ -229,34 +388,182 @@ extern "C" {
 
 int txb_imm_table_slots(void) { return TXB_IMM_SLOTS; }
 
-int txb_copy_pages(const txb_pages* j, int grid, void* stream) {
-  if (!j || !j->ticket) {
-    set_error("txb_copy_pages: null job or ticket");
-    return TXB_ERR_TRANSFER;
+static int launch_jobs(JobSet& js, int grid, void* stream) {
+  int64_t total = 0;
+  js.start[0] = 0;
+  bool sd = true;
+  for (int i = 0; i < js.njobs; ++i) {
+    const txb_pages& j = js.job[i];
+    if (!j.ticket) {
+      set_error("copy job %d: null ticket", i);
+      return TXB_ERR_TRANSFER;
+    }
+    if (j.npages < 0 || j.page_len < 0) {
+      set_error("copy job %d: negative page count or length", i);
+      return TXB_ERR_TRANSFER;
+    }
+    const int64_t per_page = j.page_len > 0 ? (j.page_len + kPiece - 1) / kPiece : 0;
+    total += j.npages * per_page;
+    js.start[i + 1] = total;
+    sd &= j.single_device != 0;
   }
-  if (j->npages < 0 || j->page_len < 0) {
-    set_error("negative page count or length");
-    return TXB_ERR_TRANSFER;
-  }
-  DeviceFor on_dev(stream, j->src_base);
-  txb_pages job = *j;
-  const int64_t per_page = job.page_len > 0 ? (job.page_len + kPiece - 1) / kPiece : 0;
-  const int64_t total = job.npages * per_page;
+  js.use_tma = 1;
+  for (int i = 0; i < js.njobs; ++i) js.use_tma &= js.job[i].use_tma != 0;
   if (grid <= 0) {
-    const int64_t want = job.use_tma ? total : (total + 7) / 8;
+    const int64_t want = (total + kCopyWarps - 1) / kCopyWarps;
     const int cap = sms(0);
     grid = (int)(want < 1 ? 1 : (want < cap ? want : cap));
   }
-  if (total == 0) job.npages = 0;
-  const size_t smem = job.use_tma ? (size_t)kStages * kPiece : 0;
+  const size_t smem = js.use_tma ? (size_t)kCopyWarps * kWarpStages * kPiece : 0;
   static bool attr_set[64] = {false};
   int dev = 0;
   cudaGetDevice(&dev);
   if (smem > 48 * 1024 && (dev < 0 || dev >= 64 || !attr_set[dev])) {
-    TXB_CUDA(cudaFuncSetAttribute(k_copy_pages, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kStages * kPiece)));
+    TXB_CUDA(cudaFuncSetAttribute(k_copy_jobs, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(kCopyWarps * kWarpStages * kPiece)));
     if (dev >= 0 && dev < 64) attr_set[dev] = true;
   }
-  k_copy_pages<<<grid, kCopyThreads, smem, (cudaStream_t)stream>>>(job);
+  (void)sd;
+  k_copy_jobs<<<grid, kCopyThreads, smem, (cudaStream_t)stream>>>(js);
+  TXB_CUDA(cudaGetLastError());
+  return TXB_OK;
+}
+
+int txb_copy_pages(const txb_pages* j, int grid, void* stream) {
+  if (!j) {
+    set_error("txb_copy_pages: null job");
+    return TXB_ERR_TRANSFER;
+  }
+  DeviceFor on_dev(stream, j->src_base);
+  static thread_local JobSet js;
+  js.njobs = 1;
+  js.job[0] = *j;
+  return launch_jobs(js, grid, stream);
+}
+
+int txb_copy_jobs(const txb_pages* jobs, int njobs, int grid, void* stream) {
+  if (!jobs || njobs < 1 || njobs > kMaxJobs) {
+    set_error("txb_copy_jobs: %d jobs outside 1..%d", njobs, kMaxJobs);
+    return TXB_ERR_TRANSFER;
+  }
+  DeviceFor on_dev(stream, jobs[0].src_base);
+  static thread_local JobSet js;
+  js.njobs = njobs;
+  for (int i = 0; i < njobs; ++i) js.job[i] = jobs[i];
+  return launch_jobs(js, grid, stream);
+}
+
+int txb_kv_stream(const txb_stream_job* ks, int grid, void* stream) {
+  if (!ks || !ks->tickets || !ks->clock || !ks->src_idx || !ks->dst_idx) {
+    set_error("txb_kv_stream: null job, tickets, clock or page indices");
+    return TXB_ERR_TRANSFER;
+  }
+  if (ks->nsteps < 0 || ks->pages_per_step < 0 || ks->page_len <= 0) {
+    set_error("txb_kv_stream: bad step / page counts");
+    return TXB_ERR_TRANSFER;
+  }
+  DeviceFor on_dev(stream, ks->src);
+  if (grid <= 0) grid = sms(0);
+  const size_t smem = ks->use_tma ? (size_t)kCopyWarps * kWarpStages * kPiece : 0;
+  static bool attr_set[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (smem > 48 * 1024 && (dev < 0 || dev >= 64 || !attr_set[dev])) {
+    TXB_CUDA(cudaFuncSetAttribute(k_kv_stream, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(kCopyWarps * kWarpStages * kPiece)));
+    if (dev >= 0 && dev < 64) attr_set[dev] = true;
+  }
+  k_kv_stream<<<grid, kCopyThreads, smem, (cudaStream_t)stream>>>(*ks);
+  TXB_CUDA(cudaGetLastError());
+  return TXB_OK;
+}
+
+int txb_imm_slot(uint64_t* table, uint32_t imm, int insert, int64_t* out_slot) {
+  if (!table || !out_slot) {
+    set_error("txb_imm_slot: null table or output");
+    return TXB_ERR_TRANSFER;
+  }
+  DeviceFor on_dev(nullptr, table);
+  static thread_local cudaStream_t side[64] = {nullptr};
+  static thread_local int64_t* host_out[64] = {nullptr};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int d = dev >= 0 && dev < 64 ? dev : 0;
+  if (!side[d]) TXB_CUDA(cudaStreamCreateWithFlags(&side[d], cudaStreamNonBlocking));
+  if (!host_out[d]) TXB_CUDA(cudaHostAlloc(&host_out[d], sizeof(int64_t), cudaHostAllocMapped | cudaHostAllocPortable));
+  int64_t* dptr = nullptr;
+  TXB_CUDA(cudaHostGetDevicePointer(&dptr, host_out[d], 0));
+  *host_out[d] = -2;
+  k_imm_probe<<<1, 32, 0, side[d]>>>(table, imm, insert, dptr);
+  TXB_CUDA(cudaGetLastError());
+  TXB_CUDA(cudaStreamSynchronize(side[d]));
+  *out_slot = *host_out[d];
+  if (*out_slot < 0 && insert) {
+    set_error("ImmCounter table full (%d slots)", TXB_IMM_SLOTS);
+    return TXB_ERR_TRANSFER;
+  }
+  return TXB_OK;
+}
+
+// Stream memory operations (the device layer clock): the copy stream waits
+// in the GPU front end until a u64 word reaches a value, the compute stream
+// writes the word -- no SM and no host thread involved.  Through the driver
+// entry points (cuStreamWaitValue64 / cuStreamWriteValue64); a one-thread
+// kernel stands in where the driver lacks 64-bit stream memory operations.
+typedef int (*PFN_wait64)(void*, uint64_t, uint64_t, unsigned int);
+typedef int (*PFN_write64)(void*, uint64_t, uint64_t, unsigned int);
+
+static bool stream_memops(PFN_wait64* w, PFN_write64* wr) {
+  static int state = -1;
+  static PFN_wait64 fw = nullptr;
+  static PFN_write64 fwr = nullptr;
+  if (state < 0) {
+    cudaDriverEntryPointQueryResult q1, q2;
+    void* a = nullptr;
+    void* b = nullptr;
+    const bool ok = cudaGetDriverEntryPoint("cuStreamWaitValue64", &a, cudaEnableDefault, &q1) == cudaSuccess &&
+                    cudaGetDriverEntryPoint("cuStreamWriteValue64", &b, cudaEnableDefault, &q2) == cudaSuccess &&
+                    q1 == cudaDriverEntryPointSuccess && q2 == cudaDriverEntryPointSuccess && a && b;
+    cudaGetLastError();
+    int dev = 0, attr = 0;
+    cudaGetDevice(&dev);
+    // CU_DEVICE_ATTRIBUTE_CAN_USE_64_BIT_STREAM_MEM_OPS = 118 (cudaDevAttr has no alias)
+    cudaDeviceGetAttribute(&attr, (cudaDeviceAttr)118, dev);
+    cudaGetLastError();
+    state = ok && attr ? 1 : 0;
+    if (state) {
+      fw = reinterpret_cast<PFN_wait64>(a);
+      fwr = reinterpret_cast<PFN_write64>(b);
+    }
+    if (getenv("TXB_NO_STREAM_MEMOPS")) state = 0;
+  }
+  *w = fw;
+  *wr = fwr;
+  return state == 1;
+}
+
+int txb_stream_write_value64(uint64_t* addr, uint64_t value, void* stream) {
+  DeviceFor on_dev(stream, addr);
+  PFN_wait64 w;
+  PFN_write64 wr;
+  if (stream_memops(&w, &wr)) {
+    const int rc = wr(stream, (uint64_t)(uintptr_t)addr, value, 0 /* CU_STREAM_WRITE_VALUE_DEFAULT */);
+    if (rc == 0) return TXB_OK;
+  }
+  k_write_value<<<1, 32, 0, (cudaStream_t)stream>>>(addr, value);
+  TXB_CUDA(cudaGetLastError());
+  return TXB_OK;
+}
+
+int txb_stream_wait_value64(const uint64_t* addr, uint64_t value, uint64_t timeout_ns, uint32_t* err, void* stream) {
+  DeviceFor on_dev(stream, addr);
+  PFN_wait64 w;
+  PFN_write64 wr;
+  if (stream_memops(&w, &wr)) {
+    const int rc = w(stream, (uint64_t)(uintptr_t)addr, value, 0x1 /* CU_STREAM_WAIT_VALUE_GEQ */);
+    if (rc == 0) return TXB_OK;
+  }
+  k_imm_wait<<<1, 32, 0, (cudaStream_t)stream>>>(addr, value, timeout_ns, err);
   TXB_CUDA(cudaGetLastError());
   return TXB_OK;
 }

@@ -217,10 +217,14 @@ class CompletionFlag:
 class ImmFlag:
     """Fires when an armed immediate count is reached (engine.py:80-103).
 
-    Receipts are counted on the device (one u64 slot per imm value); the
-    flag holds the threshold `consumed + count` fixed when it was armed.
-    `wait_device(stream)` makes GPU work queued behind it wait on the device
-    instead of the host."""
+    Receipts are counted on the device (one u64 counter per imm value, in
+    the engine's full-u32 ImmCounter table); the flag holds the threshold
+    `consumed + count` fixed when it was armed.  A flag armed with a
+    callback is watched by the engine's callback thread, which runs the
+    callback when the count is reached (engine.py:527-543); a flag that
+    fires in a caller's wait()/done() also hands its callback to that
+    thread.  `wait_device(stream)` makes GPU work queued behind it wait on
+    the device instead of the host."""
 
     def __init__(self, engine: "TransferEngine", imm: int, threshold: int,
                  cb: Callable | None = None) -> None:
@@ -231,13 +235,20 @@ class ImmFlag:
         self.vtime = 0.0
         self._fired = False
 
-    def _check(self) -> bool:
-        if not self._fired and self.engine.imm_received_total(self.imm) >= self.threshold:
-            self._fired = True
+    def _check(self, total: int | None = None) -> bool:
+        if self._fired:
+            return True
+        if total is None:
+            total = self.engine.imm_received_total(self.imm)
+        if total >= self.threshold:
+            with self.engine._lock:
+                if self._fired:
+                    return True
+                self._fired = True
             self.engine._disarm(self.imm, self)
             self.engine.trace.record("imm_fire", imm=self.imm)
             if self.cb is not None:
-                self.cb(self)
+                self.engine._callbacks().post(lambda: self.cb(self))
         return self._fired
 
     def done(self) -> bool:
@@ -264,6 +275,162 @@ class ImmFlag:
                   int(timeout * 1e9), C.c_void_p(self.engine._err.data_ptr()), C.c_void_p(st.cuda_stream))
 
 
+class Watcher:
+    """Shared word the application side bumps to trigger engine callbacks
+    (engine.py:106-121).  The word lives in page-locked host memory mapped
+    into the GPU: `store(v)` from the host, or a device store through
+    `device_ptr` from any kernel or stream (txb_stream_write_value64), and
+    the engine's callback thread calls cb(old, new) with a strictly
+    increasing subsequence of the values, ending at the latest one."""
+
+    __slots__ = ("_word", "device_ptr", "last_seen", "cb")
+
+    def __init__(self, cb: Callable[[int, int], None], initial: int = 0) -> None:
+        self._word = torch.full((1,), int(initial), dtype=torch.int64).pin_memory()
+        out = C.c_void_p()
+        _lib.call("txb_host_device_ptr", C.c_void_p(self._word.data_ptr()), C.byref(out))
+        self.device_ptr = int(out.value)
+        self.last_seen = int(initial)
+        self.cb = cb
+
+    @property
+    def value(self) -> int:
+        return int(self._word[0])
+
+    def store(self, v: int) -> None:
+        self._word[0] = int(v)
+
+
+class _CallbackThread:
+    """The engine's callback thread (the reference runs callbacks, watcher
+    polling and completion delivery off its worker, engine.py:642-813):
+    watches armed ImmFlags that carry a callback, pending on_done
+    completions and watchers, and runs every callback in order.  Callbacks
+    must not block (SPEC.md:268)."""
+
+    def __init__(self, engine: "TransferEngine") -> None:
+        self.engine = engine
+        self._cv = threading.Condition()
+        self._flags: list[ImmFlag] = []
+        self._done: list[tuple[CompletionFlag, Callable]] = []
+        self._watchers: list[Watcher] = []
+        self._queue: list[Callable[[], None]] = []
+        self._stop = False
+        self.errors: list[BaseException] = []
+        self._th = threading.Thread(target=self._run, name=f"{engine.name}-callbacks", daemon=True)
+        self._th.start()
+
+    def post(self, fn: Callable[[], None]) -> None:
+        with self._cv:
+            self._queue.append(fn)
+            self._cv.notify()
+
+    def watch_flag(self, flag: ImmFlag) -> None:
+        with self._cv:
+            self._flags.append(flag)
+            self._cv.notify()
+
+    def watch_done(self, flag: CompletionFlag, cb: Callable) -> None:
+        with self._cv:
+            self._done.append((flag, cb))
+            self._cv.notify()
+
+    def add_watcher(self, w: Watcher) -> None:
+        with self._cv:
+            self._watchers.append(w)
+            self._cv.notify()
+
+    def remove_watcher(self, w: Watcher) -> None:
+        with self._cv:
+            if w in self._watchers:
+                self._watchers.remove(w)
+
+    def close(self) -> None:
+        with self._cv:
+            self._stop = True
+            self._cv.notify()
+        if threading.current_thread() is not self._th:
+            self._th.join(5.0)
+
+    def _run(self) -> None:
+        sleep = 2e-5
+        while True:
+            with self._cv:
+                if self._stop:
+                    return
+                if not (self._flags or self._done or self._watchers or self._queue):
+                    self._cv.wait(0.05)
+                    sleep = 2e-5
+                    continue
+                flags, done, watchers = list(self._flags), list(self._done), list(self._watchers)
+            busy = False
+            if flags:
+                totals = self.engine.imm_received_totals([f.imm for f in flags])
+                fired = [f for f, t in zip(flags, totals) if f._check(t)]
+                if fired:
+                    busy = True
+                    with self._cv:
+                        self._flags = [f for f in self._flags if f not in fired]
+            for cf, cb in done:
+                if cf.done():
+                    busy = True
+                    with self._cv:
+                        self._done.remove((cf, cb))
+                    self.post(lambda cf=cf, cb=cb: cb(cf))
+            for w in watchers:
+                v = w.value
+                if v != w.last_seen:
+                    busy = True
+                    old, w.last_seen = w.last_seen, v
+                    self.post(lambda w=w, old=old, v=v: w.cb(old, v))
+            with self._cv:
+                queue, self._queue = self._queue, []
+            for fn in queue:
+                busy = True
+                try:
+                    fn()
+                except BaseException as exc:  # noqa: BLE001  (a callback must not kill the thread)
+                    self.errors.append(exc)
+            sleep = 2e-5 if busy else min(sleep * 2, 1e-3)
+            time.sleep(sleep)
+
+
+class DeviceClock:
+    """A monotone u64 word in device memory, advanced in stream order and
+    waited on in stream order (the LayerClock of kvcache.py:317-334 moved
+    onto the GPU): `advance(stream)` appends a write of the next value to
+    the compute stream; consumers queued on other streams -- or a running
+    kernel polling the word -- see it without a host round trip."""
+
+    def __init__(self, engine: "TransferEngine", steps: int | None = None) -> None:
+        self.engine = engine
+        self.steps = steps
+        self._t = torch.zeros(1, dtype=torch.int64, device=torch.device("cuda", engine.device))
+        self.ptr = self._t.data_ptr()
+        self._value = 0
+
+    @property
+    def value(self) -> int:
+        """Value as last advanced from the host (stream order may lag)."""
+        return self._value
+
+    def device_value(self) -> int:
+        return int(self._t.cpu()[0])
+
+    def advance(self, stream=None, by: int = 1) -> int:
+        if self.steps is not None and self._value + by > self.steps:
+            raise ProtocolError(f"layer clock past its final value {self.steps}")
+        self._value += by
+        st = stream or torch.cuda.current_stream(self.engine.device)
+        _lib.call("txb_stream_write_value64", C.c_void_p(self.ptr), self._value, C.c_void_p(st.cuda_stream))
+        return self._value
+
+    def wait_device(self, value: int, stream=None, timeout: float = 30.0) -> None:
+        st = stream or torch.cuda.current_stream(self.engine.device)
+        _lib.call("txb_stream_wait_value64", C.c_void_p(self.ptr), int(value), int(timeout * 1e9),
+                  C.c_void_p(self.engine._err.data_ptr()), C.c_void_p(st.cuda_stream))
+
+
 class TransferEngine:
     """One rank's endpoint on one CUDA device.
 
@@ -276,7 +443,7 @@ class TransferEngine:
     ImmCounter slot after the payload is visible.  There are no rails, no
     worker thread and no host proxy."""
 
-    _TICKETS = 64
+    _TICKETS = 256
 
     def __init__(self, fabric: NvlinkFabric | None = None, *, device: int = 0,
                  name: str | None = None, rails: int = 1, engine_id: int | None = None,
@@ -299,7 +466,11 @@ class TransferEngine:
         self._armed: dict[int, ImmFlag] = {}
         self._groups: dict[int, tuple] = {}
         self._opened: dict[tuple, memory.Region] = {}
-        self.use_tma = True        # TMA bulk copies for 16-byte aligned pages
+        # 16-byte vector copies by default: at layer-step sizes they beat the
+        # TMA bulk-copy pipeline (profiles/r02/kv); TMA stays selectable
+        self.use_tma = False
+        self._slots: dict[tuple[int, int], int] = {}
+        self._cbt: _CallbackThread | None = None
         self.timing: list | None = None
         self.trace = TraceRecorder(self.name, enabled=trace)
         self._op_ids = itertools.count(1)
@@ -325,9 +496,16 @@ class TransferEngine:
             raise RegionError("region not registered with this engine")
         region.close()
 
+    def _callbacks(self) -> _CallbackThread:
+        with self._lock:
+            if self._cbt is None:
+                self._cbt = _CallbackThread(self)
+            return self._cbt
+
     def _ensure_imm(self) -> None:
         if self._imm is None:
-            self._imm = self.alloc_region(_lib.TXB_IMM_SLOTS * 8 + 4096)
+            # full-u32 ImmCounter table: keys[SLOTS] then counts[SLOTS]
+            self._imm = self.alloc_region(2 * _lib.TXB_IMM_SLOTS * 8 + 4096)
             dev = torch.device("cuda", self.device)
             self._tickets = torch.zeros(self._TICKETS, dtype=torch.int32, device=dev)
             self._ticket_i = 0
@@ -407,13 +585,27 @@ class TransferEngine:
             got = self._opened.get(key)
             if got is None:
                 reg = memory.Region.open_ipc(self.device, desc.ipc, desc.ipc_offset + desc.length)
-                imm = memory.Region.open_ipc(self.device, desc.imm_ipc, _lib.TXB_IMM_SLOTS * 8)
+                imm = memory.Region.open_ipc(self.device, desc.imm_ipc, 2 * _lib.TXB_IMM_SLOTS * 8)
                 got = self._opened[key] = (reg, imm)
         return got[0].ptr + desc.ipc_offset, got[1].ptr
 
-    def _imm_slot_ptr(self, imm: int, imm_base: int | None = None) -> int:
+    def _imm_slot(self, imm: int, imm_base: int | None = None) -> int:
+        """Slot of `imm` in an ImmCounter table (own, or a peer's), claimed
+        on first use with a system-scope CAS on the table; cached."""
+        self._ensure_imm()
         base = self._imm.ptr if imm_base is None else imm_base
-        return base + (imm % _lib.TXB_IMM_SLOTS) * 8
+        key = (base, int(imm))
+        slot = self._slots.get(key)
+        if slot is None:
+            out = C.c_int64(-1)
+            _lib.call("txb_imm_slot", C.c_void_p(base), C.c_uint32(int(imm)), 1, C.byref(out))
+            slot = self._slots[key] = int(out.value)
+        return slot
+
+    def _imm_slot_ptr(self, imm: int, imm_base: int | None = None) -> int:
+        """Address of imm's receipt counter in a table (counts follow keys)."""
+        base = self._imm.ptr if imm_base is None else imm_base
+        return base + (_lib.TXB_IMM_SLOTS + self._imm_slot(imm, base)) * 8
 
     # --------------------------------------------------------- submissions
 
@@ -481,6 +673,38 @@ class TransferEngine:
                 ev = torch.cuda.Event()
                 ev.record(self._stream)
         return CompletionFlag(ev)
+
+    def _launch_jobs(self, jobs: list, label: str = "") -> CompletionFlag:
+        """Several contiguous writes (src_base, src Pages, desc, dst Pages,
+        page_len, npages, imm) in ONE kernel launch (txb_copy_jobs): the
+        per-peer slices of a scatter, each completing on its own."""
+        self._ensure_imm()
+        out = []
+        for k in range(0, len(jobs), _lib.TXB_MAX_JOBS):
+            chunk = jobs[k:k + _lib.TXB_MAX_JOBS]
+            arr = (_lib.Pages * len(chunk))()
+            for j, (src_base, sp, desc, dp, page_len, npages, imm) in zip(arr, chunk):
+                self.post_op(label, desc.owner, page_len * npages, imm)
+                dst_base, dst_imm = self._peer_base(desc)
+                j.src_base, j.src_offset, j.src_stride = src_base, sp.offset, sp.stride
+                j.dst_base, j.dst_offset, j.dst_stride = dst_base, dp.offset, dp.stride
+                j.npages, j.page_len = npages, page_len
+                j.imm_ctr = self._imm_slot_ptr(imm, dst_imm) if imm is not None else None
+                with self._lock:
+                    t = self._ticket_i
+                    self._ticket_i = (t + 1) % self._TICKETS
+                j.ticket = self._tickets.data_ptr() + 4 * t
+                aligned = all(v % 16 == 0 for v in (src_base + sp.offset, dst_base + dp.offset, page_len))
+                j.use_tma = 1 if aligned and page_len >= 1024 and self.use_tma else 0
+                j.single_device = self._single_device(desc)
+            with torch.cuda.device(self.device):
+                self._stream.wait_stream(torch.cuda.current_stream(self.device))
+                with torch.cuda.stream(self._stream):
+                    _lib.call("txb_copy_jobs", arr, len(chunk), 0, C.c_void_p(self._stream.cuda_stream))
+                    ev = torch.cuda.Event()
+                    ev.record(self._stream)
+            out.append(ev)
+        return CompletionFlag(out[-1])
 
     @staticmethod
     def _check_imm(imm) -> None:
@@ -572,11 +796,10 @@ class TransferEngine:
                 raise TransferError(f"scatter source slice {i} out of bounds")
             if d.offset + d.length > d.desc.length:
                 raise TransferError(f"scatter destination slice {i} out of bounds")
-        for d in dsts:
-            if d.length == 0 and imm is None:
-                continue
-            flag = self._launch_pages(rec.base, Pages((0,), 0, d.src), d.desc, Pages((0,), 0, d.offset),
-                                      d.length, 1 if d.length else 0, imm, label=label)
+        live = [d for d in dsts if d.length or imm is not None]
+        if live:
+            flag = self._launch_jobs([(rec.base, Pages((0,), 0, d.src), d.desc, Pages((0,), 0, d.offset),
+                                       d.length, 1 if d.length else 0, imm) for d in live], label)
         return self._done(flag, on_done)
 
     def submit_barrier(self, group: int, imm: int, dsts: Sequence[tuple], on_done: Callable | None = None,
@@ -607,20 +830,33 @@ class TransferEngine:
         return self._done(CompletionFlag(ev), on_done)
 
     def _done(self, flag: CompletionFlag, on_done: Callable | None) -> CompletionFlag:
+        """on_done runs on the engine's callback thread once the operation
+        has completed (engine.py:563-619); the submitter never blocks."""
         if on_done is not None:
-            flag.wait()
-            on_done(flag)
+            self._callbacks().watch_done(flag, on_done)
         return flag
 
     # ----------------------------------------------------------- ImmCounter
 
     def imm_received_total(self, imm: int) -> int:
         """Receipts counted for `imm` so far (ImmCounterTable.received_total)."""
+        return self.imm_received_totals([imm])[0]
+
+    def imm_received_totals(self, imms: Sequence[int]) -> list[int]:
+        """Receipt counts of several imms with one device gather and one
+        device-to-host copy (what the callback thread polls)."""
         self._ensure_imm()
-        out = torch.empty(1, dtype=torch.int64)
+        if not imms:
+            return []
+        slots = [self._imm_slot(i) for i in imms]
         with torch.cuda.device(self.device), torch.cuda.stream(self._read_stream):
-            out.copy_(self._imm.tensor((imm % _lib.TXB_IMM_SLOTS) * 8, (1,), torch.int64))
-        return int(out[0])
+            counts = self._imm.tensor(_lib.TXB_IMM_SLOTS * 8, (_lib.TXB_IMM_SLOTS,), torch.int64)
+            if len(slots) == 1:
+                out = counts[slots[0]:slots[0] + 1].cpu()
+            else:
+                idx = torch.tensor(slots, dtype=torch.int64).to(counts.device, non_blocking=True)
+                out = counts.index_select(0, idx).cpu()
+        return [int(v) for v in out.tolist()]
 
     def expect_imm_count(self, imm: int, count: int, cb: Callable | None = None) -> ImmFlag:
         """Arm a threshold (engine.py:527-543 / ImmCounterTable.arm): fires
@@ -639,13 +875,32 @@ class TransferEngine:
             flag = ImmFlag(self, imm, base + count, cb)
             self._armed[imm] = flag
         self.trace.record("imm_arm", imm=imm, count=count)
-        flag._check()
+        if not flag._check() and cb is not None:
+            self._callbacks().watch_flag(flag)
         return flag
 
     def _disarm(self, imm: int, flag: ImmFlag) -> None:
         with self._lock:
             if self._armed.get(imm) is flag:
                 del self._armed[imm]
+
+    def alloc_watcher(self, cb: Callable[[int, int], None], initial: int = 0) -> Watcher:
+        """engine.py:621-632: a word the application bumps (host store or a
+        device store through Watcher.device_ptr); the callback thread calls
+        cb(old, new) when it changes."""
+        w = Watcher(cb, initial)
+        self._callbacks().add_watcher(w)
+        return w
+
+    def free_watcher(self, w: Watcher) -> None:
+        """engine.py:634-638."""
+        if self._cbt is not None:
+            self._cbt.remove_watcher(w)
+
+    def device_clock(self, steps: int | None = None) -> DeviceClock:
+        """A device layer clock on this engine's GPU (kvcache LayerClock)."""
+        self._ensure_imm()
+        return DeviceClock(self, steps)
 
     def cancel_imm(self, imm: int) -> None:
         """ImmCounterTable.cancel: drop the expectation and realign the
@@ -660,6 +915,8 @@ class TransferEngine:
     def close(self) -> None:
         if self._closed:
             return
+        if self._cbt is not None:
+            self._cbt.close()
         if self._stream is not None:
             self._stream.synchronize()
         for reg, imm in self._opened.values():

@@ -9,24 +9,67 @@ decoder arms `expect_imm_count(imm, layers*chunks + 1)` before the request
 can be seen, so completion never runs ahead of any payload byte
 (kvcache.py:715-728).
 
-On B200 each step is one sm_100a kernel on the prefiller's engine stream:
-the 8-KiB pages move with TMA bulk copies straight into the decoder GPU's
-page pool over NVLink, and the last CTA releases the receipt on the
-decoder's ImmCounter slot.  The host control plane of the reference
-(request messages, heartbeats, cancellation, the watcher-driven layer
-clock) is out of scope: `KvRequest` is handed over
-in-process (or pickled by the caller), and `LayerClock.advance` is the
-caller invoking `send_step`.
+On B200 the pages move with device stores straight into the decoder GPU's
+page pool over NVLink, and the CTA that completes a step releases its
+receipt on the decoder's ImmCounter.  Two ways to drive it:
+
+  * `send_step` / `send_all`: one kernel per (chunk, layer) step, the host
+    calling it as the reference's LayerClock advances;
+  * `stream_all` with a `DeviceClock`: ONE persistent kernel for the whole
+    request that moves step k as soon as the compute stream has advanced
+    the clock to k (`clock.advance(stream)` after each layer's compute) --
+    the reference's watcher-driven LayerClock (kvcache.py:317-334, 477-500)
+    with the host taken out of the loop.
+
+The host control plane of the reference (request messages, heartbeats,
+cancellation) is out of scope: `KvRequest` is handed over
+in-process (or pickled by the caller).
 """
 
 from __future__ import annotations
 
+import ctypes as C
+import threading
 from dataclasses import dataclass
 
+import numpy as np
 import torch
 
-from .engine import ImmFlag, MrDesc, MrHandle, Pages, TransferEngine
+from . import _lib
+from .engine import CompletionFlag, DeviceClock, ImmFlag, MrDesc, MrHandle, Pages, TransferEngine
 from .errors import ProtocolError, ScheduleError
+
+IMM_RING_SIZE = 1 << 16   # kvcache.py:48
+
+
+class ImmRing:
+    """Allocator over a ring of imm values; a value stays out until retired
+    (kvcache.py:289-314).  Bounds the distinct imms a decoder ever arms, so
+    the engine's ImmCounter table never fills however many requests run."""
+
+    def __init__(self, base: int = 0, size: int = IMM_RING_SIZE) -> None:
+        if base < 0 or base + size > (1 << 32):
+            raise ProtocolError("imm ring outside the u32 range")
+        self._base = base
+        self._size = size
+        self._next = 0
+        self._inuse: set[int] = set()
+        self._lock = threading.Lock()
+
+    def take(self) -> int:
+        with self._lock:
+            if len(self._inuse) >= self._size:
+                raise ProtocolError("imm ring exhausted")
+            while True:
+                imm = self._base + self._next % self._size
+                self._next += 1
+                if imm not in self._inuse:
+                    self._inuse.add(imm)
+                    return imm
+
+    def retire(self, imm: int) -> None:
+        with self._lock:
+            self._inuse.discard(imm)
 
 
 @dataclass(frozen=True)
@@ -151,7 +194,7 @@ class KvReceiver:
         self.ctx_handle, self.ctx_desc = engine.reg_mr(self.ctx)
         self._free = list(range(pool_slots))[::-1]
         self._next_rid = 1
-        self._imm_base = imm_base
+        self._ring = ImmRing(base=imm_base)
 
     def open_request(self, head_lo: int = 0, ctx_len: int = 4096) -> KvTicket:
         """Reserve pool slots, arm the completion count, describe the
@@ -164,7 +207,7 @@ class KvReceiver:
         slots = tuple(self._free.pop() for _ in range(layout.slots))
         rid = self._next_rid
         self._next_rid += 1
-        imm = self._imm_base + rid
+        imm = self._ring.take()
         req = KvRequest(rid, layout, head_lo, head_lo + self.local_heads, self.local_heads,
                         self.pool_slots, self.kv_desc, slots, self.ctx_desc, 0, ctx_len, imm,
                         layout.expected_transfers)
@@ -173,7 +216,11 @@ class KvReceiver:
         return KvTicket(req, flag, slots)
 
     def release(self, ticket: KvTicket) -> None:
+        """Return the pages and retire the imm (DecoderNode on fire /
+        cancel, kvcache.py:741-768).  The imm's receipts were consumed by
+        the fired expectation, so the value can be armed again."""
         self._free.extend(ticket.slots)
+        self._ring.retire(ticket.request.imm)
 
     def page_view(self, ticket: KvTicket, layer: int, head: int, i: int) -> torch.Tensor:
         L = self.layout
@@ -210,10 +257,18 @@ class KvSender:
     def prepare(self, req: KvRequest) -> None:
         """Precompute every step's page lists and upload their indices once,
         so each layer step is a single kernel launch."""
+        L = req.layout
+        si, di = self.step_indices(req)
+        dev = torch.device("cuda", self.engine.device)
+        si_d = torch.from_numpy(si).to(dev)
+        di_d = torch.from_numpy(di).to(dev)
+        pps = (req.head_hi - req.head_lo) * L.pages_per_chunk
         self._plan = {}
-        for k in range(1, req.layout.steps + 1):
-            sp, dp = self.step_pages(req, k)
-            self._plan[(req.request_id, k)] = (sp, dp, (self.engine.page_indices(sp), self.engine.page_indices(dp)))
+        for k in range(1, L.steps + 1):
+            lo, hi = (k - 1) * pps, k * pps
+            sp = Pages(tuple(si[lo:hi].tolist()), L.page_len)
+            dp = Pages(tuple(di[lo:hi].tolist()), L.page_len)
+            self._plan[(req.request_id, k)] = (sp, dp, (si_d[lo:hi], di_d[lo:hi]))
 
     def send_step(self, req: KvRequest, step: int):
         """Step in 1..layout.steps: chunk, layer = divmod(step - 1, layers)."""
@@ -237,3 +292,63 @@ class KvSender:
         flags = [self.send_step(req, k) for k in range(1, req.layout.steps + 1)]
         flags.append(self.send_context(req))
         return flags
+
+    def step_indices(self, req: KvRequest) -> tuple[np.ndarray, np.ndarray]:
+        """Source / destination page numbers of every step, step-major
+        ([steps * pages_per_step]); the same lists as step_pages, built with
+        array arithmetic (kvcache.py:484-498)."""
+        L = req.layout
+        nh = req.head_hi - req.head_lo
+        steps = np.arange(L.steps)
+        chunk, layer = np.divmod(steps, L.layers)
+        j = np.arange(nh)
+        k = np.arange(L.pages_per_chunk)
+        slot = chunk[:, None, None] * L.pages_per_chunk + k[None, None, :]          # [S, 1, K]
+        src = (layer[:, None, None] * nh + j[None, :, None]) * L.slots + slot         # [S, nh, K]
+        sl = np.asarray(req.slot_list, dtype=np.int64)
+        dst = (layer[:, None, None] * req.dst_heads + j[None, :, None]) * req.dst_slots + sl[slot]
+        return src.reshape(-1).astype(np.int64), dst.reshape(-1).astype(np.int64)
+
+    def stream_all(self, req: KvRequest, clock: DeviceClock, grid: int = 0, use_tma: bool | None = None,
+                   timeout: float = 60.0) -> CompletionFlag:
+        """Enqueue the whole request as ONE persistent kernel on the engine's
+        stream: step k (1-based) moves once `clock` has reached k, and its
+        receipt is released as soon as its pages are visible.  `grid` CTAs
+        (default: every SM) -- fewer leave SMs to the compute that advances
+        the clock.  Send the context with send_context afterwards (it is
+        stream-ordered behind the last step, as in _on_progress)."""
+        eng = self.engine
+        L = req.layout
+        if L.page_len % 16 or self.kv.data_ptr() % 16:
+            raise ProtocolError("streamed pages must be 16-byte aligned")
+        si, di = self.step_indices(req)
+        dev = torch.device("cuda", eng.device)
+        si_d = torch.from_numpy(si).pin_memory().to(dev, non_blocking=True)
+        di_d = torch.from_numpy(di).pin_memory().to(dev, non_blocking=True)
+        tickets = torch.zeros(max(1, L.steps), dtype=torch.int32, device=dev)
+        dst_base, dst_imm = eng._peer_base(req.kv_desc)
+        nh = req.head_hi - req.head_lo
+        j = _lib.StreamJob()
+        j.src, j.dst, j.page_len = self.kv.data_ptr(), dst_base, L.page_len
+        j.src_idx, j.dst_idx = si_d.data_ptr(), di_d.data_ptr()
+        j.pages_per_step, j.nsteps = nh * L.pages_per_chunk, L.steps
+        j.use_tma = int(eng.use_tma if use_tma is None else use_tma)
+        j.clock, j.clock_base = clock.ptr, 0
+        j.imm_ctr = eng._imm_slot_ptr(req.imm, dst_imm)
+        j.tickets = tickets.data_ptr()
+        j.timeout_ns = int(timeout * 1e9)
+        j.err = eng._err.data_ptr()
+        j.single_device = eng._single_device(req.kv_desc)
+        for k in range(L.steps):
+            eng.post_op(f"kv.{req.request_id}.s{k + 1}", req.kv_desc.owner, L.page_len * nh * L.pages_per_chunk,
+                        req.imm)
+        with torch.cuda.device(eng.device):
+            eng._stream.wait_stream(torch.cuda.current_stream(eng.device))
+            with torch.cuda.stream(eng._stream):
+                for t in (si_d, di_d, tickets):
+                    t.record_stream(eng._stream)
+                _lib.call("txb_kv_stream", C.byref(j), int(grid), C.c_void_p(eng._stream.cuda_stream))
+                ev = torch.cuda.Event()
+                ev.record(eng._stream)
+        self._keep = (si_d, di_d, tickets)
+        return CompletionFlag(ev)

@@ -223,3 +223,214 @@ def test_weights_publish_to_two_destinations():
     finally:
         a.close()
         b.close()
+
+
+def test_imm_counter_randomized_10k_writes_256_imms():
+    """SPEC.md acceptance criterion 2 (ImmCounter semantics): 10,000 writes
+    carrying 256 distinct imm values, submitted from 4 sender engines
+    ("rails": 4 independent streams into one receiver).  Half the imms are
+    armed before any write, half after every write has landed.  Every armed
+    expectation fires exactly once at its threshold (its callback runs once,
+    on the engine's callback thread), arming after arrival fires at once,
+    and at fire time every payload of that imm is already complete (the
+    atomicity probe).  Imm values are spread over the whole u32 range and
+    include pairs congruent modulo the table size, which must not alias."""
+    import threading
+    rng = np.random.default_rng(549)
+    nimm = 256
+    base = rng.choice(1 << 31, size=nimm // 2, replace=False).astype(np.int64)
+    imms = np.concatenate([base, base + 131072 * 3]).tolist()       # congruent pairs
+    counts = rng.multinomial(10_000 - nimm, np.ones(nimm) / nimm) + 1  # >= 1 write each, 10k total
+    assert counts.sum() == 10_000
+    fab = NvlinkFabric()
+    d1 = 1 if NGPU > 1 else 0
+    if d1:
+        from paper_2510_27656_b200.memory import enable_peer_access
+        enable_peer_access([0, 1])
+    recv = TransferEngine(fab, device=d1, name="recv")
+    senders = [TransferEngine(fab, device=0, name=f"rail{i}") for i in range(4)]
+    W = 16                                   # bytes per payload
+    try:
+        slot_of = np.concatenate([[0], np.cumsum(counts)[:-1]])
+        dst = _u8(recv, 10_000 * W)
+        _, desc = recv.reg_mr(dst)
+        srcs = []
+        for i, e in enumerate(senders):
+            s = _u8(e, 10_000 * W)
+            # payload of write k of imm i: bytes derived from (i, k), never zero
+            pay = np.zeros((10_000, W), np.uint8)
+            for ii in range(nimm):
+                for k in range(counts[ii]):
+                    pay[slot_of[ii] + k] = (np.arange(W) * 7 + ii * 13 + k + 1) % 255 + 1
+            s.copy_(torch.from_numpy(pay.reshape(-1)).to(s.device))
+            srcs.append((s, e.reg_mr(s)[0], pay))
+        fired: dict = {}
+        probe_bad: list = []
+        lock = threading.Lock()
+
+        def cb_for(ii):
+            def cb(flag):
+                got = dst[slot_of[ii] * W:(slot_of[ii] + counts[ii]) * W].cpu().numpy().reshape(-1, W)
+                with lock:
+                    fired[ii] = fired.get(ii, 0) + 1
+                    if not np.array_equal(got, srcs[0][2][slot_of[ii]:slot_of[ii] + counts[ii]]):
+                        probe_bad.append(ii)
+            return cb
+
+        early = {ii: recv.expect_imm_count(imms[ii], int(counts[ii]), cb=cb_for(ii)) for ii in range(0, nimm, 2)}
+        # every write of every imm, interleaved over the 4 rails in a random order
+        order = [(ii, k) for ii in range(nimm) for k in range(counts[ii])]
+        perm = rng.permutation(len(order))
+        last = [None] * 4
+        for n, p in enumerate(perm):
+            ii, k = order[p]
+            r = n % 4
+            s, h, _ = srcs[r]
+            off = (slot_of[ii] + k) * W
+            last[r] = senders[r].submit_single_write(W, (h, off), (desc, off), imm=imms[ii])
+        for f in last:
+            f.result(60.0)
+        for e in senders:
+            e._stream.synchronize()
+        for ii, f in early.items():
+            assert f.wait(20.0), f"imm {imms[ii]} never fired"
+        late = {}
+        for ii in range(1, nimm, 2):
+            assert recv.imm_received_total(imms[ii]) == counts[ii]
+            f = recv.expect_imm_count(imms[ii], int(counts[ii]), cb=cb_for(ii))
+            assert f.done(), "arming after arrival must fire immediately"
+            late[ii] = f
+        t_end = __import__("time").monotonic() + 20.0
+        while len(fired) < nimm and __import__("time").monotonic() < t_end:
+            __import__("time").sleep(0.01)
+        assert sorted(fired) == list(range(nimm)), "some callbacks never ran"
+        assert all(v == 1 for v in fired.values()), "a callback ran more than once"
+        assert not probe_bad, f"incomplete payloads at fire time for imms {probe_bad[:5]}"
+        assert not recv._cbt.errors
+        # exactly-once: re-arming needs new receipts
+        again = recv.expect_imm_count(imms[0], 1)
+        assert not again.done()
+    finally:
+        for e in senders + [recv]:
+            e.close()
+
+
+def test_callbacks_do_not_block_the_submitter():
+    """on_done and ImmFlag callbacks run on the engine's callback thread;
+    the submitting call returns before the transfer has completed."""
+    import threading
+    import time
+    a, b = _pair()
+    try:
+        n = 256 << 20
+        src, dst = _u8(a, n), _u8(b, n)
+        h, _ = a.reg_mr(src)
+        _, d = b.reg_mr(dst)
+        seen = {}
+        ev = threading.Event()
+        f_imm = b.expect_imm_count(4242, 1, cb=lambda fl: seen.setdefault("imm", threading.current_thread().name))
+        torch.cuda._sleep(50_000_000)                 # keep the GPU busy: the write cannot finish yet
+        t0 = time.perf_counter()
+        a.submit_single_write(n, (h, 0), (d, 0), imm=4242,
+                              on_done=lambda cf: (seen.setdefault("done", threading.current_thread().name),
+                                                  ev.set()))
+        assert time.perf_counter() - t0 < 0.5, "submit_single_write blocked on completion"
+        assert ev.wait(30.0) and f_imm.wait(30.0)
+        t_end = time.monotonic() + 5.0
+        while "imm" not in seen and time.monotonic() < t_end:
+            time.sleep(0.01)
+        assert seen["done"].endswith("-callbacks") and seen["imm"].endswith("-callbacks")
+    finally:
+        a.close()
+        b.close()
+
+
+def test_watcher_host_and_device_stores():
+    """alloc_watcher (engine.py:621-638): the callback thread reports a
+    strictly increasing subsequence of the stored values ending at the
+    latest, for host stores and for device stores through device_ptr."""
+    import time
+    from paper_2510_27656_b200 import _lib
+    import ctypes as C
+    a = TransferEngine(NvlinkFabric(), device=0, name="w")
+    try:
+        seen = []
+        w = a.alloc_watcher(lambda old, new: seen.append((old, new)), initial=0)
+        for v in (1, 2, 5):
+            w.store(v)
+            time.sleep(0.02)
+        st = torch.cuda.current_stream(0)
+        _lib.call("txb_stream_write_value64", C.c_void_p(w.device_ptr), 9, C.c_void_p(st.cuda_stream))
+        torch.cuda.synchronize()
+        t_end = time.monotonic() + 5.0
+        while (not seen or seen[-1][1] != 9) and time.monotonic() < t_end:
+            time.sleep(0.01)
+        news = [n for _, n in seen]
+        assert news[-1] == 9 and news == sorted(set(news))
+        assert all(o < n for o, n in seen)
+        a.free_watcher(w)
+    finally:
+        a.close()
+
+
+def test_kv_stream_device_clock_steps_and_bytes():
+    """The persistent KV stream (kvcache LayerClock on the device): nothing
+    moves before the clock, step k's receipt is released once the compute
+    stream advanced the clock to k, and the whole request lands byte for
+    byte (check_kvcache, _invariants.py:139-184)."""
+    import time
+    a, b = _pair()
+    try:
+        layers, chunks, ppc, page_len, heads = 6, 3, 4, 8192, 2
+        layout = kvcache.KvLayout(layers, chunks, ppc, page_len)
+        dec = kvcache.KvReceiver(b, layout, pool_slots=layout.slots + 5, local_heads=heads, ctx_bytes=4096)
+        t = dec.open_request(ctx_len=512)
+        req = t.request
+        rid = req.request_id
+        kvb = np.zeros(layout.region_bytes(heads, layout.slots), np.uint8)
+        for layer in range(layers):
+            for j in range(heads):
+                for slot in range(layout.slots):
+                    idx = layout.page_index(heads, layout.slots, layer, j, slot)
+                    kvb[idx * page_len:(idx + 1) * page_len] = np.frombuffer(
+                        to.page_bytes(rid, layer, j, slot, page_len), np.uint8)
+        kv = a.alloc_buffer(kvb.size)
+        kv.copy_(torch.from_numpy(kvb).to(kv.device))
+        ctx = a.alloc_buffer(512)
+        ctx.copy_(torch.from_numpy(np.frombuffer(to.context_bytes(rid, 512), np.uint8).copy()).to(ctx.device))
+        send = kvcache.KvSender(a, kv, ctx)
+        # the step lists equal the per-step Pages of step_pages
+        si, di = send.step_indices(req)
+        pps = heads * ppc
+        for k in (1, 7, layout.steps):
+            sp, dp = send.step_pages(req, k)
+            assert list(si[(k - 1) * pps:k * pps]) == list(sp.indices)
+            assert list(di[(k - 1) * pps:k * pps]) == list(dp.indices)
+        clock = a.device_clock(layout.steps)
+        comp = torch.cuda.Stream(a.device)
+        flag = send.stream_all(req, clock, grid=16)
+        time.sleep(0.05)
+        assert b.imm_received_total(req.imm) == 0, "pages moved before the clock"
+        for k in range(1, layout.steps + 1):
+            clock.advance(comp)
+            comp.synchronize()
+            t_end = time.monotonic() + 10.0
+            while b.imm_received_total(req.imm) < k and time.monotonic() < t_end:
+                time.sleep(0.001)
+            assert b.imm_received_total(req.imm) == k, f"step {k} receipt"
+        flag.result(30.0)
+        assert not t.flag.done()
+        send.send_context(req).result(30.0)
+        assert t.wait(10.0)
+        for layer in range(layers):
+            for j in range(heads):
+                for i in range(layout.slots):
+                    assert dec.page_view(t, layer, j, i).cpu().numpy().tobytes() == \
+                        to.page_bytes(rid, layer, j, i, page_len)
+        dec.release(t)
+        # the retired imm can serve the next request
+        t2 = dec.open_request(ctx_len=512)
+        assert t2.request.imm != req.imm or not t2.flag.done()
+    finally:
+        a.close()
+        b.close()

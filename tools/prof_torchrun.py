@@ -32,6 +32,7 @@ ap.add_argument("--mode", default="graph", choices=["graph", "eager", "empty"])
 ap.add_argument("--noflush", action="store_true")
 ap.add_argument("--mid", action="store_true", help="a %globaltimer kernel between dispatch and combine")
 ap.add_argument("--sleep", type=int, default=0, help="GPU sleep cycles queued before the graph (host runs ahead)")
+ap.add_argument("--private", type=int, default=None, help="PrivateBufferConfig.tokens")
 a = ap.parse_args()
 
 world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -43,11 +44,13 @@ wl = bench.WORKLOADS[a.config]
 T, E, R, H = wl["tokens"], wl["experts"], wl["topk"], wl["hidden"]
 spec = moe.RoutingSpec(ranks=world, experts=E, max_tokens=T, topk=R, hidden=H, elem_size=wl["elem"],
                        scales=wl["scales"], comb_elem_size=2, comb_scales=0)
+priv = None if a.private is None else moe.PrivateBufferConfig(a.private)
 if world > 1:
     dist.init_process_group("gloo")
-    rk = moe.connect_process_group(TransferEngine(NvlinkFabric(group=dist.group.WORLD), device=local), spec)
+    rk = moe.connect_process_group(TransferEngine(NvlinkFabric(group=dist.group.WORLD), device=local), spec,
+                                   private=priv)
 else:
-    rk = moe.build_mesh([TransferEngine(NvlinkFabric(), device=local)], spec)[0]
+    rk = moe.build_mesh([TransferEngine(NvlinkFabric(), device=local)], spec, private=priv)[0]
 rk.record_stats = False
 x, routes, w = bench._inputs(wl, rank, T)
 xd = torch.from_numpy(x).to(dev).to(torch.bfloat16)
@@ -95,8 +98,8 @@ else:
     run = g.replay
 rows = []
 detail = []
-ORDER = [0, 19, 22, 24, 25, 14, 1, 2, 3, 15, 20, 16, 17, 18, 4, 7, 5, 6, 8, 9, 10, 11, 23, 12, 13]
-STAMP = {24: "seg prefix", 25: "seg sync2", 0: "start", 19: "own routes in", 22: "hist done", 14: "counted(+loads)", 1: "encoded", 2: "published+pos", 3: "routes-in", 15: "dests",
+ORDER = [0, 19, 22, 24, 25, 14, 1, 2, 26, 3, 15, 20, 16, 17, 18, 4, 7, 5, 6, 8, 9, 10, 11, 23, 12, 13]
+STAMP = {26: "priv stored", 24: "seg prefix", 25: "seg sync2", 0: "start", 19: "own routes in", 22: "hist done", 14: "counted(+loads)", 1: "encoded", 2: "published+pos", 3: "routes-in", 15: "dests",
          5: "joined", 20: "tok stored", 16: "T:loaded", 17: "T:srcpre", 18: "T:scan", 4: "tables", 6: "signalled", 7: "metadata", 8: "tokens-in", 9: "c:start", 10: "c:sent",
          11: "c:signalled", 23: "c:waited", 12: "c:reduced", 13: "c:end"}
 for k in range(a.reps + 5):
