@@ -59,6 +59,7 @@ def _args():
     ap.add_argument("--tokens", type=int, default=None)
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--flush", default="write+read", choices=["write+read", "write"])
     ap.add_argument("--private", type=int, default=None,
                     help="PrivateBufferConfig.tokens (default: build_mesh's min(32, tokens))")
     return ap.parse_args()
@@ -316,7 +317,25 @@ def run_b200(a) -> None:
     wd = torch.from_numpy(w).to(dev)
     G = int(rk._shape.grouped_rows)
     y = torch.randn(G, H, device=dev).to(torch.bfloat16)     # synthetic expert outputs
-    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    flush_buf = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+
+    class _Flush:
+        """L2 flush between timed steps: write a 512 MiB buffer (4x the L2),
+        then (default) read it back, so the step starts with a cold L2 that
+        holds no dirty lines: what a GEMM between MoE layers leaves behind
+        (it streams weights in).  --flush write keeps the
+        write-only flush, whose dirty lines the step then pays to write
+        back; both numbers are reported."""
+
+        def __init__(self, mode: str) -> None:
+            self.mode = mode
+
+        def fill_(self, v: int) -> None:
+            flush_buf.fill_(v)
+            if self.mode == "write+read":
+                flush_buf.view(torch.int32).amax()
+
+    flush = _Flush(a.flush)
     stream = torch.cuda.Stream(dev)          # graphs capture on a non-default stream
     torch.cuda.set_stream(stream)
 
@@ -391,6 +410,53 @@ def run_b200(a) -> None:
         return tuple(_max_over_ranks(v, world) for v in (tin, tout, kd, kc))
 
     tot, tot_launch = run(K, True, graph)[:2]
+    other = "write" if a.flush == "write+read" else "write+read"
+    flush.mode = other
+    tot_other = run(max(20, K // 2), True, graph)[0]
+    flush.mode = a.flush
+
+    # the same step launched eagerly (no graph): the L2 flush keeps the GPU
+    # busy while the host enqueues the step, so the event span is device
+    # time with stream launch latencies instead of graph-node latencies
+    def run_eager(n_steps: int) -> np.ndarray:
+        t = []
+        for k in range(n_steps + 3):
+            flush.fill_(k & 0xFF)
+            if world > 1:
+                rk.barrier()
+            eo[0].record(stream)
+            step()
+            eo[1].record(stream)
+            torch.cuda.synchronize()
+            if k >= 3:
+                t.append(eo[0].elapsed_time(eo[1]) * 1e3)
+        return _max_over_ranks(t, world)
+
+    eager = run_eager(max(20, K // 2))
+
+    # kernel span on the device clock: first dispatch CTA start -> last
+    # combine CTA end (%globaltimer phase stamps, one graph with stamps on)
+    from paper_2510_27656_b200 import _lib as _l
+    prof = torch.zeros(_l.TXB_MAX_CTAS * 32, dtype=torch.int64, device=dev)
+    rk._bufs.prof = prof.data_ptr()
+    graph_p = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph_p, stream=stream):
+        step()
+    rk._bufs.prof = 0
+    spans = []
+    for k in range(max(20, K // 2) + 3):
+        flush.fill_(k & 0xFF)
+        if world > 1:
+            rk.barrier()
+        prof.zero_()
+        graph_p.replay()
+        torch.cuda.synchronize()
+        if k >= 3:
+            pv = prof.view(-1, 32).cpu().numpy()
+            st0 = pv[:, 0][pv[:, 0] > 0]
+            en = pv[:, 13][pv[:, 13] > 0]
+            spans.append((en.max() - st0.min()) / 1e3 if st0.size and en.size else float("nan"))
+    kspan = _max_over_ranks(spans, world)
     # L2-warm steps (no flush between; SURVEY.md §8d asks for both numbers)
     b2b = run(max(20, K // 2), False, graph)[0]
     kdisp = run(max(20, K // 2), True, graph_k)[2]
@@ -467,13 +533,20 @@ def run_b200(a) -> None:
         "dtype": ("fp8-e4m3" if wl["elem"] == 1 else "bf16") + " dispatch / bf16 combine (fp32 accumulate)",
         "data": "synthetic",
         "config": workload_config(wl, tokens, n_gpu, rk.private_tokens),
-        "l2": "flushed before every step (512 MiB write)",
+        "l2": ("flushed before every step: 512 MiB write then read (cold, clean L2)" if a.flush == "write+read"
+               else "flushed before every step: 512 MiB write"),
+        f"p50_{other.replace('+', '_')}_flush_us": round(float(np.median(tot_other)), 2),
         "timing": "public-API step captured as a CUDA graph; CUDA event nodes inside the graph around "
                   "the step (device time, graph launch excluded), p50 over steps of the max over ranks",
         "p90_us": round(float(np.percentile(tot, 90)), 2),
         "p99_us": round(float(np.percentile(tot, 99)), 2),
         "p50_l2_warm_us": round(float(np.median(b2b)), 2),
         "p50_with_graph_launch_us": round(float(np.median(tot_launch)), 2),
+        "p50_eager_us": round(float(np.median(eager)), 2),
+        "p50_kernel_span_us": round(float(np.nanmedian(kspan)), 2),
+        "span_note": "value: CUDA event nodes inside the step graph; p50_eager_us: events around the eager "
+                     "step with the host ahead of the GPU; p50_kernel_span_us: %globaltimer first dispatch "
+                     "CTA start -> last combine CTA end (max over ranks)",
         "tokens_per_s": round(n_gpu * tokens / (p50 * 1e-6), 1),
         "kernel_us": {k: round(v, 2) for k, v in kt.items()},
         "roofline": roofline,

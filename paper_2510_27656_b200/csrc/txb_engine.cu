@@ -190,31 +190,69 @@ __global__ void __launch_bounds__(kCopyThreads, 1) k_copy_jobs(const __grid_cons
 // device): step k (0-based) of the request moves pages_per_step pages
 // (indices [k*pages_per_step, (k+1)*pages_per_step) of the index arrays)
 // as soon as *clock >= clock_base + k + 1 -- the compute stream advances the
-// clock after each layer, no host in the loop -- and the CTA that finishes
+// clock after each layer, no host in the loop -- and the warp that finishes
 // a step last releases one increment on the request's ImmCounter slot.
-// CTAs run ahead independently; a step never waits for the previous step's
-// stragglers, only for the clock.
+//
+// Every warp runs on its own (no CTA barrier): it copies its share of a
+// step and moves on; completion is booked per warp in batches of kBatch
+// steps -- one release fence (which waits for the warp's stores to land)
+// covers the batch, then one ticket increment per step; the warp that
+// brings a step's ticket to the number of warps releases the receipt.  A
+// warp that reaches a step the clock has not released yet books what it
+// has first, so receipts never wait on a future layer.  The fence is the
+// only drain, and no other warp waits for it.
+constexpr int kStreamBatch = 8;
+
 __global__ void __launch_bounds__(kCopyThreads, 1) k_kv_stream(const __grid_constant__ txb_stream_job ks) {
   extern __shared__ __align__(128) uint8_t stage[];
   __shared__ __align__(8) uint64_t bars[kCopyWarps * kWarpStages];
-  __shared__ uint32_t fail;
-  const int warp = threadIdx.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool tma = ks.use_tma != 0;
   init_warp_bars(bars + warp * kWarpStages, tma);
-  if (threadIdx.x == 0) fail = 0;
-  __syncthreads();
   uint32_t phase[kWarpStages] = {};
   const int64_t per_page = (ks.page_len + kPiece - 1) / kPiece;
   const int64_t total = ks.pages_per_step * per_page;
+  const uint32_t nwarps = gridDim.x * kCopyWarps;
+  const int64_t gw = (int64_t)blockIdx.x * kCopyWarps + warp;
   const uint64_t dl = globaltimer() + ks.timeout_ns;
+  int pend0 = 0, npend = 0;  // steps [pend0, pend0 + npend) copied, not yet booked
+  auto book = [&]() {
+    if (npend == 0) return;
+    if (lane == 0) {
+      fence_release(ks.single_device != 0);
+      for (int q = pend0; q < pend0 + npend; ++q) {
+        if (atomicAdd(&ks.tickets[q], 1u) == nwarps - 1) {
+          ks.tickets[q] = 0;
+          if (ks.imm_ctr) {
+            fence_release(ks.single_device != 0);
+            red_relaxed_sys_add(ks.imm_ctr, 1);
+          }
+        }
+      }
+    }
+    __syncwarp();
+    pend0 += npend;
+    npend = 0;
+  };
   #pragma unroll 1
   for (int k = 0; k < ks.nsteps; ++k) {
-    if (threadIdx.x == 0 && !spin_ge(ks.clock, ks.clock_base + (uint64_t)k + 1, dl)) {
-      fail = 1;
-      if (ks.err) atomicOr(ks.err, TXB_EV_WAIT_IMM);
+    uint32_t ok = 1;
+    if (lane == 0) {
+      const uint64_t want = ks.clock_base + (uint64_t)k + 1;
+      if (ld_acquire_sys(ks.clock) < want) {
+        ok = 2;  // not released yet: book the finished steps before waiting
+      }
     }
-    __syncthreads();
-    if (fail) return;
+    ok = __shfl_sync(0xffffffffu, ok, 0);
+    if (ok == 2) {
+      book();
+      if (lane == 0) {
+        ok = spin_ge(ks.clock, ks.clock_base + (uint64_t)k + 1, dl) ? 1u : 0u;
+        if (!ok && ks.err) atomicOr(ks.err, TXB_EV_WAIT_IMM);
+      }
+      ok = __shfl_sync(0xffffffffu, ok, 0);
+      if (!ok) return;
+    }
     const int64_t* si = ks.src_idx + (int64_t)k * ks.pages_per_step;
     const int64_t* di = ks.dst_idx + (int64_t)k * ks.pages_per_step;
     auto piece = [&](int64_t q) {
@@ -226,20 +264,12 @@ __global__ void __launch_bounds__(kCopyThreads, 1) k_kv_stream(const __grid_cons
       p.bytes = (uint32_t)(rem < kPiece ? rem : kPiece);
       return p;
     };
-    warp_copy_range((int64_t)blockIdx.x * kCopyWarps + warp, (int64_t)gridDim.x * kCopyWarps, total, tma,
-                    stage + (size_t)warp * kWarpStages * kPiece, bars + warp * kWarpStages, phase, piece);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      fence_release(ks.single_device != 0);
-      if (atomicAdd(&ks.tickets[k], 1u) == gridDim.x - 1) {
-        ks.tickets[k] = 0;
-        if (ks.imm_ctr) {
-          fence_release(ks.single_device != 0);
-          red_relaxed_sys_add(ks.imm_ctr, 1);
-        }
-      }
-    }
+    warp_copy_range(gw, (int64_t)nwarps, total, tma, stage + (size_t)warp * kWarpStages * kPiece,
+                    bars + warp * kWarpStages, phase, piece);
+    __syncwarp();
+    if (++npend == kStreamBatch) book();
   }
+  book();
 }
 
 // Full-u32 ImmCounter table (ImmCounterTable, engine.py:138-205): keys

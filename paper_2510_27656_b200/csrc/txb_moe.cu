@@ -58,6 +58,12 @@ constexpr int kTokWaitMin = 256;
 __host__ __device__ inline bool tok_mode(const txb_moe_shape& s) {
   return s.max_tokens > kTokWaitMin && s.ranks > 1;
 }
+// Per-token combine completion at every EP > 1: each returned row
+// release-adds its origin token's counter (tokc), so an origin reduces a
+// token as soon as that token's rows are back instead of after the last
+// row of the step.  tok_mode above only selects the large-batch layout
+// (phase-ordered return list, sender / reducer CTA roles).
+__host__ __device__ inline bool per_token(const txb_moe_shape& s) { return s.ranks > 1; }
 
 __device__ __forceinline__ int pad_up(int x) { return (x + kGroupPad - 1) / kGroupPad * kGroupPad; }
 
@@ -490,12 +496,12 @@ __device__ void route_publish(const txb_moe_shape& s, void* const* peers, Flags*
     }
     if (!bad)
       #pragma unroll 1
-      for (int d = lane; d < N; d += 32) {
-        if (d == s.me) continue;
+      for (int d = 0; d < N; ++d) {  // copies that come back from d (diagnostics)
         uint32_t c = 0;
         #pragma unroll 1
-        for (int le = 0; le < L; ++le) c += hist[d * L + le];
-        f->comb_src_t[d] += c;
+        for (int le = lane; le < L; le += 32) c += hist[d * L + le];
+        for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        if (lane == 0 && d != s.me) f->comb_src_t[d] += c;
       }
     if (lane == 0) {
       f->comb_target += bad ? 0 : (uint64_t)(n * s.topk) - self;
@@ -614,19 +620,18 @@ __device__ void book_recv(const txb_moe_shape& s, Flags* f, const uint32_t* C, i
   const int N = s.ranks, E = s.experts, L = s.local_experts, me = s.me;
   uint32_t tok = 0, pv = 0;
   #pragma unroll 1
-  for (int q = lane; q < N; q += 32) {
+  for (int q = 0; q < N; ++q) {
     uint32_t a = 0;
     #pragma unroll 1
-    for (int le = 0; le < L; ++le) a += C[q * E + me * L + le];
+    for (int le = lane; le < L; le += 32) a += C[q * E + me * L + le];
+    for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
     const uint32_t take = (q != me && s.priv_tokens > 0) ? min(a, (uint32_t)s.priv_tokens) : 0u;
-    f->tok_src_t[q] += a - take;
-    f->priv_src_t[q] += take;
+    if (lane == 0) {
+      f->tok_src_t[q] += a - take;
+      f->priv_src_t[q] += take;
+    }
     tok += a - take;
     pv += take;
-  }
-  for (int o = 16; o; o >>= 1) {
-    tok += __shfl_xor_sync(0xffffffffu, tok, o);
-    pv += __shfl_xor_sync(0xffffffffu, pv, o);
   }
   if (lane == 0) {
     f->tok_target += tok;
@@ -675,7 +680,7 @@ __device__ void own_positions(const txb_moe_shape& s, const uint32_t* hist, int6
         if (sidx < s.priv_tokens) {
           const int par = (int)(step & 1);
           pd = priv_rows_of(peers[d], s, par, s.me) + (int64_t)sidx * s.payload_bytes;
-          if (tok_mode(s)) privsrc_of(peers[d], s, par, s.me)[sidx] = sh.own_i[k] / s.topk;
+          if (per_token(s)) privsrc_of(peers[d], s, par, s.me)[sidx] = sh.own_i[k] / s.topk;
           atomicAdd(&sh.pcnt[d], 1u);
         }
       }
@@ -715,13 +720,13 @@ __device__ void own_dests(const txb_moe_shape& s, const uint32_t* C, void* const
       const int g = acc + (int)sh.own_rank[k];
       sh.dstp[k] = grouped_of(peers[d], s) + (int64_t)g * s.payload_bytes;
       gidx[sh.own_i[k]] = d == s.me ? g : -1;
-      if (tok_mode(s)) srctok_of(peers[d], s)[g] = sh.own_i[k] / s.topk;
+      if (per_token(s)) srctok_of(peers[d], s)[g] = sh.own_i[k] / s.topk;
       atomicAdd(&sh.cnt[d], 1u);
     }
   }
   g.sync();
   // one token per CTA on these paths: book its rows that will come back
-  if (tok_mode(s) && g.tid == 0) tokt_of(peers[s.me], s)[sh.own_i[0] / s.topk] += s.topk - sh.cnt[s.me];
+  if (per_token(s) && g.tid == 0) tokt_of(peers[s.me], s)[sh.own_i[0] / s.topk] += s.topk - sh.cnt[s.me];
 }
 
 // ------------------------------------------------------------------- P4
@@ -741,14 +746,14 @@ __device__ __forceinline__ uint8_t* copy_dest(const txb_moe_shape& s, void* cons
     if (sidx < s.priv_tokens) {
       const int par = (int)(step & 1);
       gidx[i] = -1;
-      if (tok_mode(s)) privsrc_of(peers[d], s, par, s.me)[sidx] = (int32_t)t;
+      if (per_token(s)) privsrc_of(peers[d], s, par, s.me)[sidx] = (int32_t)t;
       atomicAdd(&sh.pcnt[d], 1u);
       return priv_rows_of(peers[d], s, par, s.me) + sidx * s.payload_bytes;
     }
   }
   const int64_t g = (int64_t)baseg[e] + rank;
   gidx[i] = d == s.me ? (int32_t)g : -1;
-  if (tok_mode(s)) srctok_of(peers[d], s)[g] = (int32_t)t;
+  if (per_token(s)) srctok_of(peers[d], s)[g] = (int32_t)t;
   atomicAdd(&sh.cnt[d], 1u);
   return grouped_of(peers[d], s) + g * s.payload_bytes;
 }
@@ -854,13 +859,13 @@ __device__ __noinline__ bool dispatch_tokens_flat(const txb_moe_shape& s, const 
   }
 }
 
-// Per-token completion (tok_mode): book the copies of tokens t0, t0 + dt,
+// Per-token completion (EP > 1): book the copies of tokens t0, t0 + dt,
 // ... < t1 that another rank serves -- the rows that will come back through
 // tokc[t].  Every dispatch path books them, so tokc and tokt stay in step
 // whichever path (fused, split) a step takes.
 __device__ __forceinline__ void book_tok_targets(const txb_moe_shape& s, const int64_t* routes, void* region,
                                                  int64_t t0, int64_t t1, int64_t dt) {
-  if (!tok_mode(s)) return;
+  if (!per_token(s)) return;
   uint64_t* tokt = tokt_of(region, s);
   #pragma unroll 1
   for (int64_t t = t0 + (int64_t)threadIdx.x * dt; t < t1; t += (int64_t)blockDim.x * dt) {
@@ -1272,7 +1277,7 @@ __device__ void recv_private_rows(const txb_moe_shape& s, const int* sm, void* r
     } else {
       copy_row(dst, src, P, lane, 32);
     }
-    if (lane == 0 && tok_mode(s)) srctok_of(region, s)[g] = privsrc_of(region, s, par, q)[k];
+    if (lane == 0 && per_token(s)) srctok_of(region, s)[g] = privsrc_of(region, s, par, q)[k];
   }
 }
 
@@ -1310,13 +1315,13 @@ __device__ void combine_send_rows(const txb_moe_shape& s, Flags* f, const uint8_
   const int64_t Pc = s.comb_bytes;
   const int lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
   const bool vec = (Pc % 16 == 0) && (ld % 16 == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
-  if (tok_mode(s)) {
+  if (per_token(s)) {
     // per-token completion: each warp returns whole rows, walking the
     // (phase-ordered) list grid-stride, and after every kBatch rows fences
     // once and release-adds the origin token's counter of each of them.
     // Every row shape takes this branch (rows that are not 16-byte
     // vectorisable are copied with copy_row), because the origin's reduce
-    // waits on tokc whenever tok_mode holds.
+    // waits on tokc at every EP > 1.
     constexpr int kBatch = 4;
     const int32_t* srct = srctok_of(peers[s.me], s);
     const int n16 = (int)(Pc >> 4);
@@ -1418,13 +1423,18 @@ __device__ bool combine_reduce(const txb_moe_shape& s, Flags* f, const uint8_t* 
   if (cta < n) combine_prep(ct, comb, Pc, out, ld, pos, gidx, split ? nullptr : w, cta, R);
   // EP=1: every row is this rank's own and already written (stream order)
   const bool solo = s.ranks == 1;
+  // fused path at EP > 1 (`region`): each token waits for its own rows only
+  // (tokc[t] >= tokt[t]), so reducing overlaps the other tokens' returns
+  const bool per_tok = region && per_token(s);
   auto wait = [&]() -> bool {
     if (threadIdx.x == 0) {
       if (solo) {
         sh.fail = 0;
       } else {
         const uint64_t dl = globaltimer() + timeout_ns;
-        sh.fail = spin_ge(&f->comb_ctr, f->comb_target, dl) ? 0u : TXB_EV_WAIT_COMBINE;
+        const bool ok = per_tok ? spin_ge(tokc_of(region, s) + cta, tokt_of(region, s)[cta], dl)
+                                : spin_ge(&f->comb_ctr, f->comb_target, dl);
+        sh.fail = ok ? 0u : TXB_EV_WAIT_COMBINE;
         if (sh.fail) atomicOr(&f->err, sh.fail);
       }
       if (prof) prof[blockIdx.x * 32 + 23] = globaltimer();
@@ -1438,9 +1448,6 @@ __device__ bool combine_reduce(const txb_moe_shape& s, Flags* f, const uint8_t* 
     __syncthreads();
     return true;
   }
-  // large batches with per-token completion (fused path only: `region`):
-  // each token waits for its own rows, so the reduce overlaps the returns
-  const bool per_tok = region && tok_mode(s);
   if (!per_tok && !wait()) return false;
   const uint64_t* tokc = per_tok ? tokc_of(region, s) : nullptr;
   const uint64_t* tokt = per_tok ? tokt_of(region, s) : nullptr;

@@ -121,7 +121,10 @@ def one_request(mode: str) -> dict:
                 clock.advance(comp)
             ec.record(comp)
     send.send_context(req)
-    assert t.wait(120.0), "request did not complete"
+    if not t.wait(60.0):
+        raise SystemExit(f"{mode}: request did not complete: receipts {dec_e.imm_received_total(req.imm)} of "
+                         f"{req.expected}, clock on device {clock.device_value() if mode != 'launch' else None}, "
+                         f"engine error word {int(pre._err.cpu()[0])}")
     torch.cuda.synchronize(0)
     ms = e0.elapsed_time(e1)
     out["transfer_ms"] = round(ms, 3)
