@@ -103,6 +103,12 @@ int txb_ipc_export(int device, void* ptr, uint8_t* out_handle /*[64]*/);
 int txb_ipc_import(int device, const uint8_t* handle /*[64]*/, void** out_ptr);
 int txb_ipc_close(int device, void* ptr);
 int txb_enable_peer(int device, int peer_device);
+/* A dedicated non-blocking stream for an engine's copies (never one of the
+ * framework's pooled streams, which user code may also be handed: a copy
+ * kernel waiting on a device clock must not sit in front of the compute
+ * that advances it). */
+int txb_stream_create(int device, void** out_stream);
+int txb_stream_destroy(int device, void* stream);
 /* Device address of page-locked host memory (cudaHostAlloc / pinned torch
  * tensors).  The kernels read inputs from and write results to such host
  * buffers in place over PCIe (zero-copy), the way the reference's dispatch

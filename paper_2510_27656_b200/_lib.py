@@ -107,6 +107,8 @@ SIGNATURES: dict[str, list] = {
     "txb_ipc_import": [_INT, C.c_char_p, C.POINTER(_VP)],
     "txb_ipc_close": [_INT, _VP],
     "txb_enable_peer": [_INT, _INT],
+    "txb_stream_create": [_INT, C.POINTER(_VP)],
+    "txb_stream_destroy": [_INT, _VP],
     "txb_host_device_ptr": [_VP, C.POINTER(_VP)],
     "txb_moe_plan": [C.POINTER(Shape)],
     "txb_moe_dispatch_fused": [C.POINTER(Shape), C.POINTER(Bufs), _VP, _INT, _I64, _VP, _U64, _VP],

@@ -64,6 +64,9 @@ __host__ __device__ inline bool tok_mode(const txb_moe_shape& s) {
 // row of the step.  tok_mode above only selects the large-batch layout
 // (phase-ordered return list, sender / reducer CTA roles).
 __host__ __device__ inline bool per_token(const txb_moe_shape& s) { return s.ranks > 1; }
+// Completion unit of a returned row on tokc: its 2-KiB chunks.
+constexpr int kChunk = 2048;
+__host__ __device__ inline int comb_chunks(const txb_moe_shape& s) { return (int)((s.comb_bytes + kChunk - 1) / kChunk); }
 
 __device__ __forceinline__ int pad_up(int x) { return (x + kGroupPad - 1) / kGroupPad * kGroupPad; }
 
@@ -726,7 +729,8 @@ __device__ void own_dests(const txb_moe_shape& s, const uint32_t* C, void* const
   }
   g.sync();
   // one token per CTA on these paths: book its rows that will come back
-  if (per_token(s) && g.tid == 0) tokt_of(peers[s.me], s)[sh.own_i[0] / s.topk] += s.topk - sh.cnt[s.me];
+  if (per_token(s) && g.tid == 0)
+    tokt_of(peers[s.me], s)[sh.own_i[0] / s.topk] += (uint64_t)(s.topk - sh.cnt[s.me]) * comb_chunks(s);
 }
 
 // ------------------------------------------------------------------- P4
@@ -871,7 +875,7 @@ __device__ __forceinline__ void book_tok_targets(const txb_moe_shape& s, const i
   for (int64_t t = t0 + (int64_t)threadIdx.x * dt; t < t1; t += (int64_t)blockDim.x * dt) {
     int remote = 0;
     for (int j = 0; j < s.topk; ++j) remote += (int)routes[t * s.topk + j] / s.local_experts != s.me;
-    tokt[t] += remote;
+    tokt[t] += (uint64_t)remote * comb_chunks(s);
   }
 }
 
@@ -1297,10 +1301,9 @@ __device__ void wait_tokens(Flags* f, int64_t* info, int L, uint64_t timeout_ns)
 
 // ------------------------------------------------------------------- C1
 
-// Rows are moved in 2 KiB chunks (one warp, four 16-byte loads per lane in
-// flight before the four peer stores) so a step's return traffic spreads
-// over every warp of the grid instead of one warp per 14 KiB row.
-constexpr int kChunk = 2048;
+// Rows are moved in 2 KiB chunks (kChunk; one warp, four 16-byte loads per
+// lane in flight before the four peer stores) so a step's return traffic
+// spreads over every warp of the grid instead of one warp per 14 KiB row.
 
 __device__ void combine_send_rows(const txb_moe_shape& s, Flags* f, const uint8_t* out, int64_t ld,
                                   void* const* peers, const int64_t* sources, const int32_t* ret,
@@ -1316,52 +1319,66 @@ __device__ void combine_send_rows(const txb_moe_shape& s, Flags* f, const uint8_
   const int lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
   const bool vec = (Pc % 16 == 0) && (ld % 16 == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
   if (per_token(s)) {
-    // per-token completion: each warp returns whole rows, walking the
-    // (phase-ordered) list grid-stride, and after every kBatch rows fences
-    // once and release-adds the origin token's counter of each of them.
+    // per-token completion: returned rows are counted in 2-KiB chunks on
+    // their origin token's counter (tokc[t] gains comb_chunks(s) per row).
+    // Decode-size lists are cut into chunks, one chunk per warp per pass
+    // (warp-major, so a short list spreads over every SM); large batches
+    // (tok_mode) move whole rows per warp in list (phase) order.  A warp
+    // fences once per kBatch items, then release-adds each item's count.
     // Every row shape takes this branch (rows that are not 16-byte
     // vectorisable are copied with copy_row), because the origin's reduce
     // waits on tokc at every EP > 1.
     constexpr int kBatch = 4;
     const int32_t* srct = srctok_of(peers[s.me], s);
-    const int n16 = (int)(Pc >> 4);
-    const int gw = cta * nwarp + warp, ngw = ncta * nwarp;
-    int pend_q = 0, pend_t = 0, npend = 0;
+    const int cpr = comb_chunks(s);
+    const bool rows = tok_mode(s);
+    const int per = rows ? 1 : cpr;       // items per row
+    const int gw = warp * ncta + cta, ngw = ncta * nwarp;
+    int pend_q = 0, pend_t = 0, pend_n = 0, npend = 0;
     auto flush = [&]() {
       __syncwarp();
       if (lane == 0 && npend) fence_acqrel_sys();
       #pragma unroll 1
       for (int k = 0; k < npend; ++k) {
         const int qk = __shfl_sync(0xffffffffu, pend_q, k), tk = __shfl_sync(0xffffffffu, pend_t, k);
-        if (lane == 0) red_relaxed_sys_add(tokc_of(peers[qk], s) + tk, 1);
+        const int nk = __shfl_sync(0xffffffffu, pend_n, k);
+        if (lane == 0) red_relaxed_sys_add(tokc_of(peers[qk], s) + tk, (uint64_t)nk);
       }
       npend = 0;
     };
+    const int items = total * per;
     #pragma unroll 1
-    for (int r = gw; r < total; r += ngw) {  // the list is in phase order: grid-stride keeps it
+    for (int it = gw; it < items; it += ngw) {
+      const int r = it / per, c = it - r * per;
       const int g = send_list[r];
       const int q = (int)sources[g];
+      const int64_t b0 = rows ? 0 : (int64_t)c * kChunk;
+      const int64_t nb = rows ? Pc : min((int64_t)kChunk, Pc - b0);
+      const uint8_t* src = out + (int64_t)g * ld + b0;
+      uint8_t* dst = comb_of(peers[q], s) + (int64_t)ret[g] * Pc + b0;
       if (vec) {
-        const int4* src = reinterpret_cast<const int4*>(out + (int64_t)g * ld);
-        int4* dst = reinterpret_cast<int4*>(comb_of(peers[q], s) + (int64_t)ret[g] * Pc);
+        const int4* sv = reinterpret_cast<const int4*>(src);
+        int4* dv = reinterpret_cast<int4*>(dst);
+        const int n16 = (int)(nb >> 4);
         #pragma unroll 1
-        for (int c0 = 0; c0 < n16; c0 += 128) {
-          int4 v[4];
+        for (int c0 = 0; c0 < n16; c0 += 256) {
+          int4 v[8];
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (c0 + lane + 32 * u < n16) v[u] = src[c0 + lane + 32 * u];
+          for (int u = 0; u < 8; ++u)
+            if (c0 + lane + 32 * u < n16) v[u] = sv[c0 + lane + 32 * u];
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (c0 + lane + 32 * u < n16) dst[c0 + lane + 32 * u] = v[u];
+          for (int u = 0; u < 8; ++u)
+            if (c0 + lane + 32 * u < n16) dv[c0 + lane + 32 * u] = v[u];
         }
       } else {
-        copy_row(comb_of(peers[q], s) + (int64_t)ret[g] * Pc, out + (int64_t)g * ld, Pc, lane, 32);
+        copy_row(dst, src, nb, lane, 32);
       }
       if (lane == npend) {
         pend_q = q;
         pend_t = srct[g];
+        pend_n = rows ? cpr : 1;
       }
-      if (lane == 0) atomicAdd(&sh.cnt[q], 1u);
+      if (lane == 0 && c == 0) atomicAdd(&sh.cnt[q], 1u);
       if (++npend == kBatch) flush();
     }
     flush();

@@ -109,6 +109,24 @@ int txb_enable_peer(int device, int peer_device) {
   return TXB_OK;
 }
 
+int txb_stream_create(int device, void** out_stream) {
+  if (!out_stream) {
+    set_error("txb_stream_create: null out pointer");
+    return TXB_ERR_TRANSFER;
+  }
+  TXB_ON_DEVICE(device);
+  cudaStream_t st = nullptr;
+  TXB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  *out_stream = (void*)st;
+  return TXB_OK;
+}
+
+int txb_stream_destroy(int device, void* stream) {
+  TXB_ON_DEVICE(device);
+  TXB_CUDA(cudaStreamDestroy((cudaStream_t)stream));
+  return TXB_OK;
+}
+
 int txb_host_device_ptr(void* host_ptr, void** out_device_ptr) {
   cudaPointerAttributes a;
   TXB_CUDA(cudaPointerGetAttributes(&a, host_ptr));

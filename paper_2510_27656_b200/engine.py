@@ -471,6 +471,7 @@ class TransferEngine:
         self.use_tma = False
         self._slots: dict[tuple[int, int], int] = {}
         self._cbt: _CallbackThread | None = None
+        self._own_streams: list[int] = []
         self.timing: list | None = None
         self.trace = TraceRecorder(self.name, enabled=trace)
         self._op_ids = itertools.count(1)
@@ -510,8 +511,15 @@ class TransferEngine:
             self._tickets = torch.zeros(self._TICKETS, dtype=torch.int32, device=dev)
             self._ticket_i = 0
             self._err = torch.zeros(1, dtype=torch.int32, device=dev)
-            self._stream = torch.cuda.Stream(dev)
-            self._read_stream = torch.cuda.Stream(dev)   # counter snapshots
+            # dedicated streams (torch's pooled streams can alias a caller's)
+            self._stream = self._own_stream()
+            self._read_stream = self._own_stream()    # counter snapshots
+
+    def _own_stream(self):
+        out = C.c_void_p()
+        _lib.call("txb_stream_create", self.device, C.byref(out))
+        self._own_streams.append(int(out.value))
+        return torch.cuda.ExternalStream(int(out.value), device=torch.device("cuda", self.device))
 
     @property
     def stream(self):
@@ -926,6 +934,11 @@ class TransferEngine:
         for r in list(self._regions.values()):
             r.close()
         self._regions.clear()
+        if self._own_streams:
+            torch.cuda.synchronize(self.device)
+        for sp in self._own_streams:
+            _lib.call("txb_stream_destroy", self.device, C.c_void_p(sp))
+        self._own_streams.clear()
         self._closed = True
         if self in self.fabric.engines:
             self.fabric.engines.remove(self)

@@ -66,6 +66,7 @@ kv.view(torch.int64).view(-1, W).copy_(
 ctx = pre.alloc_buffer(4096)
 send = kvcache.KvSender(pre, kv, ctx)
 peak_nvl, peak_hbm = 770.0, 6555.2
+comp = torch.cuda.Stream(0)        # the "compute" stream that advances the layer clock
 peak = peak_nvl if d1 else peak_hbm
 
 
@@ -100,7 +101,6 @@ def one_request(mode: str) -> dict:
         e1.record(st)
     else:
         clock = pre.device_clock(layout.steps)
-        comp = torch.cuda.Stream(0)
         if mode == "ready":
             clock.advance(comp, by=layout.steps)
             comp.synchronize()
