@@ -58,12 +58,14 @@ constexpr int kTokWaitMin = 256;
 __host__ __device__ inline bool tok_mode(const txb_moe_shape& s) {
   return s.max_tokens > kTokWaitMin && s.ranks > 1;
 }
-// Per-token combine completion at every EP > 1: each returned row
-// release-adds its origin token's counter (tokc), so an origin reduces a
-// token as soon as that token's rows are back instead of after the last
-// row of the step.  tok_mode above only selects the large-batch layout
-// (phase-ordered return list, sender / reducer CTA roles).
-__host__ __device__ inline bool per_token(const txb_moe_shape& s) { return s.ranks > 1; }
+// Per-token combine completion (tokc / tokt / srctok) runs with tok_mode.
+// Measured at decode size (EP=2, DSv3 shape; profiles/r02/README.md):
+// counting 2-KiB chunks per origin token, one fence per warp, made the
+// returns take 18 us instead of 6-11 -- the system-scope fences of a CTA's
+// warps do not overlap -- and a token's rows come from ~56 CTAs, so it
+// completes with the slowest of them anyway.  Decode keeps one fence per
+// CTA and the step's global combine counter.
+__host__ __device__ inline bool per_token(const txb_moe_shape& s) { return tok_mode(s); }
 // Completion unit of a returned row on tokc: its 2-KiB chunks.
 constexpr int kChunk = 2048;
 __host__ __device__ inline int comb_chunks(const txb_moe_shape& s) { return (int)((s.comb_bytes + kChunk - 1) / kChunk); }
@@ -690,6 +692,65 @@ __device__ void own_positions(const txb_moe_shape& s, const uint32_t* hist, int6
       sh.pdst[k] = pd;
     }
   }
+}
+
+// EP=1 decode: everything about copy k of the CTA's token by ONE warp, no
+// CTA barrier between the steps -- its stable rank (earlier entries of the
+// batch with the same expert, counted four staged ids per lane per load),
+// pos = sum_{e' < e} hist[e'] + rank (moe.py:514-521) and its grouped row
+// group_starts[e] + rank, group_starts[e] = sum_{e' < e} pad8(hist[e'])
+// (with one rank the local expert is the expert).  One
+// barrier at the end publishes sh.dstp to the storing threads.
+__device__ void own_copies_solo(const txb_moe_shape& s, const uint32_t* hist, const int32_t* rv,
+                                const txb_moe_bufs& b, uint32_t bad, Shared& sh, const Grp& g) {
+  const int lane = g.tid & 31, warp = g.tid >> 5, nwarp = g.nt >> 5;
+  const bool v4 = (reinterpret_cast<uintptr_t>(rv) & 15) == 0;
+  #pragma unroll 1
+  for (int k = warp; k < s.topk; k += nwarp) {
+    const int e = sh.own_e[k], i = sh.own_i[k];
+    if (bad) {
+      if (lane == 0) {
+        b.pos[i] = -1;
+        sh.dstp[k] = nullptr;
+        sh.pdst[k] = nullptr;
+      }
+      continue;
+    }
+    int cnt = 0;
+    if (v4) {
+      const int4* r4 = reinterpret_cast<const int4*>(rv);
+      #pragma unroll 4
+      for (int q = lane; 4 * q < i; q += 32) {
+        const int4 v = r4[q];
+        const int j = 4 * q;
+        cnt += (v.x == e) + (j + 1 < i && v.y == e) + (j + 2 < i && v.z == e) + (j + 3 < i && v.w == e);
+      }
+    } else {
+      #pragma unroll 4
+      for (int j = lane; j < i; j += 32) cnt += rv[j] == e;
+    }
+    int acc = 0, accp = 0;
+    #pragma unroll 4
+    for (int x = lane; x < e; x += 32) {
+      const int h = (int)hist[x];
+      acc += h;
+      accp += pad_up(h);
+    }
+    for (int o = 16; o; o >>= 1) {
+      cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+      acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      accp += __shfl_xor_sync(0xffffffffu, accp, o);
+    }
+    if (lane == 0) {
+      const int gr = accp + cnt;
+      b.rank_scratch[i] = cnt;
+      b.pos[i] = (int64_t)acc + cnt;
+      b.gidx[i] = gr;
+      sh.dstp[k] = grouped_of(b.peers[0], s) + (int64_t)gr * s.payload_bytes;
+      sh.pdst[k] = nullptr;
+    }
+  }
+  g.sync();
 }
 
 // grouped row on owner d of copy k: group_starts_d[le] + sum_{s' < me}
@@ -1319,20 +1380,16 @@ __device__ void combine_send_rows(const txb_moe_shape& s, Flags* f, const uint8_
   const int lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
   const bool vec = (Pc % 16 == 0) && (ld % 16 == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
   if (per_token(s)) {
-    // per-token completion: returned rows are counted in 2-KiB chunks on
-    // their origin token's counter (tokc[t] gains comb_chunks(s) per row).
-    // Decode-size lists are cut into chunks, one chunk per warp per pass
-    // (warp-major, so a short list spreads over every SM); large batches
-    // (tok_mode) move whole rows per warp in list (phase) order.  A warp
-    // fences once per kBatch items, then release-adds each item's count.
-    // Every row shape takes this branch (rows that are not 16-byte
-    // vectorisable are copied with copy_row), because the origin's reduce
-    // waits on tokc at every EP > 1.
+    // per-token completion (large batches): each warp returns whole rows in
+    // list (phase) order, fences once per kBatch rows, then release-adds
+    // each row's count (comb_chunks(s), the unit of tokc) on its origin
+    // token's counter.  Every row shape takes this branch (rows that are not
+    // 16-byte vectorisable are copied with copy_row), because the origin's
+    // reduce waits on tokc whenever per_token holds.
     constexpr int kBatch = 4;
     const int32_t* srct = srctok_of(peers[s.me], s);
     const int cpr = comb_chunks(s);
-    const bool rows = tok_mode(s);
-    const int per = rows ? 1 : cpr;       // items per row
+    // warp-major numbering: consecutive rows go to different CTAs (SMs)
     const int gw = warp * ncta + cta, ngw = ncta * nwarp;
     int pend_q = 0, pend_t = 0, pend_n = 0, npend = 0;
     auto flush = [&]() {
@@ -1346,16 +1403,13 @@ __device__ void combine_send_rows(const txb_moe_shape& s, Flags* f, const uint8_
       }
       npend = 0;
     };
-    const int items = total * per;
     #pragma unroll 1
-    for (int it = gw; it < items; it += ngw) {
-      const int r = it / per, c = it - r * per;
+    for (int r = gw; r < total; r += ngw) {
       const int g = send_list[r];
       const int q = (int)sources[g];
-      const int64_t b0 = rows ? 0 : (int64_t)c * kChunk;
-      const int64_t nb = rows ? Pc : min((int64_t)kChunk, Pc - b0);
-      const uint8_t* src = out + (int64_t)g * ld + b0;
-      uint8_t* dst = comb_of(peers[q], s) + (int64_t)ret[g] * Pc + b0;
+      const int64_t nb = Pc;
+      const uint8_t* src = out + (int64_t)g * ld;
+      uint8_t* dst = comb_of(peers[q], s) + (int64_t)ret[g] * Pc;
       if (vec) {
         const int4* sv = reinterpret_cast<const int4*>(src);
         int4* dv = reinterpret_cast<int4*>(dst);
@@ -1376,9 +1430,9 @@ __device__ void combine_send_rows(const txb_moe_shape& s, Flags* f, const uint8_
       if (lane == npend) {
         pend_q = q;
         pend_t = srct[g];
-        pend_n = rows ? cpr : 1;
+        pend_n = cpr;
       }
-      if (lane == 0 && c == 0) atomicAdd(&sh.cnt[q], 1u);
+      if (lane == 0) atomicAdd(&sh.cnt[q], 1u);
       if (++npend == kBatch) flush();
     }
     flush();
@@ -1768,14 +1822,8 @@ __device__ __forceinline__ void dispatch_roles_solo(const txb_moe_shape& s, cons
     for (int q = tg.tid; q < s.ranks; q += tg.nt) sh.cnt[q] = 0;
     named_sync(3, kThreads);  // histogram, staged ids and own copies ready
     const uint32_t bad = bad_s;
-    const int nw = (n > cta ? (int)((n - cta + ncta - 1) / ncta) : 0) * s.topk;
+    own_copies_solo(s, hist, rv, b, bad, sh, tg);
     if (!bad) {
-      own_ranks(rv, b.rank_scratch, nw, sh, tg);
-      tg.sync();
-    }
-    own_positions(s, hist, b.pos, bad, sh, tg);
-    if (!bad) {
-      own_dests(s, hist, b.peers, b.gidx, sh, tg);
       if (b.prof && tg.tid == 0) b.prof[blockIdx.x * 32 + 15] = globaltimer();
       store_row_regs<SRC, ELEM>(pre, s.hidden, s.scales, sh.dstp, s.topk, tg);
     }

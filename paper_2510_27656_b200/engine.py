@@ -934,11 +934,8 @@ class TransferEngine:
         for r in list(self._regions.values()):
             r.close()
         self._regions.clear()
-        if self._own_streams:
-            torch.cuda.synchronize(self.device)
-        for sp in self._own_streams:
-            _lib.call("txb_stream_destroy", self.device, C.c_void_p(sp))
-        self._own_streams.clear()
+        # the engine's streams stay alive with the process: tensors that
+        # recorded use on them (record_stream) may be freed after close()
         self._closed = True
         if self in self.fabric.engines:
             self.fabric.engines.remove(self)
