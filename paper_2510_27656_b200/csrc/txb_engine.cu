@@ -216,6 +216,7 @@ __global__ void __launch_bounds__(kCopyThreads, 1) k_kv_stream(const __grid_cons
   const int64_t gw = (int64_t)blockIdx.x * kCopyWarps + warp;
   const uint64_t dl = globaltimer() + ks.timeout_ns;
   int pend0 = 0, npend = 0;  // steps [pend0, pend0 + npend) copied, not yet booked
+  uint64_t seen = 0;         // clock value this warp has already acquired
   auto book = [&]() {
     if (npend == 0) return;
     if (lane == 0) {
@@ -236,22 +237,25 @@ __global__ void __launch_bounds__(kCopyThreads, 1) k_kv_stream(const __grid_cons
   };
   #pragma unroll 1
   for (int k = 0; k < ks.nsteps; ++k) {
-    uint32_t ok = 1;
-    if (lane == 0) {
-      const uint64_t want = ks.clock_base + (uint64_t)k + 1;
-      if (ld_acquire_sys(ks.clock) < want) {
-        ok = 2;  // not released yet: book the finished steps before waiting
-      }
-    }
-    ok = __shfl_sync(0xffffffffu, ok, 0);
-    if (ok == 2) {
-      book();
+    const uint64_t want = ks.clock_base + (uint64_t)k + 1;
+    if (seen < want) {  // the clock is read only when the cached value runs out
+      uint32_t ok = 1;
       if (lane == 0) {
-        ok = spin_ge(ks.clock, ks.clock_base + (uint64_t)k + 1, dl) ? 1u : 0u;
-        if (!ok && ks.err) atomicOr(ks.err, TXB_EV_WAIT_IMM);
+        seen = ld_acquire_sys(ks.clock);
+        if (seen < want) ok = 2;  // not released yet: book the finished steps before waiting
       }
       ok = __shfl_sync(0xffffffffu, ok, 0);
-      if (!ok) return;
+      if (ok == 2) {
+        book();
+        if (lane == 0) {
+          ok = spin_ge(ks.clock, want, dl) ? 1u : 0u;
+          if (!ok && ks.err) atomicOr(ks.err, TXB_EV_WAIT_IMM);
+          seen = ld_acquire_sys(ks.clock);
+        }
+        ok = __shfl_sync(0xffffffffu, ok, 0);
+        if (!ok) return;
+      }
+      seen = __shfl_sync(0xffffffffu, seen, 0);
     }
     const int64_t* si = ks.src_idx + (int64_t)k * ks.pages_per_step;
     const int64_t* di = ks.dst_idx + (int64_t)k * ks.pages_per_step;

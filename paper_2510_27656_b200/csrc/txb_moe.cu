@@ -1877,14 +1877,13 @@ k_dispatch_roles(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
     if (b.prof && tg.tid == 0) b.prof[blockIdx.x * 32 + 1] = globaltimer();
     // speculative private copies (moe.py:556-582): their destinations need
     // only this rank's own counts, so they are stored while the route
-    // exchange is still in flight, and counted on the owners' private
-    // counters under their own release fence
+    // exchange is still in flight; they are counted with the main rows by
+    // the CTA's one release fence at the end (a second fence here would
+    // hold the whole CTA at the hand-off barrier for its drain)
     named_sync(4, kThreads);  // private destinations are in sh.pdst
     if (s.priv_tokens > 0) {
       store_row_regs<SRC, ELEM>(pre, s.hidden, s.scales, sh.pdst, s.topk, tg);
       if (b.prof && tg.tid == 0) b.prof[blockIdx.x * 32 + 26] = globaltimer();
-      tg.sync();
-      if (tg.tid == 0) signal_rows_thread(s, b.peers, 0, step, sh, false, true);
     }
     named_sync(3, kThreads);  // destinations are in sh.dstp
     if (!skip) store_row_regs<SRC, ELEM>(pre, s.hidden, s.scales, sh.dstp, s.topk, tg);
@@ -1925,8 +1924,6 @@ k_dispatch_roles(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
       // private rows that arrived before the layout was known
       recv_rows_body(s, rt, b.rows, b.sources, b.ret_slot, grouped_of(b.region, s), b.dirty, b.send_list,
                      &f->send_cnt, cta, ncta, rg, pd);
-      const int nw = rg.nt >> 5;
-      recv_private_rows(s, rt, b.region, step, timeout_ns, cta * nw + (rg.tid >> 5), ncta * nw, rg.tid & 31);
     }
     stamp(b, 7);
   }
@@ -1937,6 +1934,10 @@ k_dispatch_roles(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
   }
   stamp(b, 5);
   if (!solo) signal_counts(s, b.peers, 0, step, sh);
+  // the private rows other ranks stored here, once this CTA has signalled
+  // (waiting for them before it would make the ranks wait on each other)
+  recv_private_rows(s, rt, b.region, step, timeout_ns, cta * (kThreads >> 5) + (threadIdx.x >> 5),
+                    ncta * (kThreads >> 5), threadIdx.x & 31);
   stamp(b, 6);
   if (cta == 0) {
     if (!solo) wait_tokens(f, b.info, s.local_experts, timeout_ns);

@@ -309,6 +309,21 @@ class KvSender:
         dst = (layer[:, None, None] * req.dst_heads + j[None, :, None]) * req.dst_slots + sl[slot]
         return src.reshape(-1).astype(np.int64), dst.reshape(-1).astype(np.int64)
 
+    def prepare_stream(self, req: KvRequest):
+        """Device page lists and step tickets of a request for stream_all,
+        built once (the host arithmetic and the upload stay out of the
+        transfer)."""
+        cache = getattr(self, "_stream_plan", None)
+        if cache is not None and cache[0] == req.request_id and cache[1] is req:
+            return cache[2]
+        L = req.layout
+        si, di = self.step_indices(req)
+        dev = torch.device("cuda", self.engine.device)
+        plan = (torch.from_numpy(si).to(dev), torch.from_numpy(di).to(dev),
+                torch.zeros(max(1, L.steps), dtype=torch.int32, device=dev))
+        self._stream_plan = (req.request_id, req, plan)
+        return plan
+
     def stream_all(self, req: KvRequest, clock: DeviceClock, grid: int = 0, use_tma: bool | None = None,
                    timeout: float = 60.0) -> CompletionFlag:
         """Enqueue the whole request as ONE persistent kernel on the engine's
@@ -321,11 +336,7 @@ class KvSender:
         L = req.layout
         if L.page_len % 16 or self.kv.data_ptr() % 16:
             raise ProtocolError("streamed pages must be 16-byte aligned")
-        si, di = self.step_indices(req)
-        dev = torch.device("cuda", eng.device)
-        si_d = torch.from_numpy(si).pin_memory().to(dev, non_blocking=True)
-        di_d = torch.from_numpy(di).pin_memory().to(dev, non_blocking=True)
-        tickets = torch.zeros(max(1, L.steps), dtype=torch.int32, device=dev)
+        si_d, di_d, tickets = self.prepare_stream(req)
         dst_base, dst_imm = eng._peer_base(req.kv_desc)
         nh = req.head_hi - req.head_lo
         j = _lib.StreamJob()
@@ -350,5 +361,4 @@ class KvSender:
                 _lib.call("txb_kv_stream", C.byref(j), int(grid), C.c_void_p(eng._stream.cuda_stream))
                 ev = torch.cuda.Event()
                 ev.record(eng._stream)
-        self._keep = (si_d, di_d, tickets)
         return CompletionFlag(ev)

@@ -554,3 +554,83 @@ def test_per_token_mode_odd_rows_host_gated():
                 assert c["tok_ctr"] == c["tok_target"] and c["comb_ctr"] == c["comb_target"]
     finally:
         close_mesh(mesh)
+
+
+def _grid_cases(count: int, seed: int):
+    """A seeded subsample of the SPEC.md acceptance grid (criterion 6):
+    (N, E, T, R) in {2,4,8} x {4,8,16} x {1..16} x {1,2,4}, E a multiple of
+    N and R <= E (the reference RoutingSpec rejects the rest)."""
+    combos = [(n, e, t, r) for n in (2, 4, 8) for e in (4, 8, 16) for t in range(1, 17) for r in (1, 2, 4)
+              if e % n == 0 and r <= e]
+    rng = np.random.default_rng(seed)
+    return [combos[i] for i in rng.choice(len(combos), size=count, replace=False)]
+
+
+@pytest.mark.parametrize("n,e,t,r", _grid_cases(24, 553))
+def test_acceptance_grid_subsample(n, e, t, r):
+    """SPEC.md criterion 6 through the device path: two seeded random steps
+    (random token counts <= T, reference random_step) per grid point;
+    grouped payloads, rows, sources, pos and the fp32 combine bit-exact vs
+    the oracle (the criterion asks 1e-6; this is exact), the capacity bound
+    N*T*max(R, E/N) respected (instrumented from the device layout).  The
+    reference's own payload format (fp8, 8 scale slots, hidden 64)."""
+    spec = moe.RoutingSpec(ranks=n, experts=e, max_tokens=t, topk=r, hidden=64, elem_size=1, scales=8)
+    os_ = ospec_of(spec)
+    mesh = make_mesh(spec, private=min(4, t))
+    try:
+        for seed in range(2):
+            rng = np.random.default_rng(1000 * seed + 7 * n + 13 * e + 17 * t + r)
+            routes, values, weights = mo.random_step(os_, rng)
+            res = run_moe_round(mesh, spec, routes, values, weights)
+            ref = mo.dispatch(os_, routes, [mo.encode_tokens(os_, v) for v in values])
+            outs = mo.apply_experts(os_, ref)
+            comb = mo.combine(os_, ref, outs, weights)
+            for q in range(n):
+                g, c, pos = res[q]
+                want = ref.ranks[q].grouped
+                assert np.array_equal(_np(g.data), want.data), (seed, q)
+                assert np.array_equal(_np(g.rows), want.rows), (seed, q)
+                assert np.array_equal(_np(g.sources), want.sources), (seed, q)
+                assert np.array_equal(pos, ref.ranks[q].pos), (seed, q)
+                assert np.array_equal(c, comb[q]), (seed, q)
+            lay = mesh[0].last_layout
+            assert int(lay.recv_total.max()) <= spec.capacity
+    finally:
+        close_mesh(mesh)
+
+
+def test_dsv3_prefill_full_size_ep1():
+    """DeepSeek-V3 prefill at full size (BASELINE configs[2]: 4096 tokens,
+    hidden 7168, 256 experts, top-8, bf16 rows both ways) through the
+    large-batch fused path at EP=1: 32768 grouped rows of 14 KiB bit-exact,
+    bf16 combine bits exact, two steps."""
+    spec = moe.RoutingSpec(ranks=1, experts=256, max_tokens=4096, topk=8, hidden=7168, elem_size=2, scales=0,
+                           comb_elem_size=2, comb_scales=0)
+    mesh = moe.build_mesh(local_engines([0]), spec)
+    try:
+        for step in range(2):
+            rng = np.random.default_rng(4096 + step)
+            routes, values, weights = mo.random_step(ospec_of(spec), rng, tokens=4096 - 1000 * step)
+            xb, got = device_round(mesh, spec, routes, values, weights)
+            check_device_round(spec, routes, xb, weights, got, f"step {step}")
+    finally:
+        close_mesh(mesh)
+
+
+def test_kimi_k2_decode_ep1_full_size():
+    """Kimi-K2 shape (BASELINE configs[3]: 384 experts, top-8, hidden 7168,
+    128 tokens, bench.py's skewed routing) at EP=1 on the decode kernel,
+    fp8 dispatch encoded in-kernel, bf16 combine: bit-exact, three steps."""
+    import bench
+    spec = moe.RoutingSpec(ranks=1, experts=384, max_tokens=128, topk=8, hidden=7168, elem_size=1, scales=56,
+                           comb_elem_size=2, comb_scales=0)
+    mesh = moe.build_mesh(local_engines([0]), spec)
+    try:
+        for step in range(3):
+            rng = np.random.default_rng(3840 + step)
+            _, values, weights = mo.random_step(ospec_of(spec), rng, tokens=128)
+            routes = [bench.routes_for(bench.WORKLOADS["kimi"], rng, 128)]
+            xb, got = device_round(mesh, spec, routes, values, weights)
+            check_device_round(spec, routes, xb, weights, got, f"step {step}")
+    finally:
+        close_mesh(mesh)

@@ -351,3 +351,49 @@ def test_per_token_mode_odd_rows_alternating_paths(ranks):
             assert c["comb_ctr"] == c["comb_target"], q
     finally:
         close_mesh(mesh)
+
+
+@pytest.mark.parametrize("ranks", [2, 4])
+def test_dsv3_prefill_full_size_multi_gpu(ranks):
+    """DeepSeek-V3 prefill at full size (4096 tokens per rank, hidden 7168,
+    256 experts, top-8, bf16 both ways) at EP=2/4 over NVLink: the
+    large-batch path with per-token combine completion, bit-exact."""
+    if NGPU < ranks:
+        pytest.skip(f"needs {ranks} GPUs")
+    spec = moe.RoutingSpec(ranks=ranks, experts=256, max_tokens=4096, topk=8, hidden=7168, elem_size=2,
+                           scales=0, comb_elem_size=2, comb_scales=0)
+    mesh = moe.build_mesh(local_engines(list(range(ranks))), spec, timeout=60.0)
+    try:
+        rng = np.random.default_rng(44)
+        routes, values, weights = mo.random_step(ospec_of(spec), rng, tokens=4096)
+        xb, got = device_round(mesh, spec, routes, values, weights, timeout=60.0)
+        check_device_round(spec, routes, xb, weights, got)
+    finally:
+        close_mesh(mesh)
+
+
+@pytest.mark.parametrize("n,e,t,r", [(2, 4, 9, 2), (2, 16, 16, 4), (4, 8, 5, 1), (4, 16, 13, 4), (4, 4, 16, 2),
+                                     (8, 8, 7, 4), (8, 16, 16, 2), (8, 16, 3, 1)])
+def test_acceptance_grid_one_rank_per_gpu(n, e, t, r):
+    """SPEC.md criterion 6 grid points on real peers (fused cooperative
+    kernels, one GPU per rank): bit-exact against the oracle over three
+    seeded steps."""
+    if NGPU < n:
+        pytest.skip(f"needs {n} GPUs")
+    spec = moe.RoutingSpec(ranks=n, experts=e, max_tokens=t, topk=r, hidden=64, elem_size=1, scales=8)
+    os_ = ospec_of(spec)
+    mesh = moe.build_mesh(local_engines(list(range(n))), spec, timeout=20.0)
+    try:
+        for seed in range(3):
+            rng = np.random.default_rng(77 + seed)
+            routes, values, weights = mo.random_step(os_, rng)
+            res = run_moe_round(mesh, spec, routes, values, weights, timeout=20.0)
+            ref = mo.dispatch(os_, routes, [mo.encode_tokens(os_, v) for v in values])
+            comb = mo.combine(os_, ref, mo.apply_experts(os_, ref), weights)
+            for q in range(n):
+                g, c, pos = res[q]
+                assert np.array_equal(_np(g.data), ref.ranks[q].grouped.data), (seed, q)
+                assert np.array_equal(_np(g.rows), ref.ranks[q].grouped.rows), (seed, q)
+                assert np.array_equal(c, comb[q]), (seed, q)
+    finally:
+        close_mesh(mesh)

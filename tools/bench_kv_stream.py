@@ -101,6 +101,8 @@ def one_request(mode: str) -> dict:
         e1.record(st)
     else:
         clock = pre.device_clock(layout.steps)
+        send.prepare_stream(req)
+        torch.cuda.synchronize(0)
         if mode == "ready":
             clock.advance(comp, by=layout.steps)
             comp.synchronize()
