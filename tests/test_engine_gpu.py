@@ -434,3 +434,43 @@ def test_kv_stream_device_clock_steps_and_bytes():
     finally:
         a.close()
         b.close()
+
+
+def test_kv_stream_cfg5_whole_request_byte_identical():
+    """BASELINE configs[4] at full size: Llama-3-70B, 80 layers x 8 KV heads
+    x 2048 slots of 8-KiB pages (16-token pages, 32k context) = 10 GiB in
+    1280 (chunk, layer) steps, streamed by one persistent kernel into a
+    scattered decoder slot list (prefill cuda:0 -> decode cuda:1 when there
+    are two GPUs, else HBM loopback).  Every destination page must equal its
+    source page (device-side comparison), and the request's receipt count
+    must be steps + 1 (context write) exactly."""
+    a, b = _pair()
+    try:
+        layers, chunks, heads, slots, page = 80, 16, 8, 2048, 8192
+        layout = kvcache.KvLayout(layers, chunks, slots // chunks, page)
+        dec = kvcache.KvReceiver(b, layout, pool_slots=slots, local_heads=heads, ctx_bytes=1 << 16)
+        dec._free = list(np.random.default_rng(5).permutation(slots))
+        t = dec.open_request(ctx_len=4096)
+        total = layout.region_bytes(heads, slots)
+        W = page // 8
+        kv = a.alloc_buffer(total)
+        kv.view(torch.int64).view(-1, W).copy_(
+            torch.arange(total // 8, dtype=torch.int64, device=kv.device).view(-1, W))
+        send = kvcache.KvSender(a, kv, a.alloc_buffer(4096))
+        clock = a.device_clock(layout.steps)
+        clock.advance(by=layout.steps)
+        send.stream_all(t.request, clock).result(60.0)
+        send.send_context(t.request).result(30.0)
+        assert t.wait(30.0)
+        assert b.imm_received_total(t.request.imm) == layout.steps + 1
+        si, di = send.step_indices(t.request)
+        dstw = dec.kv.view(torch.int64).view(-1, W)
+        col = torch.arange(W, dtype=torch.int64, device=dstw.device)
+        for c0 in range(0, si.size, 65536):
+            s = torch.from_numpy(si[c0:c0 + 65536]).to(dstw.device)
+            d = torch.from_numpy(di[c0:c0 + 65536]).to(dstw.device)
+            assert torch.equal(dstw.index_select(0, d), s[:, None] * W + col[None, :]), c0
+        dec.release(t)
+    finally:
+        a.close()
+        b.close()
