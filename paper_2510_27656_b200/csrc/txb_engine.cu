@@ -569,7 +569,11 @@ static bool stream_memops(PFN_wait64* w, PFN_write64* wr) {
       fw = reinterpret_cast<PFN_wait64>(a);
       fwr = reinterpret_cast<PFN_write64>(b);
     }
-    if (getenv("TXB_NO_STREAM_MEMOPS")) state = 0;
+    // measured (tools/debug/clock_probe.py, profiles/r02/README.md): a
+    // stream write queued behind a kernel on its stream is not performed
+    // while another stream's persistent kernel polls the word, so the
+    // writes default to a one-thread kernel; TXB_STREAM_MEMOPS=1 opts in
+    if (!getenv("TXB_STREAM_MEMOPS")) state = 0;
   }
   *w = fw;
   *wr = fwr;

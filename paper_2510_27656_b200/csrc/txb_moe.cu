@@ -1106,14 +1106,22 @@ __device__ __noinline__ void recv_tables(const txb_moe_shape& s, const uint32_t*
 // the kernel's tail.  Byte i of the result = dirty[row i] (0 beyond G).
 constexpr int kPreDirty = 4;
 
-__device__ __forceinline__ uint32_t prefetch_dirty(const txb_moe_shape& s, const uint8_t* dirty, int cta, int ncta,
+// The loads stay unconsumed (separate registers) until recv_rows_body reads
+// them, so issuing them does not stall the issuing role.
+struct PreDirty {
+  uint8_t v[kPreDirty];
+  bool on;
+};
+
+__device__ __forceinline__ PreDirty prefetch_dirty(const txb_moe_shape& s, const uint8_t* dirty, int cta, int ncta,
                                                    const Grp& g) {
   const int nwarp = g.nt >> 5, warp = g.tid >> 5;
-  uint32_t pd = 0;
+  PreDirty pd;
+  pd.on = true;
 #pragma unroll
   for (int i = 0; i < kPreDirty; ++i) {
     const int64_t r = (int64_t)cta * nwarp + warp + (int64_t)i * ncta * nwarp;
-    if (r < s.grouped_rows) pd |= (uint32_t)dirty[r] << (8 * i);
+    pd.v[i] = r < s.grouped_rows ? dirty[r] : (uint8_t)0;
   }
   return pd;
 }
@@ -1122,7 +1130,7 @@ __device__ __forceinline__ uint32_t prefetch_dirty(const txb_moe_shape& s, const
 __device__ __forceinline__ void recv_rows_body(const txb_moe_shape& s, int* sm, int64_t* rows, int64_t* sources,
                                                int32_t* ret, uint8_t* G, uint8_t* dirty, int32_t* send_list,
                                                uint32_t* send_cnt, int cta, int ncta, const Grp& grp = Grp::cta(),
-                                               uint32_t pd = ~0u) {
+                                               PreDirty pd = PreDirty{{0}, false}) {
   const int N = s.ranks, L = s.local_experts;
   const RecvTables t = recv_carve(s, sm);
   const int padded_total = t.tot[0];
@@ -1149,7 +1157,16 @@ __device__ __forceinline__ void recv_rows_body(const txb_moe_shape& s, int* sm, 
     if (k >= t.gsize[le]) {
       // padding rows read as zero (moe.py:719); only rows that held data
       // since they were last zeroed need the store
-      const bool d = (pd != ~0u && it < kPreDirty) ? ((pd >> (8 * it)) & 0xFFu) != 0 : dirty[g] != 0;
+      bool d;
+      if (pd.on && it < kPreDirty) {
+        uint8_t v = 0;
+#pragma unroll
+        for (int i = 0; i < kPreDirty; ++i)
+          if (i == it) v = pd.v[i];
+        d = v != 0;
+      } else {
+        d = dirty[g] != 0;
+      }
       if (d) zero_row(G + (int64_t)g * P, P, lane, 32);
       if (lane == 0) {
         rows[g] = -1;
@@ -1481,12 +1498,18 @@ __device__ void combine_send_rows(const txb_moe_shape& s, Flags* f, const uint8_
 // token's row pointers and weights are staged before the wait; on the
 // decode path (one token per CTA, R <= 8, H % 8 == 0 rows) the rows this
 // rank served itself are already loaded into registers when the wait ends.
+// The combine's per-token staging (row pointers, weights, scales); one per
+// CTA.  The decode kernel fills the weights before its programmatic
+// dependency resolves (they are an input of the step, not an output of the
+// dispatch), so their cold load overlaps the dispatch's tail.
+static __shared__ CombTok s_comb_ct;
+
 template <int ELEM>
 __device__ bool combine_reduce(const txb_moe_shape& s, Flags* f, const uint8_t* comb, const uint8_t* out,
                                int64_t ld, const int64_t* pos, const int32_t* gidx, const float* w, int64_t n,
                                void* dst, int out_bf16, uint64_t timeout_ns, int cta, int ncta, Shared& sh,
-                               uint64_t* prof = nullptr, void* region = nullptr) {
-  __shared__ CombTok ct;
+                               uint64_t* prof = nullptr, void* region = nullptr, bool ws_ready = false) {
+  CombTok& ct = s_comb_ct;
   const int64_t Pc = s.comb_bytes;
   const int H = s.hidden, R = s.topk;
   const bool vec = combine_vec<ELEM>(Pc, comb, out, ld, H, gidx);
@@ -1515,7 +1538,7 @@ __device__ bool combine_reduce(const txb_moe_shape& s, Flags* f, const uint8_t* 
   };
   if (split) {
     __syncthreads();  // ct staged
-    if (!combine_token_split<ELEM>(ct, H, R, cta, w, dst, out_bf16, wait)) return false;
+    if (!combine_token_split<ELEM>(ct, H, R, cta, ws_ready ? nullptr : w, dst, out_bf16, wait)) return false;
     __syncthreads();
     return true;
   }
@@ -1542,11 +1565,12 @@ __device__ bool combine_reduce(const txb_moe_shape& s, Flags* f, const uint8_t* 
 // advances the local step counter.  The buffer-reuse barrier tag (done) is
 // published by the next step's route phase (route_publish), so the tail of
 // the combine carries no fence and no remote store.
-__device__ void end_of_step(Flags* f, uint64_t step, int ncta) {
+__device__ void end_of_step(Flags* f, int ncta) {
   __syncthreads();
   if (threadIdx.x == 0) {
     const uint32_t t = atomicAdd(&f->ticket, 1u);
     if (t == (uint32_t)ncta - 1) {
+      const uint64_t step = cur_step(f);  // read here: nothing waits on it at the kernel's start
       f->ticket = 0;
       f->send_cnt = 0;
       f->priv_target[step & 1] += f->priv_step;
@@ -1630,10 +1654,9 @@ k_comb_recv(txb_moe_shape s, txb_moe_bufs b, const uint8_t* __restrict__ out, in
             const float* __restrict__ w, int64_t n, void* dst, int out_bf16, uint64_t timeout_ns) {
   __shared__ Shared sh;
   Flags* f = flags_of(b.region, s);
-  const uint64_t step = cur_step(f);
   combine_reduce<ELEM>(s, f, comb_of(b.region, s), out, ld, b.pos, b.gidx, w, n, dst, out_bf16, timeout_ns,
                        blockIdx.x, gridDim.x, sh);
-  end_of_step(f, step, gridDim.x);
+  end_of_step(f, gridDim.x);
 }
 
 // ------------------------------------------------------------ fused kernels
@@ -1830,8 +1853,8 @@ __device__ __forceinline__ void dispatch_roles_solo(const txb_moe_shape& s, cons
     if (b.prof && tg.tid == 0) b.prof[blockIdx.x * 32 + 20] = globaltimer();
   } else {
     const Grp rg{(int)threadIdx.x, kRouteRole, 1};
-    const uint32_t pd = prefetch_dirty(s, b.dirty, cta, ncta, rg);
     const uint32_t bad = route_counts_direct(s, routes, n, hist, rv, b.rank_scratch, cta, ncta, sh, b, rg, false);
+    const PreDirty pd = prefetch_dirty(s, b.dirty, cta, ncta, rg);  // after the route loads
     if (rg.tid == 0) bad_s = bad;
     named_sync(3, kThreads);
     stamp(b, 14);
@@ -1890,10 +1913,10 @@ k_dispatch_roles(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
     if (b.prof && tg.tid == 0) b.prof[blockIdx.x * 32 + 20] = globaltimer();
   } else {
     const Grp rg{(int)threadIdx.x, kRouteRole, 1};
-    const uint32_t pd = prefetch_dirty(s, b.dirty, cta, ncta, rg);
     for (int q = rg.tid; q < s.ranks; q += rg.nt) sh.cnt[q] = sh.pcnt[q] = 0;
     const uint32_t bad = route_counts_direct(s, routes, n, hist, reinterpret_cast<int32_t*>(hist + s.experts),
                                              b.rank_scratch, cta, ncta, sh, b, rg);
+    const PreDirty pd = prefetch_dirty(s, b.dirty, cta, ncta, rg);  // after the route loads
     stamp(b, 14);
     route_publish(s, b.peers, f, hist, step, n, bad, cta, ncta, rg);
     own_positions(s, hist, b.pos, bad, sh, rg, b.peers, step);
@@ -1952,9 +1975,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 k_combine_fused(txb_moe_shape s, txb_moe_bufs b, const uint8_t* __restrict__ out, int64_t ld,
                 const float* __restrict__ w, int64_t n, void* dst, int out_bf16, uint64_t timeout_ns) {
   __shared__ Shared sh;
+  // decode (one token per CTA): the step's weights are an input, readable
+  // before the producing kernel has finished
+  const bool ws_ready = n <= (int64_t)gridDim.x && blockIdx.x < n;
+  if (ws_ready && threadIdx.x < s.topk) s_comb_ct.ws[threadIdx.x] = w[blockIdx.x * s.topk + threadIdx.x];
   grid_dep_wait();  // the producing dispatch (or expert) kernel has completed
   Flags* f = flags_of(b.region, s);
-  const uint64_t step = cur_step(f);
   stamp(b, 9);
   // Large batches with per-token completion (two half-size CTAs per SM):
   // even CTAs return rows, odd CTAs reduce tokens as their rows land, so
@@ -1971,14 +1997,14 @@ k_combine_fused(txb_moe_shape s, txb_moe_bufs b, const uint8_t* __restrict__ out
     __syncthreads();
   }
   stamp(b, 10);
-  signal_counts(s, b.peers, 1, step, sh);
+  signal_counts(s, b.peers, 1, 0, sh);
   __syncthreads();
   stamp(b, 11);
   if (!roles || !sender)
     combine_reduce<ELEM>(s, f, comb_of(b.region, s), out, ld, b.pos, b.gidx, w, n, dst, out_bf16, timeout_ns,
-                         ridx, nred, sh, b.prof, b.region);
+                         ridx, nred, sh, b.prof, b.region, ws_ready && !roles);
   stamp(b, 12);
-  end_of_step(f, step, ncta);
+  end_of_step(f, ncta);
   stamp(b, 13);
 }
 

@@ -507,7 +507,7 @@ __device__ bool combine_token_split(CombTok& ct, int H, int R, int64_t t, const 
     for (int u = 0; u < kCombBatch; ++u)
       if (u < R && ct.local[u] && c0 + p * nt < H / 8)
         raw[p][u] = load_chunk8<ELEM>(ct.rowp[u], (int64_t)(c0 + p * nt) * 8);
-  if (tid >= nt - 32 && tid - (nt - 32) < R) ct.ws[tid - (nt - 32)] = w[t * R + tid - (nt - 32)];
+  if (w && tid >= nt - 32 && tid - (nt - 32) < R) ct.ws[tid - (nt - 32)] = w[t * R + tid - (nt - 32)];
   if (!wait_fn()) return false;
 #pragma unroll
   for (int p = 0; p < CPT; ++p)
