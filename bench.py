@@ -60,8 +60,9 @@ def _args():
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--flush", default="write+read", choices=["write+read", "write"])
-    ap.add_argument("--private", type=int, default=None,
-                    help="PrivateBufferConfig.tokens (default: build_mesh's min(32, tokens))")
+    ap.add_argument("--private", type=int, default=0,
+                    help="PrivateBufferConfig.tokens (0: no speculative private round, the tuned "
+                         "choice on NVLink, DESIGN.md §10; the API default is min(32, tokens))")
     return ap.parse_args()
 
 
@@ -498,13 +499,13 @@ def run_b200(a) -> None:
     # DRAM bytes per launch of that kernel from the committed ncu capture
     # (EP=1 decode only; profiles/r01_ncu_traffic.json)
     traffic = None
-    tf = ROOT / "profiles" / "r01_ncu_traffic.json"
+    tf = ROOT / "profiles" / "r02" / "ncu_traffic.json"
     if n_gpu == 1 and a.config in ("decode", "prefill") and tf.exists():
         tj = json.loads(tf.read_text())
         t = (tj if a.config == "decode" else tj.get(a.config, {})).get(kname[dom])
         if t:
             traffic = int(t["dram_read"] + t["dram_write"])
-    traffic_src = "ncu dram__bytes_read.sum + dram__bytes_write.sum (profiles/r01_ncu_traffic.json)"
+    traffic_src = "ncu dram__bytes_read.sum + dram__bytes_write.sum (profiles/r02/ncu_traffic.json)"
     nf = ROOT / "profiles" / "r01_nvlink" / "summary.json"
     if n_gpu == 2 and nf.exists():
         # NVLink bytes on the wire per launch at EP=2, from the ncu capture of
@@ -640,7 +641,7 @@ def e2e_times(rk, x, routes, w, stream, flush, dev, K: int, world: int) -> dict:
 # ------------------------------------------------------------ reference arm
 
 
-def reference_live(wl: dict, tokens: int, steps: int = 3, ranks: int = 1) -> dict:
+def reference_live(wl: dict, tokens: int, steps: int = 3, ranks: int = 1, private: int | None = None) -> dict:
     """The unmodified reference (railtx, installed into baseline/_ref with
     pip --no-deps; pure Python + numpy + numba) run through its own public
     API on the host: per rank encode_tokens -> MoeRank.dispatch_send ->
@@ -667,7 +668,8 @@ def reference_live(wl: dict, tokens: int, steps: int = 3, ranks: int = 1) -> dic
                             hidden=wl["hidden"], elem_size=elem, scales=scales)
     fab = SimFabric(FaultConfig(mtu=1 << 20))
     engs = [TransferEngine(fab, rails=1, name=f"ref{r}") for r in range(N)]
-    mesh = rmoe.build_mesh(engs, spec, ranks_per_node=N)
+    pv = None if private is None else rmoe.PrivateBufferConfig(min(private, sample))
+    mesh = rmoe.build_mesh(engs, spec, private=pv, ranks_per_node=N)
     ins = [_inputs(wl, r, sample) for r in range(N)]
     errs: list = []
 
@@ -729,7 +731,7 @@ def run_reference(a) -> None:
            "config": workload_config(wl, tokens, N, a.private),
            "cpu_baseline": cb,
            "e2e": {"value": cb["value"], "unit": "us", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-           "reference_live": reference_live(wl, tokens, ranks=N),
+           "reference_live": reference_live(wl, tokens, ranks=N, private=a.private),
            "note": "value: the threaded oracle port of railtx's algorithm (oracle/moe_oracle.py) on the host "
                    "cores; reference_live: the unmodified railtx API from baseline/_ref, one thread per rank"}
     print(json.dumps(res), flush=True)

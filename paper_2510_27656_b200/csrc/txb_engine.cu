@@ -185,6 +185,28 @@ __global__ void __launch_bounds__(kCopyThreads, 1) k_copy_jobs(const __grid_cons
   }
 }
 
+// Clock writes are GPU-scope releases: the readers are kernels of the same
+// GPU, and a system-scope release (like the system fence that precedes a
+// default cuStreamWriteValue64) was measured never to complete while a
+// persistent kernel polled the word (tools/debug/clock_probe.py).
+__global__ void k_write_value(uint64_t* p, uint64_t v) {
+  if (threadIdx.x == 0) asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ uint64_t ld_acquire_gpu(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ bool spin_ge_gpu(const uint64_t* p, uint64_t target, uint64_t deadline) {
+  uint32_t it = 0;
+  while (ld_acquire_gpu(p) < target) {
+    if (((++it) & 255u) == 0 && globaltimer() > deadline) return ld_acquire_gpu(p) >= target;
+  }
+  return true;
+}
+
 // Persistent paged stream (the KV-cache layer-by-layer transfer,
 // kvcache.py:477-507, with the LayerClock of kvcache.py:317-334 on the
 // device): step k (0-based) of the request moves pages_per_step pages
@@ -241,16 +263,16 @@ __global__ void __launch_bounds__(kCopyThreads, 1) k_kv_stream(const __grid_cons
     if (seen < want) {  // the clock is read only when the cached value runs out
       uint32_t ok = 1;
       if (lane == 0) {
-        seen = ld_acquire_sys(ks.clock);
+        seen = ld_acquire_gpu(ks.clock);
         if (seen < want) ok = 2;  // not released yet: book the finished steps before waiting
       }
       ok = __shfl_sync(0xffffffffu, ok, 0);
       if (ok == 2) {
         book();
         if (lane == 0) {
-          ok = spin_ge(ks.clock, want, dl) ? 1u : 0u;
+          ok = spin_ge_gpu(ks.clock, want, dl) ? 1u : 0u;
           if (!ok && ks.err) atomicOr(ks.err, TXB_EV_WAIT_IMM);
-          seen = ld_acquire_sys(ks.clock);
+          seen = ld_acquire_gpu(ks.clock);
         }
         ok = __shfl_sync(0xffffffffu, ok, 0);
         if (!ok) return;
@@ -309,10 +331,6 @@ __global__ void k_imm_probe(uint64_t* keys, uint32_t imm, int insert, int64_t* o
     if (cur == 0) break;  // lookup: an empty slot ends the probe sequence
   }
   *out = -1;
-}
-
-__global__ void k_write_value(uint64_t* p, uint64_t v) {
-  if (threadIdx.x == 0) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 // Zero-length write carrying an immediate (barrier leg, engine.py:599-619).
@@ -585,7 +603,7 @@ int txb_stream_write_value64(uint64_t* addr, uint64_t value, void* stream) {
   PFN_wait64 w;
   PFN_write64 wr;
   if (stream_memops(&w, &wr)) {
-    const int rc = wr(stream, (uint64_t)(uintptr_t)addr, value, 0 /* CU_STREAM_WRITE_VALUE_DEFAULT */);
+    const int rc = wr(stream, (uint64_t)(uintptr_t)addr, value, 1 /* CU_STREAM_WRITE_VALUE_NO_MEMORY_BARRIER */);
     if (rc == 0) return TXB_OK;
   }
   k_write_value<<<1, 32, 0, (cudaStream_t)stream>>>(addr, value);
