@@ -185,12 +185,15 @@ __global__ void __launch_bounds__(kCopyThreads, 1) k_copy_jobs(const __grid_cons
   }
 }
 
-// Clock writes are GPU-scope releases: the readers are kernels of the same
-// GPU, and a system-scope release (like the system fence that precedes a
-// default cuStreamWriteValue64) was measured never to complete while a
-// persistent kernel polled the word (tools/debug/clock_probe.py).
+// Clock writes are plain (relaxed, GPU-scope) stores: the kernel boundary
+// orders the compute before them, and the reader acquires.  Measured
+// (tools/debug/clock_probe.py, profiles/r02/README.md): while the persistent
+// stream kernel polled the word, a writer that fenced first -- st.release
+// at .gpu or .sys scope, or the memory barrier that precedes a default
+// cuStreamWriteValue64 -- stalled its stream (only the first write of a
+// run landed); plain stores, like a torch fill kernel, went through.
 __global__ void k_write_value(uint64_t* p, uint64_t v) {
-  if (threadIdx.x == 0) asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+  if (threadIdx.x == 0) asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 __device__ __forceinline__ uint64_t ld_acquire_gpu(const uint64_t* p) {

@@ -193,7 +193,6 @@ __device__ uint32_t route_counts_direct(const txb_moe_shape& s, const int64_t* r
   // lanes of this thread's token within its warp (R | 32 and R | nt: a
   // token's copies sit in consecutive lanes of one warp in every pass)
   const bool tok_lanes = lanes && (nt % R) == 0;
-  const unsigned tokmask = tok_lanes ? (R == 32 ? 0xffffffffu : ((1u << R) - 1u) << (lane - lane % R)) : 0u;
   // one entry: stage its id, count it, flag range / duplicate errors
   auto entry = [&](int i, int64_t v) {
     const bool valid = i < m;
@@ -202,7 +201,14 @@ __device__ uint32_t route_counts_direct(const txb_moe_shape& s, const int64_t* r
     const int v32 = in_range ? (int)v : -1 - lane;
     bool dup = false;
     if (tok_lanes) {
-      dup = __popc(__match_any_sync(0xffffffffu, v32) & tokmask) > 1;
+      // the token's R ids sit in consecutive lanes: R shuffles compare
+      // each id with its token's others (cheaper than a warp-wide
+      // match.any, which the ncu source page showed dominating this loop)
+      const int tbase = lane - lane % R;
+      int same = 0;
+#pragma unroll 8
+      for (int jj = 0; jj < R; ++jj) same += __shfl_sync(0xffffffffu, v32, tbase + jj) == v32;
+      dup = same > 1;
     } else if (valid) {
       const int j = i % R;
       #pragma unroll 1
@@ -1817,6 +1823,14 @@ __device__ __forceinline__ void named_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
+// Producer side of a hand-off: the routing role marks its arrival and runs
+// on; the token role's bar.sync on the same barrier completes once both
+// roles are in, and sees the routing role's shared-memory writes (arrive
+// synchronizes with the completing sync in the PTX memory model).
+__device__ __forceinline__ void named_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
 //
 // SOLO (one rank): the route matrix is this CTA's histogram, so the roles
 // split differently right after it: the token role ranks its copies and
@@ -1856,7 +1870,7 @@ __device__ __forceinline__ void dispatch_roles_solo(const txb_moe_shape& s, cons
     const uint32_t bad = route_counts_direct(s, routes, n, hist, rv, b.rank_scratch, cta, ncta, sh, b, rg, false);
     const PreDirty pd = prefetch_dirty(s, b.dirty, cta, ncta, rg);  // after the route loads
     if (rg.tid == 0) bad_s = bad;
-    named_sync(3, kThreads);
+    named_arrive(3, kThreads);
     stamp(b, 14);
     route_publish(s, b.peers, f, hist, step, n, bad, cta, ncta, rg);
     recv_tables_body<true>(s, hist, rt, b.info, cta, sh, b, rg);
@@ -1921,7 +1935,7 @@ k_dispatch_roles(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
     route_publish(s, b.peers, f, hist, step, n, bad, cta, ncta, rg);
     own_positions(s, hist, b.pos, bad, sh, rg, b.peers, step);
     rg.sync();
-    named_sync(4, kThreads);
+    named_arrive(4, kThreads);
     stamp(b, 2);
     const uint32_t* Cm = hist;
     bool ok = true;
@@ -1937,7 +1951,7 @@ k_dispatch_roles(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
       skip = (!ok || bad) ? 1u : 0u;
       fail = ok ? 0u : 1u;
     }
-    named_sync(3, kThreads);
+    named_arrive(3, kThreads);
     stamp(b, 15);
     if (ok) {
       recv_tables_body<true>(s, Cm, rt, b.info, cta, sh, b, rg);
