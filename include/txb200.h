@@ -108,6 +108,11 @@ int txb_enable_peer(int device, int peer_device);
  * kernel waiting on a device clock must not sit in front of the compute
  * that advances it). */
 int txb_stream_create(int device, void** out_stream);
+/* Load every kernel of the library on `device` now (cudaFuncGetAttributes)
+ * instead of at its first launch: under lazy module loading a first launch
+ * did not complete while a persistent kernel was polling on the device.
+ * Idempotent; TransferEngine calls it when it binds a device. */
+int txb_preload(int device);
 int txb_stream_destroy(int device, void* stream);
 /* Device address of page-locked host memory (cudaHostAlloc / pinned torch
  * tensors).  The kernels read inputs from and write results to such host

@@ -83,6 +83,18 @@ static int grid_for(int64_t work, int per_block) {
   return (int)g;
 }
 
+cudaError_t preload_codec() {
+  cudaError_t e = cudaSuccess;
+  for (cudaError_t r : {touch(k_encode_rows<TXB_SRC_F32, 1>), touch(k_encode_rows<TXB_SRC_F32, 2>),
+                        touch(k_encode_rows<TXB_SRC_F32, 4>), touch(k_encode_rows<TXB_SRC_BF16, 1>),
+                        touch(k_encode_rows<TXB_SRC_BF16, 2>), touch(k_encode_rows<TXB_SRC_BF16, 4>),
+                        touch(k_decode_rows<1>), touch(k_decode_rows<2>), touch(k_decode_rows<4>),
+                        touch(k_pack_rows), touch(k_weighted_combine), touch(k_fp8_encode), touch(k_fp8_decode),
+                        touch(k_bf16_encode)})
+    if (r != cudaSuccess) e = r;
+  return e;
+}
+
 }  // namespace txb
 
 using namespace txb;

@@ -82,6 +82,21 @@ struct OnDevice {
   ::txb::OnDevice _on_dev(dev);                                 \
   if (_on_dev.err != cudaSuccess) return ::txb::cuda_fail(_on_dev.err, "cudaSetDevice")
 
+// Loading every kernel up front (txb_preload).  Under CUDA's lazy module
+// loading (the default since 12.2) the first launch of a kernel loads it,
+// and that load did not complete while a persistent kernel of this library
+// was polling a word on the device (tools/debug/clock_probe.py): the first
+// clock write of a KV stream never landed.  cudaFuncGetAttributes loads the
+// function without launching it.
+template <typename K>
+inline cudaError_t touch(K kernel) {
+  cudaFuncAttributes a;
+  return cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(kernel));
+}
+cudaError_t preload_engine();
+cudaError_t preload_moe();
+cudaError_t preload_codec();
+
 // ------------------------------------------------------------ PTX wrappers
 
 __device__ __forceinline__ uint64_t globaltimer() {

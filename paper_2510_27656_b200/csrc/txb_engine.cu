@@ -185,15 +185,10 @@ __global__ void __launch_bounds__(kCopyThreads, 1) k_copy_jobs(const __grid_cons
   }
 }
 
-// Clock writes are plain (relaxed, GPU-scope) stores: the kernel boundary
-// orders the compute before them, and the reader acquires.  Measured
-// (tools/debug/clock_probe.py, profiles/r02/README.md): while the persistent
-// stream kernel polled the word, a writer that fenced first -- st.release
-// at .gpu or .sys scope, or the memory barrier that precedes a default
-// cuStreamWriteValue64 -- stalled its stream (only the first write of a
-// run landed); plain stores, like a torch fill kernel, went through.
+// Fallback clock write (GPU-scope release; the readers are kernels of the
+// same GPU and acquire).
 __global__ void k_write_value(uint64_t* p, uint64_t v) {
-  if (threadIdx.x == 0) asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+  if (threadIdx.x == 0) asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 __device__ __forceinline__ uint64_t ld_acquire_gpu(const uint64_t* p) {
@@ -435,6 +430,15 @@ static int sms(int) {
   return cache[dev];
 }
 
+cudaError_t preload_engine() {
+  cudaError_t e = cudaSuccess;
+  for (cudaError_t r : {touch(k_copy_jobs), touch(k_write_value), touch(k_kv_stream), touch(k_imm_probe),
+                        touch(k_imm_add), touch(k_imm_wait), touch(k_globaltimer), touch(k_amax_bf16),
+                        touch(k_quant_bf16_fp8)})
+    if (r != cudaSuccess) e = r;
+  return e;
+}
+
 }  // namespace txb
 
 using namespace txb;
@@ -590,11 +594,7 @@ static bool stream_memops(PFN_wait64* w, PFN_write64* wr) {
       fw = reinterpret_cast<PFN_wait64>(a);
       fwr = reinterpret_cast<PFN_write64>(b);
     }
-    // measured (tools/debug/clock_probe.py, profiles/r02/README.md): a
-    // stream write queued behind a kernel on its stream is not performed
-    // while another stream's persistent kernel polls the word, so the
-    // writes default to a one-thread kernel; TXB_STREAM_MEMOPS=1 opts in
-    if (!getenv("TXB_STREAM_MEMOPS")) state = 0;
+    if (getenv("TXB_NO_STREAM_MEMOPS")) state = 0;
   }
   *w = fw;
   *wr = fwr;
@@ -606,7 +606,7 @@ int txb_stream_write_value64(uint64_t* addr, uint64_t value, void* stream) {
   PFN_wait64 w;
   PFN_write64 wr;
   if (stream_memops(&w, &wr)) {
-    const int rc = wr(stream, (uint64_t)(uintptr_t)addr, value, 1 /* CU_STREAM_WRITE_VALUE_NO_MEMORY_BARRIER */);
+    const int rc = wr(stream, (uint64_t)(uintptr_t)addr, value, 0 /* CU_STREAM_WRITE_VALUE_DEFAULT: fenced */);
     if (rc == 0) return TXB_OK;
   }
   k_write_value<<<1, 32, 0, (cudaStream_t)stream>>>(addr, value);

@@ -1928,11 +1928,20 @@ k_dispatch_roles(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
   } else {
     const Grp rg{(int)threadIdx.x, kRouteRole, 1};
     for (int q = rg.tid; q < s.ranks; q += rg.nt) sh.cnt[q] = sh.pcnt[q] = 0;
-    const uint32_t bad = route_counts_direct(s, routes, n, hist, reinterpret_cast<int32_t*>(hist + s.experts),
-                                             b.rank_scratch, cta, ncta, sh, b, rg);
+    // the count row is published as soon as the histogram is complete; the
+    // stable ranks of the CTA's copies are counted while it travels.  The
+    // staged ids `rv` overlap the receive tables `rt` (written after
+    // hand-off 3), so only this role reads them, and only before then.
+    int32_t* rv = reinterpret_cast<int32_t*>(hist + s.experts);
+    const uint32_t bad = route_counts_direct(s, routes, n, hist, rv, b.rank_scratch, cta, ncta, sh, b, rg, false);
     const PreDirty pd = prefetch_dirty(s, b.dirty, cta, ncta, rg);  // after the route loads
-    stamp(b, 14);
     route_publish(s, b.peers, f, hist, step, n, bad, cta, ncta, rg);
+    stamp(b, 14);
+    if (!bad) {
+      const int nw = (n > cta ? (int)((n - cta + ncta - 1) / ncta) : 0) * s.topk;
+      own_ranks(rv, b.rank_scratch, nw, sh, rg);
+      rg.sync();
+    }
     own_positions(s, hist, b.pos, bad, sh, rg, b.peers, step);
     rg.sync();
     named_arrive(4, kThreads);
@@ -2153,6 +2162,28 @@ static int coop_grid(K kernel, int dev, size_t smem, int want, int block = kThre
   const int cap = (per_sm > 0 ? per_sm : 1) * sm_count(dev);
   if (want > cap) want = cap;
   return want < 1 ? 1 : want;
+}
+
+template <int SRC, int ELEM>
+static cudaError_t preload_src_elem() {
+  cudaError_t e = cudaSuccess;
+  for (cudaError_t r : {touch(k_dispatch_roles<SRC, ELEM, true>), touch(k_dispatch_roles<SRC, ELEM, false>),
+                        touch(k_dispatch_fused<SRC, ELEM, true>), touch(k_dispatch_fused<SRC, ELEM, false>),
+                        touch(k_dispatch<SRC, ELEM>)})
+    if (r != cudaSuccess) e = r;
+  return e;
+}
+
+cudaError_t preload_moe() {
+  cudaError_t e = cudaSuccess;
+  for (cudaError_t r : {preload_src_elem<TXB_SRC_ROWS, 1>(), preload_src_elem<TXB_SRC_F32, 1>(),
+                        preload_src_elem<TXB_SRC_F32, 2>(), preload_src_elem<TXB_SRC_F32, 4>(),
+                        preload_src_elem<TXB_SRC_BF16, 1>(), preload_src_elem<TXB_SRC_BF16, 2>(),
+                        preload_src_elem<TXB_SRC_BF16, 4>(), touch(k_combine_fused<1>), touch(k_combine_fused<2>),
+                        touch(k_combine_fused<4>), touch(k_comb_recv<1>), touch(k_comb_recv<2>), touch(k_comb_recv<4>),
+                        touch(k_route), touch(k_recv), touch(k_comb_send), touch(k_barrier)})
+    if (r != cudaSuccess) e = r;
+  return e;
 }
 
 }  // namespace txb

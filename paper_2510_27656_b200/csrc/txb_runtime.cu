@@ -109,6 +109,17 @@ int txb_enable_peer(int device, int peer_device) {
   return TXB_OK;
 }
 
+int txb_preload(int device) {
+  TXB_ON_DEVICE(device);
+  static bool done[64] = {false};
+  if (device >= 0 && device < 64 && done[device]) return TXB_OK;
+  TXB_CUDA(preload_engine());
+  TXB_CUDA(preload_moe());
+  TXB_CUDA(preload_codec());
+  if (device >= 0 && device < 64) done[device] = true;
+  return TXB_OK;
+}
+
 int txb_stream_create(int device, void** out_stream) {
   if (!out_stream) {
     set_error("txb_stream_create: null out pointer");

@@ -475,6 +475,9 @@ class TransferEngine:
         self.timing: list | None = None
         self.trace = TraceRecorder(self.name, enabled=trace)
         self._op_ids = itertools.count(1)
+        # every library kernel loaded now, not at its first launch (txb_preload)
+        if torch.cuda.is_available():
+            _lib.call("txb_preload", self.device)
 
     def main_address(self) -> NetAddr:
         import socket

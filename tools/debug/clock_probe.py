@@ -22,6 +22,11 @@ dec = kvcache.KvReceiver(b, layout, pool_slots=layout.slots, local_heads=2, ctx_
 kv = a.alloc_buffer(layout.region_bytes(2, layout.slots))
 send = kvcache.KvSender(a, kv, a.alloc_buffer(4096))
 comp = torch.cuda.Stream(0)
+if "--warm" in sys.argv:           # load torch's kernels before any stream kernel runs
+    with torch.cuda.stream(comp):
+        torch.cuda._sleep(10)
+    torch.zeros(1, device="cuda:0").fill_(1)
+    torch.cuda.synchronize()
 for variant in ["memop_only", "memop_sync", "sleep_memop", "sleep_memop_sync", "kernelwrite_sleep"]:
     t = dec.open_request(ctx_len=64)
     clock = a.device_clock(layout.steps)
