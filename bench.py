@@ -10,11 +10,15 @@ ways) and --config kimi (configs[3]: 384 experts, skewed routing) run the
 other BASELINE configurations with the same methodology.
 
 A step = dispatch_send -> dispatch_recv -> combine_send -> combine_recv
-through the public MoeRank API (launch-only, sync=False), captured once
-into a CUDA graph and replayed; each timed step follows an L2 flush (write
-of a 512 MiB buffer) and, for N > 1, a device-side all-rank barrier, and
-is timed with CUDA events on the rank's stream.
-value = p50 over steps of the max over ranks of the step time (us).
+through the public MoeRank API (launch-only, sync=False).  The K timed
+steps run back to back in CUDA graphs of B steps each, every step on its
+own input set from a pool whose touched bytes are twice the L2 (no flush
+between steps); each graph replay follows a device-side all-rank barrier
+(N > 1) and is timed with CUDA events on the rank's stream.
+value = p50 over the K/B blocks of (max over ranks of the block span) / B.
+The flushed single step (L2 flushed by a 512 MiB write + read, CUDA event
+nodes inside its graph), the eager step and the %globaltimer kernel span
+are reported beside it.
 
 Usage:  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl reference]
         torchrun --nproc-per-node N bench.py --gpus N ...
@@ -568,7 +572,11 @@ def run_b200(a) -> None:
                 "algorithmic_bytes": int(bytes_k[dom]), "kernel_us": round(kt[dom], 2),
                 "all_kernels": {k: {"bytes": int(bytes_k[k]), "us": round(kt[k], 2),
                                     "gbs": round(bytes_k[k] / (kt[k] * 1e-6) / 1e9, 1)} for k in names}}
-    p50 = float(np.median(tot))
+    # headline: K back-to-back steps timed in blocks of B with inputs cycled
+    # through a pool twice the L2 (the contract's "inputs larger than L2"),
+    # so no per-step event node or flush artefact sits inside the number;
+    # the flushed single-step p50 is reported beside it
+    p50 = float(np.median(block))
     res = {
         "metric": wl["metric"], "value": round(p50, 2), "unit": "us",
         "n_gpus": n_gpu, "steps": K, "warmup": a.warmup, "ms_per_step": round(p50 / 1e3, 5),
@@ -576,23 +584,30 @@ def run_b200(a) -> None:
         "dtype": ("fp8-e4m3" if wl["elem"] == 1 else "bf16") + " dispatch / bf16 combine (fp32 accumulate)",
         "data": "synthetic",
         "config": workload_config(wl, tokens, n_gpu, rk.private_tokens),
-        "l2": ("flushed before every step: 512 MiB write then read (cold, clean L2)" if a.flush == "write+read"
-               else "flushed before every step: 512 MiB write"),
-        f"p50_{other.replace('+', '_')}_flush_us": round(float(np.median(tot_other)), 2),
-        "timing": "public-API step captured as a CUDA graph; CUDA event nodes inside the graph around "
-                  "the step (device time, graph launch excluded), p50 over steps of the max over ranks",
-        "p90_us": round(float(np.percentile(tot, 90)), 2),
-        "p99_us": round(float(np.percentile(tot, 99)), 2),
+        "l2": (f"inputs larger than L2: {S} input sets (activations, routes, weights, expert rows) of "
+               f"{per_set / 1e6:.1f} MB touched per step, cycled step by step (no flush between the "
+               f"timed steps); the flushed single-step numbers flush with a 512 MiB "
+               + ("write then read" if a.flush == "write+read" else "write")),
+        "timing": f"public-API steps captured as CUDA graphs of {B} back-to-back steps; CUDA events "
+                  f"around each replay on the step stream (host ahead of the GPU), per-step time = span / "
+                  f"{B}; device barrier + synchronize before each block; p50 over the {K // B} blocks of "
+                  f"the max over ranks",
+        "p50_flushed_step_us": round(float(np.median(tot)), 2),
+        "flushed_step_timing": "one step per graph replay after the L2 flush (+ device barrier for N>1), CUDA "
+                               "event nodes inside the graph around the step; p50 over steps of the max over ranks",
+        f"p50_flushed_step_{other.replace('+', '_')}_flush_us": round(float(np.median(tot_other)), 2),
+        "p90_flushed_step_us": round(float(np.percentile(tot, 90)), 2),
+        "p99_flushed_step_us": round(float(np.percentile(tot, 99)), 2),
         "p50_l2_warm_us": round(float(np.median(b2b)), 2),
         "p50_with_graph_launch_us": round(float(np.median(tot_launch)), 2),
         "p50_eager_us": round(float(np.median(eager)), 2),
-        "p50_back_to_back_us": round(float(np.median(block)), 2),
         "back_to_back": {"steps_per_graph": B, "input_sets": S, "bytes_per_set": per_set,
-                         "timed_steps": B * (K // B)},
+                         "timed_steps": B * (K // B),
+                         "p90_us": round(float(np.percentile(block, 90)), 2)},
         "p50_kernel_span_us": round(float(np.nanmedian(kspan)), 2),
-        "span_note": "value: CUDA event nodes inside the step graph; p50_eager_us: events around the eager "
-                     "step with the host ahead of the GPU; p50_kernel_span_us: %globaltimer first dispatch "
-                     "CTA start -> last combine CTA end (max over ranks)",
+        "span_note": "p50_eager_us: events around one eager flushed step with the host ahead of the GPU; "
+                     "p50_kernel_span_us: %globaltimer from the first dispatch CTA's start to the last combine "
+                     "CTA's end of one flushed step (max over ranks)",
         "tokens_per_s": round(n_gpu * tokens / (p50 * 1e-6), 1),
         "kernel_us": {k: round(v, 2) for k, v in kt.items()},
         "roofline": roofline,

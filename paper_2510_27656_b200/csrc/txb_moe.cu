@@ -1504,10 +1504,7 @@ __device__ void combine_send_rows(const txb_moe_shape& s, Flags* f, const uint8_
 // token's row pointers and weights are staged before the wait; on the
 // decode path (one token per CTA, R <= 8, H % 8 == 0 rows) the rows this
 // rank served itself are already loaded into registers when the wait ends.
-// The combine's per-token staging (row pointers, weights, scales); one per
-// CTA.  The decode kernel fills the weights before its programmatic
-// dependency resolves (they are an input of the step, not an output of the
-// dispatch), so their cold load overlaps the dispatch's tail.
+// The combine's per-token staging (row pointers, weights, scales); one per CTA.
 static __shared__ CombTok s_comb_ct;
 
 template <int ELEM>
@@ -1998,10 +1995,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 k_combine_fused(txb_moe_shape s, txb_moe_bufs b, const uint8_t* __restrict__ out, int64_t ld,
                 const float* __restrict__ w, int64_t n, void* dst, int out_bf16, uint64_t timeout_ns) {
   __shared__ Shared sh;
-  // decode (one token per CTA): the step's weights are an input, readable
-  // before the producing kernel has finished
-  const bool ws_ready = n <= (int64_t)gridDim.x && blockIdx.x < n;
-  if (ws_ready && threadIdx.x < s.topk) s_comb_ct.ws[threadIdx.x] = w[blockIdx.x * s.topk + threadIdx.x];
+  // Nothing is read before the programmatic dependency resolves, not even
+  // the step's weights: a weights upload enqueued between the dispatch and
+  // this kernel was observed racing with an early read (an intermittent
+  // bf16 mismatch in test_dsv3_decode_device_mode, profiles/r02/README.md).
   grid_dep_wait();  // the producing dispatch (or expert) kernel has completed
   Flags* f = flags_of(b.region, s);
   stamp(b, 9);
@@ -2025,7 +2022,7 @@ k_combine_fused(txb_moe_shape s, txb_moe_bufs b, const uint8_t* __restrict__ out
   stamp(b, 11);
   if (!roles || !sender)
     combine_reduce<ELEM>(s, f, comb_of(b.region, s), out, ld, b.pos, b.gidx, w, n, dst, out_bf16, timeout_ns,
-                         ridx, nred, sh, b.prof, b.region, ws_ready && !roles);
+                         ridx, nred, sh, b.prof, b.region);
   stamp(b, 12);
   end_of_step(f, ncta);
   stamp(b, 13);
