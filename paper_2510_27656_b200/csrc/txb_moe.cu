@@ -512,10 +512,10 @@ __device__ void route_publish(const txb_moe_shape& s, void* const* peers, Flags*
         #pragma unroll 1
         for (int le = lane; le < L; le += 32) c += hist[d * L + le];
         for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-        if (lane == 0 && d != s.me) f->comb_src_t[d] += c;
+        if (lane == 0 && d != s.me) f->comb_src_t[d] += (uint64_t)c * comb_chunks(s);
       }
     if (lane == 0) {
-      f->comb_target += bad ? 0 : (uint64_t)(n * s.topk) - self;
+      f->comb_target += bad ? 0 : ((uint64_t)(n * s.topk) - self) * comb_chunks(s);
       if (bad) atomicOr(&f->err, bad);
     }
   }
@@ -1388,6 +1388,12 @@ __device__ void wait_tokens(Flags* f, int64_t* info, int L, uint64_t timeout_ns)
 // Rows are moved in 2 KiB chunks (kChunk; one warp, four 16-byte loads per
 // lane in flight before the four peer stores) so a step's return traffic
 // spreads over every warp of the grid instead of one warp per 14 KiB row.
+// The combine counter counts CHUNKS (comb_chunks(s) per row): a row's
+// chunks may be stored by two CTAs (each CTA takes a contiguous run of
+// chunks), and each CTA can only vouch for the chunks it stored itself --
+// counting the row once, at its first chunk, let an origin read a row whose
+// tail another CTA had not yet delivered (an intermittent combine mismatch
+// at EP=2, found in round 2).
 
 __device__ void combine_send_rows(const txb_moe_shape& s, Flags* f, const uint8_t* out, int64_t ld,
                                   void* const* peers, const int64_t* sources, const int32_t* ret,
@@ -1455,7 +1461,7 @@ __device__ void combine_send_rows(const txb_moe_shape& s, Flags* f, const uint8_
         pend_t = srct[g];
         pend_n = cpr;
       }
-      if (lane == 0) atomicAdd(&sh.cnt[q], 1u);
+      if (lane == 0) atomicAdd(&sh.cnt[q], (uint32_t)cpr);
       if (++npend == kBatch) flush();
     }
     flush();
@@ -1483,7 +1489,7 @@ __device__ void combine_send_rows(const txb_moe_shape& s, Flags* f, const uint8_
 #pragma unroll
       for (int u = 0; u < kChunk / 512; ++u)
         if (lane + 32 * u < n16) dst[lane + 32 * u] = v[u];
-      if (c == 0 && lane == 0) atomicAdd(&sh.cnt[q], 1u);
+      if (lane == 0) atomicAdd(&sh.cnt[q], 1u);  // every chunk: the counter counts chunks
     }
     return;
   }
@@ -1492,7 +1498,7 @@ __device__ void combine_send_rows(const txb_moe_shape& s, Flags* f, const uint8_
     const int g = send_list[r];
     const int q = (int)sources[g];
     copy_row(comb_of(peers[q], s) + (int64_t)ret[g] * Pc, out + (int64_t)g * ld, Pc, lane, 32);
-    if (lane == 0) atomicAdd(&sh.cnt[q], 1u);
+    if (lane == 0) atomicAdd(&sh.cnt[q], (uint32_t)comb_chunks(s));
   }
 }
 
