@@ -1017,6 +1017,86 @@ __device__ __forceinline__ RecvTables recv_carve(const txb_moe_shape& s, const i
   return t;
 }
 
+// One rank (EP=1): the receive tables of recv_tables_body collapse to two
+// prefixes of the histogram -- group starts (padded to 8) and receive-slot
+// bases (unpadded) -- computed in ONE two-array block scan (each thread a
+// contiguous run of local experts, warp shuffles, one pass over the warp
+// totals): two barriers instead of the six of the general tables.
+__device__ __forceinline__ void recv_tables_solo(const txb_moe_shape& s, const uint32_t* hist, int* sm, int64_t* info,
+                                                 int cta, Shared& sh, const Grp& g) {
+  const int L = s.local_experts, tid = g.tid, nt = g.nt;
+  RecvTables t = recv_carve(s, sm);
+  const int per = (L + nt - 1) / nt;
+  const int lo = min(L, tid * per), hi = min(L, lo + per);
+  int sp = 0, sr = 0;
+  #pragma unroll 1
+  for (int le = lo; le < hi; ++le) {
+    const int a = (int)hist[le];
+    sp += pad_up(a);
+    sr += a;
+  }
+  const int lane = tid & 31, warp = tid >> 5;
+  int xp = sp, xr = sr;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int yp = __shfl_up_sync(0xffffffffu, xp, o), yr = __shfl_up_sync(0xffffffffu, xr, o);
+    if (lane >= o) {
+      xp += yp;
+      xr += yr;
+    }
+  }
+  // warp totals in sh.tmp (this role's scratch; sh.red belongs to the
+  // token role's amax reduce, which may still be running)
+  int* wp = sh.tmp;         // [16] padded
+  int* wr = sh.tmp + 16;    // [16] unpadded
+  if (lane == 31) {
+    wp[warp] = xp;
+    wr[warp] = xr;
+  }
+  g.sync();
+  int bp = 0, br = 0, tp = 0, tr = 0;
+  const int nw = nt >> 5;
+  #pragma unroll 1
+  for (int w = 0; w < nw; ++w) {
+    if (w < warp) {
+      bp += wp[w];
+      br += wr[w];
+    }
+    tp += wp[w];
+    tr += wr[w];
+  }
+  int rp = bp + xp - sp, rr = br + xr - sr;  // exclusive prefixes at lo
+  #pragma unroll 1
+  for (int le = lo; le < hi; ++le) {
+    const int a = (int)hist[le];
+    t.a[le] = a;
+    t.gstart[le] = rp;
+    t.rowbase[le] = rr;
+    t.retbase[le] = rr;
+    t.gsize[le] = a;
+    t.srcpre[2 * le] = 0;
+    t.srcpre[2 * le + 1] = a;
+    if (cta == 0) {
+      info[le] = a;
+      info[L + le] = rp;
+    }
+    rp += pad_up(a);
+    rr += a;
+  }
+  if (tid == 0) {
+    t.tot[0] = tp;
+    t.tot[1] = tr;
+    t.pre_all[0] = 0;
+    t.asg[0] = tr;
+    t.take[0] = 0;
+    t.take[1] = 0;
+    if (cta == 0) {
+      info[2 * L] = tp;
+      info[2 * L + 1] = tr;
+    }
+  }
+  g.sync();
+}
+
 template <bool INL>
 __device__ __forceinline__ void recv_tables_body(const txb_moe_shape& s, const uint32_t* C, int* sm, int64_t* info,
                                                  int cta, Shared& sh, const txb_moe_bufs& b,
@@ -1876,7 +1956,7 @@ __device__ __forceinline__ void dispatch_roles_solo(const txb_moe_shape& s, cons
     named_arrive(3, kThreads);
     stamp(b, 14);
     route_publish(s, b.peers, f, hist, step, n, bad, cta, ncta, rg);
-    recv_tables_body<true>(s, hist, rt, b.info, cta, sh, b, rg);
+    recv_tables_solo(s, hist, rt, b.info, cta, sh, rg);
     stamp(b, 4);
     recv_rows_body(s, rt, b.rows, b.sources, b.ret_slot, grouped_of(b.region, s), b.dirty, b.send_list,
                    &f->send_cnt, cta, ncta, rg, pd);
