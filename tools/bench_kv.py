@@ -5,9 +5,10 @@ Llama-3-70B shape, 80 layers x 8 KV heads, 16-token pages of 128 dims x
 Prefiller on cuda:0, decoder on cuda:1 when present (NVLink), else both on
 cuda:0 (HBM loopback).  One step = one (chunk, layer) paged write of
 heads x pages_per_chunk pages (kvcache.py:477-500), TMA bulk copies into a
-randomly permuted slot list of the decoder pool.  Prints one JSON line.
+randomly permuted slot list of the decoder pool (TMA by default here; the
+engine's own default is vector copies).  Prints one JSON line.
 
-python tools/bench_kv.py [--layers 80] [--chunks 16] [--steps 50]
+python tools/bench_kv.py [--layers 80] [--chunks 16] [--steps 50] [--no-tma]
 """
 import argparse
 import json
@@ -81,8 +82,9 @@ res = {"metric": "paged KV layer transfer GB/s (Llama-3-70B shape)", "value": ro
        "peak": 770.0 if d1 else 6555.2,
        "frac": round(step_bytes / (med * 1e-6) / 1e9 / (770.0 if d1 else 6555.2), 3),
        "pages_per_step": a.heads * ppc, "page_bytes": a.page, "layers": a.layers, "chunks": a.chunks,
-       "copy": ("TMA bulk (cp.async.bulk) pieces <= 32 KiB, 4 stages per CTA" if not a.no_tma else
-                "16-byte vector copies, one warp per page piece") + ", one ImmCounter receipt per step"}
+       "copy": ("k_copy_jobs: TMA bulk copies (cp.async.bulk) of 8-KiB pieces issued by lane 0 of every warp, "
+                "2 stages each" if not a.no_tma else
+                "k_copy_jobs: 16-byte vector copies, one warp per 8-KiB piece") + ", one ImmCounter receipt per step"}
 assert t.wait(60.0), "KV request did not complete"
 res["request_completed"] = True
 print(json.dumps(res))
