@@ -221,7 +221,7 @@ __device__ __forceinline__ bool spin_ge_gpu(const uint64_t* p, uint64_t target, 
 // warp that reaches a step the clock has not released yet books what it
 // has first, so receipts never wait on a future layer.  The fence is the
 // only drain, and no other warp waits for it.
-constexpr int kStreamBatch = 8;
+constexpr int kStreamBatch = 32;
 
 __global__ void __launch_bounds__(kCopyThreads, 1) k_kv_stream(const __grid_constant__ txb_stream_job ks) {
   extern __shared__ __align__(128) uint8_t stage[];
