@@ -490,7 +490,7 @@ def run_b200(a) -> None:
     with torch.cuda.graph(graph_p, stream=stream):
         step()
     rk._bufs.prof = 0
-    spans = []
+    spans, kd_span, kc_span = [], [], []
     for k in range(max(20, K // 2) + 3):
         flush.fill_(k & 0xFF)
         if world > 1:
@@ -503,7 +503,12 @@ def run_b200(a) -> None:
             st0 = pv[:, 0][pv[:, 0] > 0]
             en = pv[:, 13][pv[:, 13] > 0]
             spans.append((en.max() - st0.min()) / 1e3 if st0.size and en.size else float("nan"))
+            d_end, c0 = pv[:, 8][pv[:, 8] > 0], pv[:, 9][pv[:, 9] > 0]
+            kd_span.append((d_end.max() - st0.min()) / 1e3 if st0.size and d_end.size else float("nan"))
+            kc_span.append((en.max() - c0.min()) / 1e3 if c0.size and en.size else float("nan"))
     kspan = _max_over_ranks(spans, world)
+    kd_span = _max_over_ranks(kd_span, world)
+    kc_span = _max_over_ranks(kc_span, world)
     # L2-warm steps (no flush between; SURVEY.md §8d asks for both numbers)
     b2b = run(max(20, K // 2), False, graph)[0]
     kdisp = run(max(20, K // 2), True, graph_k)[2]
@@ -563,6 +568,7 @@ def run_b200(a) -> None:
                            f"user data {t['nvltx_user']} B")
     peak = hbm_peak if bound == "hbm" else nvl_peak
     achieved = bytes_k[dom] / (kt[dom] * 1e-6) / 1e9
+    span_k = {"dispatch": float(np.nanmedian(kd_span)), "combine": float(np.nanmedian(kc_span))}
     roofline = {"bound": bound, "kernel": kname[dom],
                 "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
@@ -570,6 +576,10 @@ def run_b200(a) -> None:
                 "peak_source": ("MEASURED_PEAKS.json hbm_gbs (burst copy)" if bound == "hbm"
                                 else "B200_PROFILING.md measured peer copy 770 GB/s (fallback)"),
                 "algorithmic_bytes": int(bytes_k[dom]), "kernel_us": round(kt[dom], 2),
+                # the same kernel's duration on the device clock (first CTA start -> last CTA end,
+                # %globaltimer phase stamps), free of the event node between the two kernels
+                "kernel_span_us": round(span_k[dom], 2),
+                "frac_on_span": round(bytes_k[dom] / (span_k[dom] * 1e-6) / 1e9 / peak, 4),
                 "all_kernels": {k: {"bytes": int(bytes_k[k]), "us": round(kt[k], 2),
                                     "gbs": round(bytes_k[k] / (kt[k] * 1e-6) / 1e9, 1)} for k in names}}
     # headline: K back-to-back steps timed in blocks of B with inputs cycled

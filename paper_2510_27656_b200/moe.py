@@ -746,7 +746,13 @@ class MoeRank:
     # ------------------------------------------------------------- combine
 
     def combine_send(self, outputs) -> None:
-        """Return expert outputs to their source ranks (moe.py:739-796)."""
+        """Return expert outputs to their source ranks (moe.py:739-796).
+
+        Host mode (numpy) snapshots `outputs` here, as the reference does.
+        Device mode is stream-ordered instead: on the fused path the combine
+        kernel, launched by combine_recv, reads the CUDA tensor `outputs` when
+        it runs -- a caller that rewrites the tensor in between must order
+        that write after combine_recv."""
         st = self._cur
         self._raise_if_failed()
         if st is None or st.grouped is None:
@@ -873,7 +879,9 @@ class MoeRank:
         with self._lock:
             self._cur = None
         if st.host:
-            return out.float().cpu().numpy() if out_dtype == torch.float32 else out.cpu()
+            # host mode returns numpy f32 like the reference (moe.py:821-833); a
+            # bf16 result is widened exactly (every bf16 value is an f32 value)
+            return out.float().cpu().numpy()
         return out
 
     def barrier(self, timeout: float | None = None) -> None:

@@ -20,7 +20,7 @@ from typing import Sequence
 import torch
 
 from . import _lib
-from .engine import MrDesc, TransferEngine
+from .engine import MrDesc, MrHandle, Pages, TransferEngine
 from .errors import ScheduleError
 
 DT_BF16 = "bf16"
@@ -96,14 +96,23 @@ def prepare_device(words: torch.Tensor, dtype: str, out: torch.Tensor | None = N
 
 
 def publish(engine: TransferEngine, prepared: torch.Tensor, dsts: Sequence[tuple[MrDesc, int]],
-            imm: int | None = None):
+            imm: int | None = None, handle: MrHandle | None = None, wait: bool = True):
     """One WriteImm of the prepared bytes to each destination
-    (RankExecutor._lane_write, weights.py:570-590)."""
-    h, _ = engine.reg_mr(prepared)
+    (RankExecutor._lane_write, weights.py:570-590), all destinations in ONE
+    kernel launch (k_copy_jobs), each releasing its own receipt.  `handle`:
+    the prepared buffer's registration, reused across updates (registered and
+    released here when None).  wait=False returns as soon as the copy is
+    enqueued; the caller waits on the returned flag (or the receivers on
+    their ImmFlags)."""
+    own = handle is None
+    h = engine.reg_mr(prepared)[0] if own else handle
     try:
-        flags = [engine.submit_single_write(prepared.numel(), (h, 0), (d, off), imm=imm) for d, off in dsts]
-        for f in flags:
-            f.wait()
+        n = prepared.numel() * prepared.element_size()
+        flag = engine._launch_jobs([(h.base, Pages((0,), 0, 0), d, Pages((0,), 0, off), n, 1 if n else 0, imm)
+                                    for d, off in dsts], label="weights.publish")
+        if wait:
+            flag.wait()
     finally:
-        engine.dereg_mr(h)
-    return flags
+        if own:
+            engine.dereg_mr(h)   # host bookkeeping only: the memory stays with the caller
+    return [flag]
