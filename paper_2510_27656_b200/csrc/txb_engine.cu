@@ -138,7 +138,7 @@ __device__ __forceinline__ int job_of(const JobSet& js, int64_t k) {
   return lo;
 }
 
-__global__ void __launch_bounds__(kCopyThreads, 1) k_copy_jobs(const __grid_constant__ JobSet js) {
+__global__ void __launch_bounds__(kCopyThreads, 2) k_copy_jobs(const __grid_constant__ JobSet js) {
   extern __shared__ __align__(128) uint8_t stage[];
   __shared__ __align__(8) uint64_t bars[kCopyWarps * kWarpStages];
   __shared__ uint32_t done[kMaxJobs];
@@ -223,7 +223,10 @@ __device__ __forceinline__ bool spin_ge_gpu(const uint64_t* p, uint64_t target, 
 // only drain, and no other warp waits for it.
 constexpr int kStreamBatch = 32;
 
-__global__ void __launch_bounds__(kCopyThreads, 1) k_kv_stream(const __grid_constant__ txb_stream_job ks) {
+// Two CTAs per SM (128 registers per thread) in vector mode: more warps in
+// flight to cover the release fences that book completed steps (the top
+// stall of the one-CTA build, profiles/r02/ncu_kv_stream_details.csv).
+__global__ void __launch_bounds__(kCopyThreads, 2) k_kv_stream(const __grid_constant__ txb_stream_job ks) {
   extern __shared__ __align__(128) uint8_t stage[];
   __shared__ __align__(8) uint64_t bars[kCopyWarps * kWarpStages];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -470,7 +473,7 @@ static int launch_jobs(JobSet& js, int grid, void* stream) {
   for (int i = 0; i < js.njobs; ++i) js.use_tma &= js.job[i].use_tma != 0;
   if (grid <= 0) {
     const int64_t want = (total + kCopyWarps - 1) / kCopyWarps;
-    const int cap = sms(0);
+    const int cap = (js.use_tma ? 1 : 2) * sms(0);  // two CTAs per SM unless TMA stages fill the smem
     grid = (int)(want < 1 ? 1 : (want < cap ? want : cap));
   }
   const size_t smem = js.use_tma ? (size_t)kCopyWarps * kWarpStages * kPiece : 0;
@@ -522,7 +525,7 @@ int txb_kv_stream(const txb_stream_job* ks, int grid, void* stream) {
     return TXB_ERR_TRANSFER;
   }
   DeviceFor on_dev(stream, ks->src);
-  if (grid <= 0) grid = sms(0);
+  if (grid <= 0) grid = (ks->use_tma ? 1 : 2) * sms(0);  // TMA stages fill one CTA's shared memory
   const size_t smem = ks->use_tma ? (size_t)kCopyWarps * kWarpStages * kPiece : 0;
   static bool attr_set[64] = {false};
   int dev = 0;
