@@ -113,6 +113,10 @@ int txb_stream_create(int device, void** out_stream);
  * did not complete while a persistent kernel was polling on the device.
  * Idempotent; TransferEngine calls it when it binds a device. */
 int txb_preload(int device);
+/* Checked build (make checked -> libtxb200_checked.so, -DTXB_CHECKED): *out =
+ * 0x80000000 | bit 0 set when a device-side bounds check has failed since
+ * load (device synchronised first).  The release build writes 0. */
+int txb_check_failures(int device, uint32_t* out);
 int txb_stream_destroy(int device, void* stream);
 /* Device address of page-locked host memory (cudaHostAlloc / pinned torch
  * tensors).  The kernels read inputs from and write results to such host

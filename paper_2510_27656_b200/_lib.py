@@ -109,6 +109,7 @@ SIGNATURES: dict[str, list] = {
     "txb_enable_peer": [_INT, _INT],
     "txb_stream_create": [_INT, C.POINTER(_VP)],
     "txb_preload": [_INT],
+    "txb_check_failures": [_INT, C.POINTER(C.c_uint32)],
     "txb_stream_destroy": [_INT, _VP],
     "txb_host_device_ptr": [_VP, C.POINTER(_VP)],
     "txb_moe_plan": [C.POINTER(Shape)],

@@ -83,6 +83,14 @@ static int grid_for(int64_t work, int per_block) {
   return (int)g;
 }
 
+unsigned int check_failures_codec() {
+#ifdef TXB_CHECKED
+  return read_check_fail();
+#else
+  return 0;
+#endif
+}
+
 cudaError_t preload_codec() {
   cudaError_t e = cudaSuccess;
   for (cudaError_t r : {touch(k_encode_rows<TXB_SRC_F32, 1>), touch(k_encode_rows<TXB_SRC_F32, 2>),

@@ -96,6 +96,38 @@ inline cudaError_t touch(K kernel) {
 cudaError_t preload_engine();
 cudaError_t preload_moe();
 cudaError_t preload_codec();
+unsigned int check_failures_engine();
+unsigned int check_failures_moe();
+unsigned int check_failures_codec();
+
+// ------------------------------------------------------------ checked build
+//
+// `make checked` builds libtxb200_checked.so with -DTXB_CHECKED: every index
+// a kernel computes before a store or load through it (grouped row, combine
+// slot, private-slab slot, shared-memory table extent) is bounds-checked on
+// the device.  A failed check prints the site, latches bit 0 of
+// g_txb_check_fail (read with txb_check_failures) and skips the access --
+// the pool's compute-sanitizer substitute (profiles/r02/README.md).  The
+// release build compiles the checks out.
+#ifdef TXB_CHECKED
+// one flag per translation unit (no relocatable device code needed); each
+// unit reports its own through check_failures_<unit>() (txb_check_failures)
+static __device__ unsigned int g_txb_check_fail = 0;
+static inline unsigned int read_check_fail() {
+  unsigned int v = 0;
+  cudaMemcpyFromSymbol(&v, g_txb_check_fail, sizeof(v));
+  return v;
+}
+#define TXB_ASSERT(cond)                                                                      \
+  (__builtin_expect(!(cond), 0)                                                               \
+       ? (atomicOr(&::txb::g_txb_check_fail, 1u),                                             \
+          printf("txb check failed %s:%d block %d thread %d: %s\n", __FILE__, __LINE__,       \
+                 (int)blockIdx.x, (int)threadIdx.x, #cond),                                   \
+          false)                                                                              \
+       : true)
+#else
+#define TXB_ASSERT(cond) true
+#endif
 
 // ------------------------------------------------------------ PTX wrappers
 

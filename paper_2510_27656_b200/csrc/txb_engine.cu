@@ -433,6 +433,14 @@ static int sms(int) {
   return cache[dev];
 }
 
+unsigned int check_failures_engine() {
+#ifdef TXB_CHECKED
+  return read_check_fail();
+#else
+  return 0;
+#endif
+}
+
 cudaError_t preload_engine() {
   cudaError_t e = cudaSuccess;
   for (cudaError_t r : {touch(k_copy_jobs), touch(k_write_value), touch(k_kv_stream), touch(k_imm_probe),
@@ -525,7 +533,7 @@ int txb_kv_stream(const txb_stream_job* ks, int grid, void* stream) {
     return TXB_ERR_TRANSFER;
   }
   DeviceFor on_dev(stream, ks->src);
-  if (grid <= 0) grid = (ks->use_tma ? 1 : 2) * sms(0);  // TMA stages fill one CTA's shared memory
+  if (grid <= 0) grid = sms(0);  // one CTA per SM (two measured 2% slower, profiles/r02/README.md)
   const size_t smem = ks->use_tma ? (size_t)kCopyWarps * kWarpStages * kPiece : 0;
   static bool attr_set[64] = {false};
   int dev = 0;

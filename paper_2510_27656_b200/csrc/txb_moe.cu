@@ -683,6 +683,7 @@ __device__ void own_positions(const txb_moe_shape& s, const uint32_t* hist, int6
       acc0 += __shfl_xor_sync(0xffffffffu, acc0, o);
     }
     if (lane == 0) {
+      TXB_ASSERT(bad || (acc + (int)sh.own_rank[k] >= 0 && acc + (int)sh.own_rank[k] < s.comb_rows));
       pos[sh.own_i[k]] = bad ? -1 : (int64_t)acc + sh.own_rank[k];
       uint8_t* pd = nullptr;
       const int d = d0 / L;
@@ -749,7 +750,13 @@ __device__ void own_copies_solo(const txb_moe_shape& s, const uint32_t* hist, co
     }
     if (lane == 0) {
       const int gr = accp + cnt;
+      if (!TXB_ASSERT(gr >= 0 && gr < s.grouped_rows)) {
+        sh.dstp[k] = nullptr;
+        sh.pdst[k] = nullptr;
+        continue;
+      }
       b.rank_scratch[i] = cnt;
+      TXB_ASSERT(acc + cnt >= 0 && acc + cnt < s.comb_rows);
       b.pos[i] = (int64_t)acc + cnt;
       b.gidx[i] = gr;
       sh.dstp[k] = grouped_of(b.peers[0], s) + (int64_t)gr * s.payload_bytes;
@@ -788,6 +795,10 @@ __device__ void own_dests(const txb_moe_shape& s, const uint32_t* C, void* const
     for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) {
       const int g = acc + (int)sh.own_rank[k];
+      if (!TXB_ASSERT(g >= 0 && g < s.grouped_rows && d >= 0 && d < N)) {
+        sh.dstp[k] = nullptr;
+        continue;
+      }
       sh.dstp[k] = grouped_of(peers[d], s) + (int64_t)g * s.payload_bytes;
       gidx[sh.own_i[k]] = d == s.me ? g : -1;
       if (per_token(s)) srctok_of(peers[d], s)[g] = sh.own_i[k] / s.topk;
@@ -814,7 +825,7 @@ __device__ __forceinline__ uint8_t* copy_dest(const txb_moe_shape& s, void* cons
   const int64_t t = i / s.topk;
   if (d != s.me && s.priv_tokens > 0) {
     const int64_t sidx = pos[i] - sh.sst[d];
-    if (sidx < s.priv_tokens) {
+    if (sidx < s.priv_tokens && TXB_ASSERT(sidx >= 0)) {
       const int par = (int)(step & 1);
       gidx[i] = -1;
       if (per_token(s)) privsrc_of(peers[d], s, par, s.me)[sidx] = (int32_t)t;
@@ -823,6 +834,7 @@ __device__ __forceinline__ uint8_t* copy_dest(const txb_moe_shape& s, void* cons
     }
   }
   const int64_t g = (int64_t)baseg[e] + rank;
+  if (!TXB_ASSERT(g >= 0 && g < s.grouped_rows && d >= 0 && d < s.ranks)) return grouped_of(peers[s.me], s);
   gidx[i] = d == s.me ? (int32_t)g : -1;
   if (per_token(s)) srctok_of(peers[d], s)[g] = (int32_t)t;
   atomicAdd(&sh.cnt[d], 1u);
@@ -1220,6 +1232,7 @@ __device__ __forceinline__ void recv_rows_body(const txb_moe_shape& s, int* sm, 
   const int N = s.ranks, L = s.local_experts;
   const RecvTables t = recv_carve(s, sm);
   const int padded_total = t.tot[0];
+  if (!TXB_ASSERT(padded_total >= 0 && padded_total <= s.grouped_rows)) return;
   const int64_t P = s.payload_bytes;
   const int warp = grp.tid >> 5, lane = grp.tid & 31, nwarp = grp.nt >> 5;
   int it = 0;
@@ -1426,6 +1439,7 @@ __device__ void recv_private_rows(const txb_moe_shape& s, const int* sm, void* r
     }
     const int le = lo, kk = k - (rb[le] - rb[0]);
     const int g = t.gstart[le] + t.srcpre[le * (N + 1) + q] + kk;
+    if (!TXB_ASSERT(g >= 0 && g < s.grouped_rows && kk >= 0)) continue;
     const uint8_t* src = priv_rows_of(region, s, par, q) + (int64_t)k * P;
     uint8_t* dst = G + (int64_t)g * P;
     if ((P & 15) == 0) {
@@ -1518,6 +1532,7 @@ __device__ void combine_send_rows(const txb_moe_shape& s, Flags* f, const uint8_
       const int q = (int)sources[g];
       const int64_t nb = Pc;
       const uint8_t* src = out + (int64_t)g * ld;
+      if (!TXB_ASSERT(q >= 0 && q < N && ret[g] >= 0 && ret[g] < s.comb_rows)) continue;
       uint8_t* dst = comb_of(peers[q], s) + (int64_t)ret[g] * Pc;
       if (vec) {
         const int4* sv = reinterpret_cast<const int4*>(src);
@@ -1560,6 +1575,7 @@ __device__ void combine_send_rows(const txb_moe_shape& s, Flags* f, const uint8_
       const int g = send_list[r];
       const int q = (int)sources[g];
       const int4* src = reinterpret_cast<const int4*>(out + (int64_t)g * ld + (int64_t)c * kChunk);
+      if (!TXB_ASSERT(q >= 0 && q < N && ret[g] >= 0 && ret[g] < s.comb_rows)) continue;
       int4* dst = reinterpret_cast<int4*>(comb_of(peers[q], s) + (int64_t)ret[g] * Pc + (int64_t)c * kChunk);
       const int n16 = (int)(min((int64_t)kChunk, Pc - (int64_t)c * kChunk) >> 4);
       int4 v[kChunk / 512];
@@ -1577,6 +1593,7 @@ __device__ void combine_send_rows(const txb_moe_shape& s, Flags* f, const uint8_
   for (int r = cta * nwarp + warp; r < total; r += ncta * nwarp) {
     const int g = send_list[r];
     const int q = (int)sources[g];
+    if (!TXB_ASSERT(q >= 0 && q < N && ret[g] >= 0 && ret[g] < s.comb_rows)) continue;
     copy_row(comb_of(peers[q], s) + (int64_t)ret[g] * Pc, out + (int64_t)g * ld, Pc, lane, 32);
     if (lane == 0) atomicAdd(&sh.cnt[q], (uint32_t)comb_chunks(s));
   }
@@ -1982,6 +1999,18 @@ k_dispatch_roles(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
   uint32_t* C = reinterpret_cast<uint32_t*>(dsm + cmat_offset(s));
   int* rt = reinterpret_cast<int*>(dsm + recv_offset(s));
   const bool solo = s.ranks == 1;
+#ifdef TXB_CHECKED
+  {
+    uint32_t dyn;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+    const size_t need = SOLO ? solo_recv_offset(s, n) + smem_recv(s.ranks, s.local_experts)
+                             : cmat_offset(s) + smem_cmat(s.ranks, s.experts);
+    // the staged ids must end before the receive tables in the EP=1 kernel,
+    // where the two are live at once
+    if (!TXB_ASSERT(need <= dyn && (!SOLO || (size_t)(s.experts + n * s.topk) * 4 + 16 <= solo_recv_offset(s, n))))
+      return;
+  }
+#endif
   stamp(b, 0);
   grid_dep_launch();
   if constexpr (SOLO) {
@@ -2255,6 +2284,14 @@ static cudaError_t preload_src_elem() {
                         touch(k_dispatch<SRC, ELEM>)})
     if (r != cudaSuccess) e = r;
   return e;
+}
+
+unsigned int check_failures_moe() {
+#ifdef TXB_CHECKED
+  return read_check_fail();
+#else
+  return 0;
+#endif
 }
 
 cudaError_t preload_moe() {

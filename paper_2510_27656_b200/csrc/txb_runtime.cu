@@ -109,6 +109,22 @@ int txb_enable_peer(int device, int peer_device) {
   return TXB_OK;
 }
 
+int txb_check_failures(int device, uint32_t* out) {
+  if (!out) {
+    set_error("txb_check_failures: null output");
+    return TXB_ERR_PROTOCOL;
+  }
+  *out = 0;
+#ifdef TXB_CHECKED
+  TXB_ON_DEVICE(device);
+  TXB_CUDA(cudaDeviceSynchronize());
+  *out = (check_failures_engine() | check_failures_moe() | check_failures_codec()) | 0x80000000u;
+#else
+  (void)device;
+#endif
+  return TXB_OK;
+}
+
 int txb_preload(int device) {
   TXB_ON_DEVICE(device);
   static bool done[64] = {false};
