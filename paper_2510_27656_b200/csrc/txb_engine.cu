@@ -223,10 +223,7 @@ __device__ __forceinline__ bool spin_ge_gpu(const uint64_t* p, uint64_t target, 
 // only drain, and no other warp waits for it.
 constexpr int kStreamBatch = 32;
 
-// Two CTAs per SM (128 registers per thread) in vector mode: more warps in
-// flight to cover the release fences that book completed steps (the top
-// stall of the one-CTA build, profiles/r02/ncu_kv_stream_details.csv).
-__global__ void __launch_bounds__(kCopyThreads, 2) k_kv_stream(const __grid_constant__ txb_stream_job ks) {
+__global__ void __launch_bounds__(kCopyThreads, 1) k_kv_stream(const __grid_constant__ txb_stream_job ks) {
   extern __shared__ __align__(128) uint8_t stage[];
   __shared__ __align__(8) uint64_t bars[kCopyWarps * kWarpStages];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
