@@ -188,40 +188,14 @@ __device__ uint32_t route_counts_direct(const txb_moe_shape& s, const int64_t* r
   }
   g.sync();
   stamp(bufs, 19);
-  const bool lanes = (32 % R) == 0;
-  const int lane = tid & 31;
-  // lanes of this thread's token within its warp (R | 32 and R | nt: a
-  // token's copies sit in consecutive lanes of one warp in every pass)
-  const bool tok_lanes = lanes && (nt % R) == 0;
-  // one entry: stage its id, count it, flag range / duplicate errors
+  // one entry: stage its id, count it, flag a range error (a short body:
+  // this code runs cold once per CTA per step, so its size is its cost)
   auto entry = [&](int i, int64_t v) {
-    const bool valid = i < m;
+    if (i >= m) return;
     const bool in_range = v >= 0 && v < E;
-    // int32 ids; out-of-range entries get lane-unique negatives (no false dups)
-    const int v32 = in_range ? (int)v : -1 - lane;
-    bool dup = false;
-    if (tok_lanes) {
-      // the token's R ids sit in consecutive lanes: R shuffles compare
-      // each id with its token's others (cheaper than a warp-wide
-      // match.any, which the ncu source page showed dominating this loop)
-      const int tbase = lane - lane % R;
-      int same = 0;
-#pragma unroll 8
-      for (int jj = 0; jj < R; ++jj) same += __shfl_sync(0xffffffffu, v32, tbase + jj) == v32;
-      dup = same > 1;
-    } else if (valid) {
-      const int j = i % R;
-      #pragma unroll 1
-      for (int jj = 1; jj <= j; ++jj) dup |= routes[i - jj] == v;
-    }
-    if (!valid) return;
-    rv[i] = in_range ? v32 : -1;
-    if (!in_range) {
-      atomicOr(&sh.bad, TXB_EV_ROUTE_RANGE);
-      return;
-    }
-    if (dup) atomicOr(&sh.bad, TXB_EV_ROUTE_DUP);
-    atomicAdd(&hist[v32], 1u);
+    rv[i] = in_range ? (int)v : -1;
+    if (in_range) atomicAdd(&hist[(int)v], 1u);
+    else atomicOr(&sh.bad, TXB_EV_ROUTE_RANGE);
   };
   if (pre_ok) {
 #pragma unroll
@@ -236,7 +210,18 @@ __device__ uint32_t route_counts_direct(const txb_moe_shape& s, const int64_t* r
   }
   g.sync();
   stamp(bufs, 22);
+  // duplicates within a token (moe.py:152-154): each staged id against the
+  // token's earlier ones (out-of-range ids are -1, already latched)
+  bool dup = false;
+  #pragma unroll 1
+  for (int i = tid; i < m; i += nt) {
+    const int j = i % R, v = rv[i];
+    #pragma unroll 1
+    for (int jj = i - j; jj < i; ++jj) dup |= v >= 0 && rv[jj] == v;
+  }
+  if (dup) atomicOr(&sh.bad, TXB_EV_ROUTE_DUP);
   if (with_ranks) own_ranks(rv, rank_out, nw, sh, g);
+  g.sync();
   const uint32_t b = sh.bad;
   if (b)
     #pragma unroll 1
