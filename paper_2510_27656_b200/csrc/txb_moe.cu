@@ -158,9 +158,29 @@ __device__ __forceinline__ void own_ranks(const int32_t* rv, int32_t* rank_out, 
 
 // with_ranks = false: histogram, staging and validation only (the caller
 // runs own_ranks on another warp group).
+// Duplicates within a token (moe.py:152-154) over the staged ids: each id
+// against the token's earlier ones (out-of-range ids are -1, already
+// latched).  Returns TXB_EV_ROUTE_DUP or 0 for the calling thread's share.
+__device__ __forceinline__ uint32_t staged_dups(const int32_t* rv, int m, int R, const Grp& g) {
+  bool dup = false;
+  #pragma unroll 1
+  for (int i = g.tid; i < m; i += g.nt) {
+    const int j = i % R, v = rv[i];
+    #pragma unroll 1
+    for (int jj = i - j; jj < i; ++jj) dup |= v >= 0 && rv[jj] == v;
+  }
+  return dup ? TXB_EV_ROUTE_DUP : 0u;
+}
+
+// check_dups = false: the caller checks duplicates later, off the critical
+// path (the decode kernels do it in CTA 0 with warps that would otherwise
+// wait; ~1.8 us of cold code measured on the routing role's path).  A
+// duplicate cannot send a store out of bounds -- every CTA counts the same
+// ids -- so the step completes and dispatch_recv raises the latched error.
 __device__ uint32_t route_counts_direct(const txb_moe_shape& s, const int64_t* routes, int64_t n, uint32_t* hist,
                                         int32_t* rv, int32_t* rank_out, int cta, int ncta, Shared& sh,
-                                        const txb_moe_bufs& bufs, const Grp& g, bool with_ranks = true) {
+                                        const txb_moe_bufs& bufs, const Grp& g, bool with_ranks = true,
+                                        bool check_dups = true) {
   const int E = s.experts, R = s.topk, tid = g.tid;
   const int m = (int)(n * R);
   const int nmine = n > cta ? (int)((n - cta + ncta - 1) / ncta) : 0;
@@ -210,18 +230,14 @@ __device__ uint32_t route_counts_direct(const txb_moe_shape& s, const int64_t* r
   }
   g.sync();
   stamp(bufs, 22);
-  // duplicates within a token (moe.py:152-154): each staged id against the
-  // token's earlier ones (out-of-range ids are -1, already latched)
-  bool dup = false;
-  #pragma unroll 1
-  for (int i = tid; i < m; i += nt) {
-    const int j = i % R, v = rv[i];
-    #pragma unroll 1
-    for (int jj = i - j; jj < i; ++jj) dup |= v >= 0 && rv[jj] == v;
+  if (check_dups) {
+    const uint32_t d = staged_dups(rv, m, R, g);
+    if (d) atomicOr(&sh.bad, d);
   }
-  if (dup) atomicOr(&sh.bad, TXB_EV_ROUTE_DUP);
+  stamp(bufs, 27);
   if (with_ranks) own_ranks(rv, rank_out, nw, sh, g);
   g.sync();
+  stamp(bufs, 28);
   const uint32_t b = sh.bad;
   if (b)
     #pragma unroll 1
@@ -1950,9 +1966,16 @@ __device__ __forceinline__ void dispatch_roles_solo(const txb_moe_shape& s, cons
       store_row_regs<SRC, ELEM>(pre, s.hidden, s.scales, sh.dstp, s.topk, tg);
     }
     if (b.prof && tg.tid == 0) b.prof[blockIdx.x * 32 + 20] = globaltimer();
+    // duplicate ids, checked once per rank by CTA 0 off the critical path
+    // (the receive tables live after the staged ids on this path)
+    if (cta == 0) {
+      const uint32_t d = staged_dups(rv, (int)(n * s.topk), s.topk, tg);
+      if (d) atomicOr(&f->err, d);
+    }
   } else {
     const Grp rg{(int)threadIdx.x, kRouteRole, 1};
-    const uint32_t bad = route_counts_direct(s, routes, n, hist, rv, b.rank_scratch, cta, ncta, sh, b, rg, false);
+    const uint32_t bad = route_counts_direct(s, routes, n, hist, rv, b.rank_scratch, cta, ncta, sh, b, rg, false,
+                                             /*check_dups=*/false);
     const PreDirty pd = prefetch_dirty(s, b.dirty, cta, ncta, rg);  // after the route loads
     if (rg.tid == 0) bad_s = bad;
     named_arrive(3, kThreads);
@@ -2019,6 +2042,12 @@ k_dispatch_roles(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
       store_row_regs<SRC, ELEM>(pre, s.hidden, s.scales, sh.pdst, s.topk, tg);
       if (b.prof && tg.tid == 0) b.prof[blockIdx.x * 32 + 26] = globaltimer();
     }
+    // duplicate ids, checked once per rank by CTA 0 while the route
+    // exchange is in flight (the staged ids are overwritten after hand-off 3)
+    if (cta == 0) {
+      const uint32_t d = staged_dups(reinterpret_cast<const int32_t*>(hist + s.experts), (int)(n * s.topk), s.topk, tg);
+      if (d) atomicOr(&f->err, d);
+    }
     named_sync(3, kThreads);  // destinations are in sh.dstp
     if (!skip) store_row_regs<SRC, ELEM>(pre, s.hidden, s.scales, sh.dstp, s.topk, tg);
     if (b.prof && tg.tid == 0) b.prof[blockIdx.x * 32 + 20] = globaltimer();
@@ -2030,7 +2059,8 @@ k_dispatch_roles(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
     // staged ids `rv` overlap the receive tables `rt` (written after
     // hand-off 3), so only this role reads them, and only before then.
     int32_t* rv = reinterpret_cast<int32_t*>(hist + s.experts);
-    const uint32_t bad = route_counts_direct(s, routes, n, hist, rv, b.rank_scratch, cta, ncta, sh, b, rg, false);
+    const uint32_t bad = route_counts_direct(s, routes, n, hist, rv, b.rank_scratch, cta, ncta, sh, b, rg, false,
+                                             /*check_dups=*/false);
     const PreDirty pd = prefetch_dirty(s, b.dirty, cta, ncta, rg);  // after the route loads
     route_publish(s, b.peers, f, hist, step, n, bad, cta, ncta, rg);
     stamp(b, 14);

@@ -98,8 +98,8 @@ else:
     run = g.replay
 rows = []
 detail = []
-ORDER = [0, 19, 22, 24, 25, 14, 1, 2, 26, 3, 15, 20, 16, 17, 18, 4, 7, 5, 6, 8, 9, 10, 11, 23, 12, 13]
-STAMP = {26: "priv stored", 24: "seg prefix", 25: "seg sync2", 0: "start", 19: "own routes in", 22: "hist done", 14: "counted(+loads)", 1: "encoded", 2: "published+pos", 3: "routes-in", 15: "dests",
+ORDER = [0, 19, 22, 27, 28, 24, 25, 14, 1, 2, 26, 3, 15, 20, 16, 17, 18, 4, 7, 5, 6, 8, 9, 10, 11, 23, 12, 13]
+STAMP = {27: "dups checked", 28: "ids synced", 26: "priv stored", 24: "seg prefix", 25: "seg sync2", 0: "start", 19: "own routes in", 22: "hist done", 14: "counted(+loads)", 1: "encoded", 2: "published+pos", 3: "routes-in", 15: "dests",
          5: "joined", 20: "tok stored", 16: "T:loaded", 17: "T:srcpre", 18: "T:scan", 4: "tables", 6: "signalled", 7: "metadata", 8: "tokens-in", 9: "c:start", 10: "c:sent",
          11: "c:signalled", 23: "c:waited", 12: "c:reduced", 13: "c:end"}
 for k in range(a.reps + 5):
