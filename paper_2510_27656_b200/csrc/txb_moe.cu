@@ -172,11 +172,37 @@ __device__ __forceinline__ uint32_t staged_dups(const int32_t* rv, int m, int R,
   return dup ? TXB_EV_ROUTE_DUP : 0u;
 }
 
-// check_dups = false: the caller checks duplicates later, off the critical
-// path (the decode kernels do it in CTA 0 with warps that would otherwise
-// wait; ~1.8 us of cold code measured on the routing role's path).  A
-// duplicate cannot send a store out of bounds -- every CTA counts the same
-// ids -- so the step completes and dispatch_recv raises the latched error.
+// check_dups = false (the decode kernels, one token per CTA): the pass over
+// the whole batch (~1.8 us measured on the routing role's critical path) is
+// replaced by own_token_dups in the token role, which checks the CTA's own
+// token while its row load is in flight.  A duplicate cannot send a store out
+// of bounds -- every CTA counts the same ids -- so the step completes, and
+// dispatch_recv reads the rank's error word after the kernel.
+__device__ __forceinline__ void own_token_dups(const txb_moe_shape& s, const int64_t* routes, int64_t n,
+                                               int cta, uint32_t* err, const Grp& g) {
+  const int R = s.topk, E = s.experts;
+  if (g.tid >= 32 || cta >= n) return;
+  const int lane = g.tid;
+  if (R <= 32) {
+    int v = -1 - lane;  // lane-unique when unused or out of range (range is checked elsewhere)
+    if (lane < R) {
+      const int64_t x = routes[(int64_t)cta * R + lane];
+      if (x >= 0 && x < E) v = (int)x;
+    }
+    int same = 0;
+    #pragma unroll 1
+    for (int j = 0; j < R; ++j) same += __shfl_sync(0xffffffffu, v, j) == v;
+    if (__any_sync(0xffffffffu, lane < R && same > 1) && lane == 0) atomicOr(err, TXB_EV_ROUTE_DUP);
+  } else if (lane == 0) {
+    const int64_t* r = routes + (int64_t)cta * R;
+    bool dup = false;
+    #pragma unroll 1
+    for (int j = 1; j < R; ++j)
+      #pragma unroll 1
+      for (int jj = 0; jj < j; ++jj) dup |= r[j] == r[jj];
+    if (dup) atomicOr(err, TXB_EV_ROUTE_DUP);
+  }
+}
 __device__ uint32_t route_counts_direct(const txb_moe_shape& s, const int64_t* routes, int64_t n, uint32_t* hist,
                                         int32_t* rv, int32_t* rank_out, int cta, int ncta, Shared& sh,
                                         const txb_moe_bufs& bufs, const Grp& g, bool with_ranks = true,
@@ -208,6 +234,7 @@ __device__ uint32_t route_counts_direct(const txb_moe_shape& s, const int64_t* r
   }
   g.sync();
   stamp(bufs, 19);
+
   // one entry: stage its id, count it, flag a range error (a short body:
   // this code runs cold once per CTA per step, so its size is its cost)
   auto entry = [&](int i, int64_t v) {
@@ -1955,6 +1982,7 @@ __device__ __forceinline__ void dispatch_roles_solo(const txb_moe_shape& s, cons
     RowRaw raw;
     RowRegs pre;
     load_row_raw<SRC, ELEM>(x, cta, s.hidden, s.payload_bytes, raw, tg);
+    own_token_dups(s, routes, n, cta, &f->err, tg);  // while the row load is in flight
     finish_row_regs<SRC, ELEM>(raw, pre, sh.red, tg);
     if (b.prof && tg.tid == 0) b.prof[blockIdx.x * 32 + 1] = globaltimer();
     for (int q = tg.tid; q < s.ranks; q += tg.nt) sh.cnt[q] = 0;
@@ -1966,12 +1994,7 @@ __device__ __forceinline__ void dispatch_roles_solo(const txb_moe_shape& s, cons
       store_row_regs<SRC, ELEM>(pre, s.hidden, s.scales, sh.dstp, s.topk, tg);
     }
     if (b.prof && tg.tid == 0) b.prof[blockIdx.x * 32 + 20] = globaltimer();
-    // duplicate ids, checked once per rank by CTA 0 off the critical path
-    // (the receive tables live after the staged ids on this path)
-    if (cta == 0) {
-      const uint32_t d = staged_dups(rv, (int)(n * s.topk), s.topk, tg);
-      if (d) atomicOr(&f->err, d);
-    }
+
   } else {
     const Grp rg{(int)threadIdx.x, kRouteRole, 1};
     const uint32_t bad = route_counts_direct(s, routes, n, hist, rv, b.rank_scratch, cta, ncta, sh, b, rg, false,
@@ -2030,6 +2053,7 @@ k_dispatch_roles(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
     RowRaw raw;
     RowRegs pre;
     load_row_raw<SRC, ELEM>(x, cta, s.hidden, s.payload_bytes, raw, tg);
+    own_token_dups(s, routes, n, cta, &f->err, tg);  // while the row load is in flight
     finish_row_regs<SRC, ELEM>(raw, pre, sh.red, tg);
     if (b.prof && tg.tid == 0) b.prof[blockIdx.x * 32 + 1] = globaltimer();
     // speculative private copies (moe.py:556-582): their destinations need
@@ -2041,12 +2065,6 @@ k_dispatch_roles(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
     if (s.priv_tokens > 0) {
       store_row_regs<SRC, ELEM>(pre, s.hidden, s.scales, sh.pdst, s.topk, tg);
       if (b.prof && tg.tid == 0) b.prof[blockIdx.x * 32 + 26] = globaltimer();
-    }
-    // duplicate ids, checked once per rank by CTA 0 while the route
-    // exchange is in flight (the staged ids are overwritten after hand-off 3)
-    if (cta == 0) {
-      const uint32_t d = staged_dups(reinterpret_cast<const int32_t*>(hist + s.experts), (int)(n * s.topk), s.topk, tg);
-      if (d) atomicOr(&f->err, d);
     }
     named_sync(3, kThreads);  // destinations are in sh.dstp
     if (!skip) store_row_regs<SRC, ELEM>(pre, s.hidden, s.scales, sh.dstp, s.topk, tg);

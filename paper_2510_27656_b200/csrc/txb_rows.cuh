@@ -194,6 +194,17 @@ struct RowRegs {
   bool ok;     // false: shape not eligible, use encode_store_row later
 };
 
+// A 16-byte global load the compiler keeps where it is written (asm
+// volatile): the row loads are issued first so their HBM latency overlaps the
+// work that follows, instead of being sunk next to their first use.
+__device__ __forceinline__ uint4 ldg_pinned(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
 // Raw source bytes of a thread's (up to) two chunks, loaded before they are
 // needed so the HBM latency overlaps other work (route counting).
 struct RowRaw {
@@ -214,7 +225,7 @@ __device__ __forceinline__ void load_row_raw(const void* x, int64_t t, int H, in
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const int c = tid + u * nt;
-      if (c < rr.nchunk) rr.r[u][0] = reinterpret_cast<const uint4*>(src)[c];
+      if (c < rr.nchunk) rr.r[u][0] = ldg_pinned(reinterpret_cast<const uint4*>(src) + c);
     }
   } else {
     constexpr int EPC = 16 / ELEM;
@@ -233,7 +244,7 @@ __device__ __forceinline__ void load_row_raw(const void* x, int64_t t, int H, in
       if (c < rr.nchunk) {
         if constexpr (CB >= 16) {
 #pragma unroll
-          for (int k = 0; k < CB / 16; ++k) rr.r[u][k] = reinterpret_cast<const uint4*>(src + (int64_t)c * CB)[k];
+          for (int k = 0; k < CB / 16; ++k) rr.r[u][k] = ldg_pinned(reinterpret_cast<const uint4*>(src + (int64_t)c * CB) + k);
         } else {
           const uint2 v = *reinterpret_cast<const uint2*>(src + (int64_t)c * CB);
           rr.r[u][0] = make_uint4(v.x, v.y, 0, 0);

@@ -691,6 +691,10 @@ class MoeRank:
         torch.cuda.current_stream(self.device).synchronize()
         info = self._info_host.numpy().copy()
         err = int(info[2 * L + 2])
+        if not err:
+            # the decode kernels latch per-CTA route checks into the rank's
+            # error word, possibly after CTA 0 copied it into info
+            err, _ = self.status()
         if err:
             self._check_err(err, st.step)
         total = int(info[2 * L])
