@@ -503,7 +503,13 @@ __device__ void route_publish(const txb_moe_shape& s, void* const* peers, Flags*
   const int slot = (int)(step & 1);
   const uint64_t tag = (uint64_t)(uint32_t)step << 32;
   #pragma unroll 1
-  for (int idx = part * g.nt + g.tid; idx < N * E; idx += nparts * g.nt) {
+  // every CTA stores an equal contiguous slice (a few words each): with the
+  // words packed into the first CTAs, those CTAs' remote stores held their
+  // routing role back ~1.5 us (EP=2 phase stamps, round 2)
+  const int NE = N * E, per = (NE + nparts - 1) / nparts;
+  const int i1 = min(NE, (part + 1) * per);
+  #pragma unroll 1
+  for (int idx = part * per + g.tid; idx < i1; idx += g.nt) {
     const int d = idx / E, e = idx - d * E;
     if (N == 1) *(route_of(peers[d], s, slot) + (size_t)s.me * E + e) = tag | hist[e];
     else st_relaxed_sys(route_of(peers[d], s, slot) + (size_t)s.me * E + e, tag | hist[e]);

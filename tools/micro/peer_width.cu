@@ -1,0 +1,90 @@
+// NVLink peer-write micro: does the store width (16 B vs 32 B per thread)
+// or the number of bytes in flight per warp change the time to move a
+// decode-sized buffer from cuda:0 HBM into cuda:1 HBM?  Kernel time with
+// CUDA events (host ahead of the GPU behind a spin kernel), median of 20.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/micro/peer_width tools/micro/peer_width.cu
+#include <cstdio>
+#include <cstdint>
+#include <vector>
+#include <algorithm>
+#include <cuda_runtime.h>
+
+__global__ void spin(long long ns) {
+  long long t0; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  long long t = t0; while (t - t0 < ns) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+}
+
+// W = bytes per store (16 or 32); U = stores in flight per thread per pass
+template <int W, int U>
+__global__ void __launch_bounds__(512, 1) copy(const uint8_t* __restrict__ s, uint8_t* d, size_t n) {
+  const size_t nv = n / W;
+  const size_t tid = blockIdx.x * (size_t)blockDim.x + threadIdx.x, nt = (size_t)gridDim.x * blockDim.x;
+  for (size_t b = tid; b < nv; b += nt * U) {
+    if constexpr (W == 16) {
+      uint4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) if (b + u * nt < nv) v[u] = reinterpret_cast<const uint4*>(s)[b + u * nt];
+#pragma unroll
+      for (int u = 0; u < U; ++u) if (b + u * nt < nv) reinterpret_cast<uint4*>(d)[b + u * nt] = v[u];
+    } else {
+      uint32_t r[U][8];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (b + u * nt < nv) {
+          const uint8_t* p = s + (b + u * nt) * 32;
+          asm volatile("ld.global.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                       : "=r"(r[u][0]), "=r"(r[u][1]), "=r"(r[u][2]), "=r"(r[u][3]), "=r"(r[u][4]), "=r"(r[u][5]),
+                         "=r"(r[u][6]), "=r"(r[u][7]) : "l"(p));
+        }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (b + u * nt < nv) {
+          uint8_t* q = d + (b + u * nt) * 32;
+          asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" :: "l"(q), "r"(r[u][0]), "r"(r[u][1]),
+                       "r"(r[u][2]), "r"(r[u][3]), "r"(r[u][4]), "r"(r[u][5]), "r"(r[u][6]), "r"(r[u][7]) : "memory");
+        }
+    }
+  }
+}
+
+template <typename F>
+static float timed(F launch, cudaStream_t st) {
+  std::vector<float> ts;
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  for (int k = 0; k < 23; ++k) {
+    spin<<<1, 1, 0, st>>>(50000);
+    cudaEventRecord(e0, st); launch(); cudaEventRecord(e1, st);
+    cudaStreamSynchronize(st);
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    if (k >= 3) ts.push_back(ms * 1e3f);
+  }
+  std::sort(ts.begin(), ts.end());
+  return ts[ts.size() / 2];
+}
+
+int main() {
+  int n = 0; cudaGetDeviceCount(&n);
+  const int peer = n > 1 ? 1 : 0;
+  cudaSetDevice(0);
+  if (peer) cudaDeviceEnablePeerAccess(1, 0);
+  int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  cudaStream_t st; cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  size_t sizes[] = {3784704, 7340032, 16777216, 67108864};
+  printf("# peer write cuda:0 -> cuda:%d, grid %d x 512, us (median of 20)\n", peer, sms);
+  printf("%12s %10s %10s %10s %10s %10s\n", "bytes", "16Bx4", "16Bx8", "32Bx2", "32Bx4", "CE");
+  for (size_t nb : sizes) {
+    uint8_t *s, *d;
+    cudaSetDevice(0); cudaMalloc(&s, nb); cudaMemset(s, 3, nb);
+    cudaSetDevice(peer); cudaMalloc(&d, nb);
+    cudaSetDevice(0);
+    float a = timed([&] { copy<16, 4><<<sms, 512, 0, st>>>(s, d, nb); }, st);
+    float b = timed([&] { copy<16, 8><<<sms, 512, 0, st>>>(s, d, nb); }, st);
+    float c = timed([&] { copy<32, 2><<<sms, 512, 0, st>>>(s, d, nb); }, st);
+    float e = timed([&] { copy<32, 4><<<sms, 512, 0, st>>>(s, d, nb); }, st);
+    float ce = timed([&] { cudaMemcpyPeerAsync(d, peer, s, 0, nb, st); }, st);
+    printf("%12zu %10.2f %10.2f %10.2f %10.2f %10.2f   (GB/s at best %.0f)\n", nb, a, b, c, e, ce,
+           nb / (std::min(std::min(a, b), std::min(c, e)) * 1e-6) / 1e9);
+    cudaFree(s); cudaSetDevice(peer); cudaFree(d); cudaSetDevice(0);
+  }
+  return 0;
+}
