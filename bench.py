@@ -439,6 +439,7 @@ def run_b200(a) -> None:
 
     eager = run_eager(max(20, K // 2))
 
+
     # back-to-back steps: B steps per graph, step i on input set i % S of a
     # pool whose touched bytes (activations + expert rows) are twice the L2,
     # so every step starts on cold inputs with no flush between steps
@@ -620,6 +621,9 @@ def run_b200(a) -> None:
                      "CTA's end of one flushed step (max over ranks)",
         "tokens_per_s": round(n_gpu * tokens / (p50 * 1e-6), 1),
         "kernel_us": {k: round(v, 2) for k, v in kt.items()},
+        "kernel_us_note": "the flushed graph step split by a CUDA event node between the two kernels (the "
+                          "node's own cost lands in the dispatch); roofline.kernel_span_us gives the same "
+                          "kernel on the device clock",
         "roofline": roofline,
         "e2e": e2e,
         "gpu_launches": 2 * K,
