@@ -1,0 +1,21 @@
+# 4-GPU measurement run: suite, bench at EP=1/2/4 (decode / kimi / prefill), reference arm, KV stream
+mkdir -p gpurun_out/r3c
+nvidia-smi -L > gpurun_out/r3c/gpus.txt
+timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/r3c/pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/r3c/pytest.log
+tail -3 gpurun_out/r3c/pytest.log
+timeout 600 python tools/bench_kv_stream.py --modes ready --reps 3 > gpurun_out/r3c/kv_ready.json 2>&1; tail -c 300 gpurun_out/r3c/kv_ready.json; echo
+timeout 600 python tools/bench_kv_stream.py --modes paced --layer-us 12 --grid 32 --reps 2 > gpurun_out/r3c/kv_paced.json 2>&1; tail -c 300 gpurun_out/r3c/kv_paced.json; echo
+TR="python -m torch.distributed.run --nnodes=1 --master-addr 127.0.0.1"
+timeout 600 python bench.py > gpurun_out/r3c/bench_decode_ep1.json 2> gpurun_out/r3c/bench_decode_ep1.err
+for CFG in kimi prefill; do timeout 600 python bench.py --config $CFG --no-cpu-baseline > gpurun_out/r3c/bench_${CFG}_ep1.json 2> gpurun_out/r3c/bench_${CFG}_ep1.err; done
+for N in 2 4; do for CFG in decode kimi prefill; do
+  timeout 600 $TR --nproc-per-node $N --master-port $((29600+N)) bench.py --config $CFG --gpus $N > gpurun_out/r3c/bench_${CFG}_ep$N.json 2> gpurun_out/r3c/bench_${CFG}_ep$N.err
+done; done
+timeout 600 python bench.py --impl reference > gpurun_out/r3c/ref_ep1.json 2> gpurun_out/r3c/ref_ep1.err
+for N in 2 4; do timeout 900 $TR --nproc-per-node $N --master-port $((29660+N)) bench.py --impl reference --gpus $N > gpurun_out/r3c/ref_ep$N.json 2> gpurun_out/r3c/ref_ep$N.err; done
+timeout 300 $TR --nproc-per-node 4 --master-port 29650 tools/prof_torchrun.py --reps 50 2>&1 | grep -v OMP | grep -v '^\*' > gpurun_out/r3c/stamps_decode_ep4.txt
+for f in gpurun_out/r3c/bench_*.json; do python -c "
+import json,sys; d=json.loads(open('$f').read().strip().splitlines()[-1]); print('$f', d['value'], d['kernel_us'], 'flushed', d.get('p50_flushed_step_us'), 'span', d.get('p50_kernel_span_us'), 'e2e', d['e2e']['value'], 'roof', d['roofline']['frac'], 'cpu', d.get('cpu_baseline',{}).get('value'), 'clk', d['clocks']['sm_mhz'], d['clocks']['reasons'])" 2>&1 | tail -1; done
+for f in gpurun_out/r3c/ref_*.json; do python -c "
+import json,sys; d=json.loads(open('$f').read().strip().splitlines()[-1]); print('$f', d['value'], d['cpu_baseline']['cores'], d['reference_live'].get('value'))" 2>&1 | tail -1; done
+TXB200_LIB=$PWD/paper_2510_27656_b200/libtxb200_checked.so timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/r3c/pytest_checked.log 2>&1; echo "rc=$?" >> gpurun_out/r3c/pytest_checked.log; tail -3 gpurun_out/r3c/pytest_checked.log
