@@ -341,6 +341,14 @@ def run_b200(a) -> None:
                 flush_buf.view(torch.int32).amax()
 
     flush = _Flush(a.flush)
+
+    def mark(name: str) -> None:
+        """TXB_BENCH_TRACE=1: sync and name the phase (device printf of a
+        checked build lands between the marks)."""
+        if os.environ.get("TXB_BENCH_TRACE"):
+            torch.cuda.synchronize()
+            print(f"[mark] rank {rank} {name} err={rk.status()[0]:#x}", flush=True)
+
     stream = torch.cuda.Stream(dev)          # graphs capture on a non-default stream
     torch.cuda.set_stream(stream)
 
@@ -355,6 +363,7 @@ def run_b200(a) -> None:
     torch.cuda.synchronize()
     err, _ = rk.status()
     assert err == 0, f"device error word {err:#x} during warm-up"
+    mark("warm-up")
 
     # The step is launch-only and keeps all per-step state on the device
     # (step counter, counter targets), so it is captured once into a CUDA
@@ -386,6 +395,7 @@ def run_b200(a) -> None:
         graph.replay()
         graph_k.replay()
     torch.cuda.synchronize()
+    mark("graph warm-up")
 
     # -------- timed: L2 flush + barrier outside the span, one step at a time
     K = a.steps
@@ -417,8 +427,10 @@ def run_b200(a) -> None:
     tot, tot_launch = run(K, True, graph)[:2]
     other = "write" if a.flush == "write+read" else "write+read"
     flush.mode = other
+    mark("flushed")
     tot_other = run(max(20, K // 2), True, graph)[0]
     flush.mode = a.flush
+    mark("flushed other")
 
     # the same step launched eagerly (no graph): the L2 flush keeps the GPU
     # busy while the host enqueues the step, so the event span is device
@@ -438,6 +450,7 @@ def run_b200(a) -> None:
         return _max_over_ranks(t, world)
 
     eager = run_eager(max(20, K // 2))
+    mark("eager")
 
 
     # back-to-back steps: B steps per graph, step i on input set i % S of a
@@ -464,6 +477,7 @@ def run_b200(a) -> None:
     for i in range(S):
         pool_step(i)
     torch.cuda.synchronize()
+    mark("pool eager")
     graph_b = torch.cuda.CUDAGraph()
     with torch.cuda.graph(graph_b, stream=stream):
         for i in range(B):
@@ -481,6 +495,7 @@ def run_b200(a) -> None:
         torch.cuda.synchronize()
         blocks.append(eo[0].elapsed_time(eo[1]) * 1e3 / B)
     block = _max_over_ranks(blocks, world)
+    mark("back to back")
 
     # kernel span on the device clock: first dispatch CTA start -> last
     # combine CTA end (%globaltimer phase stamps, one graph with stamps on)
@@ -510,9 +525,12 @@ def run_b200(a) -> None:
     kspan = _max_over_ranks(spans, world)
     kd_span = _max_over_ranks(kd_span, world)
     kc_span = _max_over_ranks(kc_span, world)
+    mark("stamped")
     # L2-warm steps (no flush between; SURVEY.md §8d asks for both numbers)
     b2b = run(max(20, K // 2), False, graph)[0]
+    mark("b2b")
     kdisp = run(max(20, K // 2), True, graph_k)[2]
+    mark("split")
     clk = clocks.stop()
     err, _ = rk.status()
     assert err == 0, f"device error word {err:#x}"
@@ -525,6 +543,7 @@ def run_b200(a) -> None:
 
     # -------- e2e through the public API with pinned host buffers
     e2e = e2e_times(rk, x, routes, w, stream, flush, dev, K, world)
+    mark("e2e")
 
     # -------- bytes / roofline
     ex = expected_rows(wl, rank, n_gpu, tokens)

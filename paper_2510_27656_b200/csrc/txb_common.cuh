@@ -125,8 +125,18 @@ static inline unsigned int read_check_fail() {
                  (int)blockIdx.x, (int)threadIdx.x, #cond),                                   \
           false)                                                                              \
        : true)
+// TXB_ASSERT_V: the same, printing up to four integer values of the site
+#define TXB_ASSERT_V(cond, a, b, c, d)                                                        \
+  (__builtin_expect(!(cond), 0)                                                               \
+       ? (atomicOr(&::txb::g_txb_check_fail, 1u),                                             \
+          printf("txb check failed %s:%d block %d thread %d: %s [%lld %lld %lld %lld]\n",     \
+                 __FILE__, __LINE__, (int)blockIdx.x, (int)threadIdx.x, #cond, (long long)(a), \
+                 (long long)(b), (long long)(c), (long long)(d)),                             \
+          false)                                                                              \
+       : true)
 #else
 #define TXB_ASSERT(cond) true
+#define TXB_ASSERT_V(cond, a, b, c, d) true
 #endif
 
 // ------------------------------------------------------------ PTX wrappers

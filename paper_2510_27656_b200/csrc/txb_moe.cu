@@ -1178,11 +1178,20 @@ __device__ __forceinline__ void recv_tables_body(const txb_moe_shape& s, const u
   }
   g.sync();
   if (tid < 32) {
-    int v = 0;
+    int v = 0, r = 0;
     #pragma unroll 1
-    for (int q = tid; q < N; q += 32) v += t.take[q];
-    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (tid == 0) t.take[N] = v;
+    for (int q = tid; q < N; q += 32) {
+      v += t.take[q];
+      r += t.asg[q];
+    }
+    for (int o = 16; o; o >>= 1) {
+      v += __shfl_xor_sync(0xffffffffu, v, o);
+      r += __shfl_xor_sync(0xffffffffu, r, o);
+    }
+    if (tid == 0) {
+      t.take[N] = v;
+      t.tot[1] = r;  // recv_total: every copy routed to this rank
+    }
   }
   stamp(b, 16);
   #pragma unroll 1
@@ -1204,13 +1213,15 @@ __device__ __forceinline__ void recv_tables_body(const txb_moe_shape& s, const u
   // total) recv_start[me][q] + sum_{le'<le} a[q][le'] (moe.py:178-184, 204-213)
   const int all = block_scan<INL>(t.gstart, L + N * L, sh.tmp, g);
   stamp(b, 18);
-  const int padded_total = N * L ? t.rowbase[0] : all;
+  // the padded total is what the scan adds before the counts part; taken
+  // from the totals, not from rowbase[0], which thread 0 rewrites in the
+  // loop below while slower warps could still be reading it (a race the
+  // checked build caught at EP=2 in round 2: a whole warp's rowbase came
+  // out unshifted and its return slots ran past comb_rows)
+  const int padded_total = all - t.tot[1];
   #pragma unroll 1
   for (int i = tid; i < N * L; i += nt) t.rowbase[i] -= padded_total;
-  if (tid == 0) {
-    t.tot[0] = padded_total;
-    t.tot[1] = all - padded_total;
-  }
+  if (tid == 0) t.tot[0] = padded_total;
   g.sync();
   #pragma unroll 1
   for (int i = tid; i < N * L; i += nt) t.retbase[i] = t.pre_all[i / L] + (t.rowbase[i] - t.rowbase[(i / L) * L]);
@@ -1566,7 +1577,7 @@ __device__ void combine_send_rows(const txb_moe_shape& s, Flags* f, const uint8_
       const int q = (int)sources[g];
       const int64_t nb = Pc;
       const uint8_t* src = out + (int64_t)g * ld;
-      if (!TXB_ASSERT(q >= 0 && q < N && ret[g] >= 0 && ret[g] < s.comb_rows)) continue;
+      if (!TXB_ASSERT_V(q >= 0 && q < N && ret[g] >= 0 && ret[g] < s.comb_rows, r, total, g, ((int64_t)q << 32) | (uint32_t)ret[g])) continue;
       uint8_t* dst = comb_of(peers[q], s) + (int64_t)ret[g] * Pc;
       if (vec) {
         const int4* sv = reinterpret_cast<const int4*>(src);
@@ -1609,7 +1620,7 @@ __device__ void combine_send_rows(const txb_moe_shape& s, Flags* f, const uint8_
       const int g = send_list[r];
       const int q = (int)sources[g];
       const int4* src = reinterpret_cast<const int4*>(out + (int64_t)g * ld + (int64_t)c * kChunk);
-      if (!TXB_ASSERT(q >= 0 && q < N && ret[g] >= 0 && ret[g] < s.comb_rows)) continue;
+      if (!TXB_ASSERT_V(q >= 0 && q < N && ret[g] >= 0 && ret[g] < s.comb_rows, r, total, g, ((int64_t)q << 32) | (uint32_t)ret[g])) continue;
       int4* dst = reinterpret_cast<int4*>(comb_of(peers[q], s) + (int64_t)ret[g] * Pc + (int64_t)c * kChunk);
       const int n16 = (int)(min((int64_t)kChunk, Pc - (int64_t)c * kChunk) >> 4);
       int4 v[kChunk / 512];
@@ -1627,7 +1638,7 @@ __device__ void combine_send_rows(const txb_moe_shape& s, Flags* f, const uint8_
   for (int r = cta * nwarp + warp; r < total; r += ncta * nwarp) {
     const int g = send_list[r];
     const int q = (int)sources[g];
-    if (!TXB_ASSERT(q >= 0 && q < N && ret[g] >= 0 && ret[g] < s.comb_rows)) continue;
+    if (!TXB_ASSERT_V(q >= 0 && q < N && ret[g] >= 0 && ret[g] < s.comb_rows, r, total, g, ((int64_t)q << 32) | (uint32_t)ret[g])) continue;
     copy_row(comb_of(peers[q], s) + (int64_t)ret[g] * Pc, out + (int64_t)g * ld, Pc, lane, 32);
     if (lane == 0) atomicAdd(&sh.cnt[q], (uint32_t)comb_chunks(s));
   }

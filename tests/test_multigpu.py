@@ -133,11 +133,38 @@ def test_torchrun_ipc_bench_smoke(ranks, config, tmp_path):
            "--gpus", str(ranks), "--steps", "60", "--warmup", "3", "--no-cpu-baseline"]
     env = dict(os.environ)
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
+    assert "txb check failed" not in p.stdout, p.stdout[:4000]
     assert p.returncode == 0, p.stderr[-4000:]
     import json
     line = [x for x in p.stdout.splitlines() if x.startswith("{")][-1]
     d = json.loads(line)
     assert d["n_gpus"] == ranks and d["value"] > 0
+
+
+CHECKED_LIB = ROOT / "paper_2510_27656_b200" / "libtxb200_checked.so"
+
+
+@pytest.mark.parametrize("ranks", [2, 4])
+def test_torchrun_bench_checked_build(ranks):
+    """The bench under torchrun on the bounds-checked library, three times:
+    no device-side check may fire.  This is the run that caught the
+    receive-table race of round 2 (recv_tables_body read rowbase[0] while
+    thread 0 rewrote it; a warp's return slots then ran past comb_rows):
+    one torchrun bench in four tripped it at EP=2, none in twelve after the
+    fix (profiles/r02/README.md)."""
+    if NGPU < ranks:
+        pytest.skip(f"needs {ranks} GPUs")
+    if not CHECKED_LIB.exists():
+        pytest.skip("libtxb200_checked.so not built (make checked)")
+    env = dict(os.environ, TXB200_LIB=str(CHECKED_LIB))
+    for rep in range(3):
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={ranks}",
+               "--master-addr", "127.0.0.1", "--master-port", str(29571 + 4 * rep + ranks),
+               str(ROOT / "bench.py"), "--config", "decode",
+               "--gpus", str(ranks), "--steps", "60", "--warmup", "3", "--no-cpu-baseline"]
+        p = subprocess.run(cmd, capture_output=True, text=True, timeout=300, env=env)
+        assert "txb check failed" not in p.stdout, f"run {rep}: " + p.stdout[:4000]
+        assert p.returncode == 0, f"run {rep}: " + p.stderr[-4000:]
 
 
 @pytest.mark.parametrize("ranks", [2, 4])
