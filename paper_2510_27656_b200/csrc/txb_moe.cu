@@ -115,7 +115,9 @@ __host__ __device__ inline size_t solo_recv_offset(const txb_moe_shape& s, int64
 }
 
 struct Shared {  // static shared state of one CTA
-  uint32_t bad, fail, recv_me, direct;
+  uint32_t bad, fail, lfail, recv_me, direct;  // lfail: dispatch_layout's own flag (it follows wait_routes
+                                               // with no barrier between: a shared flag would be reset
+                                               // while slow threads still read wait_routes' result)
   int tmp[33];
   float red[33];
   uint32_t cnt[TXB_MAX_RANKS];   // rows stored per destination (token / combine counter)
@@ -495,7 +497,9 @@ __device__ void route_positions(const txb_moe_shape& s, const int64_t* routes, i
 // Route-row scatter: own counts into row `me` of every rank's matrix as
 // (step tag << 32 | count) words -- single-copy atomic, so no fence.  Every
 // CTA holds the full histogram; CTA `part` of `nparts` stores its slice.
-// Part 0 also books the copies that will come back from other ranks.
+// The last part also books the copies that will come back from other ranks
+// (read-modify-writes of the flags, a few serial round trips): in a decode
+// step the last CTA has no token (n < grid), so the booking delays no row.
 __device__ void route_publish(const txb_moe_shape& s, void* const* peers, Flags* f, const uint32_t* hist,
                               uint64_t step, int64_t n, uint32_t bad, int part, int nparts,
                               const Grp& g = Grp::cta()) {
@@ -514,7 +518,7 @@ __device__ void route_publish(const txb_moe_shape& s, void* const* peers, Flags*
     if (N == 1) *(route_of(peers[d], s, slot) + (size_t)s.me * E + e) = tag | hist[e];
     else st_relaxed_sys(route_of(peers[d], s, slot) + (size_t)s.me * E + e, tag | hist[e]);
   }
-  if (part == 0 && g.tid < 32) {
+  if (part == nparts - 1 && g.tid < 32) {
     // copies this rank serves itself do not come back through the counter
     const int lane = g.tid;
     uint32_t self = 0;
@@ -613,7 +617,7 @@ __device__ bool wait_routes(const txb_moe_shape& s, Flags* f, const uint64_t* C,
 __device__ bool dispatch_layout(const txb_moe_shape& s, const uint32_t* C, int* baseg, int* padded, Flags* f,
                                 Shared& sh) {
   const int N = s.ranks, E = s.experts, L = s.local_experts, tid = threadIdx.x;
-  if (tid == 0) sh.fail = 0;
+  if (tid == 0) sh.lfail = 0;
   for (int d = tid; d < N; d += blockDim.x) {
     int a = 0;
     for (int le = 0; le < L; ++le) a += (int)C[s.me * E + d * L + le];
@@ -644,9 +648,9 @@ __device__ bool dispatch_layout(const txb_moe_shape& s, const uint32_t* C, int* 
   __syncthreads();
   for (int e = tid; e < E; e += blockDim.x) baseg[e] += padded[e] - padded[(e / L) * L];
   for (int d = tid; d < N; d += blockDim.x)
-    if (padded[(d + 1) * L] - padded[d * L] > s.grouped_rows) atomicOr(&sh.fail, TXB_EV_CAPACITY);
+    if (padded[(d + 1) * L] - padded[d * L] > s.grouped_rows) atomicOr(&sh.lfail, TXB_EV_CAPACITY);
   __syncthreads();
-  const uint32_t fl = sh.fail;
+  const uint32_t fl = sh.lfail;
   if (fl) {
     if (tid == 0) atomicOr(&f->err, fl);
     return false;
@@ -2043,6 +2047,9 @@ k_dispatch_roles(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
   Flags* f = flags_of(b.region, s);
   const uint64_t step = cur_step(f);
   const int cta = blockIdx.x, ncta = gridDim.x;
+  // the CTA that books the step's counter targets and waits for the tokens:
+  // the last one, which holds no token in a decode step (n < grid)
+  const int bk = ncta - 1;
   uint32_t* hist = reinterpret_cast<uint32_t*>(dsm);
   uint32_t* C = reinterpret_cast<uint32_t*>(dsm + cmat_offset(s));
   int* rt = reinterpret_cast<int*>(dsm + recv_offset(s));
@@ -2126,7 +2133,7 @@ k_dispatch_roles(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
     stamp(b, 15);
     if (ok) {
       recv_tables_body<true>(s, Cm, rt, b.info, cta, sh, b, rg);
-      if (!solo && cta == 0 && rg.tid < 32) book_recv(s, f, Cm, rg.tid);
+      if (!solo && cta == bk && rg.tid < 32) book_recv(s, f, Cm, rg.tid);
       stamp(b, 4);
       // receive metadata while the token role's stores drain, then the
       // private rows that arrived before the layout was known
@@ -2137,7 +2144,7 @@ k_dispatch_roles(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
   }
   __syncthreads();  // stores issued, receive tables and rows built
   if (fail) {
-    if (cta == 0) publish_err(f, b.info, s.local_experts);
+    if (cta == bk) publish_err(f, b.info, s.local_experts);
     return;
   }
   stamp(b, 5);
@@ -2147,7 +2154,7 @@ k_dispatch_roles(txb_moe_shape s, txb_moe_bufs b, const void* __restrict__ x, in
   recv_private_rows(s, rt, b.region, step, timeout_ns, cta * (kThreads >> 5) + (threadIdx.x >> 5),
                     ncta * (kThreads >> 5), threadIdx.x & 31);
   stamp(b, 6);
-  if (cta == 0) {
+  if (cta == bk) {
     if (!solo) wait_tokens(f, b.info, s.local_experts, timeout_ns);
     else publish_err(f, b.info, s.local_experts);
   }

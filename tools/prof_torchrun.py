@@ -98,6 +98,7 @@ else:
     run = g.replay
 rows = []
 detail = []
+lastcta = []
 ORDER = [0, 19, 22, 27, 28, 24, 25, 14, 1, 2, 26, 3, 15, 20, 16, 17, 18, 4, 7, 5, 6, 8, 9, 10, 11, 23, 12, 13]
 STAMP = {27: "dups checked", 28: "ids synced", 26: "priv stored", 24: "seg prefix", 25: "seg sync2", 0: "start", 19: "own routes in", 22: "hist done", 14: "counted(+loads)", 1: "encoded", 2: "published+pos", 3: "routes-in", 15: "dests",
          5: "joined", 20: "tok stored", 16: "T:loaded", 17: "T:srcpre", 18: "T:scan", 4: "tables", 6: "signalled", 7: "metadata", 8: "tokens-in", 9: "c:start", 10: "c:sent",
@@ -130,11 +131,13 @@ for k in range(a.reps + 5):
         v = p[:, i][p[:, i] > 0]
         return (v.max() - base) / 1e3 if v.size else np.nan
 
-    det = []
+    det, amax = [], []
     for kk in ORDER:
         v = p[:, kk][p[:, kk] > 0]
         det.append(((np.median(v) - base) / 1e3, (v.max() - base) / 1e3) if v.size else (np.nan, np.nan))
+        amax.append(int(np.argmax(p[:, kk])) if v.size else -1)
     detail.append(det)
+    lastcta.append(amax)
     rows.append([e0.elapsed_time(e1) * 1e3, (t[2] - base) / 1e3, lo(0), hi(3), hi(8), lo(9), hi(11), hi(13),
                  (t[1] - base) / 1e3, (t[3] - base) / 1e3 if a.mid else np.nan])
 med = np.median(np.asarray(rows), axis=0).tolist()
@@ -147,7 +150,17 @@ if world > 1:
 else:
     allr = [mine]
 dmed = np.nanmedian(np.asarray(detail), axis=0)
-lines = [f"  {STAMP[k]:16s} median CTA {m:7.2f}  last CTA {x:7.2f}" for k, (m, x) in zip(ORDER, dmed.tolist())]
+lc = np.asarray(lastcta)
+
+
+def _mode(col):
+    vals, cnt = np.unique(col, return_counts=True)
+    return int(vals[np.argmax(cnt)]), int(cnt.max())
+
+
+lines = [f"  {STAMP[k]:16s} median CTA {m:7.2f}  last CTA {x:7.2f}  (last is CTA {_mode(lc[:, i])[0]:>3} "
+         f"in {_mode(lc[:, i])[1]}/{lc.shape[0]} reps)"
+         for i, (k, (m, x)) in enumerate(zip(ORDER, dmed.tolist()))]
 alld = [None] * world
 if world > 1:
     dist.all_gather_object(alld, lines)
