@@ -86,5 +86,20 @@ int main() {
            nb / (std::min(std::min(a, b), std::min(c, e)) * 1e-6) / 1e9);
     cudaFree(s); cudaSetDevice(peer); cudaFree(d); cudaSetDevice(0);
   }
+  // grid-size sweep: is the peer-write rate set per SM (store injection)?
+  printf("# grid sweep, 16Bx4, 512 threads per CTA, us (median of 20)\n%12s", "bytes");
+  const int grids[] = {32, 64, 96, 128, 148, 296};
+  for (int g : grids) printf(" %9d", g);
+  printf("\n");
+  for (size_t nb : {(size_t)3784704, (size_t)67108864}) {
+    uint8_t *s, *d;
+    cudaSetDevice(0); cudaMalloc(&s, nb); cudaMemset(s, 3, nb);
+    cudaSetDevice(peer); cudaMalloc(&d, nb);
+    cudaSetDevice(0);
+    printf("%12zu", nb);
+    for (int g : grids) printf(" %9.2f", timed([&] { copy<16, 4><<<g, 512, 0, st>>>(s, d, nb); }, st));
+    printf("\n");
+    cudaFree(s); cudaSetDevice(peer); cudaFree(d); cudaSetDevice(0);
+  }
   return 0;
 }
