@@ -60,6 +60,43 @@ __global__ void spin_peer(long long ns, uint4* peer, long long gap) {
 static uint4* g_keep = nullptr;
 static long long g_gap = 0;
 
+// the dispatch token role's shape: 256 threads hold the row as two 16-byte
+// chunks each; the CTA stores `rpc` remote and `lpc` local rows (local HBM)
+__global__ void __launch_bounds__(512, 1) rows2(const uint8_t* __restrict__ src, uint8_t* dst, uint8_t* ldst,
+                                                const int* perm, int rpc, int lpc, int row_bytes,
+                                                unsigned long long* ctr, unsigned long long* span, int mode = 2,
+                                                unsigned long long* lctr = nullptr) {
+  const int n16 = row_bytes / 16, t = threadIdx.x - 256;
+  unsigned long long g0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
+  if (t >= 0) {
+    uint4 v[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+    for (int u = 0; u < 2; ++u)
+      if (t + 256 * u < n16) v[u] = reinterpret_cast<const uint4*>(src + (size_t)blockIdx.x * row_bytes)[t + 256 * u];
+    for (int u = 0; u < 2; ++u)
+      if (t + 256 * u < n16)
+        for (int k = 0; k < rpc + lpc; ++k) {
+          const int r = perm[blockIdx.x * 8 + k];
+          uint8_t* base = k < rpc ? dst : ldst;
+          *reinterpret_cast<uint4*>(base + (size_t)r * row_bytes + 16 * (t + 256 * u)) = v[u];
+        }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (mode >= 1) asm volatile("fence.acq_rel.sys;" ::: "memory");
+    if (mode >= 2) asm volatile("red.relaxed.sys.global.add.u64 [%0], 1;" :: "l"(ctr) : "memory");
+    if (mode >= 3) {
+      asm volatile("red.relaxed.sys.global.add.u64 [%0], 1;" :: "l"(ctr + 1) : "memory");
+      asm volatile("red.relaxed.sys.global.add.u64 [%0], 1;" :: "l"(lctr) : "memory");
+      asm volatile("red.relaxed.sys.global.add.u64 [%0], 1;" :: "l"(lctr + 1) : "memory");
+    }
+    unsigned long long g1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
+    span[2 * blockIdx.x] = g0;
+    span[2 * blockIdx.x + 1] = g1;
+  }
+}
+
 template <typename F>
 static float timed(F launch, cudaStream_t st) {
   std::vector<float> ts;
@@ -168,6 +205,41 @@ int main() {
       }
       std::sort(s0.begin(), s0.end()); std::sort(s1.begin(), s1.end());
       printf("%4d %9.2f %9.2f %9.2f\n", rpc, (double)T * rpc * 7392 / 1e6, s0[10], s1[10]);
+    }
+    // the dispatch's mix: 256 threads x 2 chunks, 4 remote + 4 local rows per CTA, both directions
+    uint8_t* loc0; cudaMalloc(&loc0, (size_t)T * 8 * 8192);
+    cudaSetDevice(1); uint8_t* loc1; cudaMalloc(&loc1, (size_t)T * 8 * 8192); cudaSetDevice(0);
+    printf("## dispatch mix (256 thr x 2 chunks, rpc remote + lpc local rows per CTA, both directions); mode 0 no fence, 1 fence.sys, 2 + 1 remote red, 3 + 2 remote + 2 local reds\n");
+    printf("%4s %4s %4s %9s %9s\n", "mode", "rpc", "lpc", "span0_us", "span1_us");
+    unsigned long long* lc0; cudaMalloc(&lc0, 64);
+    cudaSetDevice(1); unsigned long long* lc1; cudaMalloc(&lc1, 64); cudaSetDevice(0);
+    for (int mode : {0, 1, 2, 3})
+    for (int rl : {44, 80}) {
+      const int rpc = rl / 10, lpc = rl % 10;
+      std::vector<int> h(T * 8);
+      for (int c = 0; c < T; ++c) for (int k = 0; k < 8; ++k) h[c * 8 + k] = k < rpc ? c * rpc + k : c * 8 + k;
+      // remote slots shuffled
+      cudaMemcpy(perm, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice);
+      cudaSetDevice(1); cudaMemcpy(perm1, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice); cudaSetDevice(0);
+      std::vector<double> s0, s1;
+      for (int k = 0; k < 20; ++k) {
+        cudaSetDevice(0); spin_peer<<<1, 1, 0, st>>>(200000, nullptr, 0);
+        cudaSetDevice(1); spin_peer<<<1, 1, 0, st1>>>(200000, nullptr, 0);
+        cudaSetDevice(0); rows2<<<T, 512, 0, st>>>(src, dst, loc0, perm, rpc, lpc, 7392, ctr, span, mode, lc0);
+        cudaSetDevice(1); rows2<<<T, 512, 0, st1>>>(src1, dst0, loc1, perm1, rpc, lpc, 7392, ctr0, span1, mode, lc1);
+        cudaStreamSynchronize(st1); cudaSetDevice(0); cudaStreamSynchronize(st);
+        for (int g = 0; g < 2; ++g) {
+          std::vector<unsigned long long> hh(2 * T);
+          if (g) cudaSetDevice(1);
+          cudaMemcpy(hh.data(), g ? span1 : span, 2 * T * 8, cudaMemcpyDeviceToHost);
+          cudaSetDevice(0);
+          unsigned long long a = ~0ull, b = 0;
+          for (int c = 0; c < T; ++c) { a = std::min(a, hh[2 * c]); b = std::max(b, hh[2 * c + 1]); }
+          (g ? s1 : s0).push_back((b - a) / 1e3);
+        }
+      }
+      std::sort(s0.begin(), s0.end()); std::sort(s1.begin(), s1.end());
+      printf("%4d %4d %4d %9.2f %9.2f   (max CTA end, us; p90 %.2f)\n", mode, rpc, lpc, s0[10], s1[10], s0[18]);
     }
   }
   return 0;

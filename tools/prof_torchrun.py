@@ -33,6 +33,7 @@ ap.add_argument("--noflush", action="store_true")
 ap.add_argument("--mid", action="store_true", help="a %globaltimer kernel between dispatch and combine")
 ap.add_argument("--sleep", type=int, default=0, help="GPU sleep cycles queued before the graph (host runs ahead)")
 ap.add_argument("--private", type=int, default=None, help="PrivateBufferConfig.tokens")
+ap.add_argument("--cta", type=int, nargs="*", default=[], help="also print these CTAs' own stamps")
 a = ap.parse_args()
 
 world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -99,6 +100,7 @@ else:
 rows = []
 detail = []
 lastcta = []
+ctarows = []
 ORDER = [0, 19, 22, 27, 28, 24, 25, 14, 1, 2, 26, 3, 15, 20, 16, 17, 18, 4, 7, 5, 6, 8, 9, 10, 11, 23, 12, 13]
 STAMP = {27: "dups checked", 28: "ids synced", 26: "priv stored", 24: "seg prefix", 25: "seg sync2", 0: "start", 19: "own routes in", 22: "hist done", 14: "counted(+loads)", 1: "encoded", 2: "published+pos", 3: "routes-in", 15: "dests",
          5: "joined", 20: "tok stored", 16: "T:loaded", 17: "T:srcpre", 18: "T:scan", 4: "tables", 6: "signalled", 7: "metadata", 8: "tokens-in", 9: "c:start", 10: "c:sent",
@@ -138,6 +140,7 @@ for k in range(a.reps + 5):
         amax.append(int(np.argmax(p[:, kk])) if v.size else -1)
     detail.append(det)
     lastcta.append(amax)
+    ctarows.append([[(p[c, kk] - base) / 1e3 if p[c, kk] > 0 else np.nan for kk in ORDER] for c in a.cta])
     rows.append([e0.elapsed_time(e1) * 1e3, (t[2] - base) / 1e3, lo(0), hi(3), hi(8), lo(9), hi(11), hi(13),
                  (t[1] - base) / 1e3, (t[3] - base) / 1e3 if a.mid else np.nan])
 med = np.median(np.asarray(rows), axis=0).tolist()
@@ -161,6 +164,11 @@ def _mode(col):
 lines = [f"  {STAMP[k]:16s} median CTA {m:7.2f}  last CTA {x:7.2f}  (last is CTA {_mode(lc[:, i])[0]:>3} "
          f"in {_mode(lc[:, i])[1]}/{lc.shape[0]} reps)"
          for i, (k, (m, x)) in enumerate(zip(ORDER, dmed.tolist()))]
+if a.cta:
+    cm = np.nanmedian(np.asarray(ctarows), axis=0)  # [len(cta)][ORDER]
+    for ci, c in enumerate(a.cta):
+        lines.append(f"  -- CTA {c}: " + ", ".join(f"{STAMP[k]} {v:.2f}" for k, v in zip(ORDER, cm[ci].tolist())
+                                                 if not np.isnan(v)))
 alld = [None] * world
 if world > 1:
     dist.all_gather_object(alld, lines)
