@@ -244,6 +244,11 @@ int txb_imm_table_slots(void);
  * up (*out_slot = -1 when absent).  Synchronous, on a private stream; the
  * caller caches the slot. */
 int txb_imm_slot(uint64_t* table, uint32_t imm, int insert, int64_t* out_slot);
+/* Current values of n (<= 64) device words, e.g. ImmCounter receipt
+ * counters (ImmCounterTable.received_total, engine.py:197-205): one
+ * device-to-host copy each on a private non-blocking stream, so a poll never
+ * waits behind kernels spinning on other streams. */
+int txb_read_u64(const uint64_t* const* ptrs, int n, uint64_t* out);
 /* Move the pages and release one increment on *imm_ctr (engine.py:480-508, 759-782). */
 int txb_copy_pages(const txb_pages* job, int grid, void* stream);
 /* 1..TXB_MAX_JOBS writes in ONE launch (submit_scatter's per-peer slices,

@@ -127,6 +127,7 @@ SIGNATURES: dict[str, list] = {
     "txb_copy_jobs": [C.POINTER(Pages), _INT, _INT, _VP],
     "txb_kv_stream": [C.POINTER(StreamJob), _INT, _VP],
     "txb_imm_slot": [_VP, C.c_uint32, _INT, C.POINTER(_I64)],
+    "txb_read_u64": [_VP, _INT, _VP],
     "txb_stream_write_value64": [_VP, _U64, _VP],
     "txb_stream_wait_value64": [_VP, _U64, _U64, _VP, _VP],
     "txb_imm_add": [_VP, _INT, _U64, _INT, _VP],

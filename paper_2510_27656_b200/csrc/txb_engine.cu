@@ -564,6 +564,27 @@ int txb_kv_stream(const txb_stream_job* ks, int grid, void* stream) {
   return TXB_OK;
 }
 
+int txb_read_u64(const uint64_t* const* ptrs, int n, uint64_t* out) {
+  if (n <= 0) return TXB_OK;
+  if (!ptrs || !out || n > 64) {
+    set_error("txb_read_u64: null arguments or more than 64 words");
+    return TXB_ERR_TRANSFER;
+  }
+  DeviceFor on_dev(nullptr, ptrs[0]);
+  static thread_local cudaStream_t side[64] = {nullptr};
+  static thread_local uint64_t* host[64] = {nullptr};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int d = dev >= 0 && dev < 64 ? dev : 0;
+  if (!side[d]) TXB_CUDA(cudaStreamCreateWithFlags(&side[d], cudaStreamNonBlocking));
+  if (!host[d]) TXB_CUDA(cudaHostAlloc(&host[d], 64 * sizeof(uint64_t), cudaHostAllocPortable));
+  for (int i = 0; i < n; ++i)
+    TXB_CUDA(cudaMemcpyAsync(host[d] + i, ptrs[i], sizeof(uint64_t), cudaMemcpyDeviceToHost, side[d]));
+  TXB_CUDA(cudaStreamSynchronize(side[d]));
+  for (int i = 0; i < n; ++i) out[i] = host[d][i];
+  return TXB_OK;
+}
+
 int txb_imm_slot(uint64_t* table, uint32_t imm, int insert, int64_t* out_slot) {
   if (!table || !out_slot) {
     set_error("txb_imm_slot: null table or output");
