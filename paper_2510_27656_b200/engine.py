@@ -469,6 +469,7 @@ class TransferEngine:
         self._closed = False
         self._imm = None           # lazily: ImmCounter table region
         self._stream = None
+        self._order_tl = threading.local()
         self._consumed: dict[int, int] = {}
         self._armed: dict[int, ImmFlag] = {}
         self._groups: dict[int, tuple] = {}
@@ -648,6 +649,17 @@ class TransferEngine:
                 self.trace.record("wr_post", transfer=op, dst=dst)
         return op
 
+    def _after_current(self) -> None:
+        """Order the engine stream after the caller's current stream (where
+        the payload was produced): one reused event per calling thread
+        instead of wait_stream's fresh one."""
+        tl = self._order_tl
+        ev = getattr(tl, "ev", None)
+        if ev is None:
+            ev = tl.ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(self.device))
+        self._stream.wait_event(ev)
+
     def _launch_pages(self, src_base: int, src_pages: Pages, desc: MrDesc, dst_pages: Pages,
                       page_len: int, npages: int, imm: int | None,
                       idx: tuple | None = None, label: str = "") -> CompletionFlag:
@@ -673,23 +685,25 @@ class TransferEngine:
                                             src_pages.stride, dst_pages.stride, page_len))
         j.use_tma = 1 if aligned and page_len >= 1024 and self.use_tma else 0
         j.single_device = self._single_device(desc)
+        # every call below names its stream: no `with torch.cuda.stream`
+        # (~10 us of host time per launch on this image)
         with torch.cuda.device(self.device):
             # the payload was produced on the caller's stream
-            self._stream.wait_stream(torch.cuda.current_stream(self.device))
-            with torch.cuda.stream(self._stream):
-                for k in keep:
-                    k.record_stream(self._stream)
-                if self.timing is not None:          # bench hook: device time of the copy kernel
+            self._after_current()
+            for k in keep:
+                k.record_stream(self._stream)
+            if self.timing is not None:              # bench hook: device time of the copy kernel
+                with torch.cuda.stream(self._stream):
                     torch.cuda._sleep(200000)         # keep the GPU busy past the host launch
-                    e0 = torch.cuda.Event(enable_timing=True)
-                    e0.record(self._stream)
-                _lib.call("txb_copy_pages", C.byref(j), 0, C.c_void_p(self._stream.cuda_stream))
-                if self.timing is not None:
-                    e1 = torch.cuda.Event(enable_timing=True)
-                    e1.record(self._stream)
-                    self.timing.append((e0, e1))
-                ev = torch.cuda.Event()
-                ev.record(self._stream)
+                e0 = torch.cuda.Event(enable_timing=True)
+                e0.record(self._stream)
+            _lib.call("txb_copy_pages", C.byref(j), 0, C.c_void_p(self._stream.cuda_stream))
+            if self.timing is not None:
+                e1 = torch.cuda.Event(enable_timing=True)
+                e1.record(self._stream)
+                self.timing.append((e0, e1))
+            ev = torch.cuda.Event()
+            ev.record(self._stream)
         return CompletionFlag(ev)
 
     def _launch_jobs(self, jobs: list, label: str = "") -> CompletionFlag:
@@ -716,11 +730,10 @@ class TransferEngine:
                 j.use_tma = 1 if aligned and page_len >= 1024 and self.use_tma else 0
                 j.single_device = self._single_device(desc)
             with torch.cuda.device(self.device):
-                self._stream.wait_stream(torch.cuda.current_stream(self.device))
-                with torch.cuda.stream(self._stream):
-                    _lib.call("txb_copy_jobs", arr, len(chunk), 0, C.c_void_p(self._stream.cuda_stream))
-                    ev = torch.cuda.Event()
-                    ev.record(self._stream)
+                self._after_current()
+                _lib.call("txb_copy_jobs", arr, len(chunk), 0, C.c_void_p(self._stream.cuda_stream))
+                ev = torch.cuda.Event()
+                ev.record(self._stream)
             out.append(ev)
         return CompletionFlag(out[-1])
 
@@ -838,13 +851,12 @@ class TransferEngine:
         tab = torch.tensor(ptrs, dtype=torch.int64).to(dev, non_blocking=True)
         sd = 1 if all(self._single_device(d) for d, _ in dsts) else 0
         with torch.cuda.device(self.device):
-            self._stream.wait_stream(torch.cuda.current_stream(self.device))
-            with torch.cuda.stream(self._stream):
-                tab.record_stream(self._stream)
-                _lib.call("txb_imm_add", C.c_void_p(tab.data_ptr()), len(ptrs), 1, sd,
-                          C.c_void_p(self._stream.cuda_stream))
-                ev = torch.cuda.Event()
-                ev.record(self._stream)
+            self._after_current()
+            tab.record_stream(self._stream)
+            _lib.call("txb_imm_add", C.c_void_p(tab.data_ptr()), len(ptrs), 1, sd,
+                      C.c_void_p(self._stream.cuda_stream))
+            ev = torch.cuda.Event()
+            ev.record(self._stream)
         return self._done(CompletionFlag(ev), on_done)
 
     def _done(self, flag: CompletionFlag, on_done: Callable | None) -> CompletionFlag:

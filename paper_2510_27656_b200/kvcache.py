@@ -354,11 +354,10 @@ class KvSender:
             eng.post_op(f"kv.{req.request_id}.s{k + 1}", req.kv_desc.owner, L.page_len * nh * L.pages_per_chunk,
                         req.imm)
         with torch.cuda.device(eng.device):
-            eng._stream.wait_stream(torch.cuda.current_stream(eng.device))
-            with torch.cuda.stream(eng._stream):
-                for t in (si_d, di_d, tickets):
-                    t.record_stream(eng._stream)
-                _lib.call("txb_kv_stream", C.byref(j), int(grid), C.c_void_p(eng._stream.cuda_stream))
-                ev = torch.cuda.Event()
-                ev.record(eng._stream)
+            eng._after_current()
+            for t in (si_d, di_d, tickets):
+                t.record_stream(eng._stream)
+            _lib.call("txb_kv_stream", C.byref(j), int(grid), C.c_void_p(eng._stream.cuda_stream))
+            ev = torch.cuda.Event()
+            ev.record(eng._stream)
         return CompletionFlag(ev)
