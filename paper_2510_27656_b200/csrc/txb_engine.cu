@@ -213,14 +213,14 @@ __device__ __forceinline__ bool spin_ge_gpu(const uint64_t* p, uint64_t target, 
 // clock after each layer, no host in the loop -- and the warp that finishes
 // a step last releases one increment on the request's ImmCounter slot.
 //
-// Every warp runs on its own (no CTA barrier): it copies its share of a
-// step and moves on; completion is booked per warp in batches of kBatch
-// steps -- one release fence (which waits for the warp's stores to land)
-// covers the batch, then one ticket increment per step; the warp that
-// brings a step's ticket to the number of warps releases the receipt.  A
-// warp that reaches a step the clock has not released yet books what it
-// has first, so receipts never wait on a future layer.  The fence is the
-// only drain, and no other warp waits for it.
+// Every warp runs on its own (no CTA barrier): the request's pieces are
+// dealt round-robin across steps, and completion is booked per warp in
+// batches of kStreamBatch pieces -- one release fence (which waits for the
+// warp's stores to land) covers the batch, then one ticket increment per
+// piece on its step; the increment that brings a step's ticket to its piece
+// count releases the receipt.  A warp that reaches a step the clock has not
+// released yet books what it has first, so receipts never wait on a future
+// layer.  The fence is the only drain, and no other warp waits for it.
 constexpr int kStreamBatch = 32;
 
 __global__ void __launch_bounds__(kCopyThreads, 1) k_kv_stream(const __grid_constant__ txb_stream_job ks) {
@@ -235,15 +235,35 @@ __global__ void __launch_bounds__(kCopyThreads, 1) k_kv_stream(const __grid_cons
   const uint32_t nwarps = gridDim.x * kCopyWarps;
   const int64_t gw = (int64_t)blockIdx.x * kCopyWarps + warp;
   const uint64_t dl = globaltimer() + ks.timeout_ns;
-  int pend0 = 0, npend = 0;  // steps [pend0, pend0 + npend) copied, not yet booked
-  uint64_t seen = 0;         // clock value this warp has already acquired
+  // The request's pieces are numbered across steps (step k holds pieces
+  // [k*total, (k+1)*total)) and dealt round-robin to the warps, so every
+  // warp stays busy across step boundaries (per step, 1024 pages on 1184
+  // warps left 160 warps idle and every warp re-entered the step loop per
+  // page: 583 GB/s, against 697 for the same scattered pages copied in one
+  // pass -- tools/micro/peer_width.cu).  A step's ticket counts its pieces.
+  const int64_t all = (int64_t)ks.nsteps * total;
+  if (total == 0) {  // steps without pages still release their receipts, in clock order
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+      for (int k = 0; k < ks.nsteps; ++k) {
+        if (!spin_ge_gpu(ks.clock, ks.clock_base + (uint64_t)k + 1, dl)) {
+          if (ks.err) atomicOr(ks.err, TXB_EV_WAIT_IMM);
+          return;
+        }
+        if (ks.imm_ctr) red_relaxed_sys_add(ks.imm_ctr, 1);
+      }
+    return;
+  }
+  int64_t pend_q0 = 0;
+  int npend = 0;      // pieces pend_q0, pend_q0 + nwarps, ... copied, not yet booked
+  uint64_t seen = 0;  // clock value this warp has already acquired
   auto book = [&]() {
     if (npend == 0) return;
     if (lane == 0) {
       fence_release(ks.single_device != 0);
-      for (int q = pend0; q < pend0 + npend; ++q) {
-        if (atomicAdd(&ks.tickets[q], 1u) == nwarps - 1) {
-          ks.tickets[q] = 0;
+      for (int i = 0; i < npend; ++i) {
+        const int k = (int)((pend_q0 + (int64_t)i * nwarps) / total);
+        if (atomicAdd(&ks.tickets[k], 1u) == (uint32_t)total - 1) {
+          ks.tickets[k] = 0;
           if (ks.imm_ctr) {
             fence_release(ks.single_device != 0);
             red_relaxed_sys_add(ks.imm_ctr, 1);
@@ -252,17 +272,30 @@ __global__ void __launch_bounds__(kCopyThreads, 1) k_kv_stream(const __grid_cons
       }
     }
     __syncwarp();
-    pend0 += npend;
     npend = 0;
   };
+  // the page indices of a warp's next piece are loaded one piece ahead (a
+  // dependent round trip per 8-KiB piece otherwise)
+  auto idx_of = [&](int64_t q, int64_t& sidx, int64_t& didx) {
+    if (q >= all) return;
+    const int k = (int)(q / total);
+    const int64_t row = (int64_t)k * ks.pages_per_step + (q - (int64_t)k * total) / per_page;
+    sidx = ks.src_idx[row];
+    didx = ks.dst_idx[row];
+  };
+  int64_t s_cur = 0, d_cur = 0;
+  idx_of(gw, s_cur, d_cur);
   #pragma unroll 1
-  for (int k = 0; k < ks.nsteps; ++k) {
+  for (int64_t q = gw; q < all; q += nwarps) {
+    int64_t s_nxt = 0, d_nxt = 0;
+    idx_of(q + nwarps, s_nxt, d_nxt);
+    const int k = (int)(q / total);
     const uint64_t want = ks.clock_base + (uint64_t)k + 1;
     if (seen < want) {  // the clock is read only when the cached value runs out
       uint32_t ok = 1;
       if (lane == 0) {
         seen = ld_acquire_gpu(ks.clock);
-        if (seen < want) ok = 2;  // not released yet: book the finished steps before waiting
+        if (seen < want) ok = 2;  // not released yet: book the finished pieces before waiting
       }
       ok = __shfl_sync(0xffffffffu, ok, 0);
       if (ok == 2) {
@@ -277,20 +310,23 @@ __global__ void __launch_bounds__(kCopyThreads, 1) k_kv_stream(const __grid_cons
       }
       seen = __shfl_sync(0xffffffffu, seen, 0);
     }
-    const int64_t* si = ks.src_idx + (int64_t)k * ks.pages_per_step;
-    const int64_t* di = ks.dst_idx + (int64_t)k * ks.pages_per_step;
-    auto piece = [&](int64_t q) {
-      const int64_t page = q / per_page, pc = q - page * per_page;
-      const int64_t off = pc * kPiece, rem = ks.page_len - off;
-      PieceRef p;
-      p.src = reinterpret_cast<const uint8_t*>(ks.src) + si[page] * ks.page_len + off;
-      p.dst = reinterpret_cast<uint8_t*>(ks.dst) + di[page] * ks.page_len + off;
-      p.bytes = (uint32_t)(rem < kPiece ? rem : kPiece);
-      return p;
-    };
-    warp_copy_range(gw, (int64_t)nwarps, total, tma, stage + (size_t)warp * kWarpStages * kPiece,
-                    bars + warp * kWarpStages, phase, piece);
+    const int64_t qs = q - (int64_t)k * total;
+    const int64_t pc = qs % per_page;
+    const int64_t off = pc * kPiece, rem = ks.page_len - off;
+    PieceRef p;
+    p.src = reinterpret_cast<const uint8_t*>(ks.src) + s_cur * ks.page_len + off;
+    p.dst = reinterpret_cast<uint8_t*>(ks.dst) + d_cur * ks.page_len + off;
+    p.bytes = (uint32_t)(rem < kPiece ? rem : kPiece);
+    s_cur = s_nxt;
+    d_cur = d_nxt;
+    if (!tma) {
+      warp_copy_piece(p, lane);
+    } else {
+      warp_copy_range(0, 1, 1, true, stage + (size_t)warp * kWarpStages * kPiece, bars + warp * kWarpStages, phase,
+                      [&](int64_t) { return p; });
+    }
     __syncwarp();
+    if (npend == 0) pend_q0 = q;
     if (++npend == kStreamBatch) book();
   }
   book();

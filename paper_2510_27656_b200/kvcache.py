@@ -350,9 +350,10 @@ class KvSender:
         j.timeout_ns = int(timeout * 1e9)
         j.err = eng._err.data_ptr()
         j.single_device = eng._single_device(req.kv_desc)
-        for k in range(L.steps):
-            eng.post_op(f"kv.{req.request_id}.s{k + 1}", req.kv_desc.owner, L.page_len * nh * L.pages_per_chunk,
-                        req.imm)
+        if eng.trace.enabled:  # one traced transfer per step (1280 Python calls at cfg5: only when traced)
+            for k in range(L.steps):
+                eng.post_op(f"kv.{req.request_id}.s{k + 1}", req.kv_desc.owner,
+                            L.page_len * nh * L.pages_per_chunk, req.imm)
         with torch.cuda.device(eng.device):
             eng._after_current()
             for t in (si_d, di_d, tickets):

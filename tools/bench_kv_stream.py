@@ -98,6 +98,8 @@ def one_request(mode: str) -> dict:
     if mode == "launch":
         send.prepare(req)
         torch.cuda.synchronize(0)
+        with torch.cuda.stream(st):
+            torch.cuda._sleep(20_000_000)
         e0.record(st)
         for k in range(1, layout.steps + 1):
             send.send_step(req, k)
@@ -109,6 +111,10 @@ def one_request(mode: str) -> dict:
         if mode == "ready":
             clock.advance(comp, by=layout.steps)
             comp.synchronize()
+            # the GPU sleeps while the host enqueues the request, so the
+            # events bracket the kernel, not the host's launch path
+            with torch.cuda.stream(st):
+                torch.cuda._sleep(20_000_000)
             e0.record(st)
             send.stream_all(req, clock, grid=a.grid)
             e1.record(st)

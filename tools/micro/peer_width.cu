@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <vector>
 #include <algorithm>
+#include <random>
 #include <cuda_runtime.h>
 
 __global__ void spin(long long ns) {
@@ -44,6 +45,37 @@ __global__ void __launch_bounds__(512, 1) copy(const uint8_t* __restrict__ s, ui
                        "r"(r[u][2]), "r"(r[u][3]), "r"(r[u][4]), "r"(r[u][5]), "r"(r[u][6]), "r"(r[u][7]) : "memory");
         }
     }
+  }
+}
+
+// one warp per 8-KiB page: page p of the source to slot perm[p] of the peer
+// buffer (the KV stream's access pattern without its step loop)
+__global__ void __launch_bounds__(256, 1) pages(const uint8_t* __restrict__ s, uint8_t* d, const int* perm, int np) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (int p = gw; p < np; p += nw) {
+    const uint4* sp = reinterpret_cast<const uint4*>(s + (size_t)p * 8192);
+    uint4* dp = reinterpret_cast<uint4*>(d + (size_t)perm[p] * 8192);
+    uint4 v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) v[u] = sp[lane + 32 * u];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) dp[lane + 32 * u] = v[u];
+  }
+}
+
+__global__ void __launch_bounds__(256, 1) pages2(const uint8_t* __restrict__ s, uint8_t* d, const int* sperm,
+                                                 const int* perm, int np) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (int p = gw; p < np; p += nw) {
+    const uint4* sp = reinterpret_cast<const uint4*>(s + (size_t)sperm[p] * 8192);
+    uint4* dp = reinterpret_cast<uint4*>(d + (size_t)perm[p] * 8192);
+    uint4 v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) v[u] = sp[lane + 32 * u];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) dp[lane + 32 * u] = v[u];
   }
 }
 
@@ -131,6 +163,73 @@ int main() {
     printf("# 256 MB to the peer: SM copy %.1f us (%.0f GB/s), copy engine %.1f us (%.0f GB/s), "
            "half each at once %.1f us (%.0f GB/s)\n", t_sm, nb / (t_sm * 1e-6) / 1e9, t_ce,
            nb / (t_ce * 1e-6) / 1e9, tb[tb.size() / 2], nb / (tb[tb.size() / 2] * 1e-6) / 1e9);
+  }
+  // scattered 8-KiB pages: 256 MB as 32768 pages into a 1 GiB peer pool
+  {
+    const int np = 32768;
+    uint8_t *s, *d;
+    cudaSetDevice(0); cudaMalloc(&s, (size_t)np * 8192); cudaMemset(s, 3, (size_t)np * 8192);
+    cudaSetDevice(peer); cudaMalloc(&d, 4ull * np * 8192);
+    cudaSetDevice(0);
+    std::vector<int> h(4 * np);
+    for (int i = 0; i < 4 * np; ++i) h[i] = i;
+    std::mt19937 rng(3); std::shuffle(h.begin(), h.end(), rng);
+    int* perm; cudaMalloc(&perm, np * sizeof(int));
+    cudaMemcpy(perm, h.data(), np * sizeof(int), cudaMemcpyHostToDevice);
+    std::vector<int> seq(np); for (int i = 0; i < np; ++i) seq[i] = i;
+    int* ident; cudaMalloc(&ident, np * sizeof(int));
+    cudaMemcpy(ident, seq.data(), np * sizeof(int), cudaMemcpyHostToDevice);
+    const double nb = (double)np * 8192;
+    // and over a 10 GiB pool (the KV request's size): 256 MB into slots
+    // spread over 10 GiB of the peer, sources spread over 10 GiB locally
+    {
+      const size_t big = 10ull << 30;
+      uint8_t *sb, *db;
+      cudaSetDevice(0); cudaMalloc(&sb, big);
+      cudaSetDevice(peer); cudaMalloc(&db, big);
+      cudaSetDevice(0);
+      const int nslots = (int)(big / 8192);
+      std::vector<int> hs(nslots);
+      for (int i = 0; i < nslots; ++i) hs[i] = i;
+      std::shuffle(hs.begin(), hs.end(), rng);
+      int* pb; cudaMalloc(&pb, np * sizeof(int));
+      cudaMemcpy(pb, hs.data(), np * sizeof(int), cudaMemcpyHostToDevice);
+      float tb = timed([&] { pages<<<sms, 256, 0, st>>>(s, db, pb, np); }, st);
+      printf("# 256 MB as 8-KiB pages into random slots of a 10 GiB peer pool: %.1f us (%.0f GB/s)\n", tb,
+             nb / (tb * 1e-6) / 1e9);
+      std::shuffle(hs.begin(), hs.end(), rng);
+      int* sp2; cudaMalloc(&sp2, np * sizeof(int));
+      cudaMemcpy(sp2, hs.data(), np * sizeof(int), cudaMemcpyHostToDevice);
+      float tb2 = timed([&] { pages2<<<sms, 256, 0, st>>>(sb, db, sp2, pb, np); }, st);
+      printf("# ... and from random pages of a 10 GiB local pool: %.1f us (%.0f GB/s)\n", tb2,
+             nb / (tb2 * 1e-6) / 1e9);
+      // the whole 10 GiB (the KV request's duration), contiguous pages in order
+      {
+        const int nall = (int)(big / 8192);
+        std::vector<int> id(nall); for (int i = 0; i < nall; ++i) id[i] = i;
+        int* pid; cudaMalloc(&pid, (size_t)nall * sizeof(int));
+        cudaMemcpy(pid, id.data(), (size_t)nall * sizeof(int), cudaMemcpyHostToDevice);
+        std::vector<float> tt;
+        for (int k = 0; k < 4; ++k) {
+          cudaEvent_t a0, a1; cudaEventCreate(&a0); cudaEventCreate(&a1);
+          cudaEventRecord(a0, st);
+          pages2<<<sms, 256, 0, st>>>(sb, db, pid, pid, nall);
+          cudaEventRecord(a1, st);
+          cudaStreamSynchronize(st);
+          float ms; cudaEventElapsedTime(&ms, a0, a1); tt.push_back(ms);
+        }
+        std::sort(tt.begin(), tt.end());
+        printf("# the whole 10 GiB as 8-KiB pages in one pass: %.2f ms (%.0f GB/s)\n", tt[1],
+               (double)big / (tt[1] * 1e-3) / 1e9);
+      }
+      cudaFree(sb); cudaSetDevice(peer); cudaFree(db); cudaSetDevice(0);
+    }
+    for (int g : {sms, 2 * sms}) {
+      float tr = timed([&] { pages<<<g, 256, 0, st>>>(s, d, perm, np); }, st);
+      float ti = timed([&] { pages<<<g, 256, 0, st>>>(s, d, ident, np); }, st);
+      printf("# 256 MB as 8-KiB pages, one warp each, grid %d x 256: random slots %.1f us (%.0f GB/s), "
+             "in order %.1f us (%.0f GB/s)\n", g, tr, nb / (tr * 1e-6) / 1e9, ti, nb / (ti * 1e-6) / 1e9);
+    }
   }
   return 0;
 }
