@@ -221,7 +221,7 @@ __device__ __forceinline__ bool spin_ge_gpu(const uint64_t* p, uint64_t target, 
 // count releases the receipt.  A warp that reaches a step the clock has not
 // released yet books what it has first, so receipts never wait on a future
 // layer.  The fence is the only drain, and no other warp waits for it.
-constexpr int kStreamBatch = 128;
+constexpr int kStreamBatch = 32;
 
 __global__ void __launch_bounds__(kCopyThreads, 1) k_kv_stream(const __grid_constant__ txb_stream_job ks) {
   extern __shared__ __align__(128) uint8_t stage[];
@@ -258,24 +258,20 @@ __global__ void __launch_bounds__(kCopyThreads, 1) k_kv_stream(const __grid_cons
   uint64_t seen = 0;  // clock value this warp has already acquired
   auto book = [&]() {
     if (npend == 0) return;
-    if (lane == 0) {
-      fence_release(ks.single_device != 0);
-      int kb = (int)(pend_q0 / total);  // one division per batch; the steps advance by nwarps pieces
-      int64_t qb = pend_q0 - (int64_t)kb * total;
-      for (int i = 0; i < npend; ++i) {
-        if (i) {
-          qb += nwarps;
-          while (qb >= total) {
-            qb -= total;
-            ++kb;
-          }
-        }
-        if (atomicAdd(&ks.tickets[kb], 1u) == (uint32_t)total - 1) {
-          ks.tickets[kb] = 0;
-          if (ks.imm_ctr) {
-            fence_release(ks.single_device != 0);
-            red_relaxed_sys_add(ks.imm_ctr, 1);
-          }
+    __syncwarp();
+    // one fence (a warp instruction) makes the batch's stores visible, then
+    // the lanes book its pieces in parallel: a serial loop of returning
+    // atomics on one lane cost a round trip per piece
+    fence_release(ks.single_device != 0);
+    const int kb0 = (int)(pend_q0 / total);
+    const int64_t qb0 = pend_q0 - (int64_t)kb0 * total;
+    for (int i = lane; i < npend; i += 32) {
+      const int kb = kb0 + (int)((qb0 + (int64_t)i * nwarps) / total);
+      if (atomicAdd(&ks.tickets[kb], 1u) == (uint32_t)total - 1) {
+        ks.tickets[kb] = 0;
+        if (ks.imm_ctr) {
+          fence_release(ks.single_device != 0);
+          red_relaxed_sys_add(ks.imm_ctr, 1);
         }
       }
     }
