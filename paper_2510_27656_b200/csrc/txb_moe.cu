@@ -70,6 +70,13 @@ __host__ __device__ inline bool per_token(const txb_moe_shape& s) { return tok_m
 constexpr int kChunk = 2048;
 __host__ __device__ inline int comb_chunks(const txb_moe_shape& s) { return (int)((s.comb_bytes + kChunk - 1) / kChunk); }
 
+// Bookkeeping adds to this rank's flags (targets, per-source diagnostics):
+// a fire-and-forget reduction, not a load-add-store whose load is a round
+// trip on the issuing CTA's critical path.
+__device__ __forceinline__ void add_flag(uint64_t* p, uint64_t v) {
+  atomicAdd(reinterpret_cast<unsigned long long*>(p), (unsigned long long)v);
+}
+
 __device__ __forceinline__ int pad_up(int x) { return (x + kGroupPad - 1) / kGroupPad * kGroupPad; }
 
 // Programmatic dependent launch (sm_90+): let the next kernel on the stream
@@ -551,10 +558,10 @@ __device__ void route_publish(const txb_moe_shape& s, void* const* peers, Flags*
         #pragma unroll 1
         for (int le = lane; le < L; le += 32) c += hist[d * L + le];
         for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-        if (lane == 0 && d != s.me) f->comb_src_t[d] += (uint64_t)c * comb_chunks(s);
+        if (lane == 0 && d != s.me) add_flag(&f->comb_src_t[d], (uint64_t)c * comb_chunks(s));
       }
     if (lane == 0) {
-      f->comb_target += bad ? 0 : ((uint64_t)(n * s.topk) - self) * comb_chunks(s);
+      if (!bad) add_flag(&f->comb_target, ((uint64_t)(n * s.topk) - self) * comb_chunks(s));
       if (bad) atomicOr(&f->err, bad);
     }
   }
@@ -677,14 +684,14 @@ __device__ void book_recv(const txb_moe_shape& s, Flags* f, const uint32_t* C, i
     for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
     const uint32_t take = (q != me && s.priv_tokens > 0) ? min(a, (uint32_t)s.priv_tokens) : 0u;
     if (lane == 0) {
-      f->tok_src_t[q] += a - take;
-      f->priv_src_t[q] += take;
+      add_flag(&f->tok_src_t[q], a - take);
+      if (take) add_flag(&f->priv_src_t[q], take);
     }
     tok += a - take;
     pv += take;
   }
   if (lane == 0) {
-    f->tok_target += tok;
+    add_flag(&f->tok_target, tok);
     f->priv_step = pv;
   }
 }
@@ -1522,7 +1529,9 @@ __device__ void publish_err(Flags* f, int64_t* info, int L) {
 __device__ void wait_tokens(Flags* f, int64_t* info, int L, uint64_t timeout_ns) {
   if (threadIdx.x == 0) {
     const uint64_t dl = globaltimer() + timeout_ns;
-    if (!spin_ge(&f->tok_ctr, f->tok_target, dl)) atomicOr(&f->err, TXB_EV_WAIT_TOKEN);
+    // the target was raised by an atomic add (add_flag) at L2: read it there
+    const uint64_t target = *reinterpret_cast<volatile uint64_t*>(&f->tok_target);
+    if (!spin_ge(&f->tok_ctr, target, dl)) atomicOr(&f->err, TXB_EV_WAIT_TOKEN);
     info[2 * L + 2] = (int64_t)*reinterpret_cast<volatile uint32_t*>(&f->err);
   }
 }
@@ -1683,7 +1692,7 @@ __device__ bool combine_reduce(const txb_moe_shape& s, Flags* f, const uint8_t* 
       } else {
         const uint64_t dl = globaltimer() + timeout_ns;
         const bool ok = per_tok ? spin_ge(tokc_of(region, s) + cta, tokt_of(region, s)[cta], dl)
-                                : spin_ge(&f->comb_ctr, f->comb_target, dl);
+                                : spin_ge(&f->comb_ctr, *reinterpret_cast<volatile uint64_t*>(&f->comb_target), dl);
         sh.fail = ok ? 0u : TXB_EV_WAIT_COMBINE;
         if (sh.fail) atomicOr(&f->err, sh.fail);
       }
