@@ -1733,13 +1733,20 @@ __device__ bool combine_reduce(const txb_moe_shape& s, Flags* f, const uint8_t* 
 __device__ void end_of_step(Flags* f, int ncta) {
   __syncthreads();
   if (threadIdx.x == 0) {
+    // the fields the last CTA updates are loaded before the ticket: nothing
+    // changes them during the combine, and the kernel's tail (the next
+    // step's dispatch waits on it) then carries one round trip, the ticket
+    const uint64_t step = cur_step(f);
+    const uint64_t pstep = *reinterpret_cast<volatile uint64_t*>(&f->priv_step);
+    const uint64_t ptgt = *reinterpret_cast<volatile uint64_t*>(&f->priv_target[step & 1]);
     const uint32_t t = atomicAdd(&f->ticket, 1u);
     if (t == (uint32_t)ncta - 1) {
-      const uint64_t step = cur_step(f);  // read here: nothing waits on it at the kernel's start
       f->ticket = 0;
       f->send_cnt = 0;
-      f->priv_target[step & 1] += f->priv_step;
-      f->priv_step = 0;
+      if (pstep) {
+        f->priv_target[step & 1] = ptgt + pstep;
+        f->priv_step = 0;
+      }
       for (int ph = 0; ph < kPhases; ++ph) f->phase_cnt[ph] = 0;
       *reinterpret_cast<volatile uint64_t*>(&f->step) = step;
     }
